@@ -1,0 +1,304 @@
+// ref_harness.cpp — drives the UNMODIFIED reference simulator (compiled from
+// /root/reference/proj/src into oracle/_ref/libhesp_ref.so) over a batch of
+// candidate partitionings.  TEST INFRASTRUCTURE ONLY: used to generate the
+// golden fixtures, to pin the CPU restatement (oracle/port) and as the
+// bench's CPU baseline / reference arm.  Never linked into the product.
+//
+// Per candidate:
+//   TaskGraph::root_cholesky(n, elem)                       graph.cpp:397
+//   partition_task(0, 1.0/s_base, min_block)                graph.cpp:456
+//   partition_task(op.task, 1.0/op.s, min_block) per op     graph.cpp:456
+//   simulate(graph, platform, model, cfg)                   sim.cpp:838
+// and records status (0 ok, 1 + hesp::Err ordinal, 100 foreign exception),
+// makespan bits, and order-independent hashes of every Assignment and
+// TransferRec (include/hesp_workload.h), so a single 40-byte record pins the
+// whole schedule bit-for-bit.
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hesp/graph.hpp"
+#include "hesp/platform.hpp"
+#include "hesp/sim.hpp"
+#include "hesp_workload.h"
+
+namespace {
+
+struct Record {
+  uint64_t index;
+  int32_t status;
+  int32_t n_leaves;
+  double makespan;
+  uint64_t assign_hash;
+  uint64_t xfer_hash;
+};
+static_assert(sizeof(Record) == 40, "record layout");
+
+struct Args {
+  std::string platform, model, out, detail_out;
+  bool model_csv = false;
+  int64_t n = 16384;
+  int elem = 4;
+  int s_base = 16;
+  hesp_gen_config gen{};
+  std::string ordering = "PL", selection = "EFT-P", caching = "WB";
+  uint64_t sched_seed = 0;
+  uint64_t first = 0, count = 100;
+  int threads = 1;
+  double time_limit = 0;  // seconds; 0 = none
+  long detail = -1;
+  bool quiet = false;
+};
+
+std::string slurp(const std::string& path) {
+  std::ifstream f(path);
+  if (!f) {
+    std::fprintf(stderr, "cannot open %s\n", path.c_str());
+    std::exit(2);
+  }
+  std::stringstream ss;
+  ss << f.rdbuf();
+  return ss.str();
+}
+
+uint64_t bits(double x) {
+  uint64_t u;
+  std::memcpy(&u, &x, 8);
+  return u;
+}
+
+struct Ctx {
+  const Args* a;
+  const hesp::Platform* plat;
+  const hesp::PerfModel* model;
+  hesp::SchedConfig cfg;
+  int32_t n_base;
+  int64_t base_b;
+  int32_t s_base_snapped;
+};
+
+Record evaluate(const Ctx& c, uint64_t index, hesp::SimResult* keep, hesp::TaskGraph** keep_graph) {
+  Record r{};
+  r.index = index;
+  hesp_cand_desc d;
+  hesp_generate(&c.a->gen, c.s_base_snapped, c.n_base, c.base_b, index, &d);
+  try {
+    auto g = hesp::TaskGraph::root_cholesky(c.a->n, c.a->elem);
+    g.partition_task(0, 1.0 / c.a->s_base, c.a->gen.min_block);
+    for (int k = 0; k < d.n_ops; ++k)
+      g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, c.a->gen.min_block);
+    r.n_leaves = static_cast<int32_t>(g.leaf_tasks().size());
+    auto res = hesp::simulate(g, *c.plat, *c.model, c.cfg);
+    r.makespan = res.makespan;
+    uint64_t ah = 0, xh = 0;
+    for (const auto& [id, asg] : res.assignments)
+      ah += hesp_assign_term(asg.task, asg.proc, bits(asg.start), bits(asg.end));
+    for (const auto& x : res.transfers) {
+      int64_t fr = 0, fc = 0, frs = 0, fcs = 0;
+      if (x.fragment) {
+        fr = x.fragment->row;
+        fc = x.fragment->col;
+        frs = x.fragment->rows;
+        fcs = x.fragment->cols;
+      }
+      xh += hesp_xfer_term(x.block, x.route.front().first, x.dst_space, x.bytes, bits(x.start),
+                           bits(x.end), fr, fc, frs, fcs);
+    }
+    r.assign_hash = ah;
+    r.xfer_hash = xh;
+    if (keep) *keep = std::move(res);
+    if (keep_graph) *keep_graph = new hesp::TaskGraph(std::move(g));
+  } catch (const hesp::Error& e) {
+    r.status = 1 + static_cast<int32_t>(e.code());
+    r.makespan = 0;
+  } catch (const std::exception& e) {
+    r.status = 100;
+    r.makespan = 0;
+  }
+  return r;
+}
+
+bool parse_int_list(const char* s, hesp_gen_config* g) {
+  g->n_s_choices = 0;
+  const char* p = s;
+  while (*p && g->n_s_choices < 4) {
+    g->s_choices[g->n_s_choices++] = std::atoi(p);
+    while (*p && *p != ',') ++p;
+    if (*p == ',') ++p;
+  }
+  return g->n_s_choices > 0;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  Args a;
+  a.gen.seed = 1;
+  a.gen.k_max = 8;
+  a.gen.max_depth = 3;
+  a.gen.min_block = 64;
+  a.gen.n_s_choices = 2;
+  a.gen.s_choices[0] = 2;
+  a.gen.s_choices[1] = 4;
+  for (int i = 1; i < argc; ++i) {
+    std::string k = argv[i];
+    auto v = [&]() -> const char* {
+      if (i + 1 >= argc) {
+        std::fprintf(stderr, "missing value for %s\n", k.c_str());
+        std::exit(2);
+      }
+      return argv[++i];
+    };
+    if (k == "--platform") a.platform = v();
+    else if (k == "--model") a.model = v();
+    else if (k == "--model-csv") { a.model = v(); a.model_csv = true; }
+    else if (k == "--n") a.n = std::atoll(v());
+    else if (k == "--elem") a.elem = std::atoi(v());
+    else if (k == "--sbase") a.s_base = std::atoi(v());
+    else if (k == "--seed") a.gen.seed = std::strtoull(v(), nullptr, 0);
+    else if (k == "--kmax") a.gen.k_max = std::atoi(v());
+    else if (k == "--maxdepth") a.gen.max_depth = std::atoi(v());
+    else if (k == "--min-block") a.gen.min_block = std::atoll(v());
+    else if (k == "--s-choices") parse_int_list(v(), &a.gen);
+    else if (k == "--ordering") a.ordering = v();
+    else if (k == "--selection") a.selection = v();
+    else if (k == "--caching") a.caching = v();
+    else if (k == "--sched-seed") a.sched_seed = std::strtoull(v(), nullptr, 0);
+    else if (k == "--first") a.first = std::strtoull(v(), nullptr, 0);
+    else if (k == "--count") a.count = std::strtoull(v(), nullptr, 0);
+    else if (k == "--threads") a.threads = std::atoi(v());
+    else if (k == "--time-limit") a.time_limit = std::atof(v());
+    else if (k == "--out") a.out = v();
+    else if (k == "--detail") a.detail = std::atol(v());
+    else if (k == "--detail-out") a.detail_out = v();
+    else if (k == "--quiet") a.quiet = true;
+    else {
+      std::fprintf(stderr, "unknown argument %s\n", k.c_str());
+      return 2;
+    }
+  }
+  if (a.threads <= 0) a.threads = static_cast<int>(std::thread::hardware_concurrency());
+
+  const auto plat = hesp::Platform::from_json(slurp(a.platform));
+  const auto model = a.model_csv ? hesp::PerfModel::from_table_csv(slurp(a.model))
+                                 : hesp::PerfModel::from_analytic_json(slurp(a.model));
+  Ctx c{&a, &plat, &model, {}, 0, 0, 0};
+  c.cfg.ordering = hesp::ordering_from(a.ordering);
+  c.cfg.selection = hesp::selection_from(a.selection);
+  c.cfg.caching = hesp::caching_from(a.caching);
+  c.cfg.seed = a.sched_seed;
+  c.cfg.min_block = a.gen.min_block;
+  {
+    // base tiling facts for the generator, taken from the reference itself
+    auto g = hesp::TaskGraph::root_cholesky(a.n, a.elem);
+    const int cl = g.partition_task(0, 1.0 / a.s_base, a.gen.min_block);
+    c.n_base = static_cast<int32_t>(g.cluster(cl).members.size());
+    c.base_b = g.task(g.cluster(cl).members.front()).b;
+    c.s_base_snapped = static_cast<int32_t>(a.n / c.base_b);
+  }
+
+  if (a.detail >= 0) {
+    hesp::SimResult res;
+    hesp::TaskGraph* g = nullptr;
+    Record r = evaluate(c, static_cast<uint64_t>(a.detail), &res, &g);
+    FILE* f = a.detail_out.empty() ? stdout : std::fopen(a.detail_out.c_str(), "w");
+    hesp_cand_desc d;
+    hesp_generate(&a.gen, c.s_base_snapped, c.n_base, c.base_b, r.index, &d);
+    std::fprintf(f, "index %llu status %d leaves %d makespan %.17g bits %016llx ah %016llx xh %016llx\n",
+                 (unsigned long long)r.index, r.status, r.n_leaves, r.makespan,
+                 (unsigned long long)bits(r.makespan), (unsigned long long)r.assign_hash,
+                 (unsigned long long)r.xfer_hash);
+    std::fprintf(f, "ops");
+    for (int k = 0; k < d.n_ops; ++k) std::fprintf(f, " %d/%d", d.ops[k].task, d.ops[k].s);
+    std::fprintf(f, "\n");
+    if (g) {
+      for (const auto& [id, blk] : g->data().blocks())
+        std::fprintf(f, "B %d %lld %lld %lld %lld %d\n", id, (long long)blk.region.row,
+                     (long long)blk.region.col, (long long)blk.region.rows,
+                     (long long)blk.region.cols, blk.is_intersection ? 1 : 0);
+      for (int id : g->leaf_tasks()) {
+        const auto& t = g->task(id);
+        std::fprintf(f, "L %d %d %lld r", id, static_cast<int>(t.kind), (long long)t.b);
+        for (int b : t.reads) std::fprintf(f, " %d", b);
+        std::fprintf(f, " w");
+        for (int b : t.writes) std::fprintf(f, " %d", b);
+        std::fprintf(f, " p");
+        for (int p : g->preds(id)) std::fprintf(f, " %d", p);
+        std::fprintf(f, "\n");
+      }
+      delete g;
+    }
+    for (const auto& [id, asg] : res.assignments)
+      std::fprintf(f, "A %d %d %.17g %.17g %016llx %016llx\n", asg.task, asg.proc, asg.start, asg.end,
+                   (unsigned long long)bits(asg.start), (unsigned long long)bits(asg.end));
+    for (const auto& x : res.transfers) {
+      std::fprintf(f, "X %d %d->%d %lld %.17g %.17g", x.block, x.route.front().first, x.dst_space,
+                   (long long)x.bytes, x.start, x.end);
+      if (x.fragment)
+        std::fprintf(f, " frag %lld %lld %lld %lld", (long long)x.fragment->row,
+                     (long long)x.fragment->col, (long long)x.fragment->rows,
+                     (long long)x.fragment->cols);
+      std::fprintf(f, "\n");
+    }
+    if (f != stdout) std::fclose(f);
+    return 0;
+  }
+
+  std::vector<Record> recs(a.count);
+  std::vector<char> done(a.count, 0);
+  std::atomic<uint64_t> next{0};
+  std::atomic<bool> stop{false};
+  const auto t0 = std::chrono::steady_clock::now();
+  auto worker = [&]() {
+    for (;;) {
+      if (stop.load(std::memory_order_relaxed)) return;
+      const uint64_t k = next.fetch_add(1);
+      if (k >= a.count) return;
+      recs[k] = evaluate(c, a.first + k, nullptr, nullptr);
+      done[k] = 1;
+      if (a.time_limit > 0) {
+        const double el =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (el > a.time_limit) stop = true;
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 0; t < a.threads; ++t) pool.emplace_back(worker);
+  for (auto& t : pool) t.join();
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+  uint64_t n_done = 0, n_ok = 0;
+  std::vector<Record> out;
+  out.reserve(a.count);
+  for (uint64_t k = 0; k < a.count; ++k)
+    if (done[k]) {
+      ++n_done;
+      n_ok += recs[k].status == 0;
+      out.push_back(recs[k]);
+    }
+  if (!a.out.empty()) {
+    FILE* f = std::fopen(a.out.c_str(), "wb");
+    const char magic[8] = {'H', 'E', 'S', 'P', 'G', 'L', 'D', '1'};
+    std::fwrite(magic, 1, 8, f);
+    const uint64_t n = out.size();
+    std::fwrite(&n, 8, 1, f);
+    std::fwrite(out.data(), sizeof(Record), out.size(), f);
+    std::fclose(f);
+  }
+  if (!a.quiet) {
+    std::printf(
+        "{\"candidates\": %llu, \"ok\": %llu, \"failed\": %llu, \"wall_s\": %.6f, "
+        "\"cand_per_s\": %.6f, \"threads\": %d, \"hw_threads\": %u}\n",
+        (unsigned long long)n_done, (unsigned long long)n_ok, (unsigned long long)(n_done - n_ok), wall,
+        n_done / wall, a.threads, std::thread::hardware_concurrency());
+  }
+  return 0;
+}
