@@ -1,0 +1,185 @@
+/* hesp_engine.h — C ABI of the B200 batched candidate-schedule engine.
+ *
+ * Drop-in for the reference path:
+ *   TaskGraph::root_cholesky + partition_task      graph.hpp:119,136  (graph.cpp:397-513)
+ *   simulate(graph, platform, model, cfg)          sim.hpp:150-151    (sim.cpp:838-842)
+ *   the batch caller solve()/collect_candidates    solver.hpp:74-84   (declared only)
+ * Inputs mirror the reference's value types field for field:
+ *   hesp_platform      <- hesp::Platform::make(spaces, types, processors, links)  platform.hpp:57
+ *   hesp_perf_model    <- PerfModel::analytic / PerfModel::tabulated             platform.hpp:118-121
+ *   hesp_sched_config  <- hesp::SchedConfig                                       sim.hpp:26-32
+ *   hesp_workload      <- root_cholesky(n, elem) + partition_task(0, 1/s_base)    graph.hpp:119,136
+ * Errors never cross the ABI as exceptions: calls return 0 or a negative
+ * HESP_E_* code (message via hesp_last_error), and every candidate carries a
+ * status = 0 (ok) or 1 + hesp::Err ordinal (errors.hpp:10-32) of the error
+ * the reference would have thrown for it; >= 200 are engine limits.
+ *
+ * One engine handle per GPU; a handle is not thread-safe.  No torch types.
+ */
+#ifndef HESP_ENGINE_H
+#define HESP_ENGINE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "hesp_workload.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- reference value types ------------------------------------------- */
+typedef struct {
+  int32_t id;
+  int64_t capacity_bytes;
+  int32_t is_main;
+} hesp_space; /* MemorySpace, platform.hpp:29-33 */
+
+typedef struct {
+  int32_t id;
+  int32_t type;  /* index into type_names */
+  int32_t space; /* memory space id */
+} hesp_processor; /* Processor, platform.hpp:35-39 */
+
+typedef struct {
+  int32_t src, dst;
+  double latency_s;
+  double bandwidth_bps;
+} hesp_link; /* Link, platform.hpp:41-46 */
+
+typedef struct {
+  int32_t n_spaces;
+  const hesp_space* spaces;
+  int32_t n_types;
+  const char* const* type_names; /* ProcessorType::name, platform.hpp:24-27 */
+  int32_t n_procs;
+  const hesp_processor* procs;
+  int32_t n_links;
+  const hesp_link* links;
+} hesp_platform;
+
+typedef struct {
+  int32_t kind; /* HESP_CHOL .. HESP_GEMM */
+  int32_t type; /* index into hesp_platform.type_names */
+  double peak_flops;
+  double b_half;
+} hesp_analytic_entry; /* PerfModel::analytic tuple, platform.hpp:118-119 */
+
+typedef struct {
+  int32_t kind;
+  int32_t type;
+  int64_t b;
+  double seconds;
+} hesp_table_row; /* PerfModel::tabulated tuple, platform.hpp:120-121 */
+
+enum { HESP_MODEL_TABULATED = 0, HESP_MODEL_ANALYTIC = 1 }; /* PerfModel::Variant */
+
+typedef struct {
+  int32_t variant;
+  int32_t n_entries;
+  const hesp_analytic_entry* entries;
+  int32_t n_rows;
+  const hesp_table_row* rows;
+} hesp_perf_model;
+
+enum { HESP_FCFS = 0, HESP_PL = 1 };                              /* Ordering  */
+enum { HESP_RP = 0, HESP_FP = 1, HESP_EITP = 2, HESP_EFTP = 3 };  /* Selection */
+enum { HESP_WT = 0, HESP_WB = 1, HESP_WA = 2 };                   /* Caching   */
+
+typedef struct {
+  int32_t ordering, selection, caching;
+  int32_t reserved;
+  uint64_t seed;
+  int64_t min_block;
+} hesp_sched_config; /* SchedConfig, sim.hpp:26-32 */
+
+typedef struct {
+  int64_t n;          /* matrix side (root_cholesky) */
+  int32_t elem_size;  /* bytes per element */
+  int32_t s_base;     /* base tiling applied to task 0: partition_task(0, 1.0/s_base) */
+  hesp_gen_config gen; /* candidate generator (include/hesp_workload.h) */
+} hesp_workload;
+
+/* ---- results ---------------------------------------------------------- */
+typedef struct {
+  int32_t status;      /* 0 ok; 1 + hesp::Err ordinal; >= 200 engine limit */
+  int32_t n_leaves;    /* leaf tasks of the expanded DAG (0 if the build failed) */
+  double makespan;     /* SimResult::makespan (0 when status != 0) */
+  uint64_t assign_hash; /* sum of hesp_assign_term over SimResult::assignments */
+  uint64_t xfer_hash;   /* sum of hesp_xfer_term over SimResult::transfers */
+} hesp_outcome;
+
+typedef struct {
+  double makespan;    /* best makespan over status == 0 candidates */
+  int64_t index;      /* lowest global candidate index achieving it (-1 if none) */
+  int64_t n_ok;       /* candidates with status == 0 */
+  int64_t n_evaluated;
+} hesp_best;
+
+enum {
+  HESP_OK = 0,
+  HESP_E_INVALID = -1, /* bad argument / platform / model (message in hesp_last_error) */
+  HESP_E_CUDA = -2,    /* CUDA runtime failure */
+  HESP_E_NODEV = -3    /* no usable sm_100 device */
+};
+
+typedef struct hesp_engine hesp_engine;
+
+/* Validate inputs, precompute the model tables and the base tiling, upload
+ * them and size the per-warp scratch.  Returns NULL on error. */
+hesp_engine* hesp_engine_create(int device, const hesp_platform* platform,
+                                const hesp_perf_model* model, const hesp_sched_config* sched,
+                                const hesp_workload* workload);
+
+/* Candidates first_index .. first_index+count-1 generated on the device from
+ * workload.gen (no H2D traffic).  out (host, may be NULL) receives one
+ * outcome per candidate; best (host, may be NULL) the argmin. */
+int hesp_eval_generated(hesp_engine* e, uint64_t first_index, uint64_t count, hesp_outcome* out,
+                        hesp_best* best);
+
+/* Explicit candidate descriptors from HOST memory (copied in through pinned
+ * staging; outcomes copied back).  Candidate k is reported as index first_index+k. */
+int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
+                    uint64_t first_index, hesp_outcome* out, hesp_best* best);
+
+/* Device-resident variant: descs_dev / out_dev are device pointers (out_dev
+ * may be NULL), stream is a cudaStream_t (NULL = the engine's stream).
+ * best (host, may be NULL) is synchronised before return. */
+int hesp_eval_descs_device(hesp_engine* e, const hesp_cand_desc* descs_dev, uint64_t count,
+                           uint64_t first_index, hesp_outcome* out_dev, hesp_best* best,
+                           void* stream);
+
+/* Write descriptors for candidates first..first+count-1 (device generator)
+ * into a device buffer. */
+int hesp_generate_device(hesp_engine* e, uint64_t first_index, uint64_t count,
+                         hesp_cand_desc* descs_dev, void* stream);
+
+/* Host copy of the device generator (same function), for callers that want
+ * descriptors in host memory. */
+int hesp_generate_host(const hesp_engine* e, uint64_t first_index, uint64_t count,
+                       hesp_cand_desc* descs);
+
+/* Per-task schedule of one candidate: for every task id < cap, proc/start/end
+ * (proc = -1 for non-leaf or unscheduled ids).  Returns the outcome status. */
+int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, int32_t* proc,
+                     double* start, double* end, hesp_outcome* out);
+
+/* Engine facts: kernel launches issued so far, base tiling sizes, slots. */
+typedef struct {
+  int64_t kernel_launches;
+  int32_t n_base_tasks, n_base_blocks, n_slots, sm_count;
+  int64_t slot_bytes;
+  int32_t warps_per_block, blocks_per_sm;
+} hesp_engine_info;
+int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info);
+
+void hesp_engine_destroy(hesp_engine* e);
+
+const char* hesp_last_error(void);
+const char* hesp_status_name(int32_t status);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HESP_ENGINE_H */

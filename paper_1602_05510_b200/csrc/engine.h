@@ -1,0 +1,1800 @@
+// engine.h — one candidate partitioning -> expanded task DAG -> simulated
+// schedule -> makespan, executed cooperatively by one warp.
+//
+// The same source is instantiated twice:
+//   * Engine<DevWarp>  (nvcc, sm_100a): the product — one warp per candidate,
+//     lanes = processors / blocks / cells, ballots and shuffles for selection,
+//     compaction and release;
+//   * Engine<HostWarp> (g++): width-1 build used on the host to precompute
+//     the shared base tiling and, in tests/tools, to debug the engine logic
+//     on a CPU.  It is never called on the product path.
+//
+// Reference behaviour restated here (file:line under /root/reference/proj):
+//   graph build      graph.cpp:142-212 (DataDag), 301-392 (partitioners),
+//                    397-513 (root_cholesky / partition_task), 632-737 (deps)
+//   simulation       sim.cpp:92-192 (ct, ordering, selection), 341-668
+//                    (coherence, transfers, commit), 704-834 (event loop)
+//
+// Equivalences this engine relies on (DESIGN.md §3 proves each):
+//   E1 DataDag links form the Hasse diagram of strict region containment, so
+//      descendants/ancestors/invalidation cones are geometric queries.
+//   E2 Only the transitive closure of the dependence relation affects a
+//      schedule; per-cell last-writer/readers tracking generates it.
+//   E3 Every commit and transfer ends strictly after the current epoch, so
+//      epochs strictly increase, a pin is live iff its release time > now,
+//      and epochs that release nothing can be skipped.  Checked at run time
+//      (ST_ENGINE_INVARIANT if ever violated).
+#pragma once
+
+#include "engine_types.h"
+
+#if defined(__CUDACC__)
+#define HX __device__ __forceinline__
+#define HXN __device__ __noinline__
+#else
+#include <cstring>
+#define HX inline
+#define HXN inline
+#endif
+
+namespace hx {
+
+constexpr double ABSENT = 1.0e308;  // "no valid copy" / "no pin"
+constexpr double NOPIN = -1.0;
+constexpr double HOLD = 1.0e307;    // pinned for the commit in progress
+
+// ---------------------------------------------------------------------------
+// Warp policies
+
+struct HostWarp {
+  static constexpr int W = 1;
+  int lane() const { return 0; }
+  unsigned ballot(bool p) const { return p ? 1u : 0u; }
+  unsigned lt() const { return 0u; }
+  void sync() const {}
+  template <class T>
+  T bcast(T v, int) const { return v; }
+  bool any(bool p) const { return p; }
+  int sumi(int v) const { return v; }
+  long long suml(long long v) const { return v; }
+  double maxd(double v) const { return v; }
+  double mind(double v) const { return v; }
+  int mini(int v) const { return v; }
+  int maxi(int v) const { return v; }
+  // lexicographic argmin of (a, b, id); lanes with id < 0 do not participate
+  void argmin3(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
+  int atomic_add(int* p, int v) const {
+    int o = *p;
+    *p += v;
+    return o;
+  }
+};
+
+#if defined(__CUDACC__)
+struct DevWarp {
+  static constexpr int W = 32;
+  static constexpr unsigned FULL = 0xffffffffu;
+  __device__ __forceinline__ int lane() const { return (int)(threadIdx.x & 31u); }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(FULL, p); }
+  __device__ __forceinline__ unsigned lt() const { return (1u << lane()) - 1u; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+  __device__ __forceinline__ int bcast(int v, int src) const { return __shfl_sync(FULL, v, src); }
+  __device__ __forceinline__ double bcast(double v, int src) const { return __shfl_sync(FULL, v, src); }
+  __device__ __forceinline__ bool any(bool p) const { return __any_sync(FULL, p); }
+  __device__ __forceinline__ int sumi(int v) const { return __reduce_add_sync(FULL, (unsigned)v); }
+  __device__ __forceinline__ long long suml(long long v) const {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+  }
+  __device__ __forceinline__ double maxd(double v) const {
+    for (int o = 16; o; o >>= 1) {
+      double w = __shfl_xor_sync(FULL, v, o);
+      v = v < w ? w : v;
+    }
+    return v;
+  }
+  __device__ __forceinline__ double mind(double v) const {
+    for (int o = 16; o; o >>= 1) {
+      double w = __shfl_xor_sync(FULL, v, o);
+      v = w < v ? w : v;
+    }
+    return v;
+  }
+  __device__ __forceinline__ int mini(int v) const { return __reduce_min_sync(FULL, v); }
+  __device__ __forceinline__ int maxi(int v) const { return __reduce_max_sync(FULL, v); }
+  __device__ __forceinline__ void argmin3(double& a, double& b, int& id) const {
+    for (int o = 16; o; o >>= 1) {
+      const double a2 = __shfl_xor_sync(FULL, a, o);
+      const double b2 = __shfl_xor_sync(FULL, b, o);
+      const int i2 = __shfl_xor_sync(FULL, id, o);
+      bool take;
+      if (i2 < 0) take = false;
+      else if (id < 0) take = true;
+      else if (a2 != a) take = a2 < a;
+      else if (b2 != b) take = b2 < b;
+      else take = i2 < id;
+      if (take) {
+        a = a2;
+        b = b2;
+        id = i2;
+      }
+    }
+  }
+  __device__ __forceinline__ int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
+};
+#endif
+
+HX double dmax(double a, double b) { return a < b ? b : a; }  // == std::max
+#if defined(__CUDACC__)
+HX int ctz32(unsigned m) { return __ffs((int)m) - 1; }
+HX int popc32(unsigned m) { return __popc(m); }
+#else
+HX int ctz32(unsigned m) { return __builtin_ctz(m); }
+HX int popc32(unsigned m) { return __builtin_popcount(m); }
+#endif
+HX bool rcontains(const Region& o, const Region& i) {           // graph.cpp:34-38
+  return i.row >= o.row && i.col >= o.col && i.row + i.rows <= o.row + o.rows &&
+         i.col + i.cols <= o.col + o.cols;
+}
+HX bool roverlap(const Region& a, const Region& b) {  // graph.cpp:40-43
+  return a.row < b.row + b.rows && b.row < a.row + a.rows && a.col < b.col + b.cols &&
+         b.col < a.col + a.cols;
+}
+HX bool rsame(const Region& a, const Region& b) {
+  return a.row == b.row && a.col == b.col && a.rows == b.rows && a.cols == b.cols;
+}
+HX uint64_t dbits(double x) {
+  uint64_t u;
+#if defined(__CUDACC__)
+  u = (uint64_t)__double_as_longlong(x);
+#else
+  std::memcpy(&u, &x, 8);
+#endif
+  return u;
+}
+
+// Small per-warp state (shared memory on the device).
+struct Small {
+  double proc_free[MAXP];
+  double link_free[MAXL];
+  long long used[MAXS];
+  double est[MAXS];
+  PartEntry part[MAXPART];
+  int32_t tmp_i[64];
+  double tmp_d[8];
+};
+
+// ---------------------------------------------------------------------------
+// Engine
+
+template <class WP>
+struct Engine {
+  WP wp;
+  const Problem& pb;
+  Small* sm;
+  // slot arrays
+  TaskMeta* tm;
+  int32_t *t_missing, *t_poff, *t_pcnt, *t_soff, *t_scnt, *leaf;
+  double *t_rel, *t_ct;
+  uint8_t* t_flag;
+  BlockMeta* bm;
+  uint32_t* bflags;  // bits 0-7 mat per space, 8-15 dirty per space, 16 written
+  double *valid, *lastu, *pinu;
+  int32_t *tl_head, *tl_cnt, *tl_boff, *tl_nrb, *tl_ncb, *tl_coff, *tl_ids;
+  int32_t *bnd, *c_writer, *c_rhead, *rnode, *preds, *succs, *pool, *ready, *pbuf;
+  int32_t *gs_a, *gs_b;
+  Region *gs_reg, *gs_reg2;
+  // scalars (uniform across lanes)
+  int32_t status = 0;
+  int32_t nbt, nbb;        // base task / block counts (overlay boundary)
+  int32_t ntasks, nblocks;  // next ids
+  int32_t npart = 0;
+  int32_t nleaves = 0;
+  int32_t n_tl_ids = 0;
+  int32_t nedges = 0;
+  int32_t pool_n = 0;
+  double now = 0.0;
+  double makespan = 0.0;
+  uint64_t ahash = 0, xhash = 0;
+  uint64_t rng = 0;
+  int32_t S, mainsp;
+
+  HX Engine(WP w, const Problem& p, uint8_t* slot, const SlotLayout& L, Small* s)
+      : wp(w), pb(p), sm(s) {
+    tm = (TaskMeta*)(slot + L.tm);
+    t_missing = (int32_t*)(slot + L.t_missing);
+    t_rel = (double*)(slot + L.t_rel);
+    t_ct = (double*)(slot + L.t_ct);
+    t_poff = (int32_t*)(slot + L.t_poff);
+    t_pcnt = (int32_t*)(slot + L.t_pcnt);
+    t_soff = (int32_t*)(slot + L.t_soff);
+    t_scnt = (int32_t*)(slot + L.t_scnt);
+    t_flag = (uint8_t*)(slot + L.t_flag);
+    leaf = (int32_t*)(slot + L.leaf);
+    bm = (BlockMeta*)(slot + L.bm);
+    bflags = (uint32_t*)(slot + L.bflags);
+    valid = (double*)(slot + L.valid);
+    lastu = (double*)(slot + L.lastu);
+    pinu = (double*)(slot + L.pinu);
+    tl_head = (int32_t*)(slot + L.tl_head);
+    tl_cnt = (int32_t*)(slot + L.tl_cnt);
+    tl_boff = (int32_t*)(slot + L.tl_boff);
+    tl_nrb = (int32_t*)(slot + L.tl_nrb);
+    tl_ncb = (int32_t*)(slot + L.tl_ncb);
+    tl_coff = (int32_t*)(slot + L.tl_coff);
+    tl_ids = (int32_t*)(slot + L.tl_ids);
+    bnd = (int32_t*)(slot + L.bnd);
+    c_writer = (int32_t*)(slot + L.c_writer);
+    c_rhead = (int32_t*)(slot + L.c_rhead);
+    rnode = (int32_t*)(slot + L.rnode);
+    preds = (int32_t*)(slot + L.preds);
+    succs = (int32_t*)(slot + L.succs);
+    pool = (int32_t*)(slot + L.pool);
+    ready = (int32_t*)(slot + L.ready);
+    pbuf = (int32_t*)(slot + L.pbuf);
+    gs_a = (int32_t*)(slot + L.gs_a);
+    gs_b = (int32_t*)(slot + L.gs_b);
+    gs_reg = (Region*)(slot + L.gs_reg);
+    gs_reg2 = (Region*)(slot + L.gs_reg2);
+    nbt = p.n_base_tasks;
+    nbb = p.n_base_blocks;
+    S = p.S;
+    mainsp = p.main_space;
+  }
+
+  HX void fail(int32_t code) {
+    if (status == 0) status = code;
+  }
+
+  // ---- overlay accessors (base graph shared, candidate deltas private) ----
+  HX TaskMeta task(int id) const { return id < nbt ? pb.base_tasks[id] : tm[id - nbt]; }
+  HX const BlockMeta& bmeta(int b) const { return b < nbb ? pb.base_blocks[b] : bm[b - nbb]; }
+  HX Region reg(int b) const { return bmeta(b).r; }
+  HX int tile_of(int b) const { return bmeta(b).tile; }
+  HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * pb.elem; }
+  HX long long bbytes(int b) const { return rbytes(reg(b)); }
+  HX double& V(int b, int s) { return valid[(size_t)b * S + s]; }
+  HX double& LU(int b, int s) { return lastu[(size_t)b * S + s]; }
+  HX double& PIN(int b, int s) { return pinu[(size_t)b * S + s]; }
+  HX bool is_mat(int b, int s) const { return (bflags[b] >> s) & 1u; }
+  HX bool is_dirty(int b, int s) const { return (bflags[b] >> (8 + s)) & 1u; }
+  HX int part_index(int task) const {
+    for (int i = 0; i < npart; ++i)
+      if (sm->part[i].task == task) return i;
+    return -1;
+  }
+  HX int bidx_of(long long b) const {
+    for (int i = 0; i < pb.nbv; ++i)
+      if (pb.bval[i] == b) return i;
+    return -1;
+  }
+
+  // =========================================================================
+  // Graph build: DataDag::get_or_create / partition_task
+  // =========================================================================
+
+  // Existing block with exactly region r (DataDag::find_by_region).  t >= 0:
+  // r lies inside base tile t, so only the root, the tile and the tile's
+  // blocks can match.  t < 0 (base build): every block.
+  HX int find_block(const Region& r, int t) {
+    if (t < 0) {
+      int found = -1;
+      for (int base = 0; base < nblocks; base += WP::W) {
+        const int b = base + wp.lane();
+        const bool hit = b < nblocks && rsame(reg(b), r);
+        const unsigned m = wp.ballot(hit);
+        if (m) {
+          found = base + ctz32(m);
+          break;
+        }
+      }
+      return found;
+    }
+    if (rsame(reg(0), r)) return 0;
+    if (rsame(reg(t), r)) return t;
+    for (int base = nbb; base < nblocks; base += WP::W) {
+      const int b = base + wp.lane();
+      const bool hit = b < nblocks && bm[b - nbb].tile == t && rsame(bm[b - nbb].r, r);
+      const unsigned m = wp.ballot(hit);
+      if (m) return base + ctz32(m);
+    }
+    return -1;
+  }
+
+  HX int create_block(const Region& r, bool isint, int t) {  // DataDag::create, graph.cpp:142-189
+    if (nblocks >= pb.maxb) {
+      fail(ST_ENGINE_LIMIT);
+      return -1;
+    }
+    const int id = nblocks++;
+    BlockMeta m;
+    m.r = r;
+    m.tile = t < 0 ? id : t;  // base build: every new block is a base tile
+    m.next = -1;
+    m.isint = isint ? 1 : 0;
+    m.pad = 0;
+    if (wp.lane() == 0) bm[id - nbb] = m;
+    wp.sync();
+    return id;
+  }
+
+  HX int get_or_create(const Region& r, int t) {  // graph.cpp:191-212
+    const int ex = find_block(r, t);
+    if (ex >= 0) return ex;
+    const int id = create_block(r, false, t);
+    if (id < 0) return -1;
+    // Partial overlaps with existing non-intersection blocks get an
+    // intersection descriptor (id order).  Inside tile t only the tile's own
+    // blocks can partially overlap r (root and tile contain it).
+    int nsect = 0;
+    const int lo = t < 0 ? 0 : nbb;
+    for (int base = lo; base < id; base += WP::W) {
+      const int b = base + wp.lane();
+      bool hit = false;
+      if (b < id) {
+        const BlockMeta& o = bmeta(b);
+        hit = (t < 0 || o.tile == t) && !o.isint && !rcontains(o.r, r) && !rcontains(r, o.r) &&
+              roverlap(o.r, r);
+      }
+      const unsigned m = wp.ballot(hit);
+      if (hit) {
+        const int slot = nsect + popc32(m & wp.lt());
+        if (slot < pb.maxgs) gs_a[slot] = b;
+      }
+      nsect += popc32(m);
+    }
+    wp.sync();
+    if (nsect > pb.maxgs) {
+      fail(ST_ENGINE_LIMIT);
+      return -1;
+    }
+    if (nsect > 0 && t < 0) {
+      fail(ST_ENGINE_LIMIT);  // the base tiling never overlaps partially
+      return -1;
+    }
+    for (int k = 0; k < nsect; ++k) {
+      const Region o = reg(gs_a[k]);
+      Region sct;
+      sct.row = o.row > r.row ? o.row : r.row;
+      sct.col = o.col > r.col ? o.col : r.col;
+      const int r1 = (o.row + o.rows < r.row + r.rows) ? o.row + o.rows : r.row + r.rows;
+      const int c1 = (o.col + o.cols < r.col + r.cols) ? o.col + o.cols : r.col + r.cols;
+      sct.rows = r1 - sct.row;
+      sct.cols = c1 - sct.col;
+      if (find_block(sct, t) < 0) {
+        if (create_block(sct, true, t) < 0) return -1;
+      }
+    }
+    return id;
+  }
+
+  // Region of tile (i, j) of an s x s tiling of r (graph.cpp:294-297).
+  static HX Region sub(const Region& r, int s, int i, int j) {
+    const int tb = r.rows / s;
+    Region o;
+    o.row = r.row + i * tb;
+    o.col = r.col + j * tb;
+    o.rows = tb;
+    o.cols = tb;
+    return o;
+  }
+
+  // One emitted sub-task: resolve its regions to blocks (reads in spec order,
+  // then the write: graph.cpp:500-501) and append it with the next task id.
+  HX void emit(int kind, int nr, const Region* rr, const int* rt, const Region& w, int wt) {
+    if (ntasks >= pb.maxt) {
+      fail(ST_ENGINE_LIMIT);
+      return;
+    }
+    TaskMeta m;
+    m.pad = 0;
+    for (int k = 0; k < nr; ++k) {
+      m.blk[k] = get_or_create(rr[k], rt[k]);
+      if (status) return;
+    }
+    m.blk[nr] = get_or_create(w, wt);
+    if (status) return;
+    for (int k = nr + 1; k < 4; ++k) m.blk[k] = -1;
+    m.kind = (int8_t)kind;
+    m.nrd = (int8_t)nr;
+    m.b = w.rows;
+    const int bi = bidx_of(w.rows);
+    if (bi < 0) {
+      fail(ST_ENGINE_LIMIT);  // block side missing from the host time table
+      return;
+    }
+    m.bidx = (int8_t)bi;
+    const int id = ntasks++;
+    if (wp.lane() == 0) tm[id - nbt] = m;
+    wp.sync();
+  }
+
+  // TaskGraph::partition_task (graph.cpp:456-513) followed by the
+  // enumerate_partition loop nests (graph.cpp:301-392).
+  HX void apply_op(int task_id, int s_req) {
+    if (task_id < 0 || task_id >= ntasks) return fail(ST_VALIDATION);
+    if (part_index(task_id) >= 0) return fail(ST_NOT_A_LEAF);
+    const double p = 1.0 / (double)s_req;
+    if (!(p > 0.0 && p < 1.0)) return fail(ST_VALIDATION);
+    const TaskMeta t = task(task_id);
+    const int s = (int)hesp_snap_tiles(t.b, s_req, pb.min_block);
+    if (s == 0) return fail(ST_INDIVISIBLE);
+    if (npart >= MAXPART) return fail(ST_ENGINE_LIMIT);
+    // operands = reads minus writes, in read order; write = writes.front()
+    const int wb = t.blk[t.nrd];
+    Region opr[3];
+    int opt[3];
+    int nop = 0;
+    for (int k = 0; k < t.nrd; ++k)
+      if (t.blk[k] != wb) {
+        opr[nop] = reg(t.blk[k]);
+        opt[nop] = tile_of(t.blk[k]);
+        ++nop;
+      }
+    const Region a = reg(wb);
+    const int at = tile_of(wb);
+    const int child0 = ntasks;
+    Region rr[3];
+    int rt[3];
+    switch (t.kind) {
+      case HESP_CHOL:
+        for (int k = 0; k < s && !status; ++k) {
+          const Region akk = sub(a, s, k, k);
+          rr[0] = akk;
+          rt[0] = at;
+          emit(HESP_CHOL, 1, rr, rt, akk, at);
+          for (int i = k + 1; i < s && !status; ++i) {
+            rr[0] = akk;
+            rr[1] = sub(a, s, i, k);
+            rt[0] = rt[1] = at;
+            emit(HESP_TRSM, 2, rr, rt, rr[1], at);
+          }
+          for (int i = k + 1; i < s && !status; ++i) {
+            const Region aik = sub(a, s, i, k);
+            for (int j = k + 1; j < i && !status; ++j) {
+              rr[0] = aik;
+              rr[1] = sub(a, s, j, k);
+              rr[2] = sub(a, s, i, j);
+              rt[0] = rt[1] = rt[2] = at;
+              emit(HESP_GEMM, 3, rr, rt, rr[2], at);
+            }
+            if (status) break;
+            rr[0] = aik;
+            rr[1] = sub(a, s, i, i);
+            rt[0] = rt[1] = at;
+            emit(HESP_SYRK, 2, rr, rt, rr[1], at);
+          }
+        }
+        break;
+      case HESP_TRSM: {
+        if (nop != 1) return fail(ST_INTERNAL);
+        const Region l = opr[0];
+        const int lt = opt[0];
+        for (int j = 0; j < s && !status; ++j) {
+          const Region ljj = sub(l, s, j, j);
+          for (int i = 0; i < s && !status; ++i) {
+            const Region bij = sub(a, s, i, j);
+            for (int k = 0; k < j && !status; ++k) {
+              rr[0] = sub(a, s, i, k);
+              rr[1] = sub(l, s, j, k);
+              rr[2] = bij;
+              rt[0] = at;
+              rt[1] = lt;
+              rt[2] = at;
+              emit(HESP_GEMM, 3, rr, rt, bij, at);
+            }
+            if (status) break;
+            rr[0] = ljj;
+            rr[1] = bij;
+            rt[0] = lt;
+            rt[1] = at;
+            emit(HESP_TRSM, 2, rr, rt, bij, at);
+          }
+        }
+        break;
+      }
+      case HESP_SYRK: {
+        if (nop != 1) return fail(ST_INTERNAL);
+        const Region src = opr[0];
+        const int st = opt[0];
+        for (int i = 0; i < s && !status; ++i)
+          for (int j = 0; j <= i && !status; ++j) {
+            const Region cij = sub(a, s, i, j);
+            for (int k = 0; k < s && !status; ++k) {
+              rr[0] = sub(src, s, i, k);
+              rt[0] = st;
+              if (i == j) {
+                rr[1] = cij;
+                rt[1] = at;
+                emit(HESP_SYRK, 2, rr, rt, cij, at);
+              } else {
+                rr[1] = sub(src, s, j, k);
+                rr[2] = cij;
+                rt[1] = st;
+                rt[2] = at;
+                emit(HESP_GEMM, 3, rr, rt, cij, at);
+              }
+            }
+          }
+        break;
+      }
+      default: {
+        if (nop != 2) return fail(ST_INTERNAL);
+        const Region ma = opr[0], mb = opr[1];
+        for (int i = 0; i < s && !status; ++i)
+          for (int j = 0; j < s && !status; ++j) {
+            const Region cij = sub(a, s, i, j);
+            for (int k = 0; k < s && !status; ++k) {
+              rr[0] = sub(ma, s, i, k);
+              rr[1] = sub(mb, s, j, k);
+              rr[2] = cij;
+              rt[0] = opt[0];
+              rt[1] = opt[1];
+              rt[2] = at;
+              emit(HESP_GEMM, 3, rr, rt, cij, at);
+            }
+          }
+        break;
+      }
+    }
+    if (status) return;
+    if (wp.lane() == 0) {
+      sm->part[npart].task = task_id;
+      sm->part[npart].child0 = child0;
+      sm->part[npart].nchild = ntasks - child0;
+      sm->part[npart].leaves = 0;
+    }
+    wp.sync();
+    ++npart;
+  }
+
+  // =========================================================================
+  // Post-build indexing: per-tile block lists, leaf program order, deps
+  // =========================================================================
+
+  // Per-tile CSR of the candidate's own blocks (order inside a tile is
+  // irrelevant: every consumer is order-independent or sorts).
+  HX void build_tiles() {
+    for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt[i] = 0;
+    wp.sync();
+    for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt[bm[b - nbb].tile], 1);
+    wp.sync();
+    // exclusive scan over base tiles
+    int run = 0;
+    for (int base = 0; base < nbb; base += WP::W) {
+      const int i = base + wp.lane();
+      const int c = i < nbb ? tl_cnt[i] : 0;
+      int incl = c;
+#if defined(__CUDACC__)
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (wp.lane() >= o) incl += v;
+      }
+#endif
+      if (i < nbb) tl_head[i] = run + incl - c;
+      run += wp.bcast(incl, WP::W - 1);
+    }
+    wp.sync();
+    for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb[i] = 0;  // fill cursor
+    wp.sync();
+    for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
+      const int t = bm[b - nbb].tile;
+      const int pos = wp.atomic_add(&tl_ncb[t], 1);
+      tl_ids[tl_head[t] + pos] = b;
+    }
+    wp.sync();
+    n_tl_ids = run;
+  }
+
+  // Leaf program order: lexicographic seq, i.e. depth-first over clusters
+  // with members in emission order (graph.cpp:552-562).
+  HX void build_order() {
+    // subtree leaf counts, innermost partitions last in op order
+    for (int i = npart - 1; i >= 0; --i) {
+      const PartEntry pe = sm->part[i];
+      int cnt = 0;
+      for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
+        const int pi = part_index(c);
+        cnt += pi >= 0 ? sm->part[pi].leaves : 1;
+      }
+      if (wp.lane() == 0) sm->part[i].leaves = cnt;
+      wp.sync();
+    }
+    // explicit stack of (first child, count, output position)
+    int sf[MAXPART], sc[MAXPART], sp[MAXPART];
+    int top = 0;
+    const int r = part_index(0);
+    if (r < 0) {  // unpartitioned root: a single leaf
+      if (wp.lane() == 0) leaf[0] = 0;
+      wp.sync();
+      nleaves = 1;
+      return;
+    }
+    sf[0] = sm->part[r].child0;
+    sc[0] = sm->part[r].nchild;
+    sp[0] = 0;
+    top = 1;
+    nleaves = sm->part[r].leaves;
+    while (top > 0) {
+      --top;
+      const int f = sf[top], c = sc[top];
+      int pos = sp[top];
+      for (int base = 0; base < c; base += WP::W) {
+        const int k = base + wp.lane();
+        int pi = -1, sz = 0;
+        if (k < c) {
+          pi = part_index(f + k);
+          sz = pi >= 0 ? sm->part[pi].leaves : 1;
+        }
+        int incl = sz;
+#if defined(__CUDACC__)
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (wp.lane() >= o) incl += v;
+        }
+#endif
+        const int my = pos + incl - sz;
+        if (k < c && pi < 0) leaf[my] = f + k;
+        const unsigned m = wp.ballot(k < c && pi >= 0);
+        for (unsigned mm = m; mm; mm &= mm - 1) {
+          const int ln = ctz32(mm);
+          const int q = wp.bcast(pi, ln);
+          const int qp = wp.bcast(my, ln);
+          if (top < MAXPART) {
+            sf[top] = sm->part[q].child0;
+            sc[top] = sm->part[q].nchild;
+            sp[top] = qp;
+            ++top;
+          }
+        }
+        pos += wp.bcast(incl, WP::W - 1);
+      }
+    }
+    wp.sync();
+  }
+
+  // Column/row boundaries of every tile's blocks -> cell grids.
+  HX void build_cells() {
+    int nb_used = 0, nc_used = 0;
+    for (int t = 1; t < nbb && !status; ++t) {
+      const int cnt = tl_cnt[t];
+      if (cnt == 0) {
+        if (wp.lane() == 0) {
+          tl_boff[t] = -1;
+          tl_nrb[t] = 2;
+          tl_ncb[t] = 2;
+          tl_coff[t] = nc_used;
+          c_writer[nc_used] = -1;
+          c_rhead[nc_used] = -1;
+        }
+        wp.sync();
+        ++nc_used;
+        continue;
+      }
+      const Region tr = reg(t);
+      // candidate boundaries: tile edges + every member's edges (rows, then cols)
+      const int nraw = 2 * cnt + 2;
+      if (nb_used + 2 * nraw > pb.maxbnd) return fail(ST_ENGINE_LIMIT);
+      int* rows = bnd + nb_used;
+      int* cols = rows + nraw;
+      // raw values into gs_a / gs_reg scratch, then rank-unique into place
+      int* raw_r = gs_a;
+      int* raw_c = gs_a + nraw;
+      if (2 * nraw > pb.maxgs) return fail(ST_ENGINE_LIMIT);
+      for (int k = wp.lane(); k < nraw; k += WP::W) {
+        int vr, vc;
+        if (k < 2) {
+          vr = k == 0 ? tr.row : tr.row + tr.rows;
+          vc = k == 0 ? tr.col : tr.col + tr.cols;
+        } else {
+          const Region m = reg(tl_ids[tl_head[t] + (k - 2) / 2]);
+          vr = (k & 1) ? m.row + m.rows : m.row;
+          vc = (k & 1) ? m.col + m.cols : m.col;
+        }
+        raw_r[k] = vr;
+        raw_c[k] = vc;
+      }
+      wp.sync();
+      // sort (value, index) then keep first occurrences: rows -> rows[], cols -> cols[]
+      for (int k = wp.lane(); k < nraw; k += WP::W) {
+        const int vr = raw_r[k], vc = raw_c[k];
+        int rr = 0, rc = 0;
+        for (int q = 0; q < nraw; ++q) {
+          const int ur = raw_r[q], uc = raw_c[q];
+          rr += (ur < vr) || (ur == vr && q < k);
+          rc += (uc < vc) || (uc == vc && q < k);
+        }
+        rows[rr] = vr;
+        cols[rc] = vc;
+      }
+      wp.sync();
+      int nr = 0, nc = 0;
+      for (int base = 0; base < nraw; base += WP::W) {
+        const int k = base + wp.lane();
+        int vr = 0, vc = 0;
+        bool kr = false, kc = false;
+        if (k < nraw) {
+          vr = rows[k];
+          vc = cols[k];
+          kr = k == 0 || rows[k - 1] != vr;
+          kc = k == 0 || cols[k - 1] != vc;
+        }
+        const unsigned mr = wp.ballot(kr), mc = wp.ballot(kc);
+        wp.sync();
+        if (kr) gs_a[nr + popc32(mr & wp.lt())] = vr;
+        if (kc) gs_a[nraw + nc + popc32(mc & wp.lt())] = vc;
+        nr += popc32(mr);
+        nc += popc32(mc);
+      }
+      wp.sync();
+      for (int k = wp.lane(); k < nr; k += WP::W) rows[k] = gs_a[k];
+      wp.sync();
+      // cols right after the nr distinct rows
+      for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a[nraw + k];
+      wp.sync();
+      const int ncell = (nr - 1) * (nc - 1);
+      if (nc_used + ncell > pb.maxcells) return fail(ST_ENGINE_LIMIT);
+      for (int k = wp.lane(); k < ncell; k += WP::W) {
+        c_writer[nc_used + k] = -1;
+        c_rhead[nc_used + k] = -1;
+      }
+      if (wp.lane() == 0) {
+        tl_boff[t] = nb_used;
+        tl_nrb[t] = nr;
+        tl_ncb[t] = nc;
+        tl_coff[t] = nc_used;
+      }
+      wp.sync();
+      nb_used += nr + nc;
+      nc_used += ncell;
+    }
+  }
+
+  // Cell rectangle [r0,r1) x [c0,c1) of block b inside its tile.
+  HX void cell_range(int b, int& t, int& r0, int& r1, int& c0, int& c1) {
+    t = tile_of(b);
+    const int off = tl_boff[t];
+    if (off < 0) {
+      r0 = c0 = 0;
+      r1 = c1 = 1;
+      return;
+    }
+    const int nr = tl_nrb[t], nc = tl_ncb[t];
+    const Region r = reg(b);
+    const int* rows = bnd + off;
+    const int* cols = rows + nr;
+    r0 = r1 = c0 = c1 = 0;
+    for (int k = 0; k < nr; ++k) {
+      if (rows[k] == r.row) r0 = k;
+      if (rows[k] == r.row + r.rows) r1 = k;
+    }
+    for (int k = 0; k < nc; ++k) {
+      if (cols[k] == r.col) c0 = k;
+      if (cols[k] == r.col + r.cols) c1 = k;
+    }
+  }
+
+  // Dependences (E2): per cell, last writer + readers since that write.
+  // For each leaf j in program order: reads -> pred last writer, join
+  // readers; writes -> preds last writer and all readers, become writer.
+  HX void build_deps() {
+    int rn_used = 0;
+    nedges = 0;
+    for (int li = 0; li < nleaves && !status; ++li) {
+      const int j = leaf[li];
+      const TaskMeta t = task(j);
+      const int wb = t.blk[t.nrd];
+      int npb = 0;
+      // distinct blocks, read-only ones first in read order, then the write
+      for (int k = 0; k <= t.nrd; ++k) {
+        const int b = t.blk[k];
+        if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
+        bool dup = false;
+        for (int q = 0; q < k; ++q)
+          if (t.blk[q] == b && q < t.nrd) dup = true;
+        if (dup && k < t.nrd) continue;
+        const bool writes = (k == t.nrd);
+        int tt, r0, r1, c0, c1;
+        cell_range(b, tt, r0, r1, c0, c1);
+        const int nc = tl_ncb[tt] - 1;
+        const int w = c1 - c0;
+        const int ncells = (r1 - r0) * w;
+        const int cbase = tl_coff[tt];
+        for (int base = 0; base < ncells; base += WP::W) {
+          const int q = base + wp.lane();
+          int cell = -1;
+          if (q < ncells) cell = cbase + (r0 + q / w) * nc + (c0 + q % w);
+          // last writer
+          int wr = cell >= 0 ? c_writer[cell] : -1;
+          bool e = wr >= 0 && wr != j;
+          unsigned m = wp.ballot(e);
+          if (e) {
+            const int at = npb + popc32(m & wp.lt());
+            if (at < pb.maxpb) pbuf[at] = wr;
+          }
+          npb += popc32(m);
+          if (!writes) {
+            // join readers
+            unsigned mr = wp.ballot(cell >= 0);
+            if (cell >= 0) {
+              const int at = rn_used + popc32(mr & wp.lt());
+              if (at < pb.maxrn) {
+                rnode[2 * at] = j;
+                rnode[2 * at + 1] = c_rhead[cell];
+                c_rhead[cell] = at;
+              }
+            }
+            rn_used += popc32(mr);
+          } else {
+            // consume readers (per-lane list walks, lock-stepped emission)
+            int node = cell >= 0 ? c_rhead[cell] : -1;
+            while (wp.any(node >= 0)) {
+              int rd = -1;
+              if (node >= 0) {
+                rd = rnode[2 * node];
+                node = rnode[2 * node + 1];
+              }
+              const bool ee = rd >= 0 && rd != j;
+              const unsigned me = wp.ballot(ee);
+              if (ee) {
+                const int at = npb + popc32(me & wp.lt());
+                if (at < pb.maxpb) pbuf[at] = rd;
+              }
+              npb += popc32(me);
+            }
+            if (cell >= 0) {
+              c_writer[cell] = j;
+              c_rhead[cell] = -1;
+            }
+          }
+          wp.sync();
+        }
+        if (rn_used > pb.maxrn || npb > pb.maxpb) return fail(ST_ENGINE_LIMIT);
+      }
+      // dedup -> preds CSR
+      int m = 0;
+      for (int base = 0; base < npb; base += WP::W) {
+        const int q = base + wp.lane();
+        bool keep = false;
+        int v = -1;
+        if (q < npb) {
+          v = pbuf[q];
+          keep = true;
+          for (int z = 0; z < q; ++z)
+            if (pbuf[z] == v) {
+              keep = false;
+              break;
+            }
+        }
+        const unsigned mk = wp.ballot(keep);
+        if (keep) {
+          const int at = nedges + m + popc32(mk & wp.lt());
+          if (at < pb.maxedges) preds[at] = v;
+        }
+        m += popc32(mk);
+      }
+      if (nedges + m > pb.maxedges) return fail(ST_ENGINE_LIMIT);
+      if (wp.lane() == 0) {
+        t_poff[j] = nedges;
+        t_pcnt[j] = m;
+        t_missing[j] = m;
+      }
+      wp.sync();
+      nedges += m;
+    }
+    if (status) return;
+    // successors CSR from the preds lists
+    for (int li = wp.lane(); li < nleaves; li += WP::W) t_scnt[leaf[li]] = 0;
+    wp.sync();
+    for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&t_scnt[preds[e]], 1);
+    wp.sync();
+    int run = 0;
+    for (int base = 0; base < nleaves; base += WP::W) {
+      const int li = base + wp.lane();
+      const int c = li < nleaves ? t_scnt[leaf[li]] : 0;
+      int incl = c;
+#if defined(__CUDACC__)
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (wp.lane() >= o) incl += v;
+      }
+#endif
+      if (li < nleaves) {
+        t_soff[leaf[li]] = run + incl - c;
+        t_scnt[leaf[li]] = 0;  // reused as fill cursor
+      }
+      run += wp.bcast(incl, WP::W - 1);
+    }
+    wp.sync();
+    for (int li = 0; li < nleaves; ++li) {  // fill (per dst; order within a list is irrelevant)
+      const int j = leaf[li];
+      const int off = t_poff[j], cnt = t_pcnt[j];
+      for (int q = wp.lane(); q < cnt; q += WP::W) {
+        const int p = preds[off + q];
+        const int pos = wp.atomic_add(&t_scnt[p], 1);
+        succs[t_soff[p] + pos] = j;
+      }
+      wp.sync();
+    }
+  }
+
+  // critical_times (sim.cpp:92-115): ct = avg + max(0, max_succ ct), reverse
+  // program order; pushed to preds so each pred sees all its successors.
+  HX void build_ct() {
+    for (int li = wp.lane(); li < nleaves; li += WP::W) t_rel[leaf[li]] = 0.0;  // t_rel holds best_succ here
+    wp.sync();
+    for (int li = nleaves - 1; li >= 0; --li) {
+      const int j = leaf[li];
+      const TaskMeta t = task(j);
+      const double c = pb.ctavg[t.kind][t.bidx] + t_rel[j];
+      const int off = t_poff[j], cnt = t_pcnt[j];
+      for (int q = wp.lane(); q < cnt; q += WP::W) {
+        const int p = preds[off + q];
+        t_rel[p] = dmax(t_rel[p], c);
+      }
+      if (wp.lane() == 0) t_ct[j] = c;
+      wp.sync();
+    }
+  }
+
+  // =========================================================================
+  // Coherence / memory model (sim.cpp:323-590)
+  // =========================================================================
+
+  // Blocks that can overlap a block of tile t: root, the tile, its CSR list.
+  // Visit order is irrelevant for every caller.
+  template <class F>
+  HX void for_scope(int t, F&& f) {
+    if (t < 0) {  // the root: everything
+      for (int b = wp.lane(); b < nblocks; b += WP::W) f(b);
+      wp.sync();
+      return;
+    }
+    const int cnt = 2 + tl_cnt[t];
+    const int head = tl_head[t];
+    for (int k = wp.lane(); k < cnt; k += WP::W) {
+      const int b = k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]);
+      f(b);
+    }
+    wp.sync();
+  }
+
+  HX int source_space(int b, int exclude) {  // source_spaces().front() minus `exclude` (sim.cpp:341-350)
+    if (mainsp != exclude && V(b, mainsp) != ABSENT) return mainsp;
+    for (int s = 0; s < S; ++s)
+      if (s != mainsp && s != exclude && V(b, s) != ABSENT) return s;
+    return -1;
+  }
+
+  // Engine::plan_transfer (sim.cpp:468-499): FIFO per directed link.
+  HX double plan_transfer(int blk, const Region* frag, long long bytes, int src, int dst,
+                          double data_ready, double tnow) {
+    const int nh = pb.route_n[src * MAXS + dst];
+    if (nh == 0) {
+      fail(ST_NO_ROUTE);
+      return 0.0;
+    }
+    double rdy = dmax(data_ready, tnow);
+    double start0 = 0.0;
+    for (int h = 0; h < nh; ++h) {
+      const int l = pb.route_l[src * MAXS + dst][h];
+      const double st = dmax(sm->link_free[l], rdy);
+      const double en = st + pb.link_lat[l] + (double)bytes / pb.link_bw[l];
+      if (wp.lane() == 0) sm->link_free[l] = en;
+      wp.sync();
+      rdy = en;
+      if (h == 0) start0 = st;
+    }
+    if (!(rdy > now)) fail(ST_ENGINE_INVARIANT);
+    if (frag)
+      xhash += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), frag->row, frag->col,
+                              frag->rows, frag->cols);
+    else
+      xhash += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+    return rdy;
+  }
+
+  HX void set_flag(int b, uint32_t bit, bool on) {
+    if (wp.lane() == 0) bflags[b] = on ? (bflags[b] | bit) : (bflags[b] & ~bit);
+    wp.sync();
+  }
+  HX void setV(int b, int s, double v) {
+    if (wp.lane() == 0) V(b, s) = v;
+    wp.sync();
+  }
+  HX void setLU(int b, int s, double v) {
+    if (wp.lane() == 0) LU(b, s) = v;
+    wp.sync();
+  }
+  HX void setPIN(int b, int s, double v) {
+    if (wp.lane() == 0) PIN(b, s) = v;
+    wp.sync();
+  }
+  HX void add_used(int s, long long d) {
+    if (wp.lane() == 0) sm->used[s] += d;
+    wp.sync();
+  }
+
+  // x strictly inside b (== DataDag::descendants by E1), for x in b's scope
+  HX bool inside(int x, int b, int t, const Region& rb) const {
+    if (b == 0) return x != 0;
+    return x != 0 && x != t && x != b && rcontains(rb, reg(x));
+  }
+
+  // validate_from (sim.cpp:452-461): block and descendants valid at min(., at)
+  HX void validate_from(int b, int s, double at) {
+    const int t = b == 0 ? -1 : tile_of(b);
+    const Region rb = reg(b);
+    for_scope(t, [&](int x) {
+      if (x == b || inside(x, b, t, rb)) {
+        double& v = V(x, s);
+        if (v > at) v = at;
+      }
+    });
+    if (wp.lane() == 0) LU(b, s) = dmax(LU(b, s), at);
+    wp.sync();
+  }
+
+  // ensure_capacity (sim.cpp:374-439).  `depth` guards the single legal
+  // recursion: a dirty flush from an accelerator into main.
+  HX void ensure_capacity(int s, long long bytes, double at, int depth) {
+    const long long cap = pb.cap[s];
+    if (bytes > cap) return fail(ST_CAPACITY);
+    while (sm->used[s] + bytes > cap) {
+      // LRU victim: min (stamp, id) among unpinned materialised blocks
+      double bst = ABSENT;
+      double dummy = 0.0;
+      int bid = -1;
+      for (int base = 0; base < nblocks; base += WP::W) {
+        const int b = base + wp.lane();
+        if (b < nblocks && is_mat(b, s) && !(PIN(b, s) > now)) {
+          bool ok = true;
+          if (s == mainsp) {
+            if (b == 0) ok = false;  // roots are never evicted from main
+            else {
+              bool elsewhere = false;
+              for (int s2 = 0; s2 < S; ++s2)
+                if (s2 != s && V(b, s2) != ABSENT) elsewhere = true;
+              ok = elsewhere;
+            }
+          }
+          if (ok) {
+            const double st = LU(b, s);
+            if (bid < 0 || st < bst || (st == bst && b < bid)) {
+              bst = st;
+              bid = b;
+            }
+          }
+        }
+      }
+      wp.argmin3(bst, dummy, bid);
+      if (bid < 0) return fail(ST_CAPACITY);
+      const int victim = bid;
+      const long long vbytes = bbytes(victim);
+      if (is_dirty(victim, s)) {
+        if (depth > 0) return fail(ST_ENGINE_INVARIANT);
+        const double rdy = V(victim, s);
+        const double arr = plan_transfer(victim, nullptr, vbytes, s, mainsp, rdy, at);  // sim.cpp:408-409 passes `at`
+        if (status) return;
+        set_flag(victim, 1u << (8 + s), false);
+        materialize(victim, mainsp, arr, depth + 1);
+        if (status) return;
+      }
+      set_flag(victim, 1u << s, false);
+      setV(victim, s, ABSENT);
+      add_used(s, -vbytes);
+      setLU(victim, s, 0.0);
+      if (s != mainsp) {
+        // views lose their backing when no materialised block covers them
+        const Region vr = reg(victim);
+        for (int base = 0; base < nblocks; base += WP::W) {
+          const int x = base + wp.lane();
+          bool drop = false;
+          if (x < nblocks && V(x, s) != ABSENT && !is_mat(x, s)) {
+            const Region xr = reg(x);
+            if (roverlap(xr, vr)) {
+              bool covered = false;
+              for (int m = 0; m < nblocks && !covered; ++m)
+                if (is_mat(m, s) && rcontains(reg(m), xr)) covered = true;
+              drop = !covered;
+            }
+          }
+          wp.sync();
+          if (drop) V(x, s) = ABSENT;
+        }
+        wp.sync();
+      }
+    }
+  }
+
+  HX void reserve_bytes(int b, int s, double at, int depth) {  // sim.cpp:441-450
+    if (is_mat(b, s)) return;
+    const long long bytes = bbytes(b);
+    ensure_capacity(s, bytes, at, depth);
+    if (status) return;
+    set_flag(b, 1u << s, true);
+    add_used(s, bytes);
+    setLU(b, s, at);
+  }
+
+  HX void materialize(int b, int s, double at, int depth) {  // sim.cpp:463-466
+    reserve_bytes(b, s, at, depth);
+    if (status) return;
+    validate_from(b, s, at);
+  }
+
+  HX void pin(int s, int b, double until) {  // sim.cpp:352-355 (E3 representation)
+    if (wp.lane() == 0) PIN(b, s) = dmax(PIN(b, s), until);
+    wp.sync();
+  }
+
+  // acquire (sim.cpp:501-519) without the gather fallback.
+  HX double acquire_direct(int b, int s, bool& need_gather) {
+    need_gather = false;
+    const double v = V(b, s);
+    if (v != ABSENT) {
+      if (wp.lane() == 0) LU(b, s) = dmax(LU(b, s), now);
+      wp.sync();
+      return v;
+    }
+    const int src = source_space(b, s);
+    if (src >= 0) {
+      const double rdy = V(b, src);
+      const double arr = plan_transfer(b, nullptr, bbytes(b), src, s, rdy, now);
+      if (status) return 0.0;
+      pin(src, b, arr);
+      materialize(b, s, arr, 0);
+      return arr;
+    }
+    need_gather = true;
+    return 0.0;
+  }
+
+  HX double acquire(int b, int s) {
+    bool g;
+    const double r = acquire_direct(b, s, g);
+    if (!g || status) return r;
+    return gather(b, s);
+  }
+
+  // subtract_regions (graph.cpp:45-84) restricted to what callers need:
+  // mode 0 -> returns 1 if base minus cuts is non-empty; mode 1 -> writes the
+  // row-sweep fragments into out[] and returns their count.
+  HX int subtract(const Region& base, const Region* cuts, int ncut, Region* out, int mode) {
+    int nx = 0, ny = 0;
+    // computed redundantly by every lane (uniform), stored by lane 0
+    int lx[32], ly[32];
+    auto insl = [&](int* arr, int& n, int v) {
+      for (int k = 0; k < n; ++k)
+        if (arr[k] == v) return true;
+      if (n >= 32) return false;
+      int k = n++;
+      while (k > 0 && arr[k - 1] > v) {
+        arr[k] = arr[k - 1];
+        --k;
+      }
+      arr[k] = v;
+      return true;
+    };
+    bool ok = insl(lx, nx, base.col) && insl(lx, nx, base.col + base.cols) && insl(ly, ny, base.row) &&
+              insl(ly, ny, base.row + base.rows);
+    for (int c = 0; c < ncut && ok; ++c) {
+      const Region& cr = cuts[c];
+      if (!roverlap(base, cr)) continue;
+      auto clampi = [](int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); };
+      ok = insl(lx, nx, clampi(cr.col, base.col, base.col + base.cols)) &&
+           insl(lx, nx, clampi(cr.col + cr.cols, base.col, base.col + base.cols)) &&
+           insl(ly, ny, clampi(cr.row, base.row, base.row + base.rows)) &&
+           insl(ly, ny, clampi(cr.row + cr.rows, base.row, base.row + base.rows));
+    }
+    if (!ok) {
+      fail(ST_ENGINE_LIMIT);
+      return 0;
+    }
+    int nout = 0;
+    for (int yi = 0; yi + 1 < ny; ++yi) {
+      bool have = false;
+      Region run;
+      run.row = run.col = run.rows = run.cols = 0;
+      for (int xi = 0; xi + 1 < nx; ++xi) {
+        Region cell;
+        cell.row = ly[yi];
+        cell.col = lx[xi];
+        cell.rows = ly[yi + 1] - ly[yi];
+        cell.cols = lx[xi + 1] - lx[xi];
+        bool covered = false;
+        for (int c = 0; c < ncut; ++c)
+          if (rcontains(cuts[c], cell)) {
+            covered = true;
+            break;
+          }
+        if (covered) {
+          if (have) {
+            if (mode == 0) return 1;
+            if (nout >= pb.maxgs) {
+              fail(ST_ENGINE_LIMIT);
+              return 0;
+            }
+            if (wp.lane() == 0) out[nout] = run;
+            ++nout;
+          }
+          have = false;
+        } else if (have) {
+          run.cols += cell.cols;
+        } else {
+          run = cell;
+          have = true;
+        }
+      }
+      if (have) {
+        if (mode == 0) return 1;
+        if (nout >= pb.maxgs) {
+          fail(ST_ENGINE_LIMIT);
+          return 0;
+        }
+        if (wp.lane() == 0) out[nout] = run;
+        ++nout;
+      }
+    }
+    wp.sync();
+    return nout;
+  }
+
+  // gather (sim.cpp:521-572): assemble a block with no whole valid copy.
+  HXN double gather(int blk, int s) {
+    const Region target = reg(blk);
+    const int t = blk == 0 ? -1 : tile_of(blk);
+    // candidate pieces: contained blocks valid here or anywhere
+    int np = 0;
+    {
+      const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
+      const int head = t < 0 ? 0 : tl_head[t];
+      for (int base = 0; base < cnt; base += WP::W) {
+        const int k = base + wp.lane();
+        int b = -1;
+        bool hit = false;
+        if (k < cnt) {
+          b = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
+          if (b != blk && rcontains(target, reg(b))) {
+            bool any = false;
+            for (int q = 0; q < S; ++q)
+              if (V(b, q) != ABSENT) any = true;
+            hit = any;
+          }
+        }
+        const unsigned m = wp.ballot(hit);
+        if (hit) {
+          const int at = np + popc32(m & wp.lt());
+          if (at < pb.maxgs) gs_a[at] = b;
+        }
+        np += popc32(m);
+      }
+      wp.sync();
+      if (np > pb.maxgs) {
+        fail(ST_ENGINE_LIMIT);
+        return 0.0;
+      }
+    }
+    // sort pieces: local first, then area descending, then id (sim.cpp:540-544)
+    for (int k = wp.lane(); k < np; k += WP::W) {
+      const int a = gs_a[k];
+      const bool la = V(a, s) != ABSENT;
+      const Region ra = reg(a);
+      const long long aa = (long long)ra.rows * ra.cols;
+      int rank = 0;
+      for (int q = 0; q < np; ++q) {
+        const int c = gs_a[q];
+        if (c == a) continue;
+        const bool lc = V(c, s) != ABSENT;
+        const Region rc = reg(c);
+        const long long ac = (long long)rc.rows * rc.cols;
+        bool before;
+        if (lc != la) before = lc;
+        else if (ac != aa) before = ac > aa;
+        else before = c < a;
+        rank += before;
+      }
+      gs_reg2[rank].row = a;  // stash sorted ids in gs_reg2[].row
+    }
+    wp.sync();
+    double arrival = 0.0;
+    int ncov = 0;
+    for (int k = 0; k < np; ++k) {
+      const int piece = gs_reg2[k].row;
+      const Region pr = reg(piece);
+      if (subtract(pr, gs_reg, ncov, nullptr, 0) == 0) {
+        if (status) return 0.0;
+        continue;  // adds nothing
+      }
+      bool g;
+      const double a = acquire_direct(piece, s, g);
+      if (status) return 0.0;
+      if (g) {  // a listed piece is valid somewhere, so this cannot happen
+        fail(ST_ENGINE_INVARIANT);
+        return 0.0;
+      }
+      arrival = dmax(arrival, a);
+      if (wp.lane() == 0) gs_reg[ncov] = pr;
+      wp.sync();
+      ++ncov;
+    }
+    // residue from main, unless it overlaps data written since the start
+    const int nfr = subtract(target, gs_reg, ncov, gs_reg2, 1);
+    if (status) return 0.0;
+    if (nfr > 0) {
+      bool bad = false;
+      for (int f = 0; f < nfr && !bad; ++f) {
+        const Region fr = gs_reg2[f];
+        bool hit = false;
+        for_scope(t, [&](int x) {
+          if ((bflags[x] >> 16) & 1u)
+            if (roverlap(fr, reg(x))) hit = true;
+        });
+        bad = wp.any(hit);
+      }
+      if (bad) {
+        fail(ST_COHERENCE);
+        return 0.0;
+      }
+      if (s != mainsp)
+        for (int f = 0; f < nfr; ++f) {
+          const Region fr = gs_reg2[f];
+          arrival = dmax(arrival, plan_transfer(blk, &fr, rbytes(fr), mainsp, s, 0.0, now));
+          if (status) return 0.0;
+        }
+    }
+    if (V(blk, s) > arrival) setV(blk, s, arrival);
+    return arrival;
+  }
+
+  // invalidate_elsewhere (sim.cpp:574-590) over the invalidation cone
+  // (sim.cpp:204-212), which by E1 is: blocks inside b, plus blocks strictly
+  // containing some block inside b.
+  HX void invalidate_elsewhere(int b, int ws) {
+    const int t = b == 0 ? -1 : tile_of(b);
+    const Region rb = reg(b);
+    long long freed[MAXS];
+    for (int q = 0; q < MAXS; ++q) freed[q] = 0;
+    const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
+    const int head = t < 0 ? 0 : tl_head[t];
+    for (int k = wp.lane(); k < cnt; k += WP::W) {
+      const int x = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
+      const Region rx = reg(x);
+      bool in = false;
+      if (rcontains(rb, rx) || rcontains(rx, rb)) in = true;
+      else if (roverlap(rx, rb)) {
+        // partial overlap: in the cone iff some block inside b is strictly inside x
+        for (int q = 0; q < cnt && !in; ++q) {
+          const int c = t < 0 ? q : (q == 0 ? 0 : (q == 1 ? t : tl_ids[head + q - 2]));
+          const Region rc = reg(c);
+          if (c != x && rcontains(rb, rc) && rcontains(rx, rc) && !rsame(rx, rc)) in = true;
+        }
+      }
+      if (!in) continue;
+      uint32_t f = bflags[x];
+      for (int q = 0; q < S; ++q) {
+        if (q == ws) continue;
+        if ((f >> q) & 1u) {
+          freed[q] += rbytes(rx);
+          LU(x, q) = 0.0;
+        }
+        V(x, q) = ABSENT;
+      }
+      const uint32_t keep = (1u << ws) | (1u << (8 + ws)) | (1u << 16);
+      bflags[x] = f & keep;
+    }
+    wp.sync();
+    for (int q = 0; q < S; ++q) {
+      if (q == ws) continue;
+      const long long fr = wp.suml(freed[q]);
+      if (fr) add_used(q, -fr);
+    }
+  }
+
+  // =========================================================================
+  // Scheduling (sim.cpp:704-834)
+  // =========================================================================
+
+  HX void commit(int j, int p) {  // Engine::commit, sim.cpp:592-668
+    const TaskMeta t = task(j);
+    const int s = pb.proc_space[p];
+    const int type = pb.proc_type[p];
+    // working set: distinct blocks in id order
+    int w[4];
+    int nw = 0;
+    for (int k = 0; k <= t.nrd; ++k) {
+      const int b = t.blk[k];
+      bool dup = false;
+      for (int q = 0; q < nw; ++q)
+        if (w[q] == b) dup = true;
+      if (dup) continue;
+      int q = nw++;
+      while (q > 0 && w[q - 1] > b) {
+        w[q] = w[q - 1];
+        --q;
+      }
+      w[q] = b;
+    }
+    long long wset = 0;
+    for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
+    if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+    double inputs = 0.0;
+    double saved[4];
+    for (int k = 0; k < nw; ++k) {
+      const double a = acquire(w[k], s);
+      if (status) return;
+      inputs = dmax(inputs, a);
+      saved[k] = PIN(w[k], s);
+      setPIN(w[k], s, HOLD);
+    }
+    const int out = t.blk[t.nrd];
+    reserve_bytes(out, s, now, 0);
+    if (status) return;
+    const double start = dmax(dmax(sm->proc_free[p], t_rel[j]), inputs);
+    const double end = start + pb.ttime[t.kind][t.bidx][type];
+    if (!(end > now) || start < now) return fail(ST_ENGINE_INVARIANT);
+    if (wp.lane() == 0) sm->proc_free[p] = end;
+    wp.sync();
+    ahash += hesp_assign_term(j, p, dbits(start), dbits(end));
+    makespan = dmax(makespan, end);
+    for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
+    invalidate_elsewhere(out, s);
+    validate_from(out, s, end);
+    setV(out, s, end);
+    set_flag(out, 1u << 16, true);
+    if (s != mainsp) {
+      if (pb.caching == CACHE_WB) {
+        set_flag(out, 1u << (8 + s), true);
+      } else {
+        const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
+        if (status) return;
+        pin(s, out, arr);
+        materialize(out, mainsp, arr, 1);
+        if (status) return;
+        if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
+          set_flag(out, 1u << s, false);
+          add_used(s, -bbytes(out));
+          setLU(out, s, 0.0);
+          setV(out, s, ABSENT);
+          const Region ro = reg(out);
+          const int tt = out == 0 ? -1 : tile_of(out);
+          for_scope(tt, [&](int x) {
+            if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
+          });
+        }
+      }
+    }
+    // mark committed, release successors (sim.cpp:660-667)
+    if (wp.lane() == 0) t_flag[j] = 1;
+    const int off = t_soff[j], cnt = t_scnt[j];
+    int added = 0;
+    for (int base = 0; base < cnt; base += WP::W) {
+      const int q = base + wp.lane();
+      bool rel = false;
+      int sj = -1;
+      if (q < cnt) {
+        sj = succs[off + q];
+        const int left = --t_missing[sj];
+        t_rel[sj] = dmax(t_rel[sj], end);
+        rel = left == 0;
+      }
+      const unsigned m = wp.ballot(rel);
+      if (rel) pool[pool_n + added + popc32(m & wp.lt())] = sj;
+      added += popc32(m);
+    }
+    wp.sync();
+    pool_n += added;
+  }
+
+  HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
+
+  HX void simulate() {
+    const int P = pb.P;
+    if (nleaves == 0) return fail(ST_VALIDATION);
+    if (P < 1) return fail(ST_NO_PROCESSORS);
+    // check_models (sim.cpp:312-321)
+    bool miss = false;
+    for (int li = wp.lane(); li < nleaves; li += WP::W) {
+      const TaskMeta t = task(leaf[li]);
+      for (int ty = 0; ty < pb.n_types; ++ty)
+        if (!pb.known[t.kind][ty]) miss = true;
+    }
+    if (wp.any(miss)) return fail(ST_MODEL_MISS);
+    // init_memory (sim.cpp:323-339): root materialised in main, every block
+    // valid in main at t=0 (views into the root data)
+    for (int x = wp.lane(); x < nblocks; x += WP::W) {
+      for (int q = 0; q < S; ++q) {
+        V(x, q) = q == mainsp ? 0.0 : ABSENT;
+        LU(x, q) = 0.0;
+        PIN(x, q) = NOPIN;
+      }
+      bflags[x] = x == 0 ? (1u << mainsp) : 0u;
+    }
+    if (wp.lane() < MAXS) sm->used[wp.lane()] = wp.lane() == mainsp ? bbytes(0) : 0;
+    if (wp.lane() < MAXP) sm->proc_free[wp.lane()] = 0.0;
+    if (wp.lane() < MAXL) sm->link_free[wp.lane()] = 0.0;
+#if !defined(__CUDACC__)
+    for (int q = 0; q < MAXS; ++q) sm->used[q] = q == mainsp ? bbytes(0) : 0;
+    for (int q = 0; q < MAXP; ++q) sm->proc_free[q] = 0.0;
+    for (int q = 0; q < MAXL; ++q) sm->link_free[q] = 0.0;
+#endif
+    wp.sync();
+    if (sm->used[mainsp] > pb.cap[mainsp]) return fail(ST_CAPACITY);
+    if (pb.ordering == ORD_PL) build_ct();
+    // initial pool: leaves without predecessors, release 0
+    pool_n = 0;
+    for (int base = 0; base < nleaves; base += WP::W) {
+      const int li = base + wp.lane();
+      bool z = false;
+      int j = -1;
+      if (li < nleaves) {
+        j = leaf[li];
+        t_rel[j] = 0.0;
+        t_flag[j] = 0;
+        z = t_missing[j] == 0;
+      }
+      const unsigned m = wp.ballot(z);
+      if (z) pool[pool_n + popc32(m & wp.lt())] = j;
+      pool_n += popc32(m);
+    }
+    wp.sync();
+    rng = pb.sched_seed;
+    now = 0.0;
+    int committed = 0;
+    bool first = true;
+    const bool waits = pb.selection == SEL_RP || pb.selection == SEL_FP;
+    while (committed < nleaves) {
+      if (!first) {
+        // next epoch (E3): smallest pending release / processor-free time > now
+        double nx = ABSENT;
+        for (int k = wp.lane(); k < pool_n; k += WP::W) {
+          const double r = t_rel[pool[k]];
+          if (r > now && r < nx) nx = r;
+        }
+        if (waits && wp.lane() < P) {
+          const double f = sm->proc_free[wp.lane()];
+          if (f > now && f < nx) nx = f;
+        }
+#if !defined(__CUDACC__)
+        if (waits)
+          for (int q = 0; q < P; ++q) {
+            const double f = sm->proc_free[q];
+            if (f > now && f < nx) nx = f;
+          }
+#endif
+        nx = wp.mind(nx);
+        if (nx == ABSENT) return fail(ST_INTERNAL);  // scheduler stalled
+        now = nx;
+      }
+      first = false;
+      // ready = released, uncommitted, rel <= now; ordered (sim.cpp:117-134)
+      int nr = 0;
+      for (int base = 0; base < pool_n; base += WP::W) {
+        const int k = base + wp.lane();
+        bool r = false;
+        int j = -1;
+        if (k < pool_n) {
+          j = pool[k];
+          r = t_rel[j] <= now;
+        }
+        const unsigned m = wp.ballot(r);
+        if (r) gs_a[nr + popc32(m & wp.lt())] = j;
+        nr += popc32(m);
+      }
+      wp.sync();
+      if (nr == 0) continue;
+      for (int k = wp.lane(); k < nr; k += WP::W) {
+        const int a = gs_a[k];
+        int rank = 0;
+        const double ka = pb.ordering == ORD_PL ? t_ct[a] : t_rel[a];
+        for (int q = 0; q < nr; ++q) {
+          const int c = gs_a[q];
+          const double kc = pb.ordering == ORD_PL ? t_ct[c] : t_rel[c];
+          bool before;
+          if (kc != ka) before = pb.ordering == ORD_PL ? kc > ka : kc < ka;
+          else before = c < a;
+          rank += before;
+        }
+        ready[rank] = a;
+      }
+      wp.sync();
+      for (int r = 0; r < nr; ++r) {
+        const int j = ready[r];
+        const TaskMeta t = task(j);
+        const double rel = t_rel[j];
+        const int lane = wp.lane();
+        const bool idle = lane < P && sm->proc_free[lane] <= now;
+        const unsigned idle_m = wp.ballot(idle);
+        int p = -1;
+#if !defined(__CUDACC__)
+        unsigned idle_h = 0;
+        for (int q = 0; q < P; ++q)
+          if (sm->proc_free[q] <= now) idle_h |= 1u << q;
+        (void)idle_m;
+        const unsigned idle_mask = idle_h;
+#else
+        const unsigned idle_mask = idle_m;
+#endif
+        if (waits && idle_mask == 0) break;  // R-P/F-P wait for a processor
+        if (pb.selection == SEL_RP) {
+          const int n = popc32(idle_mask);
+          const double u = (double)(rng_next() >> 11) * 0x1.0p-53;
+          const int k = (int)((unsigned long long)(u * (double)n) % (unsigned long long)n);
+          unsigned mm = idle_mask;
+          for (int q = 0; q < k; ++q) mm &= mm - 1;
+          p = ctz32(mm);
+        } else {
+          // per-space EFT transfer estimate (sim.cpp:762-793): depends only on the space
+          if (pb.selection == SEL_EFTP) eft_estimate(t);
+          if (status) return;
+          double a = ABSENT, b = 0.0;
+          int id = -1;
+#if defined(__CUDACC__)
+          if (lane < P) {
+            const double nf = sm->proc_free[lane];
+            const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[lane]];
+            if (pb.selection == SEL_EFTP) {
+              a = dmax(dmax(nf, rel), sm->est[pb.proc_space[lane]]) + tt;
+              b = nf;
+              id = lane;
+            } else if (pb.selection == SEL_EITP) {
+              a = nf;
+              id = lane;
+            } else if (idle) {  // F-P
+              a = tt;
+              id = lane;
+            }
+          }
+          wp.argmin3(a, b, id);
+#else
+          for (int q = 0; q < P; ++q) {
+            const double nf = sm->proc_free[q];
+            const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
+            double qa, qb = 0.0;
+            if (pb.selection == SEL_EFTP) {
+              qa = dmax(dmax(nf, rel), sm->est[pb.proc_space[q]]) + tt;
+              qb = nf;
+            } else if (pb.selection == SEL_EITP) {
+              qa = nf;
+            } else {
+              if (!((idle_mask >> q) & 1u)) continue;
+              qa = tt;
+            }
+            if (id < 0 || qa < a || (qa == a && qb < b)) {
+              a = qa;
+              b = qb;
+              id = q;
+            }
+          }
+#endif
+          p = id;
+        }
+        if (p < 0) return fail(ST_NO_PROCESSORS);
+        commit(j, p);
+        if (status) return;
+        ++committed;
+      }
+      // drop committed entries from the pool
+      int keep = 0;
+      for (int base = 0; base < pool_n; base += WP::W) {
+        const int k = base + wp.lane();
+        int j = -1;
+        bool kp = false;
+        if (k < pool_n) {
+          j = pool[k];
+          kp = t_flag[j] == 0;
+        }
+        const unsigned m = wp.ballot(kp);
+        wp.sync();
+        if (kp) pool[keep + popc32(m & wp.lt())] = j;
+        keep += popc32(m);
+        wp.sync();
+      }
+      pool_n = keep;
+    }
+  }
+
+  // est_transfer_ready per memory space for task t (sim.cpp:762-793).
+  HX void eft_estimate(const TaskMeta& t) {
+    int w[4];
+    int nw = 0;
+    for (int k = 0; k <= t.nrd; ++k) {
+      const int b = t.blk[k];
+      bool dup = false;
+      for (int q = 0; q < nw; ++q)
+        if (w[q] == b) dup = true;
+      if (dup) continue;
+      int q = nw++;
+      while (q > 0 && w[q - 1] > b) {
+        w[q] = w[q - 1];
+        --q;
+      }
+      w[q] = b;
+    }
+    bool noroute = false;
+    for (int sp = wp.lane(); sp < S; sp += WP::W) {
+      double est = 0.0;
+      int accl[8];
+      double accv[8];
+      int na = 0;
+      for (int k = 0; k < nw; ++k) {
+        const int b = w[k];
+        const double v = V(b, sp);
+        if (v != ABSENT) {
+          est = dmax(est, v);
+          continue;
+        }
+        const int src = source_space(b, sp);
+        if (src < 0) continue;
+        const int nh = pb.route_n[src * MAXS + sp];
+        if (nh == 0) {
+          noroute = true;
+          continue;
+        }
+        const double bytes = (double)bbytes(b);
+        double tarr = dmax(now, V(b, src));
+        for (int h = 0; h < nh; ++h) {
+          const int l = pb.route_l[src * MAXS + sp][h];
+          int ai = -1;
+          for (int z = 0; z < na; ++z)
+            if (accl[z] == l) ai = z;
+          if (ai < 0) {
+            ai = na++;
+            accl[ai] = l;
+            accv[ai] = 0.0;
+          }
+          accv[ai] += pb.link_lat[l] + bytes / pb.link_bw[l];
+          tarr += accv[ai];
+        }
+        est = dmax(est, tarr);
+      }
+      sm->est[sp] = est;
+    }
+    wp.sync();
+    if (wp.any(noroute)) fail(ST_NO_ROUTE);
+  }
+
+  // =========================================================================
+  // One candidate, end to end
+  // =========================================================================
+
+  // Starts from the base tiling (root + base cluster, shared tables).
+  HX void reset_to_base() {
+    status = 0;
+    ntasks = nbt;
+    nblocks = nbb;
+    npart = 0;
+    makespan = 0.0;
+    ahash = xhash = 0;
+    if (nbt > 1) {  // the base op partitioned the root into tasks 1..nbt-1
+      if (wp.lane() == 0) {
+        sm->part[0].task = 0;
+        sm->part[0].child0 = 1;
+        sm->part[0].nchild = nbt - 1;
+        sm->part[0].leaves = 0;
+      }
+      wp.sync();
+      npart = 1;
+    }
+  }
+
+  HX Outcome run(const hesp_cand_desc& d) {
+    reset_to_base();
+    for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
+    Outcome o;
+    o.n_leaves = 0;
+    if (!status) build_tiles();
+    if (!status) build_order();
+    o.n_leaves = status ? 0 : nleaves;
+    if (!status) build_cells();
+    if (!status) build_deps();
+    if (!status) simulate();
+    o.status = status;
+    o.makespan = status ? 0.0 : makespan;
+    o.assign_hash = status ? 0 : ahash;
+    o.xfer_hash = status ? 0 : xhash;
+    return o;
+  }
+};
+
+}  // namespace hx

@@ -1,0 +1,168 @@
+// engine_types.h — device-resident problem tables and per-candidate slot
+// layout of the batched candidate-schedule engine.  Plain structs, no torch.
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "hesp_workload.h"
+
+namespace hx {
+
+constexpr int MAXP = 32;      // processors (one warp lane each)
+constexpr int MAXS = 8;       // memory spaces
+constexpr int MAXL = 32;      // directed links
+constexpr int MAXTYPES = 8;   // processor types
+constexpr int MAXBV = 48;     // distinct block sides with tabulated times
+constexpr int MAXPART = HESP_MAX_OPS + 2;
+
+// Status codes: 0 ok, 1 + hesp::Err ordinal (errors.hpp:10-32), engine codes >= 200.
+enum : int32_t {
+  ST_OK = 0,
+  ST_VALIDATION = 1 + 1,
+  ST_NO_ROUTE = 1 + 5,
+  ST_NOT_A_LEAF = 1 + 7,
+  ST_INDIVISIBLE = 1 + 8,
+  ST_MODEL_MISS = 1 + 12,
+  ST_CAPACITY = 1 + 13,
+  ST_NO_PROCESSORS = 1 + 14,
+  ST_COHERENCE = 1 + 19,
+  ST_INTERNAL = 1 + 20,
+  ST_ENGINE_LIMIT = 201,      // a per-candidate buffer of the engine overflowed
+  ST_ENGINE_INVARIANT = 202,  // an equivalence assumption of the engine was violated
+};
+
+enum : int32_t { ORD_FCFS = 0, ORD_PL = 1 };
+enum : int32_t { SEL_RP = 0, SEL_FP = 1, SEL_EITP = 2, SEL_EFTP = 3 };
+enum : int32_t { CACHE_WT = 0, CACHE_WB = 1, CACHE_WA = 2 };
+
+struct Region {
+  int32_t row, col, rows, cols;
+};
+
+// Static description of one task: blk[0..nrd) are its reads in spec order,
+// blk[nrd] its single write (reference Task::reads/writes, graph.hpp:90-102).
+struct TaskMeta {
+  int32_t blk[4];
+  int32_t b;
+  int8_t kind, nrd, bidx, pad;
+};
+
+struct BlockMeta {
+  Region r;
+  int32_t tile;    // base tile containing the block (itself for a tile, -1 for the root)
+  int32_t next;    // next block of the same tile, creation (= id) order
+  int32_t isint;   // intersection descriptor (DataBlock::is_intersection)
+  int32_t pad;
+};
+
+struct PartEntry {
+  int32_t task, child0, nchild, leaves;
+};
+
+struct Problem {
+  // ---- platform (platform.hpp:24-86) ----
+  int32_t P, S, main_space, n_types, L;
+  int32_t proc_type[MAXP], proc_space[MAXP];
+  int64_t cap[MAXS];
+  int32_t route_n[MAXS * MAXS];  // hops of transfer_time's route (0 = NoRoute)
+  int32_t route_l[MAXS * MAXS][2];
+  double link_lat[MAXL], link_bw[MAXL];
+  int32_t link_src[MAXL], link_dst[MAXL];
+  // ---- performance model, precomputed on the host (platform.cpp:347-390) ----
+  int32_t nbv;
+  int64_t bval[MAXBV];
+  double ttime[4][MAXBV][MAXTYPES];  // task_time(kind, b, type)
+  double ctavg[4][MAXBV];            // critical_times' per-task mean over processors (sim.cpp:96-106)
+  uint8_t known[4][MAXTYPES];        // PerfModel::knows
+  // ---- workload ----
+  int64_t n;
+  int32_t elem;
+  int32_t s_base;
+  int64_t min_block;
+  int32_t n_base_tasks;   // ids 0..n_base_tasks-1 (root + base tiling)
+  int32_t n_base_blocks;  // ids 0..n_base_blocks-1 (root + base tiles)
+  int32_t n_base_leaves;  // = n_base_tasks - 1
+  int64_t base_b;
+  hesp_gen_config gen;
+  // ---- scheduling policy (SchedConfig, sim.hpp:26-32) ----
+  int32_t ordering, selection, caching;
+  uint64_t sched_seed;
+  // ---- capacities of the per-candidate slot ----
+  int32_t maxt, maxb, maxbnd, maxcells, maxrn, maxedges, maxpb, maxgs;
+  // ---- base graph (shared by every candidate) ----
+  const TaskMeta* base_tasks;    // [n_base_tasks]
+  const BlockMeta* base_blocks;  // [n_base_blocks]
+};
+
+// Per-candidate result record (also the golden-record payload).
+struct Outcome {
+  int32_t status;
+  int32_t n_leaves;
+  double makespan;
+  uint64_t assign_hash;
+  uint64_t xfer_hash;
+};
+
+// Byte layout of one per-warp slot (all arrays in global memory).
+struct SlotLayout {
+  size_t tm, t_missing, t_rel, t_ct, t_poff, t_pcnt, t_soff, t_scnt, t_flag, leaf;
+  size_t bm, bflags, valid, lastu, pinu;
+  size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
+  size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, ready, pbuf;
+  size_t gs_a, gs_b, gs_reg, gs_reg2;
+  size_t total;
+};
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+inline SlotLayout slot_layout(const Problem& p) {
+  SlotLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    o = align_up(o, 16);
+    size_t at = o;
+    o += bytes;
+    return at;
+  };
+  const size_t T = (size_t)p.maxt, B = (size_t)p.maxb, S = (size_t)p.S, NB = (size_t)p.n_base_blocks;
+  L.tm = take(sizeof(TaskMeta) * T);
+  L.t_missing = take(4 * T);
+  L.t_rel = take(8 * T);
+  L.t_ct = take(8 * T);
+  L.t_poff = take(4 * T);
+  L.t_pcnt = take(4 * T);
+  L.t_soff = take(4 * T);
+  L.t_scnt = take(4 * T);
+  L.t_flag = take(T);
+  L.leaf = take(4 * T);
+  L.bm = take(sizeof(BlockMeta) * B);
+  L.bflags = take(4 * B);
+  L.valid = take(8 * B * S);
+  L.lastu = take(8 * B * S);
+  L.pinu = take(8 * B * S);
+  L.tl_head = take(4 * NB);
+  L.tl_cnt = take(4 * NB);
+  L.tl_boff = take(4 * NB);
+  L.tl_nrb = take(4 * NB);
+  L.tl_ncb = take(4 * NB);
+  L.tl_coff = take(4 * NB);
+  L.tl_ids = take(4 * B);
+  L.bnd = take(4 * (size_t)p.maxbnd);
+  L.c_writer = take(4 * (size_t)p.maxcells);
+  L.c_rhead = take(4 * (size_t)p.maxcells);
+  L.rnode = take(8 * (size_t)p.maxrn);
+  L.preds = take(4 * (size_t)p.maxedges);
+  L.succs = take(4 * (size_t)p.maxedges);
+  L.pool = take(4 * T);
+  L.ready = take(4 * T);
+  L.pbuf = take(4 * (size_t)p.maxpb);
+  L.gs_a = take(4 * (size_t)p.maxgs);
+  L.gs_b = take(4 * (size_t)p.maxgs);
+  L.gs_reg = take(sizeof(Region) * (size_t)p.maxgs);
+  L.gs_reg2 = take(sizeof(Region) * (size_t)p.maxgs);
+  L.total = align_up(o, 256);
+  return L;
+}
+
+}  // namespace hx

@@ -1,0 +1,28 @@
+// problem.h — host-side construction of the engine's Problem tables.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "engine_types.h"
+#include "hesp_engine.h"
+
+namespace hx {
+
+// Host copy of a fully built problem: the POD tables plus the base graph
+// arrays the device copies point at after upload.
+struct HostProblem {
+  Problem p{};
+  std::vector<TaskMeta> base_tasks;
+  std::vector<BlockMeta> base_blocks;
+};
+
+// Validates (Platform::validate, platform.cpp:91-138; PerfModel::analytic,
+// platform.cpp:312-325) and precomputes everything; throws std::runtime_error.
+HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& model,
+                          const hesp_sched_config& sched, const hesp_workload& wl);
+
+// PerfModel::task_time restated for one (kind, b, type); throws on miss.
+double host_task_time(const hesp_perf_model& m, int kind, long long b, int type, bool* known);
+
+}  // namespace hx
