@@ -198,6 +198,10 @@ struct Engine {
   uint64_t ahash = 0, xhash = 0;
   uint64_t rng = 0;
   int32_t S, mainsp;
+  // optional per-task schedule trace (hesp_eval_detail): proc/start/end by task id
+  int32_t* tr_proc = nullptr;
+  double *tr_start = nullptr, *tr_end = nullptr;
+  int32_t tr_cap = 0;
 
   HX Engine(WP w, const Problem& p, uint8_t* slot, const SlotLayout& L, Small* s)
       : wp(w), pb(p), sm(s) {
@@ -1436,6 +1440,11 @@ struct Engine {
     if (wp.lane() == 0) sm->proc_free[p] = end;
     wp.sync();
     ahash += hesp_assign_term(j, p, dbits(start), dbits(end));
+    if (tr_proc && j < tr_cap && wp.lane() == 0) {
+      tr_proc[j] = p;
+      tr_start[j] = start;
+      tr_end[j] = end;
+    }
     makespan = dmax(makespan, end);
     for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
     invalidate_elsewhere(out, s);

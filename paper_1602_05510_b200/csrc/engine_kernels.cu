@@ -1,0 +1,491 @@
+// engine_kernels.cu — sm_100a kernels and the C ABI (include/hesp_engine.h).
+//
+// K1 eval_kernel: persistent warps; each warp pulls candidate indices from a
+//    global atomic counter, generates (or loads) the descriptor, expands the
+//    DAG, simulates the schedule in its private scratch slot and writes a
+//    32-byte outcome.  Candidates vary ~10x in cost (early CoherenceError vs a
+//    full 1.3k-task schedule), hence dynamic pulling instead of a static split.
+// K2 reduce_best: grid-level argmin of (makespan, index) over status == 0.
+// The multi-GPU min-reduce over NVLink (K3) lives in the host driver
+// (paper_1602_05510_b200/engine.py) on 16 bytes per rank.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "hesp_engine.h"
+#include "problem.h"
+
+using namespace hx;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct WarpBest {
+  double makespan;
+  long long index;
+  long long n_ok;
+  long long n_eval;
+};
+
+constexpr int WARPS_PER_BLOCK = 4;
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
+    eval_kernel(const Problem* __restrict__ pbp, const hesp_cand_desc* __restrict__ descs,
+                unsigned long long first_index, unsigned long long count,
+                hesp_outcome* __restrict__ out, WarpBest* __restrict__ wbest, uint8_t* scratch,
+                SlotLayout L, unsigned long long* counter) {
+  __shared__ Small smem[WARPS_PER_BLOCK];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
+  uint8_t* slot = scratch + (size_t)gw * L.total;
+  const Problem& pb = *pbp;
+  double best_mk = 0.0;
+  long long best_idx = -1, n_ok = 0, n_eval = 0;
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1ULL);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= count) break;
+    hesp_cand_desc d;
+    if (descs) {
+      d = descs[k];
+    } else {
+      hesp_generate(&pb.gen, pb.s_base == 0 ? 0 : (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b,
+                    first_index + k, &d);
+    }
+    Engine<DevWarp> eng(DevWarp{}, pb, slot, L, &smem[wib]);
+    const Outcome o = eng.run(d);
+    if (lane == 0 && out) {
+      hesp_outcome r;
+      r.status = o.status;
+      r.n_leaves = o.n_leaves;
+      r.makespan = o.makespan;
+      r.assign_hash = o.assign_hash;
+      r.xfer_hash = o.xfer_hash;
+      out[k] = r;
+    }
+    ++n_eval;
+    if (o.status == 0) {
+      ++n_ok;
+      const long long gi = (long long)(first_index + k);
+      if (best_idx < 0 || o.makespan < best_mk || (o.makespan == best_mk && gi < best_idx)) {
+        best_mk = o.makespan;
+        best_idx = gi;
+      }
+    }
+  }
+  if (lane == 0) {
+    WarpBest b;
+    b.makespan = best_mk;
+    b.index = best_idx;
+    b.n_ok = n_ok;
+    b.n_eval = n_eval;
+    wbest[gw] = b;
+  }
+}
+
+__global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* __restrict__ best) {
+  __shared__ double smk[32];
+  __shared__ long long sidx[32], sok[32], sev[32];
+  double mk = 0.0;
+  long long idx = -1, ok = 0, ev = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const WarpBest b = wb[i];
+    ok += b.n_ok;
+    ev += b.n_eval;
+    if (b.index >= 0 && (idx < 0 || b.makespan < mk || (b.makespan == mk && b.index < idx))) {
+      mk = b.makespan;
+      idx = b.index;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, mk, o);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+    ok += __shfl_xor_sync(0xffffffffu, ok, o);
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    if (i2 >= 0 && (idx < 0 || m2 < mk || (m2 == mk && i2 < idx))) {
+      mk = m2;
+      idx = i2;
+    }
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    smk[w] = mk;
+    sidx[w] = idx;
+    sok[w] = ok;
+    sev[w] = ev;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    hesp_best r{0.0, -1, 0, 0};
+    for (int i = 0; i < nw; ++i) {
+      r.n_ok += sok[i];
+      r.n_evaluated += sev[i];
+      if (sidx[i] >= 0 && (r.index < 0 || smk[i] < r.makespan ||
+                           (smk[i] == r.makespan && sidx[i] < r.index))) {
+        r.makespan = smk[i];
+        r.index = sidx[i];
+      }
+    }
+    *best = r;
+  }
+}
+
+__global__ void gen_kernel(const Problem* __restrict__ pbp, unsigned long long first, unsigned long long count,
+                           hesp_cand_desc* __restrict__ out) {
+  const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const Problem& pb = *pbp;
+  hesp_cand_desc d;
+  hesp_generate(&pb.gen, (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b, first + i, &d);
+  out[i] = d;
+}
+
+__global__ void detail_kernel(const Problem* __restrict__ pbp, const hesp_cand_desc* __restrict__ desc,
+                              uint8_t* slot, SlotLayout L, int32_t cap, int32_t* proc, double* start,
+                              double* end, hesp_outcome* out) {
+  __shared__ Small smem;
+  Engine<DevWarp> eng(DevWarp{}, *pbp, slot, L, &smem);
+  eng.tr_proc = proc;
+  eng.tr_start = start;
+  eng.tr_end = end;
+  eng.tr_cap = cap;
+  const Outcome o = eng.run(*desc);
+  if (threadIdx.x == 0) {
+    out->status = o.status;
+    out->n_leaves = o.n_leaves;
+    out->makespan = o.makespan;
+    out->assign_hash = o.assign_hash;
+    out->xfer_hash = o.xfer_hash;
+  }
+}
+
+}  // namespace
+
+struct hesp_engine {
+  int device = 0;
+  HostProblem hp;
+  Problem* d_problem = nullptr;
+  TaskMeta* d_base_tasks = nullptr;
+  BlockMeta* d_base_blocks = nullptr;
+  SlotLayout L{};
+  uint8_t* d_scratch = nullptr;
+  int n_slots = 0, n_blocks = 0, sm_count = 0, blocks_per_sm = 0;
+  WarpBest* d_wbest = nullptr;
+  hesp_best* d_best = nullptr;
+  hesp_best* h_best = nullptr;  // pinned
+  unsigned long long* d_counter = nullptr;
+  hesp_outcome* d_out = nullptr;
+  size_t out_cap = 0;
+  hesp_cand_desc* d_descs = nullptr;
+  size_t desc_cap = 0;
+  hesp_cand_desc* h_descs = nullptr;  // pinned staging
+  hesp_outcome* h_out = nullptr;      // pinned staging
+  size_t h_cap = 0;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+};
+
+namespace {
+
+bool ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return true;
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return false;
+}
+
+bool grow_out(hesp_engine* e, size_t n) {
+  if (n <= e->out_cap) return true;
+  if (e->d_out) cudaFree(e->d_out);
+  e->d_out = nullptr;
+  if (!ck(cudaMalloc(&e->d_out, n * sizeof(hesp_outcome)), "cudaMalloc outcomes")) return false;
+  e->out_cap = n;
+  return true;
+}
+
+bool grow_host(hesp_engine* e, size_t n) {
+  if (n <= e->h_cap) return true;
+  if (e->h_descs) cudaFreeHost(e->h_descs);
+  if (e->h_out) cudaFreeHost(e->h_out);
+  e->h_descs = nullptr;
+  e->h_out = nullptr;
+  if (!ck(cudaMallocHost(&e->h_descs, n * sizeof(hesp_cand_desc)), "cudaMallocHost descs")) return false;
+  if (!ck(cudaMallocHost(&e->h_out, n * sizeof(hesp_outcome)), "cudaMallocHost outcomes")) return false;
+  e->h_cap = n;
+  return true;
+}
+
+int launch_eval(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
+                hesp_outcome* d_out, cudaStream_t st) {
+  if (!ck(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned long long), st), "memset counter"))
+    return HESP_E_CUDA;
+  eval_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(e->d_problem, d_descs, first, count, d_out,
+                                                            e->d_wbest, e->d_scratch, e->L, e->d_counter);
+  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
+  e->launches += 2;
+  if (!ck(cudaGetLastError(), "eval launch")) return HESP_E_CUDA;
+  return HESP_OK;
+}
+
+int finish_best(hesp_engine* e, hesp_best* best, cudaStream_t st) {
+  if (!best) return HESP_OK;
+  if (!ck(cudaMemcpyAsync(e->h_best, e->d_best, sizeof(hesp_best), cudaMemcpyDeviceToHost, st), "best D2H"))
+    return HESP_E_CUDA;
+  if (!ck(cudaStreamSynchronize(st), "sync")) return HESP_E_CUDA;
+  *best = *e->h_best;
+  return HESP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hesp_last_error(void) { return g_last_error.c_str(); }
+
+const char* hesp_status_name(int32_t s) {
+  static const char* names[] = {"ok",
+                                "ParseError",
+                                "ValidationError",
+                                "DuplicateEntry",
+                                "UnknownKindOrType",
+                                "EmptyModel",
+                                "NoRoute",
+                                "InvalidSize",
+                                "NotALeaf",
+                                "IndivisibleGrain",
+                                "UnknownPartitioner",
+                                "NestedCluster",
+                                "UnknownCluster",
+                                "ModelMiss",
+                                "CapacityInfeasible",
+                                "NoProcessors",
+                                "GrainTooSmall",
+                                "EmptyCandidates",
+                                "MissingTrace",
+                                "ConfigError",
+                                "CoherenceError",
+                                "InternalError"};
+  if (s >= 0 && s <= 21) return names[s];
+  if (s == 100) return "ForeignException";
+  if (s == ST_ENGINE_LIMIT) return "EngineLimit";
+  if (s == ST_ENGINE_INVARIANT) return "EngineInvariant";
+  return "Unknown";
+}
+
+hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const hesp_perf_model* model,
+                                const hesp_sched_config* sched, const hesp_workload* workload) {
+  if (!platform || !model || !sched || !workload) {
+    g_last_error = "null argument";
+    return nullptr;
+  }
+  auto* e = new hesp_engine();
+  e->device = device;
+  try {
+    e->hp = build_problem(*platform, *model, *sched, *workload);
+  } catch (const std::exception& ex) {
+    g_last_error = ex.what();
+    delete e;
+    return nullptr;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    g_last_error = "no CUDA device " + std::to_string(device);
+    delete e;
+    return nullptr;
+  }
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major != 10) {
+    g_last_error = "engine is built for sm_100a; device is sm_" + std::to_string(prop.major * 10 + prop.minor);
+    delete e;
+    return nullptr;
+  }
+  auto fail = [&](cudaError_t c, const char* what) -> hesp_engine* {
+    ck(c, what);
+    hesp_engine_destroy(e);
+    return nullptr;
+  };
+  cudaError_t c;
+  if ((c = cudaSetDevice(device)) != cudaSuccess) return fail(c, "cudaSetDevice");
+  if ((c = cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return fail(c, "stream");
+  e->sm_count = prop.multiProcessorCount;
+  int bps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, eval_kernel, WARPS_PER_BLOCK * 32, 0);
+  if (bps < 1) bps = 1;
+  e->blocks_per_sm = bps;
+  e->n_blocks = e->sm_count * bps;
+  e->n_slots = e->n_blocks * WARPS_PER_BLOCK;
+  Problem p = e->hp.p;
+  const size_t nt = e->hp.base_tasks.size(), nb = e->hp.base_blocks.size();
+  if ((c = cudaMalloc(&e->d_base_tasks, nt * sizeof(TaskMeta))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMalloc(&e->d_base_blocks, nb * sizeof(BlockMeta))) != cudaSuccess) return fail(c, "malloc");
+  cudaMemcpy(e->d_base_tasks, e->hp.base_tasks.data(), nt * sizeof(TaskMeta), cudaMemcpyHostToDevice);
+  cudaMemcpy(e->d_base_blocks, e->hp.base_blocks.data(), nb * sizeof(BlockMeta), cudaMemcpyHostToDevice);
+  p.base_tasks = e->d_base_tasks;
+  p.base_blocks = e->d_base_blocks;
+  e->L = slot_layout(p);
+  if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
+  cudaMemcpy(e->d_problem, &p, sizeof(Problem), cudaMemcpyHostToDevice);
+  if ((c = cudaMalloc(&e->d_scratch, (size_t)e->n_slots * e->L.total)) != cudaSuccess)
+    return fail(c, "malloc scratch");
+  if ((c = cudaMalloc(&e->d_wbest, (size_t)e->n_slots * sizeof(WarpBest))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMalloc(&e->d_counter, sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMallocHost(&e->h_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc host");
+  e->hp.p = p;
+  return e;
+}
+
+void hesp_engine_destroy(hesp_engine* e) {
+  if (!e) return;
+  cudaFree(e->d_problem);
+  cudaFree(e->d_base_tasks);
+  cudaFree(e->d_base_blocks);
+  cudaFree(e->d_scratch);
+  cudaFree(e->d_wbest);
+  cudaFree(e->d_best);
+  cudaFree(e->d_counter);
+  cudaFree(e->d_out);
+  cudaFree(e->d_descs);
+  if (e->h_best) cudaFreeHost(e->h_best);
+  if (e->h_descs) cudaFreeHost(e->h_descs);
+  if (e->h_out) cudaFreeHost(e->h_out);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+}
+
+int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info) {
+  if (!e || !info) return HESP_E_INVALID;
+  info->kernel_launches = e->launches;
+  info->n_base_tasks = e->hp.p.n_base_tasks;
+  info->n_base_blocks = e->hp.p.n_base_blocks;
+  info->n_slots = e->n_slots;
+  info->sm_count = e->sm_count;
+  info->slot_bytes = (int64_t)e->L.total;
+  info->warps_per_block = WARPS_PER_BLOCK;
+  info->blocks_per_sm = e->blocks_per_sm;
+  return HESP_OK;
+}
+
+int hesp_eval_generated(hesp_engine* e, uint64_t first_index, uint64_t count, hesp_outcome* out,
+                        hesp_best* best) {
+  if (!e) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  hesp_outcome* dout = nullptr;
+  if (out) {
+    if (!grow_out(e, count)) return HESP_E_CUDA;
+    dout = e->d_out;
+  }
+  int r = launch_eval(e, nullptr, first_index, count, dout, e->stream);
+  if (r) return r;
+  if (out && !ck(cudaMemcpyAsync(out, dout, count * sizeof(hesp_outcome), cudaMemcpyDeviceToHost, e->stream),
+                 "outcomes D2H"))
+    return HESP_E_CUDA;
+  if (best) return finish_best(e, best, e->stream);
+  return ck(cudaStreamSynchronize(e->stream), "sync") ? HESP_OK : HESP_E_CUDA;
+}
+
+int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count, uint64_t first_index,
+                    hesp_outcome* out, hesp_best* best) {
+  if (!e || !descs) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  if (count > e->desc_cap) {
+    if (e->d_descs) cudaFree(e->d_descs);
+    e->d_descs = nullptr;
+    if (!ck(cudaMalloc(&e->d_descs, count * sizeof(hesp_cand_desc)), "malloc descs")) return HESP_E_CUDA;
+    e->desc_cap = count;
+  }
+  if (!grow_out(e, count) || !grow_host(e, count)) return HESP_E_CUDA;
+  std::memcpy(e->h_descs, descs, count * sizeof(hesp_cand_desc));
+  if (!ck(cudaMemcpyAsync(e->d_descs, e->h_descs, count * sizeof(hesp_cand_desc), cudaMemcpyHostToDevice,
+                          e->stream),
+          "descs H2D"))
+    return HESP_E_CUDA;
+  int r = launch_eval(e, e->d_descs, first_index, count, e->d_out, e->stream);
+  if (r) return r;
+  if (!ck(cudaMemcpyAsync(e->h_out, e->d_out, count * sizeof(hesp_outcome), cudaMemcpyDeviceToHost, e->stream),
+          "outcomes D2H"))
+    return HESP_E_CUDA;
+  r = finish_best(e, best, e->stream);
+  if (r) return r;
+  if (!ck(cudaStreamSynchronize(e->stream), "sync")) return HESP_E_CUDA;
+  if (out) std::memcpy(out, e->h_out, count * sizeof(hesp_outcome));
+  return HESP_OK;
+}
+
+int hesp_eval_descs_device(hesp_engine* e, const hesp_cand_desc* descs_dev, uint64_t count, uint64_t first_index,
+                           hesp_outcome* out_dev, hesp_best* best, void* stream) {
+  if (!e || !descs_dev) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+  int r = launch_eval(e, descs_dev, first_index, count, out_dev, st);
+  if (r) return r;
+  return finish_best(e, best, st);
+}
+
+int hesp_generate_device(hesp_engine* e, uint64_t first_index, uint64_t count, hesp_cand_desc* descs_dev,
+                         void* stream) {
+  if (!e || !descs_dev) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
+  const unsigned blocks = (unsigned)((count + 255) / 256);
+  if (blocks) gen_kernel<<<blocks, 256, 0, st>>>(e->d_problem, first_index, count, descs_dev);
+  e->launches += blocks ? 1 : 0;
+  return ck(cudaGetLastError(), "gen launch") ? HESP_OK : HESP_E_CUDA;
+}
+
+int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, int32_t* proc, double* start,
+                     double* end, hesp_outcome* out) {
+  if (!e || !desc || cap < 0) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  hesp_cand_desc* dd = nullptr;
+  int32_t* dp = nullptr;
+  double *ds = nullptr, *de = nullptr;
+  hesp_outcome* dout = nullptr;
+  const size_t n = cap > 0 ? (size_t)cap : 1;
+  bool ok = ck(cudaMalloc(&dd, sizeof(hesp_cand_desc)), "malloc") && ck(cudaMalloc(&dp, n * 4), "malloc") &&
+            ck(cudaMalloc(&ds, n * 8), "malloc") && ck(cudaMalloc(&de, n * 8), "malloc") &&
+            ck(cudaMalloc(&dout, sizeof(hesp_outcome)), "malloc");
+  if (ok) {
+    cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
+    cudaMemset(dp, 0xff, n * 4);
+    cudaMemset(ds, 0, n * 8);
+    cudaMemset(de, 0, n * 8);
+    detail_kernel<<<1, 32, 0, e->stream>>>(e->d_problem, dd, e->d_scratch, e->L, cap, dp, ds, de, dout);
+    e->launches += 1;
+    ok = ck(cudaStreamSynchronize(e->stream), "detail");
+  }
+  hesp_outcome o{};
+  if (ok) {
+    cudaMemcpy(&o, dout, sizeof(o), cudaMemcpyDeviceToHost);
+    if (proc) cudaMemcpy(proc, dp, (size_t)cap * 4, cudaMemcpyDeviceToHost);
+    if (start) cudaMemcpy(start, ds, (size_t)cap * 8, cudaMemcpyDeviceToHost);
+    if (end) cudaMemcpy(end, de, (size_t)cap * 8, cudaMemcpyDeviceToHost);
+    if (out) *out = o;
+  }
+  cudaFree(dd);
+  cudaFree(dp);
+  cudaFree(ds);
+  cudaFree(de);
+  cudaFree(dout);
+  return ok ? o.status : HESP_E_CUDA;
+}
+
+int hesp_generate_host(const hesp_engine* e, uint64_t first_index, uint64_t count, hesp_cand_desc* descs) {
+  if (!e || !descs) return HESP_E_INVALID;
+  const Problem& p = e->hp.p;
+  for (uint64_t i = 0; i < count; ++i)
+    hesp_generate(&p.gen, (int)(p.n / p.base_b), p.n_base_leaves, p.base_b, first_index + i, &descs[i]);
+  return HESP_OK;
+}
+
+}  // extern "C"

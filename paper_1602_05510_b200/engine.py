@@ -1,0 +1,339 @@
+"""ctypes binding of the C ABI in include/hesp_engine.h.
+
+Python-side plumbing for tests and bench.py: loads the in-tree sm_100a
+library (there is no CPU fallback — a missing library or device raises),
+builds the reference-shaped inputs from the same JSON/CSV fixtures the
+reference parses (Platform::from_json, PerfModel::from_analytic_json /
+from_table_csv: platform.cpp:157-338) and exposes batch evaluation.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .build import LIB
+
+KINDS = {"CHOL": 0, "TRSM": 1, "SYRK": 2, "GEMM": 3}
+ORDERING = {"FCFS": 0, "PL": 1}
+SELECTION = {"R-P": 0, "F-P": 1, "EIT-P": 2, "EFT-P": 3}
+CACHING = {"WT": 0, "WB": 1, "WA": 2}
+
+MAX_OPS = 16
+
+
+class Space(C.Structure):
+    _fields_ = [("id", C.c_int32), ("capacity_bytes", C.c_int64), ("is_main", C.c_int32)]
+
+
+class Processor(C.Structure):
+    _fields_ = [("id", C.c_int32), ("type", C.c_int32), ("space", C.c_int32)]
+
+
+class Link(C.Structure):
+    _fields_ = [("src", C.c_int32), ("dst", C.c_int32), ("latency_s", C.c_double),
+                ("bandwidth_bps", C.c_double)]
+
+
+class PlatformC(C.Structure):
+    _fields_ = [("n_spaces", C.c_int32), ("spaces", C.POINTER(Space)),
+                ("n_types", C.c_int32), ("type_names", C.POINTER(C.c_char_p)),
+                ("n_procs", C.c_int32), ("procs", C.POINTER(Processor)),
+                ("n_links", C.c_int32), ("links", C.POINTER(Link))]
+
+
+class AnalyticEntry(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("type", C.c_int32), ("peak_flops", C.c_double),
+                ("b_half", C.c_double)]
+
+
+class TableRow(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("type", C.c_int32), ("b", C.c_int64), ("seconds", C.c_double)]
+
+
+class PerfModelC(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("n_entries", C.c_int32),
+                ("entries", C.POINTER(AnalyticEntry)), ("n_rows", C.c_int32),
+                ("rows", C.POINTER(TableRow))]
+
+
+class SchedConfigC(C.Structure):
+    _fields_ = [("ordering", C.c_int32), ("selection", C.c_int32), ("caching", C.c_int32),
+                ("reserved", C.c_int32), ("seed", C.c_uint64), ("min_block", C.c_int64)]
+
+
+class GenConfig(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("k_max", C.c_int32), ("max_depth", C.c_int32),
+                ("min_block", C.c_int64), ("n_s_choices", C.c_int32), ("s_choices", C.c_int32 * 4)]
+
+
+class WorkloadC(C.Structure):
+    _fields_ = [("n", C.c_int64), ("elem_size", C.c_int32), ("s_base", C.c_int32), ("gen", GenConfig)]
+
+
+class Op(C.Structure):
+    _fields_ = [("task", C.c_int32), ("s", C.c_int32)]
+
+
+class CandDesc(C.Structure):
+    _fields_ = [("n_ops", C.c_int32), ("reserved", C.c_int32), ("ops", Op * MAX_OPS)]
+
+
+class Outcome(C.Structure):
+    _fields_ = [("status", C.c_int32), ("n_leaves", C.c_int32), ("makespan", C.c_double),
+                ("assign_hash", C.c_uint64), ("xfer_hash", C.c_uint64)]
+
+
+class Best(C.Structure):
+    _fields_ = [("makespan", C.c_double), ("index", C.c_int64), ("n_ok", C.c_int64),
+                ("n_evaluated", C.c_int64)]
+
+
+class EngineInfo(C.Structure):
+    _fields_ = [("kernel_launches", C.c_int64), ("n_base_tasks", C.c_int32),
+                ("n_base_blocks", C.c_int32), ("n_slots", C.c_int32), ("sm_count", C.c_int32),
+                ("slot_bytes", C.c_int64), ("warps_per_block", C.c_int32),
+                ("blocks_per_sm", C.c_int32)]
+
+
+OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
+                          ("assign_hash", "<u8"), ("xfer_hash", "<u8")])
+assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 32
+DESC_DTYPE = np.dtype([("n_ops", "<i4"), ("reserved", "<i4"), ("ops", "<i4", (MAX_OPS, 2))])
+assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 136
+
+EXPORTS = [
+    "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
+    "hesp_generate_device", "hesp_generate_host", "hesp_eval_detail", "hesp_engine_get_info",
+    "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
+]
+
+_lib = None
+
+
+def load_library(path: str = LIB) -> C.CDLL:
+    """Load the in-tree engine library; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"engine library {path} is missing: run __graft_entry__.build()")
+    lib = C.CDLL(path)
+    lib.hesp_engine_create.restype = C.c_void_p
+    lib.hesp_engine_create.argtypes = [C.c_int, C.POINTER(PlatformC), C.POINTER(PerfModelC),
+                                       C.POINTER(SchedConfigC), C.POINTER(WorkloadC)]
+    lib.hesp_eval_generated.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.POINTER(Best)]
+    lib.hesp_eval_descs.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                    C.POINTER(Best)]
+    lib.hesp_eval_descs_device.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                           C.POINTER(Best), C.c_void_p]
+    lib.hesp_generate_device.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]
+    lib.hesp_generate_host.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+    lib.hesp_eval_detail.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.POINTER(Outcome)]
+    lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
+    lib.hesp_engine_destroy.argtypes = [C.c_void_p]
+    lib.hesp_last_error.restype = C.c_char_p
+    lib.hesp_status_name.restype = C.c_char_p
+    lib.hesp_status_name.argtypes = [C.c_int32]
+    _lib = lib
+    return lib
+
+
+def status_name(code: int) -> str:
+    return load_library().hesp_status_name(int(code)).decode()
+
+
+# ---------------------------------------------------------------------------
+# Reference-shaped inputs
+
+
+@dataclass
+class Platform:
+    """hesp::Platform (platform.hpp:50-86): spaces, types, processors, links."""
+    spaces: list[tuple[int, int, bool]]
+    types: list[str]
+    processors: list[tuple[int, str, int]]
+    links: list[tuple[int, int, float, float]] = field(default_factory=list)
+
+    @staticmethod
+    def from_json(text: str) -> "Platform":  # Platform::from_json, platform.cpp:157-196
+        d = json.loads(text)
+        return Platform(
+            spaces=[(s["id"], int(s["capacity_bytes"]), bool(s.get("is_main", False))) for s in d["spaces"]],
+            types=[t["name"] for t in d["types"]],
+            processors=[(p["id"], p["type"], p["space"]) for p in d["processors"]],
+            links=[(l["src"], l["dst"], float(l["latency_s"]), float(l["bandwidth_Bps"]))
+                   for l in d.get("links", [])],
+        )
+
+    def _c(self, keep: list):
+        sp = (Space * len(self.spaces))(*[Space(i, c, int(m)) for i, c, m in self.spaces])
+        names = (C.c_char_p * len(self.types))(*[t.encode() for t in self.types])
+        tix = {t: i for i, t in enumerate(self.types)}
+        pr = (Processor * len(self.processors))(*[Processor(i, tix[t], s) for i, t, s in self.processors])
+        nl = max(1, len(self.links))
+        lk = (Link * nl)(*[Link(a, b, la, bw) for a, b, la, bw in self.links])
+        keep += [sp, names, pr, lk]
+        return PlatformC(len(self.spaces), sp, len(self.types), names, len(self.processors), pr,
+                         len(self.links), lk)
+
+
+@dataclass
+class PerfModel:
+    """hesp::PerfModel (platform.hpp:104-140), analytic or tabulated."""
+    analytic: list[tuple[str, str, float, float]] | None = None  # (kind, type, peak, b_half)
+    table: list[tuple[str, str, int, float]] | None = None       # (kind, type, b, seconds)
+
+    @staticmethod
+    def from_analytic_json(text: str) -> "PerfModel":
+        return PerfModel(analytic=[(e["kind"], e["proc_type"], float(e["peak_flops"]), float(e["b_half"]))
+                                   for e in json.loads(text)])
+
+    @staticmethod
+    def from_table_csv(text: str) -> "PerfModel":
+        rows = []
+        lines = [l for l in text.splitlines() if l.strip()]
+        hdr = [f.strip() for f in lines[0].split(",")]
+        if hdr != ["kind", "proc_type", "b", "seconds"]:
+            raise ValueError("perf table: expected header kind,proc_type,b,seconds")
+        for l in lines[1:]:
+            k, t, b, s = [f.strip() for f in l.split(",")]
+            rows.append((k, t, int(b), float(s)))
+        return PerfModel(table=rows)
+
+    def _c(self, platform: Platform, keep: list):
+        tix = {t: i for i, t in enumerate(platform.types)}
+        if self.analytic is not None:
+            ents = [AnalyticEntry(KINDS[k], tix[t], p, bh) for k, t, p, bh in self.analytic if t in tix]
+            arr = (AnalyticEntry * max(1, len(ents)))(*ents)
+            keep.append(arr)
+            return PerfModelC(1, len(ents), arr, 0, None)
+        rows = [TableRow(KINDS[k], tix[t], b, s) for k, t, b, s in self.table if t in tix]
+        arr = (TableRow * max(1, len(rows)))(*rows)
+        keep.append(arr)
+        return PerfModelC(0, 0, None, len(rows), arr)
+
+
+@dataclass
+class SchedConfig:
+    """hesp::SchedConfig (sim.hpp:26-32)."""
+    ordering: str = "PL"
+    selection: str = "EFT-P"
+    caching: str = "WB"
+    seed: int = 0
+    min_block: int = 64
+
+
+@dataclass
+class Workload:
+    """root_cholesky(n, elem) + partition_task(0, 1/s_base) + generated candidates."""
+    n: int = 16384
+    elem_size: int = 4
+    s_base: int = 16
+    seed: int = 1
+    k_max: int = 8
+    max_depth: int = 3
+    min_block: int = 64
+    s_choices: tuple = (2, 4)
+
+
+class BatchEngine:
+    """One engine handle on one GPU (hesp_engine_create)."""
+
+    def __init__(self, platform: Platform, model: PerfModel, sched: SchedConfig, workload: Workload,
+                 device: int = 0):
+        self.lib = load_library()
+        keep: list = []
+        self._pc = platform._c(keep)
+        self._mc = model._c(platform, keep)
+        self._sc = SchedConfigC(ORDERING[sched.ordering], SELECTION[sched.selection], CACHING[sched.caching],
+                                0, sched.seed, sched.min_block)
+        sc = (C.c_int32 * 4)(*(list(workload.s_choices) + [0] * (4 - len(workload.s_choices))))
+        g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block,
+                      len(workload.s_choices), sc)
+        self._wc = WorkloadC(workload.n, workload.elem_size, workload.s_base, g)
+        self._keep = keep
+        h = self.lib.hesp_engine_create(device, C.byref(self._pc), C.byref(self._mc), C.byref(self._sc),
+                                        C.byref(self._wc))
+        if not h:
+            raise RuntimeError("hesp_engine_create: " + self.lib.hesp_last_error().decode())
+        self.h = C.c_void_p(h)
+        self.workload, self.sched = workload, sched
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.hesp_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc: int, what: str):
+        if rc != 0:
+            raise RuntimeError(f"{what} failed ({rc}): {self.lib.hesp_last_error().decode()}")
+
+    def info(self) -> EngineInfo:
+        i = EngineInfo()
+        self._check(self.lib.hesp_engine_get_info(self.h, C.byref(i)), "get_info")
+        return i
+
+    def eval_generated(self, first: int, count: int, outcomes: bool = True):
+        out = np.zeros(count, OUTCOME_DTYPE) if outcomes else None
+        best = Best()
+        self._check(self.lib.hesp_eval_generated(self.h, first, count,
+                                                 out.ctypes.data if out is not None else None,
+                                                 C.byref(best)), "eval_generated")
+        return out, best
+
+    def eval_descs(self, descs: np.ndarray, first: int = 0):
+        descs = np.ascontiguousarray(descs, DESC_DTYPE)
+        out = np.zeros(len(descs), OUTCOME_DTYPE)
+        best = Best()
+        self._check(self.lib.hesp_eval_descs(self.h, descs.ctypes.data, len(descs), first, out.ctypes.data,
+                                             C.byref(best)), "eval_descs")
+        return out, best
+
+    def eval_descs_device(self, descs_ptr: int, count: int, first: int, out_ptr: int | None, stream: int = 0):
+        best = Best()
+        self._check(self.lib.hesp_eval_descs_device(self.h, C.c_void_p(descs_ptr), count, first,
+                                                    C.c_void_p(out_ptr) if out_ptr else None, C.byref(best),
+                                                    C.c_void_p(stream) if stream else None),
+                    "eval_descs_device")
+        return best
+
+    def generate_device(self, first: int, count: int, descs_ptr: int, stream: int = 0):
+        self._check(self.lib.hesp_generate_device(self.h, first, count, C.c_void_p(descs_ptr),
+                                                  C.c_void_p(stream) if stream else None), "generate_device")
+
+    def generate_host(self, first: int, count: int) -> np.ndarray:
+        d = np.zeros(count, DESC_DTYPE)
+        self._check(self.lib.hesp_generate_host(self.h, first, count, d.ctypes.data), "generate_host")
+        return d
+
+
+# ---------------------------------------------------------------------------
+# Fixtures
+
+FIXTURES = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fixtures")
+
+
+def fixture_path(name: str) -> str:
+    return os.path.join(FIXTURES, name)
+
+
+def load_platform(name: str) -> Platform:
+    with open(fixture_path(name)) as f:
+        return Platform.from_json(f.read())
+
+
+def load_model(name: str) -> PerfModel:
+    with open(fixture_path(name)) as f:
+        text = f.read()
+    return PerfModel.from_table_csv(text) if name.endswith(".csv") else PerfModel.from_analytic_json(text)
