@@ -1039,9 +1039,12 @@ struct Engine {
     wp.sync();
   }
 
-  // ensure_capacity (sim.cpp:374-439).  `depth` guards the single legal
-  // recursion: a dirty flush from an accelerator into main.
-  HX void ensure_capacity(int s, long long bytes, double at, int depth) {
+  // ensure_capacity (sim.cpp:374-439).  The only recursion in the reference
+  // is a dirty flush from an accelerator into main (materialize in main),
+  // and main never holds dirty blocks, so FLUSH=false is the flush's own
+  // instance: no device recursion, no call stack.
+  template <bool FLUSH>
+  HX void ensure_capacity(int s, long long bytes, double at) {
     const long long cap = pb.cap[s];
     if (bytes > cap) return fail(ST_CAPACITY);
     while (sm->used[s] + bytes > cap) {
@@ -1076,13 +1079,14 @@ struct Engine {
       const int victim = bid;
       const long long vbytes = bbytes(victim);
       if (is_dirty(victim, s)) {
-        if (depth > 0) return fail(ST_ENGINE_INVARIANT);
+        if (!FLUSH) return fail(ST_ENGINE_INVARIANT);
         const double rdy = V(victim, s);
         const double arr = plan_transfer(victim, nullptr, vbytes, s, mainsp, rdy, at);  // sim.cpp:408-409 passes `at`
         if (status) return;
         set_flag(victim, 1u << (8 + s), false);
-        materialize(victim, mainsp, arr, depth + 1);
+        reserve_bytes<false>(victim, mainsp, arr);
         if (status) return;
+        validate_from(victim, mainsp, arr);
       }
       set_flag(victim, 1u << s, false);
       setV(victim, s, ABSENT);
@@ -1111,18 +1115,20 @@ struct Engine {
     }
   }
 
-  HX void reserve_bytes(int b, int s, double at, int depth) {  // sim.cpp:441-450
+  template <bool FLUSH = true>
+  HX void reserve_bytes(int b, int s, double at) {  // sim.cpp:441-450
     if (is_mat(b, s)) return;
     const long long bytes = bbytes(b);
-    ensure_capacity(s, bytes, at, depth);
+    ensure_capacity<FLUSH>(s, bytes, at);
     if (status) return;
     set_flag(b, 1u << s, true);
     add_used(s, bytes);
     setLU(b, s, at);
   }
 
-  HX void materialize(int b, int s, double at, int depth) {  // sim.cpp:463-466
-    reserve_bytes(b, s, at, depth);
+  template <bool FLUSH = true>
+  HX void materialize(int b, int s, double at) {  // sim.cpp:463-466
+    reserve_bytes<FLUSH>(b, s, at);
     if (status) return;
     validate_from(b, s, at);
   }
@@ -1147,7 +1153,7 @@ struct Engine {
       const double arr = plan_transfer(b, nullptr, bbytes(b), src, s, rdy, now);
       if (status) return 0.0;
       pin(src, b, arr);
-      materialize(b, s, arr, 0);
+      materialize(b, s, arr);
       return arr;
     }
     need_gather = true;
@@ -1432,7 +1438,7 @@ struct Engine {
       setPIN(w[k], s, HOLD);
     }
     const int out = t.blk[t.nrd];
-    reserve_bytes(out, s, now, 0);
+    reserve_bytes(out, s, now);
     if (status) return;
     const double start = dmax(dmax(sm->proc_free[p], t_rel[j]), inputs);
     const double end = start + pb.ttime[t.kind][t.bidx][type];
@@ -1458,7 +1464,7 @@ struct Engine {
         const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
         if (status) return;
         pin(s, out, arr);
-        materialize(out, mainsp, arr, 1);
+        materialize<false>(out, mainsp, arr);
         if (status) return;
         if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
           set_flag(out, 1u << s, false);
