@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""bench.py — simulated Cholesky candidate schedules per second on B200.
+
+Contract (see task brief): `python bench.py --gpus N --steps K --warmup W`
+(torchrun for N>1, one rank per GPU) prints ONE JSON line on rank 0.
+
+A step = one pass of the hot path over one batch of synthetic candidates:
+BASELINE.json configs[1] (C2): random recursive partitionings of the 16x16
+tiled Cholesky on the CPU-GPU platform model, PL/EFT-P/WB, 1e5 candidates
+per GPU per step (weak scaling), each expanded, simulated and reduced to the
+best makespan; for N>1 the per-GPU winners meet in one NCCL min-reduce.
+
+  value  : device-resident descriptors (generated into HBM before timing),
+           CUDA events on the launching stream, L2 flushed between steps.
+  e2e    : the same batch through the C ABI with HOST buffers
+           (hesp_eval_descs: H2D descriptors, kernels, D2H outcomes + best).
+  --impl reference : the unmodified reference (oracle/_ref) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "simulated schedules/sec (Cholesky DAG) at 1/2/4/8 B200 vs host-CPU ref"
+UNIT = "schedules/s"
+HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+WORKLOAD_DESC = ("C2: random recursive partitionings (K~U[0,8] partition ops, s in {2,4}, depth<=3) "
+                 "of the 16x16-tile Cholesky (n=16384, SP) on the CPU-GPU platform model "
+                 "(25 cpu + 3 gpu, 4 spaces), PL/EFT-P/WB")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=100_000, help="candidates per GPU per step")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample bound")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), "measured", d
+    return 6650.0, "fallback", {}
+
+
+def config_block(name, p, n_gpus, batch):
+    return {"workload": WORKLOAD_DESC if name == "C2" else name, "preset": name, "n": p["n"],
+            "elem_size": p["elem"], "s_base": p["s_base"], "k_max": p["k_max"], "max_depth": p["max_depth"],
+            "s_choices": list(p["s_choices"]),
+            "policy": f"{p['ordering']}/{p['selection']}/{p['caching']}",
+            "platform": p["platform"], "model": p["model"], "batch_per_gpu": batch,
+            "global_batch": batch * n_gpus, "parallelism": f"dp{n_gpus} (candidate shards, NCCL min-reduce)",
+            "l2": "flushed between steps (256 MiB write), flush outside the timed events"}
+
+
+def cpu_baseline(p, seconds, first=0):
+    """The unmodified reference on this host's cores (oracle/_ref/ref_harness)."""
+    from paper_1602_05510_b200.configs import harness_args
+    from paper_1602_05510_b200.engine import FIXTURES
+    if not os.path.exists(HARNESS):
+        return None, "oracle/_ref/ref_harness not built"
+    threads = os.cpu_count() or 1
+    cmd = [HARNESS, *harness_args(p, FIXTURES), "--first", str(first), "--count", "10000000",
+           "--threads", str(threads), "--time-limit", str(seconds)]
+    r = subprocess.run(cmd, capture_output=True, text=True, check=True)
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    return d, None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.path = device, None, f"/tmp/hesp_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9 and parts[1].replace(".", "").isdigit():
+                    rows.append(parts)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
+
+
+def roofline(best_steps, kernel_ms, P, S, n_types, peak_gbs, peak_kind, traffic):
+    # Algorithmic scheduler-state bytes per batch:
+    #   B = 8 * sum_t (P + S*k_t + n_types + 4) + 12 * E
+    leaves = sum(b.sum_leaves for b in best_steps)
+    ksum = sum(b.sum_k for b in best_steps)
+    edges = sum(b.sum_edges for b in best_steps)
+    B = 8 * (leaves * (P + n_types + 4) + S * ksum) + 12 * edges
+    per_launch = B / len(best_steps)
+    ms = statistics.mean(kernel_ms)
+    achieved = per_launch / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
+            "frac": round(achieved / peak_gbs, 6), "traffic": traffic, "peak_source": peak_kind,
+            "algorithmic_bytes_per_launch": int(per_launch), "kernel": "eval_kernel",
+            "kernel_ms_per_launch": round(ms, 4),
+            "note": ("latency-bound serial event loop (one warp per candidate); neither HBM nor tensor "
+                     "bound — issue-slot and memory-latency evidence in profiles/")}
+
+
+def ncu_traffic(config, batch):
+    path = os.path.join(ROOT, "profiles", "ncu_eval_kernel.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    if d.get("config") == config and d.get("batch") == batch:
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+def run_reference(args, p):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    total, wall = 0, 0.0
+    per_step = []
+    for step in range(args.warmup + args.steps):
+        budget = 2.0 if step < args.warmup else args.cpu_seconds
+        d, err = cpu_baseline(p, budget, first=step * 1_000_000)
+        if err:
+            print(json.dumps({"impl": "reference", "unavailable": err}))
+            return 0
+        if step >= args.warmup:
+            total += d["candidates"]
+            wall += d["wall_s"]
+            per_step.append(d)
+    value = total / wall
+    threads = per_step[0]["threads"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(args.config, p, 1, int(total / args.steps)),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"{total} candidates of {args.config} over {args.steps} steps of "
+                                       f"~{args.cpu_seconds:.0f} s each (time-bounded), {cpu_model()}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    args = parse()
+    from paper_1602_05510_b200.configs import CONFIGS
+    p = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, p)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1602_05510_b200.build import build
+    from paper_1602_05510_b200.configs import make_engine
+    from paper_1602_05510_b200.engine import DESC_DTYPE, OUTCOME_DTYPE
+    if rank == 0:
+        build()
+    if world > 1:
+        dist.barrier()
+    eng = make_engine(p, device=local)
+    info = eng.info()
+    B = args.batch
+    nsteps = args.warmup + args.steps
+    stream = torch.cuda.Stream()
+    # candidate indices: disjoint per (step, rank)
+    firsts = [(s * world + rank) * B for s in range(nsteps)]
+    descs = torch.empty((nsteps, B * DESC_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    outs = torch.empty((B * OUTCOME_DTYPE.itemsize,), dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(stream):
+        for s in range(nsteps):
+            eng.generate_device(firsts[s], B, descs[s].data_ptr(), stream.cuda_stream)
+    stream.synchronize()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def global_best(b):
+        if world == 1:
+            return b.makespan, b.index
+        bits = np.float64(b.makespan).view(np.int64) if b.index >= 0 else np.iinfo(np.int64).max
+        t = torch.tensor([int(bits)], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        idx = b.index if (b.index >= 0 and int(bits) == int(t.item())) else np.iinfo(np.int64).max
+        u = torch.tensor([int(idx)], dtype=torch.int64, device="cuda")
+        dist.all_reduce(u, op=dist.ReduceOp.MIN)
+        return float(np.int64(t.item()).view(np.float64)), int(u.item())
+
+    for s in range(args.warmup):
+        b = eng.eval_descs_device(descs[s].data_ptr(), B, firsts[s], outs.data_ptr(), stream.cuda_stream)
+        global_best(b)
+    launches0 = eng.info().kernel_launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, kernel_ms, bests, winners = [], [], [], []
+    for s in range(args.warmup, nsteps):
+        with torch.cuda.stream(stream):
+            flush.fill_(s & 0xff)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        b = eng.eval_descs_device(descs[s].data_ptr(), B, firsts[s], outs.data_ptr(), stream.cuda_stream)
+        winners.append(global_best(b))
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        kernel_ms.append(b.kernel_ms)
+        bests.append(b)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    launches = eng.info().kernel_launches - launches0
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = world * B * args.steps / (max_ms * 1e-3)
+
+    # ---- e2e through the C ABI with host buffers (H2D descs, D2H outcomes) ----
+    host_descs = [eng.generate_host(firsts[s], B) for s in range(args.warmup, nsteps)]
+    eng.eval_descs(host_descs[0], first=firsts[args.warmup])  # warm the pinned staging
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i, s in enumerate(range(args.warmup, nsteps)):
+        out, b = eng.eval_descs(host_descs[i], first=firsts[s])
+        global_best(b)
+    e2e_s = time.perf_counter() - t0
+    te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = world * B * args.steps / float(te.item())
+
+    if rank == 0:
+        peak, peak_kind, _ = measured_peaks()
+        P = eng._pc.n_procs
+        rf = roofline(bests, kernel_ms, P, eng._pc.n_spaces, eng._pc.n_types, peak, peak_kind,
+                      ncu_traffic(args.config, B))
+        cpu = None
+        if not args.no_cpu_baseline:
+            d, err = cpu_baseline(p, args.cpu_seconds)
+            if d:
+                cpu = {"value": d["cand_per_s"], "unit": UNIT, "cores": d["threads"], "kind": "reference",
+                       "sample": f"{d['candidates']} candidates of {args.config} (indices 0..), "
+                                 f"time-bounded {args.cpu_seconds:.0f} s, {d['threads']} threads, {cpu_model()}"}
+            else:
+                cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": err}
+        n_ok = sum(b.n_ok for b in bests)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(args.config, p, world, B),
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": B * DESC_DTYPE.itemsize,
+                    "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64},
+            "gpu_launches": int(launches),
+            "roofline": rf,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "valid_fraction": n_ok / (B * args.steps),
+            "best": {"makespan": winners[-1][0], "index": winners[-1][1]},
+            "engine": {"slots": info.n_slots, "sm_count": info.sm_count, "blocks_per_sm": info.blocks_per_sm,
+                       "warps_per_block": info.warps_per_block, "slot_bytes": info.slot_bytes},
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

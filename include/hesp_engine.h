@@ -114,6 +114,11 @@ typedef struct {
   int64_t index;      /* lowest global candidate index achieving it (-1 if none) */
   int64_t n_ok;       /* candidates with status == 0 */
   int64_t n_evaluated;
+  /* work actually done by the batch (roofline accounting) */
+  int64_t sum_leaves; /* leaf tasks of all expanded DAGs */
+  int64_t sum_k;      /* sum over leaves of distinct blocks accessed */
+  int64_t sum_edges;  /* dependence edges generated */
+  double kernel_ms;   /* CUDA-event duration of the evaluation kernel (same stream) */
 } hesp_best;
 
 enum {

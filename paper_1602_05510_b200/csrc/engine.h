@@ -192,6 +192,7 @@ struct Engine {
   int32_t nleaves = 0;
   int32_t n_tl_ids = 0;
   int32_t nedges = 0;
+  int32_t sum_k = 0;  // sum over leaves of distinct blocks accessed (k_t)
   int32_t pool_n = 0;
   double now = 0.0;
   double makespan = 0.0;
@@ -789,6 +790,16 @@ struct Engine {
       const TaskMeta t = task(j);
       const int wb = t.blk[t.nrd];
       int npb = 0;
+      {
+        int kt = 0;
+        for (int k = 0; k <= t.nrd; ++k) {
+          bool dup = false;
+          for (int q = 0; q < k; ++q)
+            if (t.blk[q] == t.blk[k]) dup = true;
+          kt += !dup;
+        }
+        sum_k += kt;
+      }
       // distinct blocks, read-only ones first in read order, then the write
       for (int k = 0; k <= t.nrd; ++k) {
         const int b = t.blk[k];
@@ -1798,6 +1809,7 @@ struct Engine {
     for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
     Outcome o;
     o.n_leaves = 0;
+    sum_k = 0;
     if (!status) build_tiles();
     if (!status) build_order();
     o.n_leaves = status ? 0 : nleaves;
@@ -1808,6 +1820,8 @@ struct Engine {
     o.makespan = status ? 0.0 : makespan;
     o.assign_hash = status ? 0 : ahash;
     o.xfer_hash = status ? 0 : xhash;
+    o.sum_k = sum_k;
+    o.n_edges = nedges;
     return o;
   }
 };

@@ -31,6 +31,7 @@ struct WarpBest {
   long long index;
   long long n_ok;
   long long n_eval;
+  long long leaves, k, edges;
 };
 
 constexpr int WARPS_PER_BLOCK = 4;
@@ -47,7 +48,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
   uint8_t* slot = scratch + (size_t)gw * L.total;
   const Problem& pb = *pbp;
   double best_mk = 0.0;
-  long long best_idx = -1, n_ok = 0, n_eval = 0;
+  long long best_idx = -1, n_ok = 0, n_eval = 0, s_leaves = 0, s_k = 0, s_edges = 0;
   for (;;) {
     unsigned long long k = 0;
     if (lane == 0) k = atomicAdd(counter, 1ULL);
@@ -72,6 +73,9 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
       out[k] = r;
     }
     ++n_eval;
+    s_leaves += o.n_leaves;
+    s_k += o.sum_k;
+    s_edges += o.n_edges;
     if (o.status == 0) {
       ++n_ok;
       const long long gi = (long long)(first_index + k);
@@ -87,19 +91,25 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
     b.index = best_idx;
     b.n_ok = n_ok;
     b.n_eval = n_eval;
+    b.leaves = s_leaves;
+    b.k = s_k;
+    b.edges = s_edges;
     wbest[gw] = b;
   }
 }
 
 __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* __restrict__ best) {
   __shared__ double smk[32];
-  __shared__ long long sidx[32], sok[32], sev[32];
+  __shared__ long long sidx[32], sok[32], sev[32], sl[32], sk[32], se[32];
   double mk = 0.0;
-  long long idx = -1, ok = 0, ev = 0;
+  long long idx = -1, ok = 0, ev = 0, lv = 0, kk = 0, ed = 0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const WarpBest b = wb[i];
     ok += b.n_ok;
     ev += b.n_eval;
+    lv += b.leaves;
+    kk += b.k;
+    ed += b.edges;
     if (b.index >= 0 && (idx < 0 || b.makespan < mk || (b.makespan == mk && b.index < idx))) {
       mk = b.makespan;
       idx = b.index;
@@ -110,6 +120,9 @@ __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* _
     const long long i2 = __shfl_xor_sync(0xffffffffu, idx, o);
     ok += __shfl_xor_sync(0xffffffffu, ok, o);
     ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    lv += __shfl_xor_sync(0xffffffffu, lv, o);
+    kk += __shfl_xor_sync(0xffffffffu, kk, o);
+    ed += __shfl_xor_sync(0xffffffffu, ed, o);
     if (i2 >= 0 && (idx < 0 || m2 < mk || (m2 == mk && i2 < idx))) {
       mk = m2;
       idx = i2;
@@ -121,14 +134,20 @@ __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* _
     sidx[w] = idx;
     sok[w] = ok;
     sev[w] = ev;
+    sl[w] = lv;
+    sk[w] = kk;
+    se[w] = ed;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     const int nw = (blockDim.x + 31) >> 5;
-    hesp_best r{0.0, -1, 0, 0};
+    hesp_best r{0.0, -1, 0, 0, 0, 0, 0, 0.0};
     for (int i = 0; i < nw; ++i) {
       r.n_ok += sok[i];
       r.n_evaluated += sev[i];
+      r.sum_leaves += sl[i];
+      r.sum_k += sk[i];
+      r.sum_edges += se[i];
       if (sidx[i] >= 0 && (r.index < 0 || smk[i] < r.makespan ||
                            (smk[i] == r.makespan && sidx[i] < r.index))) {
         r.makespan = smk[i];
@@ -192,6 +211,7 @@ struct hesp_engine {
   size_t h_cap = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
 namespace {
@@ -227,8 +247,10 @@ int launch_eval(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, u
                 hesp_outcome* d_out, cudaStream_t st) {
   if (!ck(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned long long), st), "memset counter"))
     return HESP_E_CUDA;
+  cudaEventRecord(e->ev0, st);
   eval_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(e->d_problem, d_descs, first, count, d_out,
                                                             e->d_wbest, e->d_scratch, e->L, e->d_counter);
+  cudaEventRecord(e->ev1, st);
   reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
   e->launches += 2;
   if (!ck(cudaGetLastError(), "eval launch")) return HESP_E_CUDA;
@@ -241,6 +263,9 @@ int finish_best(hesp_engine* e, hesp_best* best, cudaStream_t st) {
     return HESP_E_CUDA;
   if (!ck(cudaStreamSynchronize(st), "sync")) return HESP_E_CUDA;
   *best = *e->h_best;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e->ev0, e->ev1);
+  best->kernel_ms = ms;
   return HESP_OK;
 }
 
@@ -341,6 +366,8 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_counter, sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMallocHost(&e->h_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc host");
+  if ((c = cudaEventCreate(&e->ev0)) != cudaSuccess) return fail(c, "event");
+  if ((c = cudaEventCreate(&e->ev1)) != cudaSuccess) return fail(c, "event");
   e->hp.p = p;
   return e;
 }
@@ -359,6 +386,8 @@ void hesp_engine_destroy(hesp_engine* e) {
   if (e->h_best) cudaFreeHost(e->h_best);
   if (e->h_descs) cudaFreeHost(e->h_descs);
   if (e->h_out) cudaFreeHost(e->h_out);
+  if (e->ev0) cudaEventDestroy(e->ev0);
+  if (e->ev1) cudaEventDestroy(e->ev1);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }

@@ -102,6 +102,8 @@ struct Outcome {
   double makespan;
   uint64_t assign_hash;
   uint64_t xfer_hash;
+  int32_t sum_k;    // work counters for the roofline accounting (not part of parity)
+  int32_t n_edges;
 };
 
 // Byte layout of one per-warp slot (all arrays in global memory).

@@ -89,7 +89,8 @@ class Outcome(C.Structure):
 
 class Best(C.Structure):
     _fields_ = [("makespan", C.c_double), ("index", C.c_int64), ("n_ok", C.c_int64),
-                ("n_evaluated", C.c_int64)]
+                ("n_evaluated", C.c_int64), ("sum_leaves", C.c_int64), ("sum_k", C.c_int64),
+                ("sum_edges", C.c_int64), ("kernel_ms", C.c_double)]
 
 
 class EngineInfo(C.Structure):
