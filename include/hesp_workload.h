@@ -26,9 +26,11 @@
 #include <stdint.h>
 
 #if defined(__CUDACC__)
-#define HESP_HD __host__ __device__ __forceinline__
+#define HESP_HD __host__ __device__ inline
+#define HESP_NOUNROLL _Pragma("unroll 1")
 #else
 #define HESP_HD static inline
+#define HESP_NOUNROLL
 #endif
 
 #ifdef __cplusplus
@@ -86,7 +88,7 @@ HESP_HD int64_t hesp_snap_tiles(int64_t d, int32_t s_req, int64_t min_block) {
   const int64_t s0 = r > 2 ? r : 2;
   const int64_t mb = min_block > 1 ? min_block : 1;
   const int64_t s_hi = d / mb;
-  for (int64_t delta = 0; delta <= s0 + s_hi; ++delta) {
+  HESP_NOUNROLL for (int64_t delta = 0; delta <= s0 + s_hi; ++delta) {
     int64_t c = s0 - delta;
     if (c >= 2 && c <= s_hi && d % c == 0) return c;
     c = s0 + delta;
@@ -109,12 +111,12 @@ HESP_HD int32_t hesp_member_count(int32_t kind, int32_t s) {
  * graph.cpp:313-389 (CHOL k-loop; TRSM j,i,k; SYRK i,j<=i,k; GEMM i,j,k). */
 HESP_HD int32_t hesp_member_kind(int32_t kind, int32_t s, int32_t m) {
   if (kind == HESP_CHOL) {
-    for (int32_t k = 0; k < s; ++k) {
+    HESP_NOUNROLL for (int32_t k = 0; k < s; ++k) {
       const int32_t t = s - k - 1; /* trailing tiles below the diagonal */
       if (m == 0) return HESP_CHOL;
       if (m <= t) return HESP_TRSM;
       m -= 1 + t;
-      for (int32_t i = k + 1; i < s; ++i) {
+      HESP_NOUNROLL for (int32_t i = k + 1; i < s; ++i) {
         const int32_t g = i - k - 1; /* GEMMs before this row's SYRK */
         if (m < g) return HESP_GEMM;
         if (m == g) return HESP_SYRK;
@@ -124,7 +126,7 @@ HESP_HD int32_t hesp_member_kind(int32_t kind, int32_t s, int32_t m) {
     return -1;
   }
   if (kind == HESP_TRSM) {
-    for (int32_t j = 0; j < s; ++j) {
+    HESP_NOUNROLL for (int32_t j = 0; j < s; ++j) {
       const int32_t blk = s * (j + 1);
       if (m < blk) return (m % (j + 1)) < j ? HESP_GEMM : HESP_TRSM;
       m -= blk;
@@ -132,8 +134,8 @@ HESP_HD int32_t hesp_member_kind(int32_t kind, int32_t s, int32_t m) {
     return -1;
   }
   if (kind == HESP_SYRK) {
-    for (int32_t i = 0; i < s; ++i)
-      for (int32_t j = 0; j <= i; ++j) {
+    HESP_NOUNROLL for (int32_t i = 0; i < s; ++i)
+      HESP_NOUNROLL for (int32_t j = 0; j <= i; ++j) {
         if (m < s) return i == j ? HESP_SYRK : HESP_GEMM;
         m -= s;
       }
@@ -163,27 +165,27 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
   rg[0].pkind = HESP_CHOL;
   rg[0].s = s_base;
   int32_t next_id = 1 + n_base;
-  for (int32_t op = 0; op < K; ++op) {
+  HESP_NOUNROLL for (int32_t op = 0; op < K; ++op) {
     uint64_t total = 0;
-    for (int32_t r = 0; r < nr; ++r) {
+    HESP_NOUNROLL for (int32_t r = 0; r < nr; ++r) {
       if (!(rg[r].b / 2 >= cfg->min_block && rg[r].depth < cfg->max_depth)) continue;
       int32_t live = rg[r].count;
-      for (int32_t q = 0; q < nrem; ++q)
+      HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
         if (removed[q] >= rg[r].first && removed[q] < rg[r].first + rg[r].count) --live;
       total += (uint64_t)live;
     }
     if (total == 0) break;
     uint64_t pick = hesp_splitmix_next(&st) % total;
     int32_t id = -1, rsel = -1;
-    for (int32_t r = 0; r < nr && id < 0; ++r) {
+    HESP_NOUNROLL for (int32_t r = 0; r < nr && id < 0; ++r) {
       if (!(rg[r].b / 2 >= cfg->min_block && rg[r].depth < cfg->max_depth)) continue;
       int32_t live = rg[r].count;
-      for (int32_t q = 0; q < nrem; ++q)
+      HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
         if (removed[q] >= rg[r].first && removed[q] < rg[r].first + rg[r].count) --live;
       if (pick < (uint64_t)live) {
         id = rg[r].first + (int32_t)pick;
         /* removed[] is sorted ascending: skip removed ids at or below id */
-        for (int32_t q = 0; q < nrem; ++q)
+        HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
           if (removed[q] >= rg[r].first && removed[q] <= id) ++id;
         rsel = r;
       } else {
@@ -216,7 +218,7 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
   }
   out->n_ops = nops;
   out->reserved = 0;
-  for (int32_t r = nops; r < HESP_MAX_OPS; ++r) {
+  HESP_NOUNROLL for (int32_t r = nops; r < HESP_MAX_OPS; ++r) {
     out->ops[r].task = -1;
     out->ops[r].s = 0;
   }

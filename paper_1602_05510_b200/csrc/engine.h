@@ -29,12 +29,14 @@
 #include "engine_types.h"
 
 #if defined(__CUDACC__)
-#define HX __device__ __forceinline__
-#define HXN __device__ __noinline__
+#define HX __device__ __forceinline__   // tiny accessors
+#define HXN __device__ __noinline__     // engine phases: one copy each keeps the kernel i-cache sized
+#define NOUNROLL _Pragma("unroll 1")
 #else
 #include <cstring>
 #define HX inline
 #define HXN inline
+#define NOUNROLL
 #endif
 
 namespace hx {
@@ -174,14 +176,14 @@ struct Engine {
   Small* sm;
   // slot arrays
   TaskMeta* tm;
-  int32_t *t_missing, *t_poff, *t_pcnt, *t_soff, *t_scnt, *leaf;
-  double *t_rel, *t_ct;
-  uint8_t* t_flag;
+  TState* ts;
+  int32_t *t_poff, *t_pcnt, *leaf;
   BlockMeta* bm;
   uint32_t* bflags;  // bits 0-7 mat per space, 8-15 dirty per space, 16 written
   double *valid, *lastu, *pinu;
   int32_t *tl_head, *tl_cnt, *tl_boff, *tl_nrb, *tl_ncb, *tl_coff, *tl_ids;
   int32_t *bnd, *c_writer, *c_rhead, *rnode, *preds, *succs, *pool, *ready, *pbuf;
+  double *pool_rel, *pool_key, *ready_key;
   int32_t *gs_a, *gs_b;
   Region *gs_reg, *gs_reg2;
   // scalars (uniform across lanes)
@@ -199,6 +201,11 @@ struct Engine {
   uint64_t ahash = 0, xhash = 0;
   uint64_t rng = 0;
   int32_t S, mainsp;
+  // No-eviction fast path (DESIGN.md §3 E4): when every block but the root
+  // fits in every space (plus the root in main), ensure_capacity can never
+  // evict, so LRU stamps, pins, mat/dirty flags and `used` -- read only by
+  // eviction -- need not be maintained.
+  bool fast = false;
   // optional per-task schedule trace (hesp_eval_detail): proc/start/end by task id
   int32_t* tr_proc = nullptr;
   double *tr_start = nullptr, *tr_end = nullptr;
@@ -207,14 +214,9 @@ struct Engine {
   HX Engine(WP w, const Problem& p, uint8_t* slot, const SlotLayout& L, Small* s)
       : wp(w), pb(p), sm(s) {
     tm = (TaskMeta*)(slot + L.tm);
-    t_missing = (int32_t*)(slot + L.t_missing);
-    t_rel = (double*)(slot + L.t_rel);
-    t_ct = (double*)(slot + L.t_ct);
+    ts = (TState*)(slot + L.ts);
     t_poff = (int32_t*)(slot + L.t_poff);
     t_pcnt = (int32_t*)(slot + L.t_pcnt);
-    t_soff = (int32_t*)(slot + L.t_soff);
-    t_scnt = (int32_t*)(slot + L.t_scnt);
-    t_flag = (uint8_t*)(slot + L.t_flag);
     leaf = (int32_t*)(slot + L.leaf);
     bm = (BlockMeta*)(slot + L.bm);
     bflags = (uint32_t*)(slot + L.bflags);
@@ -235,6 +237,9 @@ struct Engine {
     preds = (int32_t*)(slot + L.preds);
     succs = (int32_t*)(slot + L.succs);
     pool = (int32_t*)(slot + L.pool);
+    pool_rel = (double*)(slot + L.pool_rel);
+    pool_key = (double*)(slot + L.pool_key);
+    ready_key = (double*)(slot + L.ready_key);
     ready = (int32_t*)(slot + L.ready);
     pbuf = (int32_t*)(slot + L.pbuf);
     gs_a = (int32_t*)(slot + L.gs_a);
@@ -264,12 +269,12 @@ struct Engine {
   HX bool is_mat(int b, int s) const { return (bflags[b] >> s) & 1u; }
   HX bool is_dirty(int b, int s) const { return (bflags[b] >> (8 + s)) & 1u; }
   HX int part_index(int task) const {
-    for (int i = 0; i < npart; ++i)
+    NOUNROLL for (int i = 0; i < npart; ++i)
       if (sm->part[i].task == task) return i;
     return -1;
   }
   HX int bidx_of(long long b) const {
-    for (int i = 0; i < pb.nbv; ++i)
+    NOUNROLL for (int i = 0; i < pb.nbv; ++i)
       if (pb.bval[i] == b) return i;
     return -1;
   }
@@ -281,10 +286,10 @@ struct Engine {
   // Existing block with exactly region r (DataDag::find_by_region).  t >= 0:
   // r lies inside base tile t, so only the root, the tile and the tile's
   // blocks can match.  t < 0 (base build): every block.
-  HX int find_block(const Region& r, int t) {
+  HXN int find_block(const Region& r, int t) {
     if (t < 0) {
       int found = -1;
-      for (int base = 0; base < nblocks; base += WP::W) {
+      NOUNROLL for (int base = 0; base < nblocks; base += WP::W) {
         const int b = base + wp.lane();
         const bool hit = b < nblocks && rsame(reg(b), r);
         const unsigned m = wp.ballot(hit);
@@ -297,7 +302,7 @@ struct Engine {
     }
     if (rsame(reg(0), r)) return 0;
     if (rsame(reg(t), r)) return t;
-    for (int base = nbb; base < nblocks; base += WP::W) {
+    NOUNROLL for (int base = nbb; base < nblocks; base += WP::W) {
       const int b = base + wp.lane();
       const bool hit = b < nblocks && bm[b - nbb].tile == t && rsame(bm[b - nbb].r, r);
       const unsigned m = wp.ballot(hit);
@@ -306,7 +311,7 @@ struct Engine {
     return -1;
   }
 
-  HX int create_block(const Region& r, bool isint, int t) {  // DataDag::create, graph.cpp:142-189
+  HXN int create_block(const Region& r, bool isint, int t) {  // DataDag::create, graph.cpp:142-189
     if (nblocks >= pb.maxb) {
       fail(ST_ENGINE_LIMIT);
       return -1;
@@ -323,7 +328,7 @@ struct Engine {
     return id;
   }
 
-  HX int get_or_create(const Region& r, int t) {  // graph.cpp:191-212
+  HXN int get_or_create(const Region& r, int t) {  // graph.cpp:191-212
     const int ex = find_block(r, t);
     if (ex >= 0) return ex;
     const int id = create_block(r, false, t);
@@ -333,7 +338,7 @@ struct Engine {
     // blocks can partially overlap r (root and tile contain it).
     int nsect = 0;
     const int lo = t < 0 ? 0 : nbb;
-    for (int base = lo; base < id; base += WP::W) {
+    NOUNROLL for (int base = lo; base < id; base += WP::W) {
       const int b = base + wp.lane();
       bool hit = false;
       if (b < id) {
@@ -357,7 +362,7 @@ struct Engine {
       fail(ST_ENGINE_LIMIT);  // the base tiling never overlaps partially
       return -1;
     }
-    for (int k = 0; k < nsect; ++k) {
+    NOUNROLL for (int k = 0; k < nsect; ++k) {
       const Region o = reg(gs_a[k]);
       Region sct;
       sct.row = o.row > r.row ? o.row : r.row;
@@ -386,20 +391,20 @@ struct Engine {
 
   // One emitted sub-task: resolve its regions to blocks (reads in spec order,
   // then the write: graph.cpp:500-501) and append it with the next task id.
-  HX void emit(int kind, int nr, const Region* rr, const int* rt, const Region& w, int wt) {
+  HXN void emit(int kind, int nr, const Region* rr, const int* rt, const Region& w, int wt) {
     if (ntasks >= pb.maxt) {
       fail(ST_ENGINE_LIMIT);
       return;
     }
     TaskMeta m;
     m.pad = 0;
-    for (int k = 0; k < nr; ++k) {
+    NOUNROLL for (int k = 0; k < nr; ++k) {
       m.blk[k] = get_or_create(rr[k], rt[k]);
       if (status) return;
     }
     m.blk[nr] = get_or_create(w, wt);
     if (status) return;
-    for (int k = nr + 1; k < 4; ++k) m.blk[k] = -1;
+    NOUNROLL for (int k = nr + 1; k < 4; ++k) m.blk[k] = -1;
     m.kind = (int8_t)kind;
     m.nrd = (int8_t)nr;
     m.b = w.rows;
@@ -416,7 +421,7 @@ struct Engine {
 
   // TaskGraph::partition_task (graph.cpp:456-513) followed by the
   // enumerate_partition loop nests (graph.cpp:301-392).
-  HX void apply_op(int task_id, int s_req) {
+  HXN void apply_op(int task_id, int s_req) {
     if (task_id < 0 || task_id >= ntasks) return fail(ST_VALIDATION);
     if (part_index(task_id) >= 0) return fail(ST_NOT_A_LEAF);
     const double p = 1.0 / (double)s_req;
@@ -430,7 +435,7 @@ struct Engine {
     Region opr[3];
     int opt[3];
     int nop = 0;
-    for (int k = 0; k < t.nrd; ++k)
+    NOUNROLL for (int k = 0; k < t.nrd; ++k)
       if (t.blk[k] != wb) {
         opr[nop] = reg(t.blk[k]);
         opt[nop] = tile_of(t.blk[k]);
@@ -443,20 +448,20 @@ struct Engine {
     int rt[3];
     switch (t.kind) {
       case HESP_CHOL:
-        for (int k = 0; k < s && !status; ++k) {
+        NOUNROLL for (int k = 0; k < s && !status; ++k) {
           const Region akk = sub(a, s, k, k);
           rr[0] = akk;
           rt[0] = at;
           emit(HESP_CHOL, 1, rr, rt, akk, at);
-          for (int i = k + 1; i < s && !status; ++i) {
+          NOUNROLL for (int i = k + 1; i < s && !status; ++i) {
             rr[0] = akk;
             rr[1] = sub(a, s, i, k);
             rt[0] = rt[1] = at;
             emit(HESP_TRSM, 2, rr, rt, rr[1], at);
           }
-          for (int i = k + 1; i < s && !status; ++i) {
+          NOUNROLL for (int i = k + 1; i < s && !status; ++i) {
             const Region aik = sub(a, s, i, k);
-            for (int j = k + 1; j < i && !status; ++j) {
+            NOUNROLL for (int j = k + 1; j < i && !status; ++j) {
               rr[0] = aik;
               rr[1] = sub(a, s, j, k);
               rr[2] = sub(a, s, i, j);
@@ -475,11 +480,11 @@ struct Engine {
         if (nop != 1) return fail(ST_INTERNAL);
         const Region l = opr[0];
         const int lt = opt[0];
-        for (int j = 0; j < s && !status; ++j) {
+        NOUNROLL for (int j = 0; j < s && !status; ++j) {
           const Region ljj = sub(l, s, j, j);
-          for (int i = 0; i < s && !status; ++i) {
+          NOUNROLL for (int i = 0; i < s && !status; ++i) {
             const Region bij = sub(a, s, i, j);
-            for (int k = 0; k < j && !status; ++k) {
+            NOUNROLL for (int k = 0; k < j && !status; ++k) {
               rr[0] = sub(a, s, i, k);
               rr[1] = sub(l, s, j, k);
               rr[2] = bij;
@@ -502,10 +507,10 @@ struct Engine {
         if (nop != 1) return fail(ST_INTERNAL);
         const Region src = opr[0];
         const int st = opt[0];
-        for (int i = 0; i < s && !status; ++i)
-          for (int j = 0; j <= i && !status; ++j) {
+        NOUNROLL for (int i = 0; i < s && !status; ++i)
+          NOUNROLL for (int j = 0; j <= i && !status; ++j) {
             const Region cij = sub(a, s, i, j);
-            for (int k = 0; k < s && !status; ++k) {
+            NOUNROLL for (int k = 0; k < s && !status; ++k) {
               rr[0] = sub(src, s, i, k);
               rt[0] = st;
               if (i == j) {
@@ -526,10 +531,10 @@ struct Engine {
       default: {
         if (nop != 2) return fail(ST_INTERNAL);
         const Region ma = opr[0], mb = opr[1];
-        for (int i = 0; i < s && !status; ++i)
-          for (int j = 0; j < s && !status; ++j) {
+        NOUNROLL for (int i = 0; i < s && !status; ++i)
+          NOUNROLL for (int j = 0; j < s && !status; ++j) {
             const Region cij = sub(a, s, i, j);
-            for (int k = 0; k < s && !status; ++k) {
+            NOUNROLL for (int k = 0; k < s && !status; ++k) {
               rr[0] = sub(ma, s, i, k);
               rr[1] = sub(mb, s, j, k);
               rr[2] = cij;
@@ -559,19 +564,19 @@ struct Engine {
 
   // Per-tile CSR of the candidate's own blocks (order inside a tile is
   // irrelevant: every consumer is order-independent or sorts).
-  HX void build_tiles() {
-    for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt[i] = 0;
+  HXN void build_tiles() {
+    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt[i] = 0;
     wp.sync();
-    for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt[bm[b - nbb].tile], 1);
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt[bm[b - nbb].tile], 1);
     wp.sync();
     // exclusive scan over base tiles
     int run = 0;
-    for (int base = 0; base < nbb; base += WP::W) {
+    NOUNROLL for (int base = 0; base < nbb; base += WP::W) {
       const int i = base + wp.lane();
       const int c = i < nbb ? tl_cnt[i] : 0;
       int incl = c;
 #if defined(__CUDACC__)
-      for (int o = 1; o < 32; o <<= 1) {
+      NOUNROLL for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (wp.lane() >= o) incl += v;
       }
@@ -580,9 +585,9 @@ struct Engine {
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
-    for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb[i] = 0;  // fill cursor
+    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb[i] = 0;  // fill cursor
     wp.sync();
-    for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
       const int t = bm[b - nbb].tile;
       const int pos = wp.atomic_add(&tl_ncb[t], 1);
       tl_ids[tl_head[t] + pos] = b;
@@ -593,12 +598,12 @@ struct Engine {
 
   // Leaf program order: lexicographic seq, i.e. depth-first over clusters
   // with members in emission order (graph.cpp:552-562).
-  HX void build_order() {
+  HXN void build_order() {
     // subtree leaf counts, innermost partitions last in op order
-    for (int i = npart - 1; i >= 0; --i) {
+    NOUNROLL for (int i = npart - 1; i >= 0; --i) {
       const PartEntry pe = sm->part[i];
       int cnt = 0;
-      for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
+      NOUNROLL for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
         const int pi = part_index(c);
         cnt += pi >= 0 ? sm->part[pi].leaves : 1;
       }
@@ -624,7 +629,7 @@ struct Engine {
       --top;
       const int f = sf[top], c = sc[top];
       int pos = sp[top];
-      for (int base = 0; base < c; base += WP::W) {
+      NOUNROLL for (int base = 0; base < c; base += WP::W) {
         const int k = base + wp.lane();
         int pi = -1, sz = 0;
         if (k < c) {
@@ -633,7 +638,7 @@ struct Engine {
         }
         int incl = sz;
 #if defined(__CUDACC__)
-        for (int o = 1; o < 32; o <<= 1) {
+        NOUNROLL for (int o = 1; o < 32; o <<= 1) {
           const int v = __shfl_up_sync(0xffffffffu, incl, o);
           if (wp.lane() >= o) incl += v;
         }
@@ -641,7 +646,7 @@ struct Engine {
         const int my = pos + incl - sz;
         if (k < c && pi < 0) leaf[my] = f + k;
         const unsigned m = wp.ballot(k < c && pi >= 0);
-        for (unsigned mm = m; mm; mm &= mm - 1) {
+        NOUNROLL for (unsigned mm = m; mm; mm &= mm - 1) {
           const int ln = ctz32(mm);
           const int q = wp.bcast(pi, ln);
           const int qp = wp.bcast(my, ln);
@@ -659,9 +664,9 @@ struct Engine {
   }
 
   // Column/row boundaries of every tile's blocks -> cell grids.
-  HX void build_cells() {
+  HXN void build_cells() {
     int nb_used = 0, nc_used = 0;
-    for (int t = 1; t < nbb && !status; ++t) {
+    NOUNROLL for (int t = 1; t < nbb && !status; ++t) {
       const int cnt = tl_cnt[t];
       if (cnt == 0) {
         if (wp.lane() == 0) {
@@ -686,7 +691,7 @@ struct Engine {
       int* raw_r = gs_a;
       int* raw_c = gs_a + nraw;
       if (2 * nraw > pb.maxgs) return fail(ST_ENGINE_LIMIT);
-      for (int k = wp.lane(); k < nraw; k += WP::W) {
+      NOUNROLL for (int k = wp.lane(); k < nraw; k += WP::W) {
         int vr, vc;
         if (k < 2) {
           vr = k == 0 ? tr.row : tr.row + tr.rows;
@@ -701,10 +706,10 @@ struct Engine {
       }
       wp.sync();
       // sort (value, index) then keep first occurrences: rows -> rows[], cols -> cols[]
-      for (int k = wp.lane(); k < nraw; k += WP::W) {
+      NOUNROLL for (int k = wp.lane(); k < nraw; k += WP::W) {
         const int vr = raw_r[k], vc = raw_c[k];
         int rr = 0, rc = 0;
-        for (int q = 0; q < nraw; ++q) {
+        NOUNROLL for (int q = 0; q < nraw; ++q) {
           const int ur = raw_r[q], uc = raw_c[q];
           rr += (ur < vr) || (ur == vr && q < k);
           rc += (uc < vc) || (uc == vc && q < k);
@@ -714,7 +719,7 @@ struct Engine {
       }
       wp.sync();
       int nr = 0, nc = 0;
-      for (int base = 0; base < nraw; base += WP::W) {
+      NOUNROLL for (int base = 0; base < nraw; base += WP::W) {
         const int k = base + wp.lane();
         int vr = 0, vc = 0;
         bool kr = false, kc = false;
@@ -732,14 +737,14 @@ struct Engine {
         nc += popc32(mc);
       }
       wp.sync();
-      for (int k = wp.lane(); k < nr; k += WP::W) rows[k] = gs_a[k];
+      NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) rows[k] = gs_a[k];
       wp.sync();
       // cols right after the nr distinct rows
-      for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a[nraw + k];
+      NOUNROLL for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a[nraw + k];
       wp.sync();
       const int ncell = (nr - 1) * (nc - 1);
       if (nc_used + ncell > pb.maxcells) return fail(ST_ENGINE_LIMIT);
-      for (int k = wp.lane(); k < ncell; k += WP::W) {
+      NOUNROLL for (int k = wp.lane(); k < ncell; k += WP::W) {
         c_writer[nc_used + k] = -1;
         c_rhead[nc_used + k] = -1;
       }
@@ -769,11 +774,11 @@ struct Engine {
     const int* rows = bnd + off;
     const int* cols = rows + nr;
     r0 = r1 = c0 = c1 = 0;
-    for (int k = 0; k < nr; ++k) {
+    NOUNROLL for (int k = 0; k < nr; ++k) {
       if (rows[k] == r.row) r0 = k;
       if (rows[k] == r.row + r.rows) r1 = k;
     }
-    for (int k = 0; k < nc; ++k) {
+    NOUNROLL for (int k = 0; k < nc; ++k) {
       if (cols[k] == r.col) c0 = k;
       if (cols[k] == r.col + r.cols) c1 = k;
     }
@@ -782,30 +787,30 @@ struct Engine {
   // Dependences (E2): per cell, last writer + readers since that write.
   // For each leaf j in program order: reads -> pred last writer, join
   // readers; writes -> preds last writer and all readers, become writer.
-  HX void build_deps() {
+  HXN void build_deps() {
     int rn_used = 0;
     nedges = 0;
-    for (int li = 0; li < nleaves && !status; ++li) {
+    NOUNROLL for (int li = 0; li < nleaves && !status; ++li) {
       const int j = leaf[li];
       const TaskMeta t = task(j);
       const int wb = t.blk[t.nrd];
       int npb = 0;
       {
         int kt = 0;
-        for (int k = 0; k <= t.nrd; ++k) {
+        NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
           bool dup = false;
-          for (int q = 0; q < k; ++q)
+          NOUNROLL for (int q = 0; q < k; ++q)
             if (t.blk[q] == t.blk[k]) dup = true;
           kt += !dup;
         }
         sum_k += kt;
       }
       // distinct blocks, read-only ones first in read order, then the write
-      for (int k = 0; k <= t.nrd; ++k) {
+      NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
         const int b = t.blk[k];
         if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
         bool dup = false;
-        for (int q = 0; q < k; ++q)
+        NOUNROLL for (int q = 0; q < k; ++q)
           if (t.blk[q] == b && q < t.nrd) dup = true;
         if (dup && k < t.nrd) continue;
         const bool writes = (k == t.nrd);
@@ -815,7 +820,7 @@ struct Engine {
         const int w = c1 - c0;
         const int ncells = (r1 - r0) * w;
         const int cbase = tl_coff[tt];
-        for (int base = 0; base < ncells; base += WP::W) {
+        NOUNROLL for (int base = 0; base < ncells; base += WP::W) {
           const int q = base + wp.lane();
           int cell = -1;
           if (q < ncells) cell = cbase + (r0 + q / w) * nc + (c0 + q % w);
@@ -868,14 +873,14 @@ struct Engine {
       }
       // dedup -> preds CSR
       int m = 0;
-      for (int base = 0; base < npb; base += WP::W) {
+      NOUNROLL for (int base = 0; base < npb; base += WP::W) {
         const int q = base + wp.lane();
         bool keep = false;
         int v = -1;
         if (q < npb) {
           v = pbuf[q];
           keep = true;
-          for (int z = 0; z < q; ++z)
+          NOUNROLL for (int z = 0; z < q; ++z)
             if (pbuf[z] == v) {
               keep = false;
               break;
@@ -892,42 +897,42 @@ struct Engine {
       if (wp.lane() == 0) {
         t_poff[j] = nedges;
         t_pcnt[j] = m;
-        t_missing[j] = m;
+        ts[j].missing = m;
       }
       wp.sync();
       nedges += m;
     }
     if (status) return;
     // successors CSR from the preds lists
-    for (int li = wp.lane(); li < nleaves; li += WP::W) t_scnt[leaf[li]] = 0;
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts[leaf[li]].scnt = 0;
     wp.sync();
-    for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&t_scnt[preds[e]], 1);
+    NOUNROLL for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&ts[preds[e]].scnt, 1);
     wp.sync();
     int run = 0;
-    for (int base = 0; base < nleaves; base += WP::W) {
+    NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
-      const int c = li < nleaves ? t_scnt[leaf[li]] : 0;
+      const int c = li < nleaves ? ts[leaf[li]].scnt : 0;
       int incl = c;
 #if defined(__CUDACC__)
-      for (int o = 1; o < 32; o <<= 1) {
+      NOUNROLL for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xffffffffu, incl, o);
         if (wp.lane() >= o) incl += v;
       }
 #endif
       if (li < nleaves) {
-        t_soff[leaf[li]] = run + incl - c;
-        t_scnt[leaf[li]] = 0;  // reused as fill cursor
+        ts[leaf[li]].soff = run + incl - c;
+        ts[leaf[li]].scnt = 0;  // reused as fill cursor
       }
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
-    for (int li = 0; li < nleaves; ++li) {  // fill (per dst; order within a list is irrelevant)
+    NOUNROLL for (int li = 0; li < nleaves; ++li) {  // fill (per dst; order within a list is irrelevant)
       const int j = leaf[li];
       const int off = t_poff[j], cnt = t_pcnt[j];
-      for (int q = wp.lane(); q < cnt; q += WP::W) {
+      NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
         const int p = preds[off + q];
-        const int pos = wp.atomic_add(&t_scnt[p], 1);
-        succs[t_soff[p] + pos] = j;
+        const int pos = wp.atomic_add(&ts[p].scnt, 1);
+        succs[ts[p].soff + pos] = j;
       }
       wp.sync();
     }
@@ -935,19 +940,19 @@ struct Engine {
 
   // critical_times (sim.cpp:92-115): ct = avg + max(0, max_succ ct), reverse
   // program order; pushed to preds so each pred sees all its successors.
-  HX void build_ct() {
-    for (int li = wp.lane(); li < nleaves; li += WP::W) t_rel[leaf[li]] = 0.0;  // t_rel holds best_succ here
+  HXN void build_ct() {
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts[leaf[li]].rel = 0.0;  // .rel holds best_succ here
     wp.sync();
-    for (int li = nleaves - 1; li >= 0; --li) {
+    NOUNROLL for (int li = nleaves - 1; li >= 0; --li) {
       const int j = leaf[li];
       const TaskMeta t = task(j);
-      const double c = pb.ctavg[t.kind][t.bidx] + t_rel[j];
+      const double c = pb.ctavg[t.kind][t.bidx] + ts[j].rel;
       const int off = t_poff[j], cnt = t_pcnt[j];
-      for (int q = wp.lane(); q < cnt; q += WP::W) {
+      NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
         const int p = preds[off + q];
-        t_rel[p] = dmax(t_rel[p], c);
+        ts[p].rel = dmax(ts[p].rel, c);
       }
-      if (wp.lane() == 0) t_ct[j] = c;
+      if (wp.lane() == 0) ts[j].ct = c;
       wp.sync();
     }
   }
@@ -961,13 +966,13 @@ struct Engine {
   template <class F>
   HX void for_scope(int t, F&& f) {
     if (t < 0) {  // the root: everything
-      for (int b = wp.lane(); b < nblocks; b += WP::W) f(b);
+      NOUNROLL for (int b = wp.lane(); b < nblocks; b += WP::W) f(b);
       wp.sync();
       return;
     }
     const int cnt = 2 + tl_cnt[t];
     const int head = tl_head[t];
-    for (int k = wp.lane(); k < cnt; k += WP::W) {
+    NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
       const int b = k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]);
       f(b);
     }
@@ -976,13 +981,13 @@ struct Engine {
 
   HX int source_space(int b, int exclude) {  // source_spaces().front() minus `exclude` (sim.cpp:341-350)
     if (mainsp != exclude && V(b, mainsp) != ABSENT) return mainsp;
-    for (int s = 0; s < S; ++s)
+    NOUNROLL for (int s = 0; s < S; ++s)
       if (s != mainsp && s != exclude && V(b, s) != ABSENT) return s;
     return -1;
   }
 
   // Engine::plan_transfer (sim.cpp:468-499): FIFO per directed link.
-  HX double plan_transfer(int blk, const Region* frag, long long bytes, int src, int dst,
+  HXN double plan_transfer(int blk, const Region* frag, long long bytes, int src, int dst,
                           double data_ready, double tnow) {
     const int nh = pb.route_n[src * MAXS + dst];
     if (nh == 0) {
@@ -991,12 +996,11 @@ struct Engine {
     }
     double rdy = dmax(data_ready, tnow);
     double start0 = 0.0;
-    for (int h = 0; h < nh; ++h) {
+    NOUNROLL for (int h = 0; h < nh; ++h) {
       const int l = pb.route_l[src * MAXS + dst][h];
       const double st = dmax(sm->link_free[l], rdy);
       const double en = st + pb.link_lat[l] + (double)bytes / pb.link_bw[l];
-      if (wp.lane() == 0) sm->link_free[l] = en;
-      wp.sync();
+      sm->link_free[l] = en;
       rdy = en;
       if (h == 0) start0 = st;
     }
@@ -1009,22 +1013,15 @@ struct Engine {
     return rdy;
   }
 
+  // Scalar state is replicated in every lane: uniform code stores the same
+  // value from all lanes (idempotent), so no lane-0 store + __syncwarp.
   HX void set_flag(int b, uint32_t bit, bool on) {
-    if (wp.lane() == 0) bflags[b] = on ? (bflags[b] | bit) : (bflags[b] & ~bit);
-    wp.sync();
+    const uint32_t f = bflags[b];
+    bflags[b] = on ? (f | bit) : (f & ~bit);
   }
-  HX void setV(int b, int s, double v) {
-    if (wp.lane() == 0) V(b, s) = v;
-    wp.sync();
-  }
-  HX void setLU(int b, int s, double v) {
-    if (wp.lane() == 0) LU(b, s) = v;
-    wp.sync();
-  }
-  HX void setPIN(int b, int s, double v) {
-    if (wp.lane() == 0) PIN(b, s) = v;
-    wp.sync();
-  }
+  HX void setV(int b, int s, double v) { V(b, s) = v; }
+  HX void setLU(int b, int s, double v) { LU(b, s) = v; }
+  HX void setPIN(int b, int s, double v) { PIN(b, s) = v; }
   HX void add_used(int s, long long d) {
     if (wp.lane() == 0) sm->used[s] += d;
     wp.sync();
@@ -1037,7 +1034,7 @@ struct Engine {
   }
 
   // validate_from (sim.cpp:452-461): block and descendants valid at min(., at)
-  HX void validate_from(int b, int s, double at) {
+  HXN void validate_from(int b, int s, double at) {
     const int t = b == 0 ? -1 : tile_of(b);
     const Region rb = reg(b);
     for_scope(t, [&](int x) {
@@ -1046,8 +1043,7 @@ struct Engine {
         if (v > at) v = at;
       }
     });
-    if (wp.lane() == 0) LU(b, s) = dmax(LU(b, s), at);
-    wp.sync();
+    if (!fast) LU(b, s) = dmax(LU(b, s), at);
   }
 
   // ensure_capacity (sim.cpp:374-439).  The only recursion in the reference
@@ -1055,7 +1051,7 @@ struct Engine {
   // and main never holds dirty blocks, so FLUSH=false is the flush's own
   // instance: no device recursion, no call stack.
   template <bool FLUSH>
-  HX void ensure_capacity(int s, long long bytes, double at) {
+  HXN void ensure_capacity(int s, long long bytes, double at) {
     const long long cap = pb.cap[s];
     if (bytes > cap) return fail(ST_CAPACITY);
     while (sm->used[s] + bytes > cap) {
@@ -1063,7 +1059,7 @@ struct Engine {
       double bst = ABSENT;
       double dummy = 0.0;
       int bid = -1;
-      for (int base = 0; base < nblocks; base += WP::W) {
+      NOUNROLL for (int base = 0; base < nblocks; base += WP::W) {
         const int b = base + wp.lane();
         if (b < nblocks && is_mat(b, s) && !(PIN(b, s) > now)) {
           bool ok = true;
@@ -1071,7 +1067,7 @@ struct Engine {
             if (b == 0) ok = false;  // roots are never evicted from main
             else {
               bool elsewhere = false;
-              for (int s2 = 0; s2 < S; ++s2)
+              NOUNROLL for (int s2 = 0; s2 < S; ++s2)
                 if (s2 != s && V(b, s2) != ABSENT) elsewhere = true;
               ok = elsewhere;
             }
@@ -1106,14 +1102,14 @@ struct Engine {
       if (s != mainsp) {
         // views lose their backing when no materialised block covers them
         const Region vr = reg(victim);
-        for (int base = 0; base < nblocks; base += WP::W) {
+        NOUNROLL for (int base = 0; base < nblocks; base += WP::W) {
           const int x = base + wp.lane();
           bool drop = false;
           if (x < nblocks && V(x, s) != ABSENT && !is_mat(x, s)) {
             const Region xr = reg(x);
             if (roverlap(xr, vr)) {
               bool covered = false;
-              for (int m = 0; m < nblocks && !covered; ++m)
+              NOUNROLL for (int m = 0; m < nblocks && !covered; ++m)
                 if (is_mat(m, s) && rcontains(reg(m), xr)) covered = true;
               drop = !covered;
             }
@@ -1128,7 +1124,7 @@ struct Engine {
 
   template <bool FLUSH = true>
   HX void reserve_bytes(int b, int s, double at) {  // sim.cpp:441-450
-    if (is_mat(b, s)) return;
+    if (fast || is_mat(b, s)) return;
     const long long bytes = bbytes(b);
     ensure_capacity<FLUSH>(s, bytes, at);
     if (status) return;
@@ -1145,17 +1141,16 @@ struct Engine {
   }
 
   HX void pin(int s, int b, double until) {  // sim.cpp:352-355 (E3 representation)
-    if (wp.lane() == 0) PIN(b, s) = dmax(PIN(b, s), until);
-    wp.sync();
+    if (fast) return;
+    PIN(b, s) = dmax(PIN(b, s), until);
   }
 
   // acquire (sim.cpp:501-519) without the gather fallback.
-  HX double acquire_direct(int b, int s, bool& need_gather) {
+  HXN double acquire_direct(int b, int s, bool& need_gather) {
     need_gather = false;
     const double v = V(b, s);
     if (v != ABSENT) {
-      if (wp.lane() == 0) LU(b, s) = dmax(LU(b, s), now);
-      wp.sync();
+      if (!fast) LU(b, s) = dmax(LU(b, s), now);
       return v;
     }
     const int src = source_space(b, s);
@@ -1181,12 +1176,12 @@ struct Engine {
   // subtract_regions (graph.cpp:45-84) restricted to what callers need:
   // mode 0 -> returns 1 if base minus cuts is non-empty; mode 1 -> writes the
   // row-sweep fragments into out[] and returns their count.
-  HX int subtract(const Region& base, const Region* cuts, int ncut, Region* out, int mode) {
+  HXN int subtract(const Region& base, const Region* cuts, int ncut, Region* out, int mode) {
     int nx = 0, ny = 0;
     // computed redundantly by every lane (uniform), stored by lane 0
     int lx[32], ly[32];
     auto insl = [&](int* arr, int& n, int v) {
-      for (int k = 0; k < n; ++k)
+      NOUNROLL for (int k = 0; k < n; ++k)
         if (arr[k] == v) return true;
       if (n >= 32) return false;
       int k = n++;
@@ -1199,7 +1194,7 @@ struct Engine {
     };
     bool ok = insl(lx, nx, base.col) && insl(lx, nx, base.col + base.cols) && insl(ly, ny, base.row) &&
               insl(ly, ny, base.row + base.rows);
-    for (int c = 0; c < ncut && ok; ++c) {
+    NOUNROLL for (int c = 0; c < ncut && ok; ++c) {
       const Region& cr = cuts[c];
       if (!roverlap(base, cr)) continue;
       auto clampi = [](int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); };
@@ -1213,18 +1208,18 @@ struct Engine {
       return 0;
     }
     int nout = 0;
-    for (int yi = 0; yi + 1 < ny; ++yi) {
+    NOUNROLL for (int yi = 0; yi + 1 < ny; ++yi) {
       bool have = false;
       Region run;
       run.row = run.col = run.rows = run.cols = 0;
-      for (int xi = 0; xi + 1 < nx; ++xi) {
+      NOUNROLL for (int xi = 0; xi + 1 < nx; ++xi) {
         Region cell;
         cell.row = ly[yi];
         cell.col = lx[xi];
         cell.rows = ly[yi + 1] - ly[yi];
         cell.cols = lx[xi + 1] - lx[xi];
         bool covered = false;
-        for (int c = 0; c < ncut; ++c)
+        NOUNROLL for (int c = 0; c < ncut; ++c)
           if (rcontains(cuts[c], cell)) {
             covered = true;
             break;
@@ -1270,7 +1265,7 @@ struct Engine {
     {
       const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
       const int head = t < 0 ? 0 : tl_head[t];
-      for (int base = 0; base < cnt; base += WP::W) {
+      NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
         const int k = base + wp.lane();
         int b = -1;
         bool hit = false;
@@ -1278,7 +1273,7 @@ struct Engine {
           b = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
           if (b != blk && rcontains(target, reg(b))) {
             bool any = false;
-            for (int q = 0; q < S; ++q)
+            NOUNROLL for (int q = 0; q < S; ++q)
               if (V(b, q) != ABSENT) any = true;
             hit = any;
           }
@@ -1297,13 +1292,13 @@ struct Engine {
       }
     }
     // sort pieces: local first, then area descending, then id (sim.cpp:540-544)
-    for (int k = wp.lane(); k < np; k += WP::W) {
+    NOUNROLL for (int k = wp.lane(); k < np; k += WP::W) {
       const int a = gs_a[k];
       const bool la = V(a, s) != ABSENT;
       const Region ra = reg(a);
       const long long aa = (long long)ra.rows * ra.cols;
       int rank = 0;
-      for (int q = 0; q < np; ++q) {
+      NOUNROLL for (int q = 0; q < np; ++q) {
         const int c = gs_a[q];
         if (c == a) continue;
         const bool lc = V(c, s) != ABSENT;
@@ -1320,7 +1315,7 @@ struct Engine {
     wp.sync();
     double arrival = 0.0;
     int ncov = 0;
-    for (int k = 0; k < np; ++k) {
+    NOUNROLL for (int k = 0; k < np; ++k) {
       const int piece = gs_reg2[k].row;
       const Region pr = reg(piece);
       if (subtract(pr, gs_reg, ncov, nullptr, 0) == 0) {
@@ -1344,7 +1339,7 @@ struct Engine {
     if (status) return 0.0;
     if (nfr > 0) {
       bool bad = false;
-      for (int f = 0; f < nfr && !bad; ++f) {
+      NOUNROLL for (int f = 0; f < nfr && !bad; ++f) {
         const Region fr = gs_reg2[f];
         bool hit = false;
         for_scope(t, [&](int x) {
@@ -1358,7 +1353,7 @@ struct Engine {
         return 0.0;
       }
       if (s != mainsp)
-        for (int f = 0; f < nfr; ++f) {
+        NOUNROLL for (int f = 0; f < nfr; ++f) {
           const Region fr = gs_reg2[f];
           arrival = dmax(arrival, plan_transfer(blk, &fr, rbytes(fr), mainsp, s, 0.0, now));
           if (status) return 0.0;
@@ -1371,29 +1366,34 @@ struct Engine {
   // invalidate_elsewhere (sim.cpp:574-590) over the invalidation cone
   // (sim.cpp:204-212), which by E1 is: blocks inside b, plus blocks strictly
   // containing some block inside b.
-  HX void invalidate_elsewhere(int b, int ws) {
+  HXN void invalidate_elsewhere(int b, int ws) {
     const int t = b == 0 ? -1 : tile_of(b);
     const Region rb = reg(b);
     long long freed[MAXS];
-    for (int q = 0; q < MAXS; ++q) freed[q] = 0;
+    NOUNROLL for (int q = 0; q < MAXS; ++q) freed[q] = 0;
     const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
     const int head = t < 0 ? 0 : tl_head[t];
-    for (int k = wp.lane(); k < cnt; k += WP::W) {
+    NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
       const int x = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
       const Region rx = reg(x);
       bool in = false;
       if (rcontains(rb, rx) || rcontains(rx, rb)) in = true;
       else if (roverlap(rx, rb)) {
         // partial overlap: in the cone iff some block inside b is strictly inside x
-        for (int q = 0; q < cnt && !in; ++q) {
+        NOUNROLL for (int q = 0; q < cnt && !in; ++q) {
           const int c = t < 0 ? q : (q == 0 ? 0 : (q == 1 ? t : tl_ids[head + q - 2]));
           const Region rc = reg(c);
           if (c != x && rcontains(rb, rc) && rcontains(rx, rc) && !rsame(rx, rc)) in = true;
         }
       }
       if (!in) continue;
+      if (fast) {
+        NOUNROLL for (int q = 0; q < S; ++q)
+          if (q != ws) V(x, q) = ABSENT;
+        continue;
+      }
       uint32_t f = bflags[x];
-      for (int q = 0; q < S; ++q) {
+      NOUNROLL for (int q = 0; q < S; ++q) {
         if (q == ws) continue;
         if ((f >> q) & 1u) {
           freed[q] += rbytes(rx);
@@ -1405,7 +1405,8 @@ struct Engine {
       bflags[x] = f & keep;
     }
     wp.sync();
-    for (int q = 0; q < S; ++q) {
+    if (fast) return;
+    NOUNROLL for (int q = 0; q < S; ++q) {
       if (q == ws) continue;
       const long long fr = wp.suml(freed[q]);
       if (fr) add_used(q, -fr);
@@ -1416,18 +1417,14 @@ struct Engine {
   // Scheduling (sim.cpp:704-834)
   // =========================================================================
 
-  HX void commit(int j, int p) {  // Engine::commit, sim.cpp:592-668
-    const TaskMeta t = task(j);
-    const int s = pb.proc_space[p];
-    const int type = pb.proc_type[p];
-    // working set: distinct blocks in id order
-    int w[4];
+  // Working set of a task: distinct blocks of reads u writes in id order
+  // (the std::set iteration of sim.cpp:597-598 and sim.cpp:768-769).
+  static HX int working_set(const TaskMeta& t, int* w) {
     int nw = 0;
-    for (int k = 0; k <= t.nrd; ++k) {
+    NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
       const int b = t.blk[k];
       bool dup = false;
-      for (int q = 0; q < nw; ++q)
-        if (w[q] == b) dup = true;
+      for (int q = 0; q < nw; ++q) dup |= w[q] == b;
       if (dup) continue;
       int q = nw++;
       while (q > 0 && w[q - 1] > b) {
@@ -1436,26 +1433,58 @@ struct Engine {
       }
       w[q] = b;
     }
-    long long wset = 0;
-    for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
-    if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+    return nw;
+  }
+
+  // Write coherence of commit (sim.cpp:625-628) in one pass over the scope:
+  // invalidate_elsewhere(out, s) over the cone (E1) at task start, then
+  // validate_from(out, s, end) and valid[out] = end.  Both passes touch
+  // disjoint (block, space) cells except out itself, which ends at `end`.
+  HX void write_coherence(int out, int s, double end) {
+    const int t = out == 0 ? -1 : tile_of(out);
+    if (t > 0 && tl_cnt[t] == 0) {  // unsubdivided tile: cone = {root, tile}, no descendants
+      if (fast) {
+        NOUNROLL for (int q = wp.lane(); q < S; q += WP::W)
+          if (q != s) {
+            V(0, q) = ABSENT;
+            V(out, q) = ABSENT;
+          }
+        wp.sync();
+        V(out, s) = end;
+        return;
+      }
+    }
+    invalidate_elsewhere(out, s);
+    validate_from(out, s, end);
+    setV(out, s, end);
+  }
+
+  HXN void commit(int j, int p, const TaskMeta& t, const int* w, int nw, double rel) {  // sim.cpp:592-668
+    const int s = pb.proc_space[p];
+    const int type = pb.proc_type[p];
+    if (!fast) {
+      long long wset = 0;
+      NOUNROLL for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
+      if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+    }
     double inputs = 0.0;
     double saved[4];
-    for (int k = 0; k < nw; ++k) {
+    NOUNROLL for (int k = 0; k < nw; ++k) {
       const double a = acquire(w[k], s);
       if (status) return;
       inputs = dmax(inputs, a);
-      saved[k] = PIN(w[k], s);
-      setPIN(w[k], s, HOLD);
+      if (!fast) {
+        saved[k] = PIN(w[k], s);
+        setPIN(w[k], s, HOLD);
+      }
     }
     const int out = t.blk[t.nrd];
     reserve_bytes(out, s, now);
     if (status) return;
-    const double start = dmax(dmax(sm->proc_free[p], t_rel[j]), inputs);
+    const double start = dmax(dmax(sm->proc_free[p], rel), inputs);
     const double end = start + pb.ttime[t.kind][t.bidx][type];
     if (!(end > now) || start < now) return fail(ST_ENGINE_INVARIANT);
-    if (wp.lane() == 0) sm->proc_free[p] = end;
-    wp.sync();
+    sm->proc_free[p] = end;
     ahash += hesp_assign_term(j, p, dbits(start), dbits(end));
     if (tr_proc && j < tr_cap && wp.lane() == 0) {
       tr_proc[j] = p;
@@ -1463,14 +1492,13 @@ struct Engine {
       tr_end[j] = end;
     }
     makespan = dmax(makespan, end);
-    for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
-    invalidate_elsewhere(out, s);
-    validate_from(out, s, end);
-    setV(out, s, end);
+    if (!fast)
+      NOUNROLL for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
+    write_coherence(out, s, end);
     set_flag(out, 1u << 16, true);
     if (s != mainsp) {
       if (pb.caching == CACHE_WB) {
-        set_flag(out, 1u << (8 + s), true);
+        if (!fast) set_flag(out, 1u << (8 + s), true);
       } else {
         const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
         if (status) return;
@@ -1478,34 +1506,48 @@ struct Engine {
         materialize<false>(out, mainsp, arr);
         if (status) return;
         if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
-          set_flag(out, 1u << s, false);
-          add_used(s, -bbytes(out));
-          setLU(out, s, 0.0);
+          if (!fast) {
+            set_flag(out, 1u << s, false);
+            add_used(s, -bbytes(out));
+            setLU(out, s, 0.0);
+          }
           setV(out, s, ABSENT);
           const Region ro = reg(out);
           const int tt = out == 0 ? -1 : tile_of(out);
-          for_scope(tt, [&](int x) {
-            if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
-          });
+          if (!(tt > 0 && tl_cnt[tt] == 0))
+            for_scope(tt, [&](int x) {
+              if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
+            });
         }
       }
     }
-    // mark committed, release successors (sim.cpp:660-667)
-    if (wp.lane() == 0) t_flag[j] = 1;
-    const int off = t_soff[j], cnt = t_scnt[j];
+    // mark committed, release successors (sim.cpp:660-667); released tasks
+    // enter the pool with their release time and ordering key inline
+    ts[j].flag = 1;
+    const int off = ts[j].soff, cnt = ts[j].scnt;
     int added = 0;
-    for (int base = 0; base < cnt; base += WP::W) {
+    const bool pl = pb.ordering == ORD_PL;
+    NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
       const int q = base + wp.lane();
-      bool rel = false;
+      bool rl = false;
       int sj = -1;
+      double r = 0.0, key = 0.0;
       if (q < cnt) {
         sj = succs[off + q];
-        const int left = --t_missing[sj];
-        t_rel[sj] = dmax(t_rel[sj], end);
-        rel = left == 0;
+        TState& st = ts[sj];
+        const int left = --st.missing;
+        r = dmax(st.rel, end);
+        st.rel = r;
+        rl = left == 0;
+        if (rl) key = pl ? st.ct : r;
       }
-      const unsigned m = wp.ballot(rel);
-      if (rel) pool[pool_n + added + popc32(m & wp.lt())] = sj;
+      const unsigned m = wp.ballot(rl);
+      if (rl) {
+        const int at = pool_n + added + popc32(m & wp.lt());
+        pool[at] = sj;
+        pool_rel[at] = r;
+        pool_key[at] = key;
+      }
       added += popc32(m);
     }
     wp.sync();
@@ -1514,25 +1556,37 @@ struct Engine {
 
   HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
 
-  HX void simulate() {
+  HXN void simulate() {
     const int P = pb.P;
     if (nleaves == 0) return fail(ST_VALIDATION);
     if (P < 1) return fail(ST_NO_PROCESSORS);
     // check_models (sim.cpp:312-321)
     bool miss = false;
-    for (int li = wp.lane(); li < nleaves; li += WP::W) {
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) {
       const TaskMeta t = task(leaf[li]);
-      for (int ty = 0; ty < pb.n_types; ++ty)
+      NOUNROLL for (int ty = 0; ty < pb.n_types; ++ty)
         if (!pb.known[t.kind][ty]) miss = true;
     }
     if (wp.any(miss)) return fail(ST_MODEL_MISS);
+    // E4: can any space ever need to evict?  (root only ever lives in main)
+    {
+      long long nonroot = 0;
+      NOUNROLL for (int x = 1 + wp.lane(); x < nblocks; x += WP::W) nonroot += bbytes(x);
+      nonroot = wp.suml(nonroot);
+      bool ok = true;
+      NOUNROLL for (int q = 0; q < S; ++q)
+        if (nonroot + (q == mainsp ? bbytes(0) : 0) > pb.cap[q]) ok = false;
+      fast = ok;
+    }
     // init_memory (sim.cpp:323-339): root materialised in main, every block
     // valid in main at t=0 (views into the root data)
-    for (int x = wp.lane(); x < nblocks; x += WP::W) {
-      for (int q = 0; q < S; ++q) {
+    NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
+      NOUNROLL for (int q = 0; q < S; ++q) {
         V(x, q) = q == mainsp ? 0.0 : ABSENT;
-        LU(x, q) = 0.0;
-        PIN(x, q) = NOPIN;
+        if (!fast) {
+          LU(x, q) = 0.0;
+          PIN(x, q) = NOPIN;
+        }
       }
       bflags[x] = x == 0 ? (1u << mainsp) : 0u;
     }
@@ -1546,21 +1600,30 @@ struct Engine {
 #endif
     wp.sync();
     if (sm->used[mainsp] > pb.cap[mainsp]) return fail(ST_CAPACITY);
-    if (pb.ordering == ORD_PL) build_ct();
+    const bool pl = pb.ordering == ORD_PL;
+    if (pl) build_ct();
     // initial pool: leaves without predecessors, release 0
     pool_n = 0;
-    for (int base = 0; base < nleaves; base += WP::W) {
+    NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
       bool z = false;
       int j = -1;
+      double key = 0.0;
       if (li < nleaves) {
         j = leaf[li];
-        t_rel[j] = 0.0;
-        t_flag[j] = 0;
-        z = t_missing[j] == 0;
+        TState& st = ts[j];
+        st.rel = 0.0;
+        st.flag = 0;
+        z = st.missing == 0;
+        key = pl ? st.ct : 0.0;
       }
       const unsigned m = wp.ballot(z);
-      if (z) pool[pool_n + popc32(m & wp.lt())] = j;
+      if (z) {
+        const int at = pool_n + popc32(m & wp.lt());
+        pool[at] = j;
+        pool_rel[at] = 0.0;
+        pool_key[at] = key;
+      }
       pool_n += popc32(m);
     }
     wp.sync();
@@ -1569,122 +1632,126 @@ struct Engine {
     int committed = 0;
     bool first = true;
     const bool waits = pb.selection == SEL_RP || pb.selection == SEL_FP;
-    while (committed < nleaves) {
+    NOUNROLL while (committed < nleaves) {
       if (!first) {
         // next epoch (E3): smallest pending release / processor-free time > now
         double nx = ABSENT;
-        for (int k = wp.lane(); k < pool_n; k += WP::W) {
-          const double r = t_rel[pool[k]];
+        NOUNROLL for (int k = wp.lane(); k < pool_n; k += WP::W) {
+          const double r = pool_rel[k];
           if (r > now && r < nx) nx = r;
         }
-        if (waits && wp.lane() < P) {
-          const double f = sm->proc_free[wp.lane()];
-          if (f > now && f < nx) nx = f;
-        }
-#if !defined(__CUDACC__)
-        if (waits)
-          for (int q = 0; q < P; ++q) {
+        if (waits) {
+          NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
             const double f = sm->proc_free[q];
             if (f > now && f < nx) nx = f;
           }
-#endif
+        }
         nx = wp.mind(nx);
         if (nx == ABSENT) return fail(ST_INTERNAL);  // scheduler stalled
         now = nx;
       }
       first = false;
-      // ready = released, uncommitted, rel <= now; ordered (sim.cpp:117-134)
-      int nr = 0;
-      for (int base = 0; base < pool_n; base += WP::W) {
+      // ready = released, uncommitted, rel <= now; ordered (sim.cpp:117-134):
+      // FCFS (rel asc, id asc), PL (ct desc, id asc).  Non-ready entries are
+      // compacted to the front of the pool as we go.
+      int nr = 0, keep = 0;
+      NOUNROLL for (int base = 0; base < pool_n; base += WP::W) {
         const int k = base + wp.lane();
-        bool r = false;
+        bool r = false, kp = false;
         int j = -1;
+        double rl = 0.0, key = 0.0;
         if (k < pool_n) {
           j = pool[k];
-          r = t_rel[j] <= now;
+          rl = pool_rel[k];
+          key = pool_key[k];
+          r = rl <= now;
+          kp = !r;
         }
-        const unsigned m = wp.ballot(r);
-        if (r) gs_a[nr + popc32(m & wp.lt())] = j;
+        const unsigned m = wp.ballot(r), mk = wp.ballot(kp);
+        wp.sync();
+        if (r) {
+          const int at = nr + popc32(m & wp.lt());
+          gs_a[at] = j;
+          ready_key[at] = key;
+          gs_b[at] = k;  // pool slot, to restore uncommitted entries (R-P/F-P)
+        }
+        if (kp) {
+          const int at = keep + popc32(mk & wp.lt());
+          pool[at] = j;
+          pool_rel[at] = rl;
+          pool_key[at] = key;
+        }
         nr += popc32(m);
+        keep += popc32(mk);
+        wp.sync();
       }
-      wp.sync();
+      pool_n = keep;
       if (nr == 0) continue;
-      for (int k = wp.lane(); k < nr; k += WP::W) {
+      NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
         const int a = gs_a[k];
+        const double ka = ready_key[k];
         int rank = 0;
-        const double ka = pb.ordering == ORD_PL ? t_ct[a] : t_rel[a];
-        for (int q = 0; q < nr; ++q) {
+        NOUNROLL for (int q = 0; q < nr; ++q) {
           const int c = gs_a[q];
-          const double kc = pb.ordering == ORD_PL ? t_ct[c] : t_rel[c];
+          const double kc = ready_key[q];
           bool before;
-          if (kc != ka) before = pb.ordering == ORD_PL ? kc > ka : kc < ka;
+          if (kc != ka) before = pl ? kc > ka : kc < ka;
           else before = c < a;
           rank += before;
         }
         ready[rank] = a;
       }
       wp.sync();
-      for (int r = 0; r < nr; ++r) {
-        const int j = ready[r];
+      int done = 0;
+      NOUNROLL for (; done < nr; ++done) {
+        const int j = ready[done];
         const TaskMeta t = task(j);
-        const double rel = t_rel[j];
+        const double rel = ts[j].rel;
+        int w[4];
+        const int nw = working_set(t, w);
         const int lane = wp.lane();
-        const bool idle = lane < P && sm->proc_free[lane] <= now;
-        const unsigned idle_m = wp.ballot(idle);
         int p = -1;
-#if !defined(__CUDACC__)
-        unsigned idle_h = 0;
-        for (int q = 0; q < P; ++q)
-          if (sm->proc_free[q] <= now) idle_h |= 1u << q;
-        (void)idle_m;
-        const unsigned idle_mask = idle_h;
-#else
-        const unsigned idle_mask = idle_m;
-#endif
-        if (waits && idle_mask == 0) break;  // R-P/F-P wait for a processor
-        if (pb.selection == SEL_RP) {
-          const int n = popc32(idle_mask);
-          const double u = (double)(rng_next() >> 11) * 0x1.0p-53;
-          const int k = (int)((unsigned long long)(u * (double)n) % (unsigned long long)n);
-          unsigned mm = idle_mask;
-          for (int q = 0; q < k; ++q) mm &= mm - 1;
-          p = ctz32(mm);
+        if (waits) {
+          unsigned idle_mask = 0;
+          NOUNROLL for (int base = 0; base < P; base += WP::W) {
+            const int q = base + lane;
+            idle_mask |= wp.ballot(q < P && sm->proc_free[q] <= now) << base;
+          }
+          if (idle_mask == 0) break;  // R-P/F-P wait for a processor (sim.cpp:800-801)
+          if (pb.selection == SEL_RP) {
+            const int n = popc32(idle_mask);
+            const double u = (double)(rng_next() >> 11) * 0x1.0p-53;
+            const int k = (int)((unsigned long long)(u * (double)n) % (unsigned long long)n);
+            unsigned mm = idle_mask;
+            for (int q = 0; q < k; ++q) mm &= mm - 1;
+            p = ctz32(mm);
+          } else {  // F-P: fastest idle processor, lowest id
+            double a = ABSENT, b = 0.0;
+            int id = -1;
+            NOUNROLL for (int q = lane; q < P; q += WP::W) {
+              if (!((idle_mask >> q) & 1u)) continue;
+              const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
+              if (id < 0 || tt < a) {
+                a = tt;
+                id = q;
+              }
+            }
+            wp.argmin3(a, b, id);
+            p = id;
+          }
         } else {
-          // per-space EFT transfer estimate (sim.cpp:762-793): depends only on the space
-          if (pb.selection == SEL_EFTP) eft_estimate(t);
+          if (pb.selection == SEL_EFTP) eft_estimate(w, nw);  // per-space transfer estimate
           if (status) return;
           double a = ABSENT, b = 0.0;
           int id = -1;
-#if defined(__CUDACC__)
-          if (lane < P) {
-            const double nf = sm->proc_free[lane];
-            const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[lane]];
-            if (pb.selection == SEL_EFTP) {
-              a = dmax(dmax(nf, rel), sm->est[pb.proc_space[lane]]) + tt;
-              b = nf;
-              id = lane;
-            } else if (pb.selection == SEL_EITP) {
-              a = nf;
-              id = lane;
-            } else if (idle) {  // F-P
-              a = tt;
-              id = lane;
-            }
-          }
-          wp.argmin3(a, b, id);
-#else
-          for (int q = 0; q < P; ++q) {
+          NOUNROLL for (int q = lane; q < P; q += WP::W) {
             const double nf = sm->proc_free[q];
-            const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
             double qa, qb = 0.0;
             if (pb.selection == SEL_EFTP) {
-              qa = dmax(dmax(nf, rel), sm->est[pb.proc_space[q]]) + tt;
+              qa = dmax(dmax(nf, rel), sm->est[pb.proc_space[q]]) + pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
               qb = nf;
-            } else if (pb.selection == SEL_EITP) {
-              qa = nf;
             } else {
-              if (!((idle_mask >> q) & 1u)) continue;
-              qa = tt;
+              qa = nf;  // EIT-P
             }
             if (id < 0 || qa < a || (qa == a && qb < b)) {
               a = qa;
@@ -1692,58 +1759,39 @@ struct Engine {
               id = q;
             }
           }
-#endif
+          wp.argmin3(a, b, id);
           p = id;
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
-        commit(j, p);
+        commit(j, p, t, w, nw, rel);
         if (status) return;
         ++committed;
       }
-      // drop committed entries from the pool
-      int keep = 0;
-      for (int base = 0; base < pool_n; base += WP::W) {
-        const int k = base + wp.lane();
-        int j = -1;
-        bool kp = false;
-        if (k < pool_n) {
-          j = pool[k];
-          kp = t_flag[j] == 0;
+      // R-P/F-P: ready tasks that found no idle processor return to the pool
+      if (done < nr) {
+        NOUNROLL for (int k = done + wp.lane(); k < nr; k += WP::W) {
+          const int j = ready[k];
+          const int at = pool_n + (k - done);
+          pool[at] = j;
+          pool_rel[at] = ts[j].rel;
+          pool_key[at] = pl ? ts[j].ct : ts[j].rel;
         }
-        const unsigned m = wp.ballot(kp);
         wp.sync();
-        if (kp) pool[keep + popc32(m & wp.lt())] = j;
-        keep += popc32(m);
-        wp.sync();
+        pool_n += nr - done;
       }
-      pool_n = keep;
     }
   }
 
-  // est_transfer_ready per memory space for task t (sim.cpp:762-793).
-  HX void eft_estimate(const TaskMeta& t) {
-    int w[4];
-    int nw = 0;
-    for (int k = 0; k <= t.nrd; ++k) {
-      const int b = t.blk[k];
-      bool dup = false;
-      for (int q = 0; q < nw; ++q)
-        if (w[q] == b) dup = true;
-      if (dup) continue;
-      int q = nw++;
-      while (q > 0 && w[q - 1] > b) {
-        w[q] = w[q - 1];
-        --q;
-      }
-      w[q] = b;
-    }
+  // est_transfer_ready per memory space (sim.cpp:762-793).  It depends on the
+  // processor only through its space, so lane q computes space q.
+  HXN void eft_estimate(const int* w, int nw) {
     bool noroute = false;
-    for (int sp = wp.lane(); sp < S; sp += WP::W) {
+    NOUNROLL for (int sp = wp.lane(); sp < S; sp += WP::W) {
       double est = 0.0;
-      int accl[8];
-      double accv[8];
+      int accl[6];
+      double accv[6];
       int na = 0;
-      for (int k = 0; k < nw; ++k) {
+      NOUNROLL for (int k = 0; k < nw; ++k) {
         const int b = w[k];
         const double v = V(b, sp);
         if (v != ABSENT) {
@@ -1759,7 +1807,7 @@ struct Engine {
         }
         const double bytes = (double)bbytes(b);
         double tarr = dmax(now, V(b, src));
-        for (int h = 0; h < nh; ++h) {
+        NOUNROLL for (int h = 0; h < nh; ++h) {
           const int l = pb.route_l[src * MAXS + sp][h];
           int ai = -1;
           for (int z = 0; z < na; ++z)
@@ -1780,12 +1828,13 @@ struct Engine {
     if (wp.any(noroute)) fail(ST_NO_ROUTE);
   }
 
+
   // =========================================================================
   // One candidate, end to end
   // =========================================================================
 
   // Starts from the base tiling (root + base cluster, shared tables).
-  HX void reset_to_base() {
+  HXN void reset_to_base() {
     status = 0;
     ntasks = nbt;
     nblocks = nbb;
@@ -1804,9 +1853,9 @@ struct Engine {
     }
   }
 
-  HX Outcome run(const hesp_cand_desc& d) {
+  HXN Outcome run(const hesp_cand_desc& d) {
     reset_to_base();
-    for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
+    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
     Outcome o;
     o.n_leaves = 0;
     sum_k = 0;

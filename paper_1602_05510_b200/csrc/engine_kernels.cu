@@ -35,8 +35,15 @@ struct WarpBest {
 };
 
 constexpr int WARPS_PER_BLOCK = 4;
+#ifndef HESP_MIN_BLOCKS
+#define HESP_MIN_BLOCKS 8
+#endif
 
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
+__device__ __noinline__ void generate_desc(const Problem& pb, unsigned long long index, hesp_cand_desc* d) {
+  hesp_generate(&pb.gen, (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b, index, d);
+}
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
     eval_kernel(const Problem* __restrict__ pbp, const hesp_cand_desc* __restrict__ descs,
                 unsigned long long first_index, unsigned long long count,
                 hesp_outcome* __restrict__ out, WarpBest* __restrict__ wbest, uint8_t* scratch,
@@ -58,8 +65,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32)
     if (descs) {
       d = descs[k];
     } else {
-      hesp_generate(&pb.gen, pb.s_base == 0 ? 0 : (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b,
-                    first_index + k, &d);
+      generate_desc(pb, first_index + k, &d);
     }
     Engine<DevWarp> eng(DevWarp{}, pb, slot, L, &smem[wib]);
     const Outcome o = eng.run(d);

@@ -56,6 +56,15 @@ struct BlockMeta {
   int32_t pad;
 };
 
+// Per-task simulation state, one 32-byte record (a single sector).
+struct TState {
+  double rel;       // release time = running max of predecessor ends
+  double ct;        // critical time (PL) / best successor ct while building
+  int32_t missing;  // predecessors not yet committed
+  int32_t soff, scnt;  // successor list (CSR)
+  int32_t flag;     // committed
+};
+
 struct PartEntry {
   int32_t task, child0, nchild, leaves;
 };
@@ -108,10 +117,10 @@ struct Outcome {
 
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
-  size_t tm, t_missing, t_rel, t_ct, t_poff, t_pcnt, t_soff, t_scnt, t_flag, leaf;
+  size_t tm, ts, t_poff, t_pcnt, leaf;
   size_t bm, bflags, valid, lastu, pinu;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
-  size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, ready, pbuf;
+  size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;
   size_t total;
 };
@@ -129,14 +138,9 @@ inline SlotLayout slot_layout(const Problem& p) {
   };
   const size_t T = (size_t)p.maxt, B = (size_t)p.maxb, S = (size_t)p.S, NB = (size_t)p.n_base_blocks;
   L.tm = take(sizeof(TaskMeta) * T);
-  L.t_missing = take(4 * T);
-  L.t_rel = take(8 * T);
-  L.t_ct = take(8 * T);
+  L.ts = take(sizeof(TState) * T);
   L.t_poff = take(4 * T);
   L.t_pcnt = take(4 * T);
-  L.t_soff = take(4 * T);
-  L.t_scnt = take(4 * T);
-  L.t_flag = take(T);
   L.leaf = take(4 * T);
   L.bm = take(sizeof(BlockMeta) * B);
   L.bflags = take(4 * B);
@@ -157,7 +161,10 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.preds = take(4 * (size_t)p.maxedges);
   L.succs = take(4 * (size_t)p.maxedges);
   L.pool = take(4 * T);
+  L.pool_rel = take(8 * T);
+  L.pool_key = take(8 * T);
   L.ready = take(4 * T);
+  L.ready_key = take(8 * T);
   L.pbuf = take(4 * (size_t)p.maxpb);
   L.gs_a = take(4 * (size_t)p.maxgs);
   L.gs_b = take(4 * (size_t)p.maxgs);

@@ -15,7 +15,9 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .build import LIB
+from .build import LIB as _DEFAULT_LIB
+
+LIB = os.environ.get("HESP_LIB", _DEFAULT_LIB)
 
 KINDS = {"CHOL": 0, "TRSM": 1, "SYRK": 2, "GEMM": 3}
 ORDERING = {"FCFS": 0, "PL": 1}
