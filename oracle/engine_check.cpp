@@ -160,7 +160,7 @@ int main(int argc, char** argv) {
   hx::HostProblem hp = hx::build_problem(hplat, hmodel, hs, wl);
   hp.p.base_tasks = hp.base_tasks.data();
   hp.p.base_blocks = hp.base_blocks.data();
-  const hx::SlotLayout L = hx::slot_layout(hp.p);
+  const hx::SlotLayout L = hp.p.lay;
   std::vector<uint8_t> slot(L.total);
   hx::Small sm{};
   std::printf("base: tasks %d blocks %d slot %zu bytes, bvals %d\n", hp.p.n_base_tasks,
@@ -173,7 +173,7 @@ int main(int argc, char** argv) {
     hesp_cand_desc d;
     hesp_generate(&gen, (int)(n / hp.p.base_b), hp.p.n_base_leaves, hp.p.base_b, c, &d);
     auto t0 = std::chrono::steady_clock::now();
-    hx::Engine<hx::HostWarp> eng(hx::HostWarp{}, hp.p, slot.data(), L, &sm);
+    hx::Engine<hx::HostWarp> eng(hx::HostWarp{}, hp.p, slot.data(), &sm);
     std::vector<double> tr_s, tr_e;
     std::vector<int> tr_p;
     const hx::Outcome o = eng.run(d);

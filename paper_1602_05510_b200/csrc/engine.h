@@ -174,18 +174,41 @@ struct Engine {
   WP wp;
   const Problem& pb;
   Small* sm;
-  // slot arrays
-  TaskMeta* tm;
-  TState* ts;
-  int32_t *t_poff, *t_pcnt, *leaf;
-  BlockMeta* bm;
-  uint32_t* bflags;  // bits 0-7 mat per space, 8-15 dirty per space, 16 written
-  double *valid, *lastu, *pinu;
-  int32_t *tl_head, *tl_cnt, *tl_boff, *tl_nrb, *tl_ncb, *tl_coff, *tl_ids;
-  int32_t *bnd, *c_writer, *c_rhead, *rnode, *preds, *succs, *pool, *ready, *pbuf;
-  double *pool_rel, *pool_key, *ready_key;
-  int32_t *gs_a, *gs_b;
-  Region *gs_reg, *gs_reg2;
+  // slot arrays: offsets from the (constant-memory) problem, no per-lane pointer copies
+  uint8_t* slot;
+  HX TaskMeta* tm() const { return (TaskMeta*)(slot + pb.lay.tm); }
+  HX TState* ts() const { return (TState*)(slot + pb.lay.ts); }
+  HX int32_t* t_poff() const { return (int32_t*)(slot + pb.lay.t_poff); }
+  HX int32_t* t_pcnt() const { return (int32_t*)(slot + pb.lay.t_pcnt); }
+  HX int32_t* leaf() const { return (int32_t*)(slot + pb.lay.leaf); }
+  HX BlockMeta* bm() const { return (BlockMeta*)(slot + pb.lay.bm); }
+  HX uint32_t* bflags() const { return (uint32_t*)(slot + pb.lay.bflags); }
+  HX double* valid() const { return (double*)(slot + pb.lay.valid); }
+  HX double* lastu() const { return (double*)(slot + pb.lay.lastu); }
+  HX double* pinu() const { return (double*)(slot + pb.lay.pinu); }
+  HX int32_t* tl_head() const { return (int32_t*)(slot + pb.lay.tl_head); }
+  HX int32_t* tl_cnt() const { return (int32_t*)(slot + pb.lay.tl_cnt); }
+  HX int32_t* tl_boff() const { return (int32_t*)(slot + pb.lay.tl_boff); }
+  HX int32_t* tl_nrb() const { return (int32_t*)(slot + pb.lay.tl_nrb); }
+  HX int32_t* tl_ncb() const { return (int32_t*)(slot + pb.lay.tl_ncb); }
+  HX int32_t* tl_coff() const { return (int32_t*)(slot + pb.lay.tl_coff); }
+  HX int32_t* tl_ids() const { return (int32_t*)(slot + pb.lay.tl_ids); }
+  HX int32_t* bnd() const { return (int32_t*)(slot + pb.lay.bnd); }
+  HX int32_t* c_writer() const { return (int32_t*)(slot + pb.lay.c_writer); }
+  HX int32_t* c_rhead() const { return (int32_t*)(slot + pb.lay.c_rhead); }
+  HX int32_t* rnode() const { return (int32_t*)(slot + pb.lay.rnode); }
+  HX int32_t* preds() const { return (int32_t*)(slot + pb.lay.preds); }
+  HX int32_t* succs() const { return (int32_t*)(slot + pb.lay.succs); }
+  HX int32_t* pool() const { return (int32_t*)(slot + pb.lay.pool); }
+  HX double* pool_rel() const { return (double*)(slot + pb.lay.pool_rel); }
+  HX double* pool_key() const { return (double*)(slot + pb.lay.pool_key); }
+  HX double* ready_key() const { return (double*)(slot + pb.lay.ready_key); }
+  HX int32_t* ready() const { return (int32_t*)(slot + pb.lay.ready); }
+  HX int32_t* pbuf() const { return (int32_t*)(slot + pb.lay.pbuf); }
+  HX int32_t* gs_a() const { return (int32_t*)(slot + pb.lay.gs_a); }
+  HX int32_t* gs_b() const { return (int32_t*)(slot + pb.lay.gs_b); }
+  HX Region* gs_reg() const { return (Region*)(slot + pb.lay.gs_reg); }
+  HX Region* gs_reg2() const { return (Region*)(slot + pb.lay.gs_reg2); }
   // scalars (uniform across lanes)
   int32_t status = 0;
   int32_t nbt, nbb;        // base task / block counts (overlay boundary)
@@ -211,41 +234,7 @@ struct Engine {
   double *tr_start = nullptr, *tr_end = nullptr;
   int32_t tr_cap = 0;
 
-  HX Engine(WP w, const Problem& p, uint8_t* slot, const SlotLayout& L, Small* s)
-      : wp(w), pb(p), sm(s) {
-    tm = (TaskMeta*)(slot + L.tm);
-    ts = (TState*)(slot + L.ts);
-    t_poff = (int32_t*)(slot + L.t_poff);
-    t_pcnt = (int32_t*)(slot + L.t_pcnt);
-    leaf = (int32_t*)(slot + L.leaf);
-    bm = (BlockMeta*)(slot + L.bm);
-    bflags = (uint32_t*)(slot + L.bflags);
-    valid = (double*)(slot + L.valid);
-    lastu = (double*)(slot + L.lastu);
-    pinu = (double*)(slot + L.pinu);
-    tl_head = (int32_t*)(slot + L.tl_head);
-    tl_cnt = (int32_t*)(slot + L.tl_cnt);
-    tl_boff = (int32_t*)(slot + L.tl_boff);
-    tl_nrb = (int32_t*)(slot + L.tl_nrb);
-    tl_ncb = (int32_t*)(slot + L.tl_ncb);
-    tl_coff = (int32_t*)(slot + L.tl_coff);
-    tl_ids = (int32_t*)(slot + L.tl_ids);
-    bnd = (int32_t*)(slot + L.bnd);
-    c_writer = (int32_t*)(slot + L.c_writer);
-    c_rhead = (int32_t*)(slot + L.c_rhead);
-    rnode = (int32_t*)(slot + L.rnode);
-    preds = (int32_t*)(slot + L.preds);
-    succs = (int32_t*)(slot + L.succs);
-    pool = (int32_t*)(slot + L.pool);
-    pool_rel = (double*)(slot + L.pool_rel);
-    pool_key = (double*)(slot + L.pool_key);
-    ready_key = (double*)(slot + L.ready_key);
-    ready = (int32_t*)(slot + L.ready);
-    pbuf = (int32_t*)(slot + L.pbuf);
-    gs_a = (int32_t*)(slot + L.gs_a);
-    gs_b = (int32_t*)(slot + L.gs_b);
-    gs_reg = (Region*)(slot + L.gs_reg);
-    gs_reg2 = (Region*)(slot + L.gs_reg2);
+  HX Engine(WP w, const Problem& p, uint8_t* slot_, Small* s) : wp(w), pb(p), sm(s), slot(slot_) {
     nbt = p.n_base_tasks;
     nbb = p.n_base_blocks;
     S = p.S;
@@ -257,17 +246,17 @@ struct Engine {
   }
 
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
-  HX TaskMeta task(int id) const { return id < nbt ? pb.base_tasks[id] : tm[id - nbt]; }
-  HX const BlockMeta& bmeta(int b) const { return b < nbb ? pb.base_blocks[b] : bm[b - nbb]; }
+  HX TaskMeta task(int id) const { return id < nbt ? pb.base_tasks[id] : tm()[id - nbt]; }
+  HX const BlockMeta& bmeta(int b) const { return b < nbb ? pb.base_blocks[b] : bm()[b - nbb]; }
   HX Region reg(int b) const { return bmeta(b).r; }
   HX int tile_of(int b) const { return bmeta(b).tile; }
   HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * pb.elem; }
   HX long long bbytes(int b) const { return rbytes(reg(b)); }
-  HX double& V(int b, int s) { return valid[(size_t)b * S + s]; }
-  HX double& LU(int b, int s) { return lastu[(size_t)b * S + s]; }
-  HX double& PIN(int b, int s) { return pinu[(size_t)b * S + s]; }
-  HX bool is_mat(int b, int s) const { return (bflags[b] >> s) & 1u; }
-  HX bool is_dirty(int b, int s) const { return (bflags[b] >> (8 + s)) & 1u; }
+  HX double& V(int b, int s) { return valid()[(size_t)b * S + s]; }
+  HX double& LU(int b, int s) { return lastu()[(size_t)b * S + s]; }
+  HX double& PIN(int b, int s) { return pinu()[(size_t)b * S + s]; }
+  HX bool is_mat(int b, int s) const { return (bflags()[b] >> s) & 1u; }
+  HX bool is_dirty(int b, int s) const { return (bflags()[b] >> (8 + s)) & 1u; }
   HX int part_index(int task) const {
     NOUNROLL for (int i = 0; i < npart; ++i)
       if (sm->part[i].task == task) return i;
@@ -304,7 +293,7 @@ struct Engine {
     if (rsame(reg(t), r)) return t;
     NOUNROLL for (int base = nbb; base < nblocks; base += WP::W) {
       const int b = base + wp.lane();
-      const bool hit = b < nblocks && bm[b - nbb].tile == t && rsame(bm[b - nbb].r, r);
+      const bool hit = b < nblocks && bm()[b - nbb].tile == t && rsame(bm()[b - nbb].r, r);
       const unsigned m = wp.ballot(hit);
       if (m) return base + ctz32(m);
     }
@@ -323,7 +312,7 @@ struct Engine {
     m.next = -1;
     m.isint = isint ? 1 : 0;
     m.pad = 0;
-    if (wp.lane() == 0) bm[id - nbb] = m;
+    if (wp.lane() == 0) bm()[id - nbb] = m;
     wp.sync();
     return id;
   }
@@ -349,7 +338,7 @@ struct Engine {
       const unsigned m = wp.ballot(hit);
       if (hit) {
         const int slot = nsect + popc32(m & wp.lt());
-        if (slot < pb.maxgs) gs_a[slot] = b;
+        if (slot < pb.maxgs) gs_a()[slot] = b;
       }
       nsect += popc32(m);
     }
@@ -363,7 +352,7 @@ struct Engine {
       return -1;
     }
     NOUNROLL for (int k = 0; k < nsect; ++k) {
-      const Region o = reg(gs_a[k]);
+      const Region o = reg(gs_a()[k]);
       Region sct;
       sct.row = o.row > r.row ? o.row : r.row;
       sct.col = o.col > r.col ? o.col : r.col;
@@ -415,7 +404,7 @@ struct Engine {
     }
     m.bidx = (int8_t)bi;
     const int id = ntasks++;
-    if (wp.lane() == 0) tm[id - nbt] = m;
+    if (wp.lane() == 0) tm()[id - nbt] = m;
     wp.sync();
   }
 
@@ -559,21 +548,21 @@ struct Engine {
   }
 
   // =========================================================================
-  // Post-build indexing: per-tile block lists, leaf program order, deps
+  // Post-build indexing: per-tile block lists, leaf() program order, deps
   // =========================================================================
 
   // Per-tile CSR of the candidate's own blocks (order inside a tile is
   // irrelevant: every consumer is order-independent or sorts).
   HXN void build_tiles() {
-    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt[i] = 0;
+    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt()[i] = 0;
     wp.sync();
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt[bm[b - nbb].tile], 1);
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt()[bm()[b - nbb].tile], 1);
     wp.sync();
     // exclusive scan over base tiles
     int run = 0;
     NOUNROLL for (int base = 0; base < nbb; base += WP::W) {
       const int i = base + wp.lane();
-      const int c = i < nbb ? tl_cnt[i] : 0;
+      const int c = i < nbb ? tl_cnt()[i] : 0;
       int incl = c;
 #if defined(__CUDACC__)
       NOUNROLL for (int o = 1; o < 32; o <<= 1) {
@@ -581,16 +570,16 @@ struct Engine {
         if (wp.lane() >= o) incl += v;
       }
 #endif
-      if (i < nbb) tl_head[i] = run + incl - c;
+      if (i < nbb) tl_head()[i] = run + incl - c;
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
-    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb[i] = 0;  // fill cursor
+    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb()[i] = 0;  // fill cursor
     wp.sync();
     NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
-      const int t = bm[b - nbb].tile;
-      const int pos = wp.atomic_add(&tl_ncb[t], 1);
-      tl_ids[tl_head[t] + pos] = b;
+      const int t = bm()[b - nbb].tile;
+      const int pos = wp.atomic_add(&tl_ncb()[t], 1);
+      tl_ids()[tl_head()[t] + pos] = b;
     }
     wp.sync();
     n_tl_ids = run;
@@ -599,7 +588,7 @@ struct Engine {
   // Leaf program order: lexicographic seq, i.e. depth-first over clusters
   // with members in emission order (graph.cpp:552-562).
   HXN void build_order() {
-    // subtree leaf counts, innermost partitions last in op order
+    // subtree leaf() counts, innermost partitions last in op order
     NOUNROLL for (int i = npart - 1; i >= 0; --i) {
       const PartEntry pe = sm->part[i];
       int cnt = 0;
@@ -614,8 +603,8 @@ struct Engine {
     int sf[MAXPART], sc[MAXPART], sp[MAXPART];
     int top = 0;
     const int r = part_index(0);
-    if (r < 0) {  // unpartitioned root: a single leaf
-      if (wp.lane() == 0) leaf[0] = 0;
+    if (r < 0) {  // unpartitioned root: a single leaf()
+      if (wp.lane() == 0) leaf()[0] = 0;
       wp.sync();
       nleaves = 1;
       return;
@@ -644,7 +633,7 @@ struct Engine {
         }
 #endif
         const int my = pos + incl - sz;
-        if (k < c && pi < 0) leaf[my] = f + k;
+        if (k < c && pi < 0) leaf()[my] = f + k;
         const unsigned m = wp.ballot(k < c && pi >= 0);
         NOUNROLL for (unsigned mm = m; mm; mm &= mm - 1) {
           const int ln = ctz32(mm);
@@ -667,15 +656,15 @@ struct Engine {
   HXN void build_cells() {
     int nb_used = 0, nc_used = 0;
     NOUNROLL for (int t = 1; t < nbb && !status; ++t) {
-      const int cnt = tl_cnt[t];
+      const int cnt = tl_cnt()[t];
       if (cnt == 0) {
         if (wp.lane() == 0) {
-          tl_boff[t] = -1;
-          tl_nrb[t] = 2;
-          tl_ncb[t] = 2;
-          tl_coff[t] = nc_used;
-          c_writer[nc_used] = -1;
-          c_rhead[nc_used] = -1;
+          tl_boff()[t] = -1;
+          tl_nrb()[t] = 2;
+          tl_ncb()[t] = 2;
+          tl_coff()[t] = nc_used;
+          c_writer()[nc_used] = -1;
+          c_rhead()[nc_used] = -1;
         }
         wp.sync();
         ++nc_used;
@@ -685,11 +674,11 @@ struct Engine {
       // candidate boundaries: tile edges + every member's edges (rows, then cols)
       const int nraw = 2 * cnt + 2;
       if (nb_used + 2 * nraw > pb.maxbnd) return fail(ST_ENGINE_LIMIT);
-      int* rows = bnd + nb_used;
+      int* rows = bnd() + nb_used;
       int* cols = rows + nraw;
-      // raw values into gs_a / gs_reg scratch, then rank-unique into place
-      int* raw_r = gs_a;
-      int* raw_c = gs_a + nraw;
+      // raw values into gs_a() / gs_reg() scratch, then rank-unique into place
+      int* raw_r = gs_a();
+      int* raw_c = gs_a() + nraw;
       if (2 * nraw > pb.maxgs) return fail(ST_ENGINE_LIMIT);
       NOUNROLL for (int k = wp.lane(); k < nraw; k += WP::W) {
         int vr, vc;
@@ -697,7 +686,7 @@ struct Engine {
           vr = k == 0 ? tr.row : tr.row + tr.rows;
           vc = k == 0 ? tr.col : tr.col + tr.cols;
         } else {
-          const Region m = reg(tl_ids[tl_head[t] + (k - 2) / 2]);
+          const Region m = reg(tl_ids()[tl_head()[t] + (k - 2) / 2]);
           vr = (k & 1) ? m.row + m.rows : m.row;
           vc = (k & 1) ? m.col + m.cols : m.col;
         }
@@ -731,28 +720,28 @@ struct Engine {
         }
         const unsigned mr = wp.ballot(kr), mc = wp.ballot(kc);
         wp.sync();
-        if (kr) gs_a[nr + popc32(mr & wp.lt())] = vr;
-        if (kc) gs_a[nraw + nc + popc32(mc & wp.lt())] = vc;
+        if (kr) gs_a()[nr + popc32(mr & wp.lt())] = vr;
+        if (kc) gs_a()[nraw + nc + popc32(mc & wp.lt())] = vc;
         nr += popc32(mr);
         nc += popc32(mc);
       }
       wp.sync();
-      NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) rows[k] = gs_a[k];
+      NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) rows[k] = gs_a()[k];
       wp.sync();
       // cols right after the nr distinct rows
-      NOUNROLL for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a[nraw + k];
+      NOUNROLL for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a()[nraw + k];
       wp.sync();
       const int ncell = (nr - 1) * (nc - 1);
       if (nc_used + ncell > pb.maxcells) return fail(ST_ENGINE_LIMIT);
       NOUNROLL for (int k = wp.lane(); k < ncell; k += WP::W) {
-        c_writer[nc_used + k] = -1;
-        c_rhead[nc_used + k] = -1;
+        c_writer()[nc_used + k] = -1;
+        c_rhead()[nc_used + k] = -1;
       }
       if (wp.lane() == 0) {
-        tl_boff[t] = nb_used;
-        tl_nrb[t] = nr;
-        tl_ncb[t] = nc;
-        tl_coff[t] = nc_used;
+        tl_boff()[t] = nb_used;
+        tl_nrb()[t] = nr;
+        tl_ncb()[t] = nc;
+        tl_coff()[t] = nc_used;
       }
       wp.sync();
       nb_used += nr + nc;
@@ -763,15 +752,15 @@ struct Engine {
   // Cell rectangle [r0,r1) x [c0,c1) of block b inside its tile.
   HX void cell_range(int b, int& t, int& r0, int& r1, int& c0, int& c1) {
     t = tile_of(b);
-    const int off = tl_boff[t];
+    const int off = tl_boff()[t];
     if (off < 0) {
       r0 = c0 = 0;
       r1 = c1 = 1;
       return;
     }
-    const int nr = tl_nrb[t], nc = tl_ncb[t];
+    const int nr = tl_nrb()[t], nc = tl_ncb()[t];
     const Region r = reg(b);
-    const int* rows = bnd + off;
+    const int* rows = bnd() + off;
     const int* cols = rows + nr;
     r0 = r1 = c0 = c1 = 0;
     NOUNROLL for (int k = 0; k < nr; ++k) {
@@ -785,13 +774,13 @@ struct Engine {
   }
 
   // Dependences (E2): per cell, last writer + readers since that write.
-  // For each leaf j in program order: reads -> pred last writer, join
-  // readers; writes -> preds last writer and all readers, become writer.
+  // For each leaf() j in program order: reads -> pred last writer, join
+  // readers; writes -> preds() last writer and all readers, become writer.
   HXN void build_deps() {
     int rn_used = 0;
     nedges = 0;
     NOUNROLL for (int li = 0; li < nleaves && !status; ++li) {
-      const int j = leaf[li];
+      const int j = leaf()[li];
       const TaskMeta t = task(j);
       const int wb = t.blk[t.nrd];
       int npb = 0;
@@ -816,21 +805,21 @@ struct Engine {
         const bool writes = (k == t.nrd);
         int tt, r0, r1, c0, c1;
         cell_range(b, tt, r0, r1, c0, c1);
-        const int nc = tl_ncb[tt] - 1;
+        const int nc = tl_ncb()[tt] - 1;
         const int w = c1 - c0;
         const int ncells = (r1 - r0) * w;
-        const int cbase = tl_coff[tt];
+        const int cbase = tl_coff()[tt];
         NOUNROLL for (int base = 0; base < ncells; base += WP::W) {
           const int q = base + wp.lane();
           int cell = -1;
           if (q < ncells) cell = cbase + (r0 + q / w) * nc + (c0 + q % w);
           // last writer
-          int wr = cell >= 0 ? c_writer[cell] : -1;
+          int wr = cell >= 0 ? c_writer()[cell] : -1;
           bool e = wr >= 0 && wr != j;
           unsigned m = wp.ballot(e);
           if (e) {
             const int at = npb + popc32(m & wp.lt());
-            if (at < pb.maxpb) pbuf[at] = wr;
+            if (at < pb.maxpb) pbuf()[at] = wr;
           }
           npb += popc32(m);
           if (!writes) {
@@ -839,49 +828,49 @@ struct Engine {
             if (cell >= 0) {
               const int at = rn_used + popc32(mr & wp.lt());
               if (at < pb.maxrn) {
-                rnode[2 * at] = j;
-                rnode[2 * at + 1] = c_rhead[cell];
-                c_rhead[cell] = at;
+                rnode()[2 * at] = j;
+                rnode()[2 * at + 1] = c_rhead()[cell];
+                c_rhead()[cell] = at;
               }
             }
             rn_used += popc32(mr);
           } else {
             // consume readers (per-lane list walks, lock-stepped emission)
-            int node = cell >= 0 ? c_rhead[cell] : -1;
+            int node = cell >= 0 ? c_rhead()[cell] : -1;
             while (wp.any(node >= 0)) {
               int rd = -1;
               if (node >= 0) {
-                rd = rnode[2 * node];
-                node = rnode[2 * node + 1];
+                rd = rnode()[2 * node];
+                node = rnode()[2 * node + 1];
               }
               const bool ee = rd >= 0 && rd != j;
               const unsigned me = wp.ballot(ee);
               if (ee) {
                 const int at = npb + popc32(me & wp.lt());
-                if (at < pb.maxpb) pbuf[at] = rd;
+                if (at < pb.maxpb) pbuf()[at] = rd;
               }
               npb += popc32(me);
             }
             if (cell >= 0) {
-              c_writer[cell] = j;
-              c_rhead[cell] = -1;
+              c_writer()[cell] = j;
+              c_rhead()[cell] = -1;
             }
           }
           wp.sync();
         }
         if (rn_used > pb.maxrn || npb > pb.maxpb) return fail(ST_ENGINE_LIMIT);
       }
-      // dedup -> preds CSR
+      // dedup -> preds() CSR
       int m = 0;
       NOUNROLL for (int base = 0; base < npb; base += WP::W) {
         const int q = base + wp.lane();
         bool keep = false;
         int v = -1;
         if (q < npb) {
-          v = pbuf[q];
+          v = pbuf()[q];
           keep = true;
           NOUNROLL for (int z = 0; z < q; ++z)
-            if (pbuf[z] == v) {
+            if (pbuf()[z] == v) {
               keep = false;
               break;
             }
@@ -889,29 +878,29 @@ struct Engine {
         const unsigned mk = wp.ballot(keep);
         if (keep) {
           const int at = nedges + m + popc32(mk & wp.lt());
-          if (at < pb.maxedges) preds[at] = v;
+          if (at < pb.maxedges) preds()[at] = v;
         }
         m += popc32(mk);
       }
       if (nedges + m > pb.maxedges) return fail(ST_ENGINE_LIMIT);
       if (wp.lane() == 0) {
-        t_poff[j] = nedges;
-        t_pcnt[j] = m;
-        ts[j].missing = m;
+        t_poff()[j] = nedges;
+        t_pcnt()[j] = m;
+        ts()[j].missing = m;
       }
       wp.sync();
       nedges += m;
     }
     if (status) return;
-    // successors CSR from the preds lists
-    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts[leaf[li]].scnt = 0;
+    // successors CSR from the preds() lists
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].scnt = 0;
     wp.sync();
-    NOUNROLL for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&ts[preds[e]].scnt, 1);
+    NOUNROLL for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&ts()[preds()[e]].scnt, 1);
     wp.sync();
     int run = 0;
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
-      const int c = li < nleaves ? ts[leaf[li]].scnt : 0;
+      const int c = li < nleaves ? ts()[leaf()[li]].scnt : 0;
       int incl = c;
 #if defined(__CUDACC__)
       NOUNROLL for (int o = 1; o < 32; o <<= 1) {
@@ -920,39 +909,39 @@ struct Engine {
       }
 #endif
       if (li < nleaves) {
-        ts[leaf[li]].soff = run + incl - c;
-        ts[leaf[li]].scnt = 0;  // reused as fill cursor
+        ts()[leaf()[li]].soff = run + incl - c;
+        ts()[leaf()[li]].scnt = 0;  // reused as fill cursor
       }
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
     NOUNROLL for (int li = 0; li < nleaves; ++li) {  // fill (per dst; order within a list is irrelevant)
-      const int j = leaf[li];
-      const int off = t_poff[j], cnt = t_pcnt[j];
+      const int j = leaf()[li];
+      const int off = t_poff()[j], cnt = t_pcnt()[j];
       NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
-        const int p = preds[off + q];
-        const int pos = wp.atomic_add(&ts[p].scnt, 1);
-        succs[ts[p].soff + pos] = j;
+        const int p = preds()[off + q];
+        const int pos = wp.atomic_add(&ts()[p].scnt, 1);
+        succs()[ts()[p].soff + pos] = j;
       }
       wp.sync();
     }
   }
 
   // critical_times (sim.cpp:92-115): ct = avg + max(0, max_succ ct), reverse
-  // program order; pushed to preds so each pred sees all its successors.
+  // program order; pushed to preds() so each pred sees all its successors.
   HXN void build_ct() {
-    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts[leaf[li]].rel = 0.0;  // .rel holds best_succ here
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].rel = 0.0;  // .rel holds best_succ here
     wp.sync();
     NOUNROLL for (int li = nleaves - 1; li >= 0; --li) {
-      const int j = leaf[li];
+      const int j = leaf()[li];
       const TaskMeta t = task(j);
-      const double c = pb.ctavg[t.kind][t.bidx] + ts[j].rel;
-      const int off = t_poff[j], cnt = t_pcnt[j];
+      const double c = pb.ctavg[t.kind][t.bidx] + ts()[j].rel;
+      const int off = t_poff()[j], cnt = t_pcnt()[j];
       NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
-        const int p = preds[off + q];
-        ts[p].rel = dmax(ts[p].rel, c);
+        const int p = preds()[off + q];
+        ts()[p].rel = dmax(ts()[p].rel, c);
       }
-      if (wp.lane() == 0) ts[j].ct = c;
+      if (wp.lane() == 0) ts()[j].ct = c;
       wp.sync();
     }
   }
@@ -970,10 +959,10 @@ struct Engine {
       wp.sync();
       return;
     }
-    const int cnt = 2 + tl_cnt[t];
-    const int head = tl_head[t];
+    const int cnt = 2 + tl_cnt()[t];
+    const int head = tl_head()[t];
     NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
-      const int b = k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]);
+      const int b = k == 0 ? 0 : (k == 1 ? t : tl_ids()[head + k - 2]);
       f(b);
     }
     wp.sync();
@@ -1016,8 +1005,8 @@ struct Engine {
   // Scalar state is replicated in every lane: uniform code stores the same
   // value from all lanes (idempotent), so no lane-0 store + __syncwarp.
   HX void set_flag(int b, uint32_t bit, bool on) {
-    const uint32_t f = bflags[b];
-    bflags[b] = on ? (f | bit) : (f & ~bit);
+    const uint32_t f = bflags()[b];
+    bflags()[b] = on ? (f | bit) : (f & ~bit);
   }
   HX void setV(int b, int s, double v) { V(b, s) = v; }
   HX void setLU(int b, int s, double v) { LU(b, s) = v; }
@@ -1033,7 +1022,7 @@ struct Engine {
     return x != 0 && x != t && x != b && rcontains(rb, reg(x));
   }
 
-  // validate_from (sim.cpp:452-461): block and descendants valid at min(., at)
+  // validate_from (sim.cpp:452-461): block and descendants valid() at min(., at)
   HXN void validate_from(int b, int s, double at) {
     const int t = b == 0 ? -1 : tile_of(b);
     const Region rb = reg(b);
@@ -1256,21 +1245,21 @@ struct Engine {
     return nout;
   }
 
-  // gather (sim.cpp:521-572): assemble a block with no whole valid copy.
+  // gather (sim.cpp:521-572): assemble a block with no whole valid() copy.
   HXN double gather(int blk, int s) {
     const Region target = reg(blk);
     const int t = blk == 0 ? -1 : tile_of(blk);
-    // candidate pieces: contained blocks valid here or anywhere
+    // candidate pieces: contained blocks valid() here or anywhere
     int np = 0;
     {
-      const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
-      const int head = t < 0 ? 0 : tl_head[t];
+      const int cnt = t < 0 ? nblocks : 2 + tl_cnt()[t];
+      const int head = t < 0 ? 0 : tl_head()[t];
       NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
         const int k = base + wp.lane();
         int b = -1;
         bool hit = false;
         if (k < cnt) {
-          b = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
+          b = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids()[head + k - 2]));
           if (b != blk && rcontains(target, reg(b))) {
             bool any = false;
             NOUNROLL for (int q = 0; q < S; ++q)
@@ -1281,7 +1270,7 @@ struct Engine {
         const unsigned m = wp.ballot(hit);
         if (hit) {
           const int at = np + popc32(m & wp.lt());
-          if (at < pb.maxgs) gs_a[at] = b;
+          if (at < pb.maxgs) gs_a()[at] = b;
         }
         np += popc32(m);
       }
@@ -1293,13 +1282,13 @@ struct Engine {
     }
     // sort pieces: local first, then area descending, then id (sim.cpp:540-544)
     NOUNROLL for (int k = wp.lane(); k < np; k += WP::W) {
-      const int a = gs_a[k];
+      const int a = gs_a()[k];
       const bool la = V(a, s) != ABSENT;
       const Region ra = reg(a);
       const long long aa = (long long)ra.rows * ra.cols;
       int rank = 0;
       NOUNROLL for (int q = 0; q < np; ++q) {
-        const int c = gs_a[q];
+        const int c = gs_a()[q];
         if (c == a) continue;
         const bool lc = V(c, s) != ABSENT;
         const Region rc = reg(c);
@@ -1310,40 +1299,40 @@ struct Engine {
         else before = c < a;
         rank += before;
       }
-      gs_reg2[rank].row = a;  // stash sorted ids in gs_reg2[].row
+      gs_reg2()[rank].row = a;  // stash sorted ids in gs_reg2()[].row
     }
     wp.sync();
     double arrival = 0.0;
     int ncov = 0;
     NOUNROLL for (int k = 0; k < np; ++k) {
-      const int piece = gs_reg2[k].row;
+      const int piece = gs_reg2()[k].row;
       const Region pr = reg(piece);
-      if (subtract(pr, gs_reg, ncov, nullptr, 0) == 0) {
+      if (subtract(pr, gs_reg(), ncov, nullptr, 0) == 0) {
         if (status) return 0.0;
         continue;  // adds nothing
       }
       bool g;
       const double a = acquire_direct(piece, s, g);
       if (status) return 0.0;
-      if (g) {  // a listed piece is valid somewhere, so this cannot happen
+      if (g) {  // a listed piece is valid() somewhere, so this cannot happen
         fail(ST_ENGINE_INVARIANT);
         return 0.0;
       }
       arrival = dmax(arrival, a);
-      if (wp.lane() == 0) gs_reg[ncov] = pr;
+      if (wp.lane() == 0) gs_reg()[ncov] = pr;
       wp.sync();
       ++ncov;
     }
     // residue from main, unless it overlaps data written since the start
-    const int nfr = subtract(target, gs_reg, ncov, gs_reg2, 1);
+    const int nfr = subtract(target, gs_reg(), ncov, gs_reg2(), 1);
     if (status) return 0.0;
     if (nfr > 0) {
       bool bad = false;
       NOUNROLL for (int f = 0; f < nfr && !bad; ++f) {
-        const Region fr = gs_reg2[f];
+        const Region fr = gs_reg2()[f];
         bool hit = false;
         for_scope(t, [&](int x) {
-          if ((bflags[x] >> 16) & 1u)
+          if ((bflags()[x] >> 16) & 1u)
             if (roverlap(fr, reg(x))) hit = true;
         });
         bad = wp.any(hit);
@@ -1354,7 +1343,7 @@ struct Engine {
       }
       if (s != mainsp)
         NOUNROLL for (int f = 0; f < nfr; ++f) {
-          const Region fr = gs_reg2[f];
+          const Region fr = gs_reg2()[f];
           arrival = dmax(arrival, plan_transfer(blk, &fr, rbytes(fr), mainsp, s, 0.0, now));
           if (status) return 0.0;
         }
@@ -1371,17 +1360,17 @@ struct Engine {
     const Region rb = reg(b);
     long long freed[MAXS];
     NOUNROLL for (int q = 0; q < MAXS; ++q) freed[q] = 0;
-    const int cnt = t < 0 ? nblocks : 2 + tl_cnt[t];
-    const int head = t < 0 ? 0 : tl_head[t];
+    const int cnt = t < 0 ? nblocks : 2 + tl_cnt()[t];
+    const int head = t < 0 ? 0 : tl_head()[t];
     NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
-      const int x = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids[head + k - 2]));
+      const int x = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids()[head + k - 2]));
       const Region rx = reg(x);
       bool in = false;
       if (rcontains(rb, rx) || rcontains(rx, rb)) in = true;
       else if (roverlap(rx, rb)) {
         // partial overlap: in the cone iff some block inside b is strictly inside x
         NOUNROLL for (int q = 0; q < cnt && !in; ++q) {
-          const int c = t < 0 ? q : (q == 0 ? 0 : (q == 1 ? t : tl_ids[head + q - 2]));
+          const int c = t < 0 ? q : (q == 0 ? 0 : (q == 1 ? t : tl_ids()[head + q - 2]));
           const Region rc = reg(c);
           if (c != x && rcontains(rb, rc) && rcontains(rx, rc) && !rsame(rx, rc)) in = true;
         }
@@ -1392,7 +1381,7 @@ struct Engine {
           if (q != ws) V(x, q) = ABSENT;
         continue;
       }
-      uint32_t f = bflags[x];
+      uint32_t f = bflags()[x];
       NOUNROLL for (int q = 0; q < S; ++q) {
         if (q == ws) continue;
         if ((f >> q) & 1u) {
@@ -1402,7 +1391,7 @@ struct Engine {
         V(x, q) = ABSENT;
       }
       const uint32_t keep = (1u << ws) | (1u << (8 + ws)) | (1u << 16);
-      bflags[x] = f & keep;
+      bflags()[x] = f & keep;
     }
     wp.sync();
     if (fast) return;
@@ -1438,11 +1427,11 @@ struct Engine {
 
   // Write coherence of commit (sim.cpp:625-628) in one pass over the scope:
   // invalidate_elsewhere(out, s) over the cone (E1) at task start, then
-  // validate_from(out, s, end) and valid[out] = end.  Both passes touch
+  // validate_from(out, s, end) and valid()[out] = end.  Both passes touch
   // disjoint (block, space) cells except out itself, which ends at `end`.
   HX void write_coherence(int out, int s, double end) {
     const int t = out == 0 ? -1 : tile_of(out);
-    if (t > 0 && tl_cnt[t] == 0) {  // unsubdivided tile: cone = {root, tile}, no descendants
+    if (t > 0 && tl_cnt()[t] == 0) {  // unsubdivided tile: cone = {root, tile}, no descendants
       if (fast) {
         NOUNROLL for (int q = wp.lane(); q < S; q += WP::W)
           if (q != s) {
@@ -1514,7 +1503,7 @@ struct Engine {
           setV(out, s, ABSENT);
           const Region ro = reg(out);
           const int tt = out == 0 ? -1 : tile_of(out);
-          if (!(tt > 0 && tl_cnt[tt] == 0))
+          if (!(tt > 0 && tl_cnt()[tt] == 0))
             for_scope(tt, [&](int x) {
               if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
             });
@@ -1522,9 +1511,9 @@ struct Engine {
       }
     }
     // mark committed, release successors (sim.cpp:660-667); released tasks
-    // enter the pool with their release time and ordering key inline
-    ts[j].flag = 1;
-    const int off = ts[j].soff, cnt = ts[j].scnt;
+    // enter the pool() with their release time and ordering key inline
+    ts()[j].flag = 1;
+    const int off = ts()[j].soff, cnt = ts()[j].scnt;
     int added = 0;
     const bool pl = pb.ordering == ORD_PL;
     NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
@@ -1533,8 +1522,8 @@ struct Engine {
       int sj = -1;
       double r = 0.0, key = 0.0;
       if (q < cnt) {
-        sj = succs[off + q];
-        TState& st = ts[sj];
+        sj = succs()[off + q];
+        TState& st = ts()[sj];
         const int left = --st.missing;
         r = dmax(st.rel, end);
         st.rel = r;
@@ -1544,9 +1533,9 @@ struct Engine {
       const unsigned m = wp.ballot(rl);
       if (rl) {
         const int at = pool_n + added + popc32(m & wp.lt());
-        pool[at] = sj;
-        pool_rel[at] = r;
-        pool_key[at] = key;
+        pool()[at] = sj;
+        pool_rel()[at] = r;
+        pool_key()[at] = key;
       }
       added += popc32(m);
     }
@@ -1563,7 +1552,7 @@ struct Engine {
     // check_models (sim.cpp:312-321)
     bool miss = false;
     NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) {
-      const TaskMeta t = task(leaf[li]);
+      const TaskMeta t = task(leaf()[li]);
       NOUNROLL for (int ty = 0; ty < pb.n_types; ++ty)
         if (!pb.known[t.kind][ty]) miss = true;
     }
@@ -1579,7 +1568,7 @@ struct Engine {
       fast = ok;
     }
     // init_memory (sim.cpp:323-339): root materialised in main, every block
-    // valid in main at t=0 (views into the root data)
+    // valid() in main at t=0 (views into the root data)
     NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
       NOUNROLL for (int q = 0; q < S; ++q) {
         V(x, q) = q == mainsp ? 0.0 : ABSENT;
@@ -1588,7 +1577,7 @@ struct Engine {
           PIN(x, q) = NOPIN;
         }
       }
-      bflags[x] = x == 0 ? (1u << mainsp) : 0u;
+      bflags()[x] = x == 0 ? (1u << mainsp) : 0u;
     }
     if (wp.lane() < MAXS) sm->used[wp.lane()] = wp.lane() == mainsp ? bbytes(0) : 0;
     if (wp.lane() < MAXP) sm->proc_free[wp.lane()] = 0.0;
@@ -1602,7 +1591,7 @@ struct Engine {
     if (sm->used[mainsp] > pb.cap[mainsp]) return fail(ST_CAPACITY);
     const bool pl = pb.ordering == ORD_PL;
     if (pl) build_ct();
-    // initial pool: leaves without predecessors, release 0
+    // initial pool(): leaves without predecessors, release 0
     pool_n = 0;
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
@@ -1610,8 +1599,8 @@ struct Engine {
       int j = -1;
       double key = 0.0;
       if (li < nleaves) {
-        j = leaf[li];
-        TState& st = ts[j];
+        j = leaf()[li];
+        TState& st = ts()[j];
         st.rel = 0.0;
         st.flag = 0;
         z = st.missing == 0;
@@ -1620,9 +1609,9 @@ struct Engine {
       const unsigned m = wp.ballot(z);
       if (z) {
         const int at = pool_n + popc32(m & wp.lt());
-        pool[at] = j;
-        pool_rel[at] = 0.0;
-        pool_key[at] = key;
+        pool()[at] = j;
+        pool_rel()[at] = 0.0;
+        pool_key()[at] = key;
       }
       pool_n += popc32(m);
     }
@@ -1637,7 +1626,7 @@ struct Engine {
         // next epoch (E3): smallest pending release / processor-free time > now
         double nx = ABSENT;
         NOUNROLL for (int k = wp.lane(); k < pool_n; k += WP::W) {
-          const double r = pool_rel[k];
+          const double r = pool_rel()[k];
           if (r > now && r < nx) nx = r;
         }
         if (waits) {
@@ -1651,9 +1640,9 @@ struct Engine {
         now = nx;
       }
       first = false;
-      // ready = released, uncommitted, rel <= now; ordered (sim.cpp:117-134):
-      // FCFS (rel asc, id asc), PL (ct desc, id asc).  Non-ready entries are
-      // compacted to the front of the pool as we go.
+      // ready() = released, uncommitted, rel <= now; ordered (sim.cpp:117-134):
+      // FCFS (rel asc, id asc), PL (ct desc, id asc).  Non-ready() entries are
+      // compacted to the front of the pool() as we go.
       int nr = 0, keep = 0;
       NOUNROLL for (int base = 0; base < pool_n; base += WP::W) {
         const int k = base + wp.lane();
@@ -1661,9 +1650,9 @@ struct Engine {
         int j = -1;
         double rl = 0.0, key = 0.0;
         if (k < pool_n) {
-          j = pool[k];
-          rl = pool_rel[k];
-          key = pool_key[k];
+          j = pool()[k];
+          rl = pool_rel()[k];
+          key = pool_key()[k];
           r = rl <= now;
           kp = !r;
         }
@@ -1671,15 +1660,15 @@ struct Engine {
         wp.sync();
         if (r) {
           const int at = nr + popc32(m & wp.lt());
-          gs_a[at] = j;
-          ready_key[at] = key;
-          gs_b[at] = k;  // pool slot, to restore uncommitted entries (R-P/F-P)
+          gs_a()[at] = j;
+          ready_key()[at] = key;
+          gs_b()[at] = k;  // pool() slot, to restore uncommitted entries (R-P/F-P)
         }
         if (kp) {
           const int at = keep + popc32(mk & wp.lt());
-          pool[at] = j;
-          pool_rel[at] = rl;
-          pool_key[at] = key;
+          pool()[at] = j;
+          pool_rel()[at] = rl;
+          pool_key()[at] = key;
         }
         nr += popc32(m);
         keep += popc32(mk);
@@ -1688,25 +1677,25 @@ struct Engine {
       pool_n = keep;
       if (nr == 0) continue;
       NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
-        const int a = gs_a[k];
-        const double ka = ready_key[k];
+        const int a = gs_a()[k];
+        const double ka = ready_key()[k];
         int rank = 0;
         NOUNROLL for (int q = 0; q < nr; ++q) {
-          const int c = gs_a[q];
-          const double kc = ready_key[q];
+          const int c = gs_a()[q];
+          const double kc = ready_key()[q];
           bool before;
           if (kc != ka) before = pl ? kc > ka : kc < ka;
           else before = c < a;
           rank += before;
         }
-        ready[rank] = a;
+        ready()[rank] = a;
       }
       wp.sync();
       int done = 0;
       NOUNROLL for (; done < nr; ++done) {
-        const int j = ready[done];
+        const int j = ready()[done];
         const TaskMeta t = task(j);
-        const double rel = ts[j].rel;
+        const double rel = ts()[j].rel;
         int w[4];
         const int nw = working_set(t, w);
         const int lane = wp.lane();
@@ -1767,14 +1756,14 @@ struct Engine {
         if (status) return;
         ++committed;
       }
-      // R-P/F-P: ready tasks that found no idle processor return to the pool
+      // R-P/F-P: ready() tasks that found no idle processor return to the pool()
       if (done < nr) {
         NOUNROLL for (int k = done + wp.lane(); k < nr; k += WP::W) {
-          const int j = ready[k];
+          const int j = ready()[k];
           const int at = pool_n + (k - done);
-          pool[at] = j;
-          pool_rel[at] = ts[j].rel;
-          pool_key[at] = pl ? ts[j].ct : ts[j].rel;
+          pool()[at] = j;
+          pool_rel()[at] = ts()[j].rel;
+          pool_key()[at] = pl ? ts()[j].ct : ts()[j].rel;
         }
         wp.sync();
         pool_n += nr - done;

@@ -39,21 +39,27 @@ constexpr int WARPS_PER_BLOCK = 4;
 #define HESP_MIN_BLOCKS 8
 #endif
 
-__device__ __noinline__ void generate_desc(const Problem& pb, unsigned long long index, hesp_cand_desc* d) {
-  hesp_generate(&pb.gen, (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b, index, d);
+// The problem tables live in constant memory: every access is warp-uniform
+// (or nearly: per-lane processor type/space), so they are broadcast from the
+// constant cache instead of occupying L1 next to the per-warp state.
+__constant__ Problem c_problem;
+
+__device__ __noinline__ void generate_desc(unsigned long long index, hesp_cand_desc* d) {
+  hesp_generate(&c_problem.gen, (int)(c_problem.n / c_problem.base_b), c_problem.n_base_leaves, c_problem.base_b,
+                index, d);
 }
 
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
-    eval_kernel(const Problem* __restrict__ pbp, const hesp_cand_desc* __restrict__ descs,
-                unsigned long long first_index, unsigned long long count,
-                hesp_outcome* __restrict__ out, WarpBest* __restrict__ wbest, uint8_t* scratch,
-                SlotLayout L, unsigned long long* counter) {
+    eval_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
+                unsigned long long count, hesp_outcome* __restrict__ out, WarpBest* __restrict__ wbest,
+                uint8_t* scratch, unsigned long long* counter) {
   __shared__ Small smem[WARPS_PER_BLOCK];
+  __shared__ hesp_cand_desc sdesc[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
-  uint8_t* slot = scratch + (size_t)gw * L.total;
-  const Problem& pb = *pbp;
+  const Problem& pb = c_problem;
+  uint8_t* slot = scratch + (size_t)gw * pb.lay.total;
   double best_mk = 0.0;
   long long best_idx = -1, n_ok = 0, n_eval = 0, s_leaves = 0, s_k = 0, s_edges = 0;
   for (;;) {
@@ -61,14 +67,18 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
     if (lane == 0) k = atomicAdd(counter, 1ULL);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= count) break;
-    hesp_cand_desc d;
+    hesp_cand_desc& d = sdesc[wib];
     if (descs) {
-      d = descs[k];
-    } else {
-      generate_desc(pb, first_index + k, &d);
+      const int32_t* src = (const int32_t*)(descs + k);
+      int32_t* dst = (int32_t*)&d;
+      for (int i = lane; i < (int)(sizeof(hesp_cand_desc) / 4); i += 32) dst[i] = src[i];
+    } else if (lane == 0) {
+      generate_desc(first_index + k, &d);
     }
-    Engine<DevWarp> eng(DevWarp{}, pb, slot, L, &smem[wib]);
+    __syncwarp();
+    Engine<DevWarp> eng(DevWarp{}, pb, slot, &smem[wib]);
     const Outcome o = eng.run(d);
+    __syncwarp();
     if (lane == 0 && out) {
       hesp_outcome r;
       r.status = o.status;
@@ -164,26 +174,27 @@ __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* _
   }
 }
 
-__global__ void gen_kernel(const Problem* __restrict__ pbp, unsigned long long first, unsigned long long count,
-                           hesp_cand_desc* __restrict__ out) {
+__global__ void gen_kernel(unsigned long long first, unsigned long long count, hesp_cand_desc* __restrict__ out) {
   const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   if (i >= count) return;
-  const Problem& pb = *pbp;
+  const Problem& pb = c_problem;
   hesp_cand_desc d;
   hesp_generate(&pb.gen, (int)(pb.n / pb.base_b), pb.n_base_leaves, pb.base_b, first + i, &d);
   out[i] = d;
 }
 
-__global__ void detail_kernel(const Problem* __restrict__ pbp, const hesp_cand_desc* __restrict__ desc,
-                              uint8_t* slot, SlotLayout L, int32_t cap, int32_t* proc, double* start,
-                              double* end, hesp_outcome* out) {
+__global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* slot, int32_t cap, int32_t* proc,
+                              double* start, double* end, hesp_outcome* out) {
   __shared__ Small smem;
-  Engine<DevWarp> eng(DevWarp{}, *pbp, slot, L, &smem);
+  __shared__ hesp_cand_desc sd;
+  if (threadIdx.x == 0) sd = *desc;
+  __syncwarp();
+  Engine<DevWarp> eng(DevWarp{}, c_problem, slot, &smem);
   eng.tr_proc = proc;
   eng.tr_start = start;
   eng.tr_end = end;
   eng.tr_cap = cap;
-  const Outcome o = eng.run(*desc);
+  const Outcome o = eng.run(sd);
   if (threadIdx.x == 0) {
     out->status = o.status;
     out->n_leaves = o.n_leaves;
@@ -253,9 +264,12 @@ int launch_eval(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, u
                 hesp_outcome* d_out, cudaStream_t st) {
   if (!ck(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned long long), st), "memset counter"))
     return HESP_E_CUDA;
+  if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
+          "problem -> constant"))
+    return HESP_E_CUDA;
   cudaEventRecord(e->ev0, st);
-  eval_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(e->d_problem, d_descs, first, count, d_out,
-                                                            e->d_wbest, e->d_scratch, e->L, e->d_counter);
+  eval_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs, first, count, d_out, e->d_wbest,
+                                                            e->d_scratch, e->d_counter);
   cudaEventRecord(e->ev1, st);
   reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
   e->launches += 2;
@@ -363,7 +377,8 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   cudaMemcpy(e->d_base_blocks, e->hp.base_blocks.data(), nb * sizeof(BlockMeta), cudaMemcpyHostToDevice);
   p.base_tasks = e->d_base_tasks;
   p.base_blocks = e->d_base_blocks;
-  e->L = slot_layout(p);
+  p.lay = slot_layout(p);
+  e->L = p.lay;
   if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
   cudaMemcpy(e->d_problem, &p, sizeof(Problem), cudaMemcpyHostToDevice);
   if ((c = cudaMalloc(&e->d_scratch, (size_t)e->n_slots * e->L.total)) != cudaSuccess)
@@ -473,7 +488,10 @@ int hesp_generate_device(hesp_engine* e, uint64_t first_index, uint64_t count, h
   cudaSetDevice(e->device);
   cudaStream_t st = stream ? (cudaStream_t)stream : e->stream;
   const unsigned blocks = (unsigned)((count + 255) / 256);
-  if (blocks) gen_kernel<<<blocks, 256, 0, st>>>(e->d_problem, first_index, count, descs_dev);
+  if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
+          "problem -> constant"))
+    return HESP_E_CUDA;
+  if (blocks) gen_kernel<<<blocks, 256, 0, st>>>(first_index, count, descs_dev);
   e->launches += blocks ? 1 : 0;
   return ck(cudaGetLastError(), "gen launch") ? HESP_OK : HESP_E_CUDA;
 }
@@ -495,7 +513,8 @@ int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, in
     cudaMemset(dp, 0xff, n * 4);
     cudaMemset(ds, 0, n * 8);
     cudaMemset(de, 0, n * 8);
-    detail_kernel<<<1, 32, 0, e->stream>>>(e->d_problem, dd, e->d_scratch, e->L, cap, dp, ds, de, dout);
+    cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, e->stream);
+    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, cap, dp, ds, de, dout);
     e->launches += 1;
     ok = ck(cudaStreamSynchronize(e->stream), "detail");
   }

@@ -69,6 +69,16 @@ struct PartEntry {
   int32_t task, child0, nchild, leaves;
 };
 
+// Byte layout of one per-warp slot (all arrays in global memory).
+struct SlotLayout {
+  size_t tm, ts, t_poff, t_pcnt, leaf;
+  size_t bm, bflags, valid, lastu, pinu;
+  size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
+  size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
+  size_t gs_a, gs_b, gs_reg, gs_reg2;
+  size_t total;
+};
+
 struct Problem {
   // ---- platform (platform.hpp:24-86) ----
   int32_t P, S, main_space, n_types, L;
@@ -102,6 +112,8 @@ struct Problem {
   // ---- base graph (shared by every candidate) ----
   const TaskMeta* base_tasks;    // [n_base_tasks]
   const BlockMeta* base_blocks;  // [n_base_blocks]
+  // ---- per-candidate slot layout (byte offsets, identical for every slot) ----
+  SlotLayout lay;
 };
 
 // Per-candidate result record (also the golden-record payload).
@@ -113,16 +125,6 @@ struct Outcome {
   uint64_t xfer_hash;
   int32_t sum_k;    // work counters for the roofline accounting (not part of parity)
   int32_t n_edges;
-};
-
-// Byte layout of one per-warp slot (all arrays in global memory).
-struct SlotLayout {
-  size_t tm, ts, t_poff, t_pcnt, leaf;
-  size_t bm, bflags, valid, lastu, pinu;
-  size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
-  size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
-  size_t gs_a, gs_b, gs_reg, gs_reg2;
-  size_t total;
 };
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

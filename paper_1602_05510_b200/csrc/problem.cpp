@@ -263,17 +263,17 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
     bp.maxedges = 16;
     bp.maxpb = 16;
     bp.maxgs = bp.maxb + 8;
-    const SlotLayout L = slot_layout(bp);
-    std::vector<uint8_t> slot(L.total);
+    bp.lay = slot_layout(bp);
+    std::vector<uint8_t> slot(bp.lay.total);
     Small sm{};
-    Engine<HostWarp> eng(HostWarp{}, bp, slot.data(), L, &sm);
+    Engine<HostWarp> eng(HostWarp{}, bp, slot.data(), &sm);
     eng.reset_to_base();
     eng.apply_op(0, wl.s_base);
     if (eng.status) bad("base tiling failed with status " + std::to_string(eng.status));
     hp.base_tasks.push_back(root_t);
-    for (int id = 1; id < eng.ntasks; ++id) hp.base_tasks.push_back(eng.tm[id - 1]);
+    for (int id = 1; id < eng.ntasks; ++id) hp.base_tasks.push_back(eng.tm()[id - 1]);
     hp.base_blocks.push_back(root_b);
-    for (int id = 1; id < eng.nblocks; ++id) hp.base_blocks.push_back(eng.bm[id - 1]);
+    for (int id = 1; id < eng.nblocks; ++id) hp.base_blocks.push_back(eng.bm()[id - 1]);
   }
   p.n_base_tasks = static_cast<int>(hp.base_tasks.size());
   p.n_base_blocks = static_cast<int>(hp.base_blocks.size());
@@ -293,6 +293,7 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   p.maxedges = 12 * p.maxt;
   p.maxpb = 4096;
   p.maxgs = std::max(p.maxt, 4 * p.maxb + 8);
+  p.lay = slot_layout(p);
   return hp;
 }
 
