@@ -70,6 +70,21 @@ struct HostWarp {
     *p += v;
     return o;
   }
+  // per-lane owned vectors (device: one register per lane; host: the array)
+  struct LaneD {
+    double a[32];
+    double get(int i) const { return a[i]; }
+    void set(int i, double x) { a[i] = x; }
+    double& own(int i) { return a[i]; }
+    void fill(double x) {
+      for (double& v : a) v = x;
+    }
+  };
+  struct LaneI {
+    int a[32];
+    int get(int i) const { return a[i]; }
+    int& own(int i) { return a[i]; }
+  };
 };
 
 #if defined(__CUDACC__)
@@ -123,6 +138,20 @@ struct DevWarp {
     }
   }
   __device__ __forceinline__ int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
+  struct LaneD {
+    double v;
+    __device__ __forceinline__ double get(int i) const { return __shfl_sync(FULL, v, i); }
+    __device__ __forceinline__ void set(int i, double x) {
+      if ((int)(threadIdx.x & 31u) == i) v = x;
+    }
+    __device__ __forceinline__ double& own(int) { return v; }
+    __device__ __forceinline__ void fill(double x) { v = x; }
+  };
+  struct LaneI {
+    int v;
+    __device__ __forceinline__ int get(int i) const { return __shfl_sync(FULL, v, i); }
+    __device__ __forceinline__ int& own(int) { return v; }
+  };
 };
 #endif
 
@@ -1425,126 +1454,128 @@ struct Engine {
     return nw;
   }
 
-  // Write coherence of commit (sim.cpp:625-628) in one pass over the scope:
-  // invalidate_elsewhere(out, s) over the cone (E1) at task start, then
-  // validate_from(out, s, end) and valid()[out] = end.  Both passes touch
-  // disjoint (block, space) cells except out itself, which ends at `end`.
-  HX void write_coherence(int out, int s, double end) {
-    const int t = out == 0 ? -1 : tile_of(out);
-    if (t > 0 && tl_cnt()[t] == 0) {  // unsubdivided tile: cone = {root, tile}, no descendants
-      if (fast) {
-        NOUNROLL for (int q = wp.lane(); q < S; q += WP::W)
-          if (q != s) {
-            V(0, q) = ABSENT;
-            V(out, q) = ABSENT;
-          }
-        wp.sync();
-        V(out, s) = end;
-        return;
-      }
-    }
-    invalidate_elsewhere(out, s);
-    validate_from(out, s, end);
-    setV(out, s, end);
+  using LaneD = typename WP::LaneD;
+  using LaneI = typename WP::LaneI;
+
+  // Link clocks live in lane registers in the hot loop (lane l owns
+  // link_free[l]); cold member paths (gather, eviction flush) use the Small
+  // copy, so they are spilled around those calls.
+  HX void lf_spill(LaneD& lf) {
+    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) sm->link_free[i] = lf.own(i);
+    wp.sync();
+  }
+  HX void lf_load(LaneD& lf) {
+    wp.sync();
+    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) lf.own(i) = sm->link_free[i];
   }
 
-  HXN void commit(int j, int p, const TaskMeta& t, const int* w, int nw, double rel) {  // sim.cpp:592-668
-    const int s = pb.proc_space[p];
-    const int type = pb.proc_type[p];
-    if (!fast) {
-      long long wset = 0;
-      NOUNROLL for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
-      if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+  // plan_transfer (sim.cpp:468-499) on lane-owned link clocks.
+  HX double xfer(LaneD& lf, int blk, long long bytes, int src, int dst, double data_ready, double tnow,
+                 uint64_t& xh) {
+    const int nh = pb.route_n[src * MAXS + dst];
+    if (nh == 0) {
+      fail(ST_NO_ROUTE);
+      return 0.0;
     }
-    double inputs = 0.0;
-    double saved[4];
-    NOUNROLL for (int k = 0; k < nw; ++k) {
-      const double a = acquire(w[k], s);
-      if (status) return;
-      inputs = dmax(inputs, a);
+    double rdy = dmax(data_ready, tnow), start0 = 0.0;
+    NOUNROLL for (int h = 0; h < nh; ++h) {
+      const int l = pb.route_l[src * MAXS + dst][h];
+      const double st = dmax(lf.get(l), rdy);
+      const double en = st + pb.link_lat[l] + (double)bytes / pb.link_bw[l];
+      lf.set(l, en);
+      rdy = en;
+      if (h == 0) start0 = st;
+    }
+    if (!(rdy > tnow)) fail(ST_ENGINE_INVARIANT);
+    xh += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+    return rdy;
+  }
+
+  // validate_from on the hot path: a tile without sub-blocks has no
+  // descendants, so only its own cell changes.
+  HX void validate_hot(int b, int s, double at) {
+    const int t = b == 0 ? -1 : tile_of(b);
+    if (t > 0 && tl_cnt()[t] == 0 && fast) {
+      double& v = V(b, s);
+      if (v > at) v = at;
+      return;
+    }
+    validate_from(b, s, at);
+  }
+
+  // acquire (sim.cpp:501-519) on the hot path.
+  HX double acquire_hot(LaneD& lf, int b, int s, double tnow, uint64_t& xh) {
+    const double v = V(b, s);
+    if (v != ABSENT) {
+      if (!fast) LU(b, s) = dmax(LU(b, s), tnow);
+      return v;
+    }
+    const int src = source_space(b, s);
+    if (src >= 0) {
+      const double rdy = V(b, src);
+      const double arr = xfer(lf, b, bbytes(b), src, s, rdy, tnow, xh);
+      if (status) return 0.0;
       if (!fast) {
-        saved[k] = PIN(w[k], s);
-        setPIN(w[k], s, HOLD);
+        pin(src, b, arr);
+        lf_spill(lf);
+        reserve_bytes(b, s, arr);  // may evict and flush (cold)
+        lf_load(lf);
+        if (status) return 0.0;
       }
+      validate_hot(b, s, arr);
+      return arr;
     }
-    const int out = t.blk[t.nrd];
-    reserve_bytes(out, s, now);
-    if (status) return;
-    const double start = dmax(dmax(sm->proc_free[p], rel), inputs);
-    const double end = start + pb.ttime[t.kind][t.bidx][type];
-    if (!(end > now) || start < now) return fail(ST_ENGINE_INVARIANT);
-    sm->proc_free[p] = end;
-    ahash += hesp_assign_term(j, p, dbits(start), dbits(end));
-    if (tr_proc && j < tr_cap && wp.lane() == 0) {
-      tr_proc[j] = p;
-      tr_start[j] = start;
-      tr_end[j] = end;
-    }
-    makespan = dmax(makespan, end);
-    if (!fast)
-      NOUNROLL for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
-    write_coherence(out, s, end);
-    set_flag(out, 1u << 16, true);
-    if (s != mainsp) {
-      if (pb.caching == CACHE_WB) {
-        if (!fast) set_flag(out, 1u << (8 + s), true);
-      } else {
-        const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
-        if (status) return;
-        pin(s, out, arr);
-        materialize<false>(out, mainsp, arr);
-        if (status) return;
-        if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
-          if (!fast) {
-            set_flag(out, 1u << s, false);
-            add_used(s, -bbytes(out));
-            setLU(out, s, 0.0);
-          }
-          setV(out, s, ABSENT);
-          const Region ro = reg(out);
-          const int tt = out == 0 ? -1 : tile_of(out);
-          if (!(tt > 0 && tl_cnt()[tt] == 0))
-            for_scope(tt, [&](int x) {
-              if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
-            });
+    lf_spill(lf);
+    const double r = gather(b, s);  // cold: assemble from pieces + residue from main
+    lf_load(lf);
+    return r;
+  }
+
+  // est_transfer_ready of the space `sp` this lane computes (sim.cpp:762-793).
+  HX double eft_space(int sp, const int* w, int nw, double tnow, bool& noroute) {
+    double est = 0.0;
+    int accl[6];
+    double accv[6];
+    int na = 0;
+    NOUNROLL for (int k = 0; k < nw; ++k) {
+      const int b = w[k];
+      const double v = V(b, sp);
+      if (v != ABSENT) {
+        est = dmax(est, v);
+        continue;
+      }
+      const int src = source_space(b, sp);
+      if (src < 0) continue;
+      const int nh = pb.route_n[src * MAXS + sp];
+      if (nh == 0) {
+        noroute = true;
+        continue;
+      }
+      const double bytes = (double)bbytes(b);
+      double tarr = dmax(tnow, V(b, src));
+      NOUNROLL for (int h = 0; h < nh; ++h) {
+        const int l = pb.route_l[src * MAXS + sp][h];
+        int ai = -1;
+        for (int z = 0; z < na; ++z)
+          if (accl[z] == l) ai = z;
+        if (ai < 0) {
+          ai = na++;
+          accl[ai] = l;
+          accv[ai] = 0.0;
         }
+        accv[ai] += pb.link_lat[l] + bytes / pb.link_bw[l];
+        tarr += accv[ai];
       }
+      est = dmax(est, tarr);
     }
-    // mark committed, release successors (sim.cpp:660-667); released tasks
-    // enter the pool() with their release time and ordering key inline
-    ts()[j].flag = 1;
-    const int off = ts()[j].soff, cnt = ts()[j].scnt;
-    int added = 0;
-    const bool pl = pb.ordering == ORD_PL;
-    NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
-      const int q = base + wp.lane();
-      bool rl = false;
-      int sj = -1;
-      double r = 0.0, key = 0.0;
-      if (q < cnt) {
-        sj = succs()[off + q];
-        TState& st = ts()[sj];
-        const int left = --st.missing;
-        r = dmax(st.rel, end);
-        st.rel = r;
-        rl = left == 0;
-        if (rl) key = pl ? st.ct : r;
-      }
-      const unsigned m = wp.ballot(rl);
-      if (rl) {
-        const int at = pool_n + added + popc32(m & wp.lt());
-        pool()[at] = sj;
-        pool_rel()[at] = r;
-        pool_key()[at] = key;
-      }
-      added += popc32(m);
-    }
-    wp.sync();
-    pool_n += added;
+    return est;
   }
 
   HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
 
+  // The event loop (sim.cpp:704-834) with Engine::commit (sim.cpp:592-668)
+  // inlined.  Uniform hot state (clock, pool size, hashes, makespan) stays in
+  // registers; lanes own processor and link clocks.
   HXN void simulate() {
     const int P = pb.P;
     if (nleaves == 0) return fail(ST_VALIDATION);
@@ -1568,7 +1599,7 @@ struct Engine {
       fast = ok;
     }
     // init_memory (sim.cpp:323-339): root materialised in main, every block
-    // valid() in main at t=0 (views into the root data)
+    // valid in main at t=0 (views into the root data)
     NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
       NOUNROLL for (int q = 0; q < S; ++q) {
         V(x, q) = q == mainsp ? 0.0 : ABSENT;
@@ -1579,20 +1610,13 @@ struct Engine {
       }
       bflags()[x] = x == 0 ? (1u << mainsp) : 0u;
     }
-    if (wp.lane() < MAXS) sm->used[wp.lane()] = wp.lane() == mainsp ? bbytes(0) : 0;
-    if (wp.lane() < MAXP) sm->proc_free[wp.lane()] = 0.0;
-    if (wp.lane() < MAXL) sm->link_free[wp.lane()] = 0.0;
-#if !defined(__CUDACC__)
-    for (int q = 0; q < MAXS; ++q) sm->used[q] = q == mainsp ? bbytes(0) : 0;
-    for (int q = 0; q < MAXP; ++q) sm->proc_free[q] = 0.0;
-    for (int q = 0; q < MAXL; ++q) sm->link_free[q] = 0.0;
-#endif
+    NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
     wp.sync();
     if (sm->used[mainsp] > pb.cap[mainsp]) return fail(ST_CAPACITY);
     const bool pl = pb.ordering == ORD_PL;
     if (pl) build_ct();
-    // initial pool(): leaves without predecessors, release 0
-    pool_n = 0;
+    // initial pool: leaves without predecessors, release 0
+    int pool_n = 0;
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
       bool z = false;
@@ -1616,33 +1640,51 @@ struct Engine {
       pool_n += popc32(m);
     }
     wp.sync();
+    // lane-owned clocks and processor attributes
+    LaneD pf, lf, est;
+    LaneI ptype, pspace;
+    pf.fill(0.0);
+    lf.fill(0.0);
+    est.fill(0.0);
+    NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) {
+      ptype.own(q) = q < P ? pb.proc_type[q] : 0;
+      pspace.own(q) = q < P ? pb.proc_space[q] : 0;
+    }
     rng = pb.sched_seed;
+    double tnow = 0.0, mk = 0.0;
+    uint64_t ah = 0, xh = 0;
     now = 0.0;
     int committed = 0;
     bool first = true;
-    const bool waits = pb.selection == SEL_RP || pb.selection == SEL_FP;
+    const int sel = pb.selection;
+    const bool waits = sel == SEL_RP || sel == SEL_FP;
+    int* const rdy_ids = gs_a();
+    double* const rdy_key = ready_key();
+    int* const rdy_sorted = ready();
+    TState* const T = ts();
     NOUNROLL while (committed < nleaves) {
       if (!first) {
         // next epoch (E3): smallest pending release / processor-free time > now
         double nx = ABSENT;
         NOUNROLL for (int k = wp.lane(); k < pool_n; k += WP::W) {
           const double r = pool_rel()[k];
-          if (r > now && r < nx) nx = r;
+          if (r > tnow && r < nx) nx = r;
         }
         if (waits) {
           NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
-            const double f = sm->proc_free[q];
-            if (f > now && f < nx) nx = f;
+            const double f = pf.own(q);
+            if (f > tnow && f < nx) nx = f;
           }
         }
         nx = wp.mind(nx);
         if (nx == ABSENT) return fail(ST_INTERNAL);  // scheduler stalled
+        tnow = nx;
         now = nx;
       }
       first = false;
-      // ready() = released, uncommitted, rel <= now; ordered (sim.cpp:117-134):
-      // FCFS (rel asc, id asc), PL (ct desc, id asc).  Non-ready() entries are
-      // compacted to the front of the pool() as we go.
+      // ready = released, uncommitted, rel <= now, ordered FCFS (rel asc, id
+      // asc) or PL (ct desc, id asc) (sim.cpp:117-134); non-ready entries are
+      // compacted to the pool front on the way.
       int nr = 0, keep = 0;
       NOUNROLL for (int base = 0; base < pool_n; base += WP::W) {
         const int k = base + wp.lane();
@@ -1653,170 +1695,243 @@ struct Engine {
           j = pool()[k];
           rl = pool_rel()[k];
           key = pool_key()[k];
-          r = rl <= now;
+          r = rl <= tnow;
           kp = !r;
         }
-        const unsigned m = wp.ballot(r), mk = wp.ballot(kp);
-        wp.sync();
+        const unsigned m = wp.ballot(r), mk2 = wp.ballot(kp);
         if (r) {
           const int at = nr + popc32(m & wp.lt());
-          gs_a()[at] = j;
-          ready_key()[at] = key;
-          gs_b()[at] = k;  // pool() slot, to restore uncommitted entries (R-P/F-P)
+          rdy_ids[at] = j;
+          rdy_key[at] = key;
         }
         if (kp) {
-          const int at = keep + popc32(mk & wp.lt());
+          const int at = keep + popc32(mk2 & wp.lt());
           pool()[at] = j;
           pool_rel()[at] = rl;
           pool_key()[at] = key;
         }
         nr += popc32(m);
-        keep += popc32(mk);
+        keep += popc32(mk2);
         wp.sync();
       }
       pool_n = keep;
       if (nr == 0) continue;
-      NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
-        const int a = gs_a()[k];
-        const double ka = ready_key()[k];
-        int rank = 0;
-        NOUNROLL for (int q = 0; q < nr; ++q) {
-          const int c = gs_a()[q];
-          const double kc = ready_key()[q];
-          bool before;
-          if (kc != ka) before = pl ? kc > ka : kc < ka;
-          else before = c < a;
-          rank += before;
+      if (nr == 1) {
+        rdy_sorted[0] = rdy_ids[0];
+      } else {
+        NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
+          const int a = rdy_ids[k];
+          const double ka = rdy_key[k];
+          int rank = 0;
+          NOUNROLL for (int q = 0; q < nr; ++q) {
+            const int c = rdy_ids[q];
+            const double kc = rdy_key[q];
+            rank += (kc != ka) ? (pl ? kc > ka : kc < ka) : (c < a);
+          }
+          rdy_sorted[rank] = a;
         }
-        ready()[rank] = a;
+        wp.sync();
       }
-      wp.sync();
       int done = 0;
       NOUNROLL for (; done < nr; ++done) {
-        const int j = ready()[done];
+        const int j = rdy_sorted[done];
         const TaskMeta t = task(j);
-        const double rel = ts()[j].rel;
+        const double rel = T[j].rel;
         int w[4];
         const int nw = working_set(t, w);
-        const int lane = wp.lane();
         int p = -1;
+        // ---------------- processor selection (sim.cpp:136-192) ----------------
         if (waits) {
           unsigned idle_mask = 0;
-          NOUNROLL for (int base = 0; base < P; base += WP::W) {
-            const int q = base + lane;
-            idle_mask |= wp.ballot(q < P && sm->proc_free[q] <= now) << base;
-          }
+          NOUNROLL for (int q = wp.lane(); q < P; q += WP::W)
+            if (pf.own(q) <= tnow) idle_mask |= 1u << q;
+#if defined(__CUDACC__)
+          idle_mask = __reduce_or_sync(0xffffffffu, idle_mask);
+#endif
           if (idle_mask == 0) break;  // R-P/F-P wait for a processor (sim.cpp:800-801)
-          if (pb.selection == SEL_RP) {
+          if (sel == SEL_RP) {
             const int n = popc32(idle_mask);
             const double u = (double)(rng_next() >> 11) * 0x1.0p-53;
             const int k = (int)((unsigned long long)(u * (double)n) % (unsigned long long)n);
-            unsigned mm = idle_mask;
-            for (int q = 0; q < k; ++q) mm &= mm - 1;
-            p = ctz32(mm);
+            unsigned mmm = idle_mask;
+            for (int q = 0; q < k; ++q) mmm &= mmm - 1;
+            p = ctz32(mmm);
           } else {  // F-P: fastest idle processor, lowest id
-            double a = ABSENT, b = 0.0;
+            double a = ABSENT, b2 = 0.0;
             int id = -1;
-            NOUNROLL for (int q = lane; q < P; q += WP::W) {
+            NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
               if (!((idle_mask >> q) & 1u)) continue;
-              const double tt = pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
+              const double tt = pb.ttime[t.kind][t.bidx][ptype.own(q)];
               if (id < 0 || tt < a) {
                 a = tt;
                 id = q;
               }
             }
-            wp.argmin3(a, b, id);
+            wp.argmin3(a, b2, id);
             p = id;
           }
         } else {
-          if (pb.selection == SEL_EFTP) eft_estimate(w, nw);  // per-space transfer estimate
-          if (status) return;
-          double a = ABSENT, b = 0.0;
+          if (sel == SEL_EFTP) {
+            bool noroute = false;
+            NOUNROLL for (int sp = wp.lane(); sp < S; sp += WP::W) est.own(sp) = eft_space(sp, w, nw, tnow, noroute);
+            if (wp.any(noroute)) return fail(ST_NO_ROUTE);
+          }
+          double a = ABSENT, b2 = 0.0;
           int id = -1;
-          NOUNROLL for (int q = lane; q < P; q += WP::W) {
-            const double nf = sm->proc_free[q];
+          NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
+            const double nf = pf.own(q);
             double qa, qb = 0.0;
-            if (pb.selection == SEL_EFTP) {
-              qa = dmax(dmax(nf, rel), sm->est[pb.proc_space[q]]) + pb.ttime[t.kind][t.bidx][pb.proc_type[q]];
+            if (sel == SEL_EFTP) {
+              qa = dmax(dmax(nf, rel), est.get(pspace.own(q))) + pb.ttime[t.kind][t.bidx][ptype.own(q)];
               qb = nf;
             } else {
               qa = nf;  // EIT-P
             }
-            if (id < 0 || qa < a || (qa == a && qb < b)) {
+            if (id < 0 || qa < a || (qa == a && qb < b2)) {
               a = qa;
-              b = qb;
+              b2 = qb;
               id = q;
             }
           }
-          wp.argmin3(a, b, id);
+          wp.argmin3(a, b2, id);
           p = id;
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
-        commit(j, p, t, w, nw, rel);
-        if (status) return;
+        // ---------------- commit (sim.cpp:592-668) ----------------
+        const int s = pb.proc_space[p];
+        const int type = pb.proc_type[p];
+        if (!fast) {
+          long long wset = 0;
+          NOUNROLL for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
+          if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+        }
+        double inputs = 0.0;
+        double saved[4];
+        NOUNROLL for (int k = 0; k < nw; ++k) {
+          const double a = acquire_hot(lf, w[k], s, tnow, xh);
+          if (status) return;
+          inputs = dmax(inputs, a);
+          if (!fast) {
+            saved[k] = PIN(w[k], s);
+            setPIN(w[k], s, HOLD);
+          }
+        }
+        const int out = t.blk[t.nrd];
+        if (!fast) {
+          lf_spill(lf);
+          reserve_bytes(out, s, tnow);
+          lf_load(lf);
+          if (status) return;
+        }
+        const double start = dmax(dmax(pf.get(p), rel), inputs);
+        const double end = start + pb.ttime[t.kind][t.bidx][type];
+        if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
+        pf.set(p, end);
+        ah += hesp_assign_term(j, p, dbits(start), dbits(end));
+        if (tr_proc && j < tr_cap && wp.lane() == 0) {
+          tr_proc[j] = p;
+          tr_start[j] = start;
+          tr_end[j] = end;
+        }
+        mk = dmax(mk, end);
+        if (!fast)
+          NOUNROLL for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
+        // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
+        // validate out and its descendants here, valid[out] = end
+        {
+          const int tt = out == 0 ? -1 : tile_of(out);
+          if (fast && tt > 0 && tl_cnt()[tt] == 0) {  // cone = {root, tile}, no descendants
+            NOUNROLL for (int q = wp.lane(); q < S; q += WP::W)
+              if (q != s) {
+                V(0, q) = ABSENT;
+                V(out, q) = ABSENT;
+              }
+            wp.sync();
+          } else {
+            invalidate_elsewhere(out, s);
+            validate_from(out, s, end);
+          }
+          V(out, s) = end;
+        }
+        set_flag(out, 1u << 16, true);
+        if (s != mainsp) {
+          if (pb.caching == CACHE_WB) {
+            if (!fast) set_flag(out, 1u << (8 + s), true);
+          } else {
+            const double arr = xfer(lf, out, bbytes(out), s, mainsp, end, tnow, xh);
+            if (status) return;
+            pin(s, out, arr);
+            if (!fast) {
+              reserve_bytes<false>(out, mainsp, arr);
+              if (status) return;
+            }
+            validate_hot(out, mainsp, arr);
+            if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
+              if (!fast) {
+                set_flag(out, 1u << s, false);
+                add_used(s, -bbytes(out));
+                setLU(out, s, 0.0);
+              }
+              V(out, s) = ABSENT;
+              const int tt = out == 0 ? -1 : tile_of(out);
+              if (!(tt > 0 && tl_cnt()[tt] == 0)) {
+                const Region ro = reg(out);
+                for_scope(tt, [&](int x) {
+                  if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
+                });
+              }
+            }
+          }
+        }
+        // release successors (sim.cpp:660-667): running max of pred ends;
+        // released tasks enter the pool with release time and key inline
+        T[j].flag = 1;
+        const int off = T[j].soff, cnt = T[j].scnt;
+        int added = 0;
+        NOUNROLL for (int base = 0; base < cnt; base += WP::W) {
+          const int q = base + wp.lane();
+          bool rl = false;
+          int sj = -1;
+          double r = 0.0, key = 0.0;
+          if (q < cnt) {
+            sj = succs()[off + q];
+            TState& st = T[sj];
+            const int left = --st.missing;
+            r = dmax(st.rel, end);
+            st.rel = r;
+            rl = left == 0;
+            if (rl) key = pl ? st.ct : r;
+          }
+          const unsigned m = wp.ballot(rl);
+          if (rl) {
+            const int at = pool_n + added + popc32(m & wp.lt());
+            pool()[at] = sj;
+            pool_rel()[at] = r;
+            pool_key()[at] = key;
+          }
+          added += popc32(m);
+        }
+        wp.sync();
+        pool_n += added;
         ++committed;
       }
-      // R-P/F-P: ready() tasks that found no idle processor return to the pool()
+      // R-P/F-P: ready tasks that found no idle processor return to the pool
       if (done < nr) {
         NOUNROLL for (int k = done + wp.lane(); k < nr; k += WP::W) {
-          const int j = ready()[k];
+          const int j = rdy_sorted[k];
           const int at = pool_n + (k - done);
           pool()[at] = j;
-          pool_rel()[at] = ts()[j].rel;
-          pool_key()[at] = pl ? ts()[j].ct : ts()[j].rel;
+          pool_rel()[at] = T[j].rel;
+          pool_key()[at] = pl ? T[j].ct : T[j].rel;
         }
         wp.sync();
         pool_n += nr - done;
       }
     }
+    makespan = mk;
+    ahash += ah;
+    xhash += xh;
   }
-
-  // est_transfer_ready per memory space (sim.cpp:762-793).  It depends on the
-  // processor only through its space, so lane q computes space q.
-  HXN void eft_estimate(const int* w, int nw) {
-    bool noroute = false;
-    NOUNROLL for (int sp = wp.lane(); sp < S; sp += WP::W) {
-      double est = 0.0;
-      int accl[6];
-      double accv[6];
-      int na = 0;
-      NOUNROLL for (int k = 0; k < nw; ++k) {
-        const int b = w[k];
-        const double v = V(b, sp);
-        if (v != ABSENT) {
-          est = dmax(est, v);
-          continue;
-        }
-        const int src = source_space(b, sp);
-        if (src < 0) continue;
-        const int nh = pb.route_n[src * MAXS + sp];
-        if (nh == 0) {
-          noroute = true;
-          continue;
-        }
-        const double bytes = (double)bbytes(b);
-        double tarr = dmax(now, V(b, src));
-        NOUNROLL for (int h = 0; h < nh; ++h) {
-          const int l = pb.route_l[src * MAXS + sp][h];
-          int ai = -1;
-          for (int z = 0; z < na; ++z)
-            if (accl[z] == l) ai = z;
-          if (ai < 0) {
-            ai = na++;
-            accl[ai] = l;
-            accv[ai] = 0.0;
-          }
-          accv[ai] += pb.link_lat[l] + bytes / pb.link_bw[l];
-          tarr += accv[ai];
-        }
-        est = dmax(est, tarr);
-      }
-      sm->est[sp] = est;
-    }
-    wp.sync();
-    if (wp.any(noroute)) fail(ST_NO_ROUTE);
-  }
-
 
   // =========================================================================
   // One candidate, end to end
