@@ -41,6 +41,16 @@
 
 namespace hx {
 
+#if defined(__CUDACC__)
+// The device problem lives in constant memory (engine_kernels.cu uploads it
+// before every launch); device code names it statically so no lane ever
+// loads a problem pointer from its local stack.
+__constant__ Problem c_problem;
+#define PB ::hx::c_problem
+#else
+#define PB (*pbp)
+#endif
+
 constexpr double ABSENT = 1.0e308;  // "no valid copy" / "no pin"
 constexpr double NOPIN = -1.0;
 constexpr double HOLD = 1.0e307;    // pinned for the commit in progress
@@ -78,6 +88,10 @@ struct HostWarp {
     double& own(int i) { return a[i]; }
     void fill(double x) {
       for (double& v : a) v = x;
+    }
+    template <class I>
+    void gather(const LaneD& src, const I& idx) {  // a[i] = src[idx[i]]
+      for (int i = 0; i < 32; ++i) a[i] = src.a[idx.a[i]];
     }
   };
   struct LaneI {
@@ -146,6 +160,10 @@ struct DevWarp {
     }
     __device__ __forceinline__ double& own(int) { return v; }
     __device__ __forceinline__ void fill(double x) { v = x; }
+    template <class I>
+    __device__ __forceinline__ void gather(const LaneD& src, const I& idx) {  // all lanes must call
+      v = __shfl_sync(FULL, src.v, idx.v & 31);
+    }
   };
   struct LaneI {
     int v;
@@ -201,43 +219,43 @@ struct Small {
 template <class WP>
 struct Engine {
   WP wp;
-  const Problem& pb;
+  const Problem* pbp;
   Small* sm;
   // slot arrays: offsets from the (constant-memory) problem, no per-lane pointer copies
   uint8_t* slot;
-  HX TaskMeta* tm() const { return (TaskMeta*)(slot + pb.lay.tm); }
-  HX TState* ts() const { return (TState*)(slot + pb.lay.ts); }
-  HX int32_t* t_poff() const { return (int32_t*)(slot + pb.lay.t_poff); }
-  HX int32_t* t_pcnt() const { return (int32_t*)(slot + pb.lay.t_pcnt); }
-  HX int32_t* leaf() const { return (int32_t*)(slot + pb.lay.leaf); }
-  HX BlockMeta* bm() const { return (BlockMeta*)(slot + pb.lay.bm); }
-  HX uint32_t* bflags() const { return (uint32_t*)(slot + pb.lay.bflags); }
-  HX double* valid() const { return (double*)(slot + pb.lay.valid); }
-  HX double* lastu() const { return (double*)(slot + pb.lay.lastu); }
-  HX double* pinu() const { return (double*)(slot + pb.lay.pinu); }
-  HX int32_t* tl_head() const { return (int32_t*)(slot + pb.lay.tl_head); }
-  HX int32_t* tl_cnt() const { return (int32_t*)(slot + pb.lay.tl_cnt); }
-  HX int32_t* tl_boff() const { return (int32_t*)(slot + pb.lay.tl_boff); }
-  HX int32_t* tl_nrb() const { return (int32_t*)(slot + pb.lay.tl_nrb); }
-  HX int32_t* tl_ncb() const { return (int32_t*)(slot + pb.lay.tl_ncb); }
-  HX int32_t* tl_coff() const { return (int32_t*)(slot + pb.lay.tl_coff); }
-  HX int32_t* tl_ids() const { return (int32_t*)(slot + pb.lay.tl_ids); }
-  HX int32_t* bnd() const { return (int32_t*)(slot + pb.lay.bnd); }
-  HX int32_t* c_writer() const { return (int32_t*)(slot + pb.lay.c_writer); }
-  HX int32_t* c_rhead() const { return (int32_t*)(slot + pb.lay.c_rhead); }
-  HX int32_t* rnode() const { return (int32_t*)(slot + pb.lay.rnode); }
-  HX int32_t* preds() const { return (int32_t*)(slot + pb.lay.preds); }
-  HX int32_t* succs() const { return (int32_t*)(slot + pb.lay.succs); }
-  HX int32_t* pool() const { return (int32_t*)(slot + pb.lay.pool); }
-  HX double* pool_rel() const { return (double*)(slot + pb.lay.pool_rel); }
-  HX double* pool_key() const { return (double*)(slot + pb.lay.pool_key); }
-  HX double* ready_key() const { return (double*)(slot + pb.lay.ready_key); }
-  HX int32_t* ready() const { return (int32_t*)(slot + pb.lay.ready); }
-  HX int32_t* pbuf() const { return (int32_t*)(slot + pb.lay.pbuf); }
-  HX int32_t* gs_a() const { return (int32_t*)(slot + pb.lay.gs_a); }
-  HX int32_t* gs_b() const { return (int32_t*)(slot + pb.lay.gs_b); }
-  HX Region* gs_reg() const { return (Region*)(slot + pb.lay.gs_reg); }
-  HX Region* gs_reg2() const { return (Region*)(slot + pb.lay.gs_reg2); }
+  HX TaskMeta* tm() const { return (TaskMeta*)(slot + PB.lay.tm); }
+  HX TState* ts() const { return (TState*)(slot + PB.lay.ts); }
+  HX int32_t* t_poff() const { return (int32_t*)(slot + PB.lay.t_poff); }
+  HX int32_t* t_pcnt() const { return (int32_t*)(slot + PB.lay.t_pcnt); }
+  HX int32_t* leaf() const { return (int32_t*)(slot + PB.lay.leaf); }
+  HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
+  HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
+  HX double* valid() const { return (double*)(slot + PB.lay.valid); }
+  HX double* lastu() const { return (double*)(slot + PB.lay.lastu); }
+  HX double* pinu() const { return (double*)(slot + PB.lay.pinu); }
+  HX int32_t* tl_head() const { return (int32_t*)(slot + PB.lay.tl_head); }
+  HX int32_t* tl_cnt() const { return (int32_t*)(slot + PB.lay.tl_cnt); }
+  HX int32_t* tl_boff() const { return (int32_t*)(slot + PB.lay.tl_boff); }
+  HX int32_t* tl_nrb() const { return (int32_t*)(slot + PB.lay.tl_nrb); }
+  HX int32_t* tl_ncb() const { return (int32_t*)(slot + PB.lay.tl_ncb); }
+  HX int32_t* tl_coff() const { return (int32_t*)(slot + PB.lay.tl_coff); }
+  HX int32_t* tl_ids() const { return (int32_t*)(slot + PB.lay.tl_ids); }
+  HX int32_t* bnd() const { return (int32_t*)(slot + PB.lay.bnd); }
+  HX int32_t* c_writer() const { return (int32_t*)(slot + PB.lay.c_writer); }
+  HX int32_t* c_rhead() const { return (int32_t*)(slot + PB.lay.c_rhead); }
+  HX int32_t* rnode() const { return (int32_t*)(slot + PB.lay.rnode); }
+  HX int32_t* preds() const { return (int32_t*)(slot + PB.lay.preds); }
+  HX int32_t* succs() const { return (int32_t*)(slot + PB.lay.succs); }
+  HX int32_t* pool() const { return (int32_t*)(slot + PB.lay.pool); }
+  HX double* pool_rel() const { return (double*)(slot + PB.lay.pool_rel); }
+  HX double* pool_key() const { return (double*)(slot + PB.lay.pool_key); }
+  HX double* ready_key() const { return (double*)(slot + PB.lay.ready_key); }
+  HX int32_t* ready() const { return (int32_t*)(slot + PB.lay.ready); }
+  HX int32_t* pbuf() const { return (int32_t*)(slot + PB.lay.pbuf); }
+  HX int32_t* gs_a() const { return (int32_t*)(slot + PB.lay.gs_a); }
+  HX int32_t* gs_b() const { return (int32_t*)(slot + PB.lay.gs_b); }
+  HX Region* gs_reg() const { return (Region*)(slot + PB.lay.gs_reg); }
+  HX Region* gs_reg2() const { return (Region*)(slot + PB.lay.gs_reg2); }
   // scalars (uniform across lanes)
   int32_t status = 0;
   int32_t nbt, nbb;        // base task / block counts (overlay boundary)
@@ -263,7 +281,7 @@ struct Engine {
   double *tr_start = nullptr, *tr_end = nullptr;
   int32_t tr_cap = 0;
 
-  HX Engine(WP w, const Problem& p, uint8_t* slot_, Small* s) : wp(w), pb(p), sm(s), slot(slot_) {
+  HX Engine(WP w, const Problem& p, uint8_t* slot_, Small* s) : wp(w), pbp(&p), sm(s), slot(slot_) {
     nbt = p.n_base_tasks;
     nbb = p.n_base_blocks;
     S = p.S;
@@ -275,11 +293,11 @@ struct Engine {
   }
 
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
-  HX TaskMeta task(int id) const { return id < nbt ? pb.base_tasks[id] : tm()[id - nbt]; }
-  HX const BlockMeta& bmeta(int b) const { return b < nbb ? pb.base_blocks[b] : bm()[b - nbb]; }
+  HX TaskMeta task(int id) const { return id < nbt ? PB.base_tasks[id] : tm()[id - nbt]; }
+  HX const BlockMeta& bmeta(int b) const { return b < nbb ? PB.base_blocks[b] : bm()[b - nbb]; }
   HX Region reg(int b) const { return bmeta(b).r; }
   HX int tile_of(int b) const { return bmeta(b).tile; }
-  HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * pb.elem; }
+  HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * PB.elem; }
   HX long long bbytes(int b) const { return rbytes(reg(b)); }
   HX double& V(int b, int s) { return valid()[(size_t)b * S + s]; }
   HX double& LU(int b, int s) { return lastu()[(size_t)b * S + s]; }
@@ -292,8 +310,8 @@ struct Engine {
     return -1;
   }
   HX int bidx_of(long long b) const {
-    NOUNROLL for (int i = 0; i < pb.nbv; ++i)
-      if (pb.bval[i] == b) return i;
+    NOUNROLL for (int i = 0; i < PB.nbv; ++i)
+      if (PB.bval[i] == b) return i;
     return -1;
   }
 
@@ -330,7 +348,7 @@ struct Engine {
   }
 
   HXN int create_block(const Region& r, bool isint, int t) {  // DataDag::create, graph.cpp:142-189
-    if (nblocks >= pb.maxb) {
+    if (nblocks >= PB.maxb) {
       fail(ST_ENGINE_LIMIT);
       return -1;
     }
@@ -367,12 +385,12 @@ struct Engine {
       const unsigned m = wp.ballot(hit);
       if (hit) {
         const int slot = nsect + popc32(m & wp.lt());
-        if (slot < pb.maxgs) gs_a()[slot] = b;
+        if (slot < PB.maxgs) gs_a()[slot] = b;
       }
       nsect += popc32(m);
     }
     wp.sync();
-    if (nsect > pb.maxgs) {
+    if (nsect > PB.maxgs) {
       fail(ST_ENGINE_LIMIT);
       return -1;
     }
@@ -410,7 +428,7 @@ struct Engine {
   // One emitted sub-task: resolve its regions to blocks (reads in spec order,
   // then the write: graph.cpp:500-501) and append it with the next task id.
   HXN void emit(int kind, int nr, const Region* rr, const int* rt, const Region& w, int wt) {
-    if (ntasks >= pb.maxt) {
+    if (ntasks >= PB.maxt) {
       fail(ST_ENGINE_LIMIT);
       return;
     }
@@ -445,7 +463,7 @@ struct Engine {
     const double p = 1.0 / (double)s_req;
     if (!(p > 0.0 && p < 1.0)) return fail(ST_VALIDATION);
     const TaskMeta t = task(task_id);
-    const int s = (int)hesp_snap_tiles(t.b, s_req, pb.min_block);
+    const int s = (int)hesp_snap_tiles(t.b, s_req, PB.min_block);
     if (s == 0) return fail(ST_INDIVISIBLE);
     if (npart >= MAXPART) return fail(ST_ENGINE_LIMIT);
     // operands = reads minus writes, in read order; write = writes.front()
@@ -702,13 +720,13 @@ struct Engine {
       const Region tr = reg(t);
       // candidate boundaries: tile edges + every member's edges (rows, then cols)
       const int nraw = 2 * cnt + 2;
-      if (nb_used + 2 * nraw > pb.maxbnd) return fail(ST_ENGINE_LIMIT);
+      if (nb_used + 2 * nraw > PB.maxbnd) return fail(ST_ENGINE_LIMIT);
       int* rows = bnd() + nb_used;
       int* cols = rows + nraw;
       // raw values into gs_a() / gs_reg() scratch, then rank-unique into place
       int* raw_r = gs_a();
       int* raw_c = gs_a() + nraw;
-      if (2 * nraw > pb.maxgs) return fail(ST_ENGINE_LIMIT);
+      if (2 * nraw > PB.maxgs) return fail(ST_ENGINE_LIMIT);
       NOUNROLL for (int k = wp.lane(); k < nraw; k += WP::W) {
         int vr, vc;
         if (k < 2) {
@@ -761,7 +779,7 @@ struct Engine {
       NOUNROLL for (int k = wp.lane(); k < nc; k += WP::W) rows[nr + k] = gs_a()[nraw + k];
       wp.sync();
       const int ncell = (nr - 1) * (nc - 1);
-      if (nc_used + ncell > pb.maxcells) return fail(ST_ENGINE_LIMIT);
+      if (nc_used + ncell > PB.maxcells) return fail(ST_ENGINE_LIMIT);
       NOUNROLL for (int k = wp.lane(); k < ncell; k += WP::W) {
         c_writer()[nc_used + k] = -1;
         c_rhead()[nc_used + k] = -1;
@@ -848,7 +866,7 @@ struct Engine {
           unsigned m = wp.ballot(e);
           if (e) {
             const int at = npb + popc32(m & wp.lt());
-            if (at < pb.maxpb) pbuf()[at] = wr;
+            if (at < PB.maxpb) pbuf()[at] = wr;
           }
           npb += popc32(m);
           if (!writes) {
@@ -856,7 +874,7 @@ struct Engine {
             unsigned mr = wp.ballot(cell >= 0);
             if (cell >= 0) {
               const int at = rn_used + popc32(mr & wp.lt());
-              if (at < pb.maxrn) {
+              if (at < PB.maxrn) {
                 rnode()[2 * at] = j;
                 rnode()[2 * at + 1] = c_rhead()[cell];
                 c_rhead()[cell] = at;
@@ -876,7 +894,7 @@ struct Engine {
               const unsigned me = wp.ballot(ee);
               if (ee) {
                 const int at = npb + popc32(me & wp.lt());
-                if (at < pb.maxpb) pbuf()[at] = rd;
+                if (at < PB.maxpb) pbuf()[at] = rd;
               }
               npb += popc32(me);
             }
@@ -887,7 +905,7 @@ struct Engine {
           }
           wp.sync();
         }
-        if (rn_used > pb.maxrn || npb > pb.maxpb) return fail(ST_ENGINE_LIMIT);
+        if (rn_used > PB.maxrn || npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
       }
       // dedup -> preds() CSR
       int m = 0;
@@ -907,11 +925,11 @@ struct Engine {
         const unsigned mk = wp.ballot(keep);
         if (keep) {
           const int at = nedges + m + popc32(mk & wp.lt());
-          if (at < pb.maxedges) preds()[at] = v;
+          if (at < PB.maxedges) preds()[at] = v;
         }
         m += popc32(mk);
       }
-      if (nedges + m > pb.maxedges) return fail(ST_ENGINE_LIMIT);
+      if (nedges + m > PB.maxedges) return fail(ST_ENGINE_LIMIT);
       if (wp.lane() == 0) {
         t_poff()[j] = nedges;
         t_pcnt()[j] = m;
@@ -964,7 +982,7 @@ struct Engine {
     NOUNROLL for (int li = nleaves - 1; li >= 0; --li) {
       const int j = leaf()[li];
       const TaskMeta t = task(j);
-      const double c = pb.ctavg[t.kind][t.bidx] + ts()[j].rel;
+      const double c = PB.ctavg[t.kind][t.bidx] + ts()[j].rel;
       const int off = t_poff()[j], cnt = t_pcnt()[j];
       NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
         const int p = preds()[off + q];
@@ -1007,7 +1025,7 @@ struct Engine {
   // Engine::plan_transfer (sim.cpp:468-499): FIFO per directed link.
   HXN double plan_transfer(int blk, const Region* frag, long long bytes, int src, int dst,
                           double data_ready, double tnow) {
-    const int nh = pb.route_n[src * MAXS + dst];
+    const int nh = PB.route_n[src * MAXS + dst];
     if (nh == 0) {
       fail(ST_NO_ROUTE);
       return 0.0;
@@ -1015,9 +1033,9 @@ struct Engine {
     double rdy = dmax(data_ready, tnow);
     double start0 = 0.0;
     NOUNROLL for (int h = 0; h < nh; ++h) {
-      const int l = pb.route_l[src * MAXS + dst][h];
+      const int l = PB.route_l[src * MAXS + dst][h];
       const double st = dmax(sm->link_free[l], rdy);
-      const double en = st + pb.link_lat[l] + (double)bytes / pb.link_bw[l];
+      const double en = st + PB.link_lat[l] + (double)bytes / PB.link_bw[l];
       sm->link_free[l] = en;
       rdy = en;
       if (h == 0) start0 = st;
@@ -1070,7 +1088,7 @@ struct Engine {
   // instance: no device recursion, no call stack.
   template <bool FLUSH>
   HXN void ensure_capacity(int s, long long bytes, double at) {
-    const long long cap = pb.cap[s];
+    const long long cap = PB.cap[s];
     if (bytes > cap) return fail(ST_CAPACITY);
     while (sm->used[s] + bytes > cap) {
       // LRU victim: min (stamp, id) among unpinned materialised blocks
@@ -1245,7 +1263,7 @@ struct Engine {
         if (covered) {
           if (have) {
             if (mode == 0) return 1;
-            if (nout >= pb.maxgs) {
+            if (nout >= PB.maxgs) {
               fail(ST_ENGINE_LIMIT);
               return 0;
             }
@@ -1262,7 +1280,7 @@ struct Engine {
       }
       if (have) {
         if (mode == 0) return 1;
-        if (nout >= pb.maxgs) {
+        if (nout >= PB.maxgs) {
           fail(ST_ENGINE_LIMIT);
           return 0;
         }
@@ -1299,12 +1317,12 @@ struct Engine {
         const unsigned m = wp.ballot(hit);
         if (hit) {
           const int at = np + popc32(m & wp.lt());
-          if (at < pb.maxgs) gs_a()[at] = b;
+          if (at < PB.maxgs) gs_a()[at] = b;
         }
         np += popc32(m);
       }
       wp.sync();
-      if (np > pb.maxgs) {
+      if (np > PB.maxgs) {
         fail(ST_ENGINE_LIMIT);
         return 0.0;
       }
@@ -1469,123 +1487,27 @@ struct Engine {
     NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) lf.own(i) = sm->link_free[i];
   }
 
-  // plan_transfer (sim.cpp:468-499) on lane-owned link clocks.
-  HX double xfer(LaneD& lf, int blk, long long bytes, int src, int dst, double data_ready, double tnow,
-                 uint64_t& xh) {
-    const int nh = pb.route_n[src * MAXS + dst];
-    if (nh == 0) {
-      fail(ST_NO_ROUTE);
-      return 0.0;
-    }
-    double rdy = dmax(data_ready, tnow), start0 = 0.0;
-    NOUNROLL for (int h = 0; h < nh; ++h) {
-      const int l = pb.route_l[src * MAXS + dst][h];
-      const double st = dmax(lf.get(l), rdy);
-      const double en = st + pb.link_lat[l] + (double)bytes / pb.link_bw[l];
-      lf.set(l, en);
-      rdy = en;
-      if (h == 0) start0 = st;
-    }
-    if (!(rdy > tnow)) fail(ST_ENGINE_INVARIANT);
-    xh += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
-    return rdy;
-  }
 
-  // validate_from on the hot path: a tile without sub-blocks has no
-  // descendants, so only its own cell changes.
-  HX void validate_hot(int b, int s, double at) {
-    const int t = b == 0 ? -1 : tile_of(b);
-    if (t > 0 && tl_cnt()[t] == 0 && fast) {
-      double& v = V(b, s);
-      if (v > at) v = at;
-      return;
-    }
-    validate_from(b, s, at);
-  }
 
-  // acquire (sim.cpp:501-519) on the hot path.
-  HX double acquire_hot(LaneD& lf, int b, int s, double tnow, uint64_t& xh) {
-    const double v = V(b, s);
-    if (v != ABSENT) {
-      if (!fast) LU(b, s) = dmax(LU(b, s), tnow);
-      return v;
-    }
-    const int src = source_space(b, s);
-    if (src >= 0) {
-      const double rdy = V(b, src);
-      const double arr = xfer(lf, b, bbytes(b), src, s, rdy, tnow, xh);
-      if (status) return 0.0;
-      if (!fast) {
-        pin(src, b, arr);
-        lf_spill(lf);
-        reserve_bytes(b, s, arr);  // may evict and flush (cold)
-        lf_load(lf);
-        if (status) return 0.0;
-      }
-      validate_hot(b, s, arr);
-      return arr;
-    }
-    lf_spill(lf);
-    const double r = gather(b, s);  // cold: assemble from pieces + residue from main
-    lf_load(lf);
-    return r;
-  }
 
-  // est_transfer_ready of the space `sp` this lane computes (sim.cpp:762-793).
-  HX double eft_space(int sp, const int* w, int nw, double tnow, bool& noroute) {
-    double est = 0.0;
-    int accl[6];
-    double accv[6];
-    int na = 0;
-    NOUNROLL for (int k = 0; k < nw; ++k) {
-      const int b = w[k];
-      const double v = V(b, sp);
-      if (v != ABSENT) {
-        est = dmax(est, v);
-        continue;
-      }
-      const int src = source_space(b, sp);
-      if (src < 0) continue;
-      const int nh = pb.route_n[src * MAXS + sp];
-      if (nh == 0) {
-        noroute = true;
-        continue;
-      }
-      const double bytes = (double)bbytes(b);
-      double tarr = dmax(tnow, V(b, src));
-      NOUNROLL for (int h = 0; h < nh; ++h) {
-        const int l = pb.route_l[src * MAXS + sp][h];
-        int ai = -1;
-        for (int z = 0; z < na; ++z)
-          if (accl[z] == l) ai = z;
-        if (ai < 0) {
-          ai = na++;
-          accl[ai] = l;
-          accv[ai] = 0.0;
-        }
-        accv[ai] += pb.link_lat[l] + bytes / pb.link_bw[l];
-        tarr += accv[ai];
-      }
-      est = dmax(est, tarr);
-    }
-    return est;
-  }
 
   HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
 
   // The event loop (sim.cpp:704-834) with Engine::commit (sim.cpp:592-668)
-  // inlined.  Uniform hot state (clock, pool size, hashes, makespan) stays in
-  // registers; lanes own processor and link clocks.
+  // inlined.  Everything the loop touches per task -- array bases, clocks,
+  // pool size, hashes, makespan -- is copied into registers first (lanes own
+  // processor and link clocks); `this` is only touched by the cold paths
+  // (gather, eviction bookkeeping, coherence over subdivided tiles).
   HXN void simulate() {
-    const int P = pb.P;
+    const int P = PB.P;
     if (nleaves == 0) return fail(ST_VALIDATION);
     if (P < 1) return fail(ST_NO_PROCESSORS);
     // check_models (sim.cpp:312-321)
     bool miss = false;
     NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) {
       const TaskMeta t = task(leaf()[li]);
-      NOUNROLL for (int ty = 0; ty < pb.n_types; ++ty)
-        if (!pb.known[t.kind][ty]) miss = true;
+      NOUNROLL for (int ty = 0; ty < PB.n_types; ++ty)
+        if (!PB.known[t.kind][ty]) miss = true;
     }
     if (wp.any(miss)) return fail(ST_MODEL_MISS);
     // E4: can any space ever need to evict?  (root only ever lives in main)
@@ -1595,7 +1517,7 @@ struct Engine {
       nonroot = wp.suml(nonroot);
       bool ok = true;
       NOUNROLL for (int q = 0; q < S; ++q)
-        if (nonroot + (q == mainsp ? bbytes(0) : 0) > pb.cap[q]) ok = false;
+        if (nonroot + (q == mainsp ? bbytes(0) : 0) > PB.cap[q]) ok = false;
       fast = ok;
     }
     // init_memory (sim.cpp:323-339): root materialised in main, every block
@@ -1612,19 +1534,58 @@ struct Engine {
     }
     NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
     wp.sync();
-    if (sm->used[mainsp] > pb.cap[mainsp]) return fail(ST_CAPACITY);
-    const bool pl = pb.ordering == ORD_PL;
+    if (sm->used[mainsp] > PB.cap[mainsp]) return fail(ST_CAPACITY);
+    const bool pl = PB.ordering == ORD_PL;
     if (pl) build_ct();
+    if (status) return;
+
+    // ---------------- register copies for the hot loop ----------------
+    uint8_t* const sl = slot;
+    double* const VV = (double*)(sl + PB.lay.valid);
+    TState* const T = (TState*)(sl + PB.lay.ts);
+    const int* const SU = (const int*)(sl + PB.lay.succs);
+    const int* const LF = (const int*)(sl + PB.lay.leaf);
+    int* const PO = (int*)(sl + PB.lay.pool);
+    double* const PR = (double*)(sl + PB.lay.pool_rel);
+    double* const PK = (double*)(sl + PB.lay.pool_key);
+    int* const RI = (int*)(sl + PB.lay.gs_a);
+    double* const RK = (double*)(sl + PB.lay.ready_key);
+    int* const RS = (int*)(sl + PB.lay.ready);
+    const int* const TLC = (const int*)(sl + PB.lay.tl_cnt);
+    uint32_t* const BF = (uint32_t*)(sl + PB.lay.bflags);
+    const TaskMeta* const TM = (const TaskMeta*)(sl + PB.lay.tm);
+    const BlockMeta* const BM = (const BlockMeta*)(sl + PB.lay.bm);
+    const TaskMeta* const BT = PB.base_tasks;
+    const BlockMeta* const BB = PB.base_blocks;
+    const int nbt_ = nbt, nbb_ = nbb, S_ = S, ms = mainsp, nl = nleaves, elem = PB.elem;
+    const bool fst = fast;
+    const int sel = PB.selection;
+    const bool waits = sel == SEL_RP || sel == SEL_FP;
+    auto Vr = [&](int b, int s) -> double& { return VV[(size_t)b * S_ + s]; };
+    auto taskm = [&](int id) -> TaskMeta { return id < nbt_ ? BT[id] : TM[id - nbt_]; };
+    auto tileof = [&](int b) -> int { return b < nbb_ ? BB[b].tile : BM[b - nbb_].tile; };
+    auto bytesof = [&](int b) -> long long {
+      const Region r = b < nbb_ ? BB[b].r : BM[b - nbb_].r;
+      return (long long)r.rows * r.cols * elem;
+    };
+    // source_spaces().front() minus `excl` (sim.cpp:341-350): main first, then id order
+    auto srcsp = [&](int b, int excl) -> int {
+      if (ms != excl && Vr(b, ms) != ABSENT) return ms;
+      NOUNROLL for (int q = 0; q < S_; ++q)
+        if (q != ms && q != excl && Vr(b, q) != ABSENT) return q;
+      return -1;
+    };
+
     // initial pool: leaves without predecessors, release 0
     int pool_n = 0;
-    NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
+    NOUNROLL for (int base = 0; base < nl; base += WP::W) {
       const int li = base + wp.lane();
       bool z = false;
       int j = -1;
       double key = 0.0;
-      if (li < nleaves) {
-        j = leaf()[li];
-        TState& st = ts()[j];
+      if (li < nl) {
+        j = LF[li];
+        TState& st = T[j];
         st.rel = 0.0;
         st.flag = 0;
         z = st.missing == 0;
@@ -1633,41 +1594,149 @@ struct Engine {
       const unsigned m = wp.ballot(z);
       if (z) {
         const int at = pool_n + popc32(m & wp.lt());
-        pool()[at] = j;
-        pool_rel()[at] = 0.0;
-        pool_key()[at] = key;
+        PO[at] = j;
+        PR[at] = 0.0;
+        PK[at] = key;
       }
       pool_n += popc32(m);
     }
     wp.sync();
     // lane-owned clocks and processor attributes
-    LaneD pf, lf, est;
+    LaneD pf, lf, est, estp;
     LaneI ptype, pspace;
     pf.fill(0.0);
     lf.fill(0.0);
     est.fill(0.0);
+    estp.fill(0.0);
     NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) {
-      ptype.own(q) = q < P ? pb.proc_type[q] : 0;
-      pspace.own(q) = q < P ? pb.proc_space[q] : 0;
+      ptype.own(q) = q < P ? PB.proc_type[q] : 0;
+      pspace.own(q) = q < P ? PB.proc_space[q] : 0;
     }
-    rng = pb.sched_seed;
+    rng = PB.sched_seed;
     double tnow = 0.0, mk = 0.0;
     uint64_t ah = 0, xh = 0;
+    int st = 0;  // status mirror for the hot loop
     now = 0.0;
+
+    // plan_transfer (sim.cpp:468-499) on lane-owned link clocks
+    auto xfer = [&](int blk, long long nbytes, int src, int dst, double data_ready) -> double {
+      const int nh = PB.route_n[src * MAXS + dst];
+      if (nh == 0) {
+        st = ST_NO_ROUTE;
+        return 0.0;
+      }
+      double rdy = dmax(data_ready, tnow), start0 = 0.0;
+      NOUNROLL for (int h = 0; h < nh; ++h) {
+        const int l = PB.route_l[src * MAXS + dst][h];
+        const double s0 = dmax(lf.get(l), rdy);
+        const double en = s0 + PB.link_lat[l] + (double)nbytes / PB.link_bw[l];
+        lf.set(l, en);
+        rdy = en;
+        if (h == 0) start0 = s0;
+      }
+      if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
+      xh += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      return rdy;
+    };
+    // cold-call bracket: hand the uniform hot state to the member paths and back
+    auto cold_in = [&]() {
+      lf_spill(lf);
+      xhash += xh;
+      xh = 0;
+      status = st;
+    };
+    auto cold_out = [&]() {
+      lf_load(lf);
+      st = status;
+    };
+    // validate_from on the hot path: an unsubdivided tile has no descendants
+    auto validate = [&](int b, int s, double at) {
+      const int tt = b == 0 ? -1 : tileof(b);
+      if (fst && tt > 0 && TLC[tt] == 0) {
+        double& v = Vr(b, s);
+        if (v > at) v = at;
+      } else {
+        validate_from(b, s, at);
+      }
+    };
+    // acquire (sim.cpp:501-519)
+    auto acquire_h = [&](int b, int s) -> double {
+      const double v = Vr(b, s);
+      if (v != ABSENT) {
+        if (!fst) LU(b, s) = dmax(LU(b, s), tnow);
+        return v;
+      }
+      const int src = srcsp(b, s);
+      if (src >= 0) {
+        const double arr = xfer(b, bytesof(b), src, s, Vr(b, src));
+        if (st) return 0.0;
+        if (!fst) {
+          pin(src, b, arr);
+          cold_in();
+          reserve_bytes(b, s, arr);  // may evict and flush
+          cold_out();
+          if (st) return 0.0;
+        }
+        validate(b, s, arr);
+        return arr;
+      }
+      cold_in();
+      const double r = gather(b, s);  // assemble from pieces + residue from main
+      cold_out();
+      return r;
+    };
+    // est_transfer_ready of space sp (sim.cpp:762-793).  The per-link
+    // accumulators (`acc` map, fresh per processor) have at most 3 blocks x
+    // 2 hops = 6 distinct keys: kept in unrolled register slots.
+    auto eft_space_h = [&](int sp, const int* w, int nw, bool& noroute) -> double {
+      double est_ = 0.0;
+      int al[6] = {-1, -1, -1, -1, -1, -1};
+      double av[6] = {0, 0, 0, 0, 0, 0};
+      NOUNROLL for (int k = 0; k < nw; ++k) {
+        const int b = w[k];
+        const double v = Vr(b, sp);
+        if (v != ABSENT) {
+          est_ = dmax(est_, v);
+          continue;
+        }
+        const int src = srcsp(b, sp);
+        if (src < 0) continue;
+        const int nh = PB.route_n[src * MAXS + sp];
+        if (nh == 0) {
+          noroute = true;
+          continue;
+        }
+        const double nbytes = (double)bytesof(b);
+        double tarr = dmax(tnow, Vr(b, src));
+        NOUNROLL for (int h = 0; h < nh; ++h) {
+          const int l = PB.route_l[src * MAXS + sp][h];
+          const double hop = PB.link_lat[l] + nbytes / PB.link_bw[l];
+          double acc = 0.0;
+          bool placed = false;
+#pragma unroll
+          for (int z = 0; z < 6; ++z) {
+            if (!placed && (al[z] == l || al[z] < 0)) {
+              al[z] = l;
+              av[z] += hop;
+              acc = av[z];
+              placed = true;
+            }
+          }
+          tarr += acc;
+        }
+        est_ = dmax(est_, tarr);
+      }
+      return est_;
+    };
+
     int committed = 0;
     bool first = true;
-    const int sel = pb.selection;
-    const bool waits = sel == SEL_RP || sel == SEL_FP;
-    int* const rdy_ids = gs_a();
-    double* const rdy_key = ready_key();
-    int* const rdy_sorted = ready();
-    TState* const T = ts();
-    NOUNROLL while (committed < nleaves) {
+    NOUNROLL while (committed < nl) {
       if (!first) {
         // next epoch (E3): smallest pending release / processor-free time > now
         double nx = ABSENT;
         NOUNROLL for (int k = wp.lane(); k < pool_n; k += WP::W) {
-          const double r = pool_rel()[k];
+          const double r = PR[k];
           if (r > tnow && r < nx) nx = r;
         }
         if (waits) {
@@ -1692,23 +1761,23 @@ struct Engine {
         int j = -1;
         double rl = 0.0, key = 0.0;
         if (k < pool_n) {
-          j = pool()[k];
-          rl = pool_rel()[k];
-          key = pool_key()[k];
+          j = PO[k];
+          rl = PR[k];
+          key = PK[k];
           r = rl <= tnow;
           kp = !r;
         }
         const unsigned m = wp.ballot(r), mk2 = wp.ballot(kp);
         if (r) {
           const int at = nr + popc32(m & wp.lt());
-          rdy_ids[at] = j;
-          rdy_key[at] = key;
+          RI[at] = j;
+          RK[at] = key;
         }
         if (kp) {
           const int at = keep + popc32(mk2 & wp.lt());
-          pool()[at] = j;
-          pool_rel()[at] = rl;
-          pool_key()[at] = key;
+          PO[at] = j;
+          PR[at] = rl;
+          PK[at] = key;
         }
         nr += popc32(m);
         keep += popc32(mk2);
@@ -1717,25 +1786,25 @@ struct Engine {
       pool_n = keep;
       if (nr == 0) continue;
       if (nr == 1) {
-        rdy_sorted[0] = rdy_ids[0];
+        RS[0] = RI[0];
       } else {
         NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
-          const int a = rdy_ids[k];
-          const double ka = rdy_key[k];
+          const int a = RI[k];
+          const double ka = RK[k];
           int rank = 0;
           NOUNROLL for (int q = 0; q < nr; ++q) {
-            const int c = rdy_ids[q];
-            const double kc = rdy_key[q];
+            const int c = RI[q];
+            const double kc = RK[q];
             rank += (kc != ka) ? (pl ? kc > ka : kc < ka) : (c < a);
           }
-          rdy_sorted[rank] = a;
+          RS[rank] = a;
         }
         wp.sync();
       }
       int done = 0;
       NOUNROLL for (; done < nr; ++done) {
-        const int j = rdy_sorted[done];
-        const TaskMeta t = task(j);
+        const int j = RS[done];
+        const TaskMeta t = taskm(j);
         const double rel = T[j].rel;
         int w[4];
         const int nw = working_set(t, w);
@@ -1761,7 +1830,7 @@ struct Engine {
             int id = -1;
             NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
               if (!((idle_mask >> q) & 1u)) continue;
-              const double tt = pb.ttime[t.kind][t.bidx][ptype.own(q)];
+              const double tt = PB.ttime[t.kind][t.bidx][ptype.own(q)];
               if (id < 0 || tt < a) {
                 a = tt;
                 id = q;
@@ -1773,8 +1842,9 @@ struct Engine {
         } else {
           if (sel == SEL_EFTP) {
             bool noroute = false;
-            NOUNROLL for (int sp = wp.lane(); sp < S; sp += WP::W) est.own(sp) = eft_space(sp, w, nw, tnow, noroute);
+            NOUNROLL for (int sp = wp.lane(); sp < S_; sp += WP::W) est.own(sp) = eft_space_h(sp, w, nw, noroute);
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
+            estp.gather(est, pspace);  // estimate of each processor's space
           }
           double a = ABSENT, b2 = 0.0;
           int id = -1;
@@ -1782,7 +1852,7 @@ struct Engine {
             const double nf = pf.own(q);
             double qa, qb = 0.0;
             if (sel == SEL_EFTP) {
-              qa = dmax(dmax(nf, rel), est.get(pspace.own(q))) + pb.ttime[t.kind][t.bidx][ptype.own(q)];
+              qa = dmax(dmax(nf, rel), estp.own(q)) + PB.ttime[t.kind][t.bidx][ptype.own(q)];
               qb = nf;
             } else {
               qa = nf;  // EIT-P
@@ -1798,33 +1868,33 @@ struct Engine {
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
         // ---------------- commit (sim.cpp:592-668) ----------------
-        const int s = pb.proc_space[p];
-        const int type = pb.proc_type[p];
-        if (!fast) {
+        const int s = PB.proc_space[p];
+        const int type = PB.proc_type[p];
+        if (!fst) {
           long long wset = 0;
-          NOUNROLL for (int k = 0; k < nw; ++k) wset += bbytes(w[k]);
-          if (wset > pb.cap[s]) return fail(ST_CAPACITY);
+          NOUNROLL for (int k = 0; k < nw; ++k) wset += bytesof(w[k]);
+          if (wset > PB.cap[s]) return fail(ST_CAPACITY);
         }
         double inputs = 0.0;
         double saved[4];
         NOUNROLL for (int k = 0; k < nw; ++k) {
-          const double a = acquire_hot(lf, w[k], s, tnow, xh);
-          if (status) return;
+          const double a = acquire_h(w[k], s);
+          if (st) return fail(st);
           inputs = dmax(inputs, a);
-          if (!fast) {
+          if (!fst) {
             saved[k] = PIN(w[k], s);
             setPIN(w[k], s, HOLD);
           }
         }
         const int out = t.blk[t.nrd];
-        if (!fast) {
-          lf_spill(lf);
+        if (!fst) {
+          cold_in();
           reserve_bytes(out, s, tnow);
-          lf_load(lf);
-          if (status) return;
+          cold_out();
+          if (st) return fail(st);
         }
         const double start = dmax(dmax(pf.get(p), rel), inputs);
-        const double end = start + pb.ttime[t.kind][t.bidx][type];
+        const double end = start + PB.ttime[t.kind][t.bidx][type];
         if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
         pf.set(p, end);
         ah += hesp_assign_term(j, p, dbits(start), dbits(end));
@@ -1834,47 +1904,47 @@ struct Engine {
           tr_end[j] = end;
         }
         mk = dmax(mk, end);
-        if (!fast)
+        if (!fst)
           NOUNROLL for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
         // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
         // validate out and its descendants here, valid[out] = end
         {
-          const int tt = out == 0 ? -1 : tile_of(out);
-          if (fast && tt > 0 && tl_cnt()[tt] == 0) {  // cone = {root, tile}, no descendants
-            NOUNROLL for (int q = wp.lane(); q < S; q += WP::W)
+          const int tt = out == 0 ? -1 : tileof(out);
+          if (fst && tt > 0 && TLC[tt] == 0) {  // cone = {root, tile}, no descendants
+            NOUNROLL for (int q = wp.lane(); q < S_; q += WP::W)
               if (q != s) {
-                V(0, q) = ABSENT;
-                V(out, q) = ABSENT;
+                Vr(0, q) = ABSENT;
+                Vr(out, q) = ABSENT;
               }
             wp.sync();
           } else {
             invalidate_elsewhere(out, s);
             validate_from(out, s, end);
           }
-          V(out, s) = end;
+          Vr(out, s) = end;
         }
-        set_flag(out, 1u << 16, true);
-        if (s != mainsp) {
-          if (pb.caching == CACHE_WB) {
-            if (!fast) set_flag(out, 1u << (8 + s), true);
+        BF[out] |= 1u << 16;  // written (gather's coherence check)
+        if (s != ms) {
+          if (PB.caching == CACHE_WB) {
+            if (!fst) set_flag(out, 1u << (8 + s), true);
           } else {
-            const double arr = xfer(lf, out, bbytes(out), s, mainsp, end, tnow, xh);
-            if (status) return;
+            const double arr = xfer(out, bytesof(out), s, ms, end);
+            if (st) return fail(st);
             pin(s, out, arr);
-            if (!fast) {
-              reserve_bytes<false>(out, mainsp, arr);
+            if (!fst) {
+              reserve_bytes<false>(out, ms, arr);
               if (status) return;
             }
-            validate_hot(out, mainsp, arr);
-            if (pb.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
-              if (!fast) {
+            validate(out, ms, arr);
+            if (PB.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
+              if (!fst) {
                 set_flag(out, 1u << s, false);
-                add_used(s, -bbytes(out));
+                add_used(s, -bytesof(out));
                 setLU(out, s, 0.0);
               }
-              V(out, s) = ABSENT;
-              const int tt = out == 0 ? -1 : tile_of(out);
-              if (!(tt > 0 && tl_cnt()[tt] == 0)) {
+              Vr(out, s) = ABSENT;
+              const int tt = out == 0 ? -1 : tileof(out);
+              if (!(tt > 0 && TLC[tt] == 0)) {
                 const Region ro = reg(out);
                 for_scope(tt, [&](int x) {
                   if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
@@ -1894,20 +1964,20 @@ struct Engine {
           int sj = -1;
           double r = 0.0, key = 0.0;
           if (q < cnt) {
-            sj = succs()[off + q];
-            TState& st = T[sj];
-            const int left = --st.missing;
-            r = dmax(st.rel, end);
-            st.rel = r;
+            sj = SU[off + q];
+            TState& ts_ = T[sj];
+            const int left = --ts_.missing;
+            r = dmax(ts_.rel, end);
+            ts_.rel = r;
             rl = left == 0;
-            if (rl) key = pl ? st.ct : r;
+            if (rl) key = pl ? ts_.ct : r;
           }
           const unsigned m = wp.ballot(rl);
           if (rl) {
             const int at = pool_n + added + popc32(m & wp.lt());
-            pool()[at] = sj;
-            pool_rel()[at] = r;
-            pool_key()[at] = key;
+            PO[at] = sj;
+            PR[at] = r;
+            PK[at] = key;
           }
           added += popc32(m);
         }
@@ -1918,11 +1988,11 @@ struct Engine {
       // R-P/F-P: ready tasks that found no idle processor return to the pool
       if (done < nr) {
         NOUNROLL for (int k = done + wp.lane(); k < nr; k += WP::W) {
-          const int j = rdy_sorted[k];
+          const int j = RS[k];
           const int at = pool_n + (k - done);
-          pool()[at] = j;
-          pool_rel()[at] = T[j].rel;
-          pool_key()[at] = pl ? T[j].ct : T[j].rel;
+          PO[at] = j;
+          PR[at] = T[j].rel;
+          PK[at] = pl ? T[j].ct : T[j].rel;
         }
         wp.sync();
         pool_n += nr - done;

@@ -39,10 +39,9 @@ constexpr int WARPS_PER_BLOCK = 4;
 #define HESP_MIN_BLOCKS 8
 #endif
 
-// The problem tables live in constant memory: every access is warp-uniform
-// (or nearly: per-lane processor type/space), so they are broadcast from the
-// constant cache instead of occupying L1 next to the per-warp state.
-__constant__ Problem c_problem;
+// The problem tables live in constant memory (hx::c_problem, engine.h):
+// every access is warp-uniform, so they are broadcast from the constant cache
+// instead of occupying L1 next to the per-warp state.
 
 __device__ __noinline__ void generate_desc(unsigned long long index, hesp_cand_desc* d) {
   hesp_generate(&c_problem.gen, (int)(c_problem.n / c_problem.base_b), c_problem.n_base_leaves, c_problem.base_b,
