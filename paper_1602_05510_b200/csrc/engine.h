@@ -1535,32 +1535,42 @@ struct Engine {
     NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
     wp.sync();
     if (sm->used[mainsp] > PB.cap[mainsp]) return fail(ST_CAPACITY);
-    const bool pl = PB.ordering == ORD_PL;
-    if (pl) build_ct();
+    if (PB.ordering == ORD_PL) build_ct();
     if (status) return;
 
     // ---------------- register copies for the hot loop ----------------
+    // Only the slot base stays live; every array base is rematerialised from
+    // it and a constant-memory offset at the point of use (one IADD), which
+    // keeps ~30 registers of pointers out of the spill set.
     uint8_t* const sl = slot;
-    double* const VV = (double*)(sl + PB.lay.valid);
-    TState* const T = (TState*)(sl + PB.lay.ts);
-    const int* const SU = (const int*)(sl + PB.lay.succs);
-    const int* const LF = (const int*)(sl + PB.lay.leaf);
-    int* const PO = (int*)(sl + PB.lay.pool);
-    double* const PR = (double*)(sl + PB.lay.pool_rel);
-    double* const PK = (double*)(sl + PB.lay.pool_key);
-    int* const RI = (int*)(sl + PB.lay.gs_a);
-    double* const RK = (double*)(sl + PB.lay.ready_key);
-    int* const RS = (int*)(sl + PB.lay.ready);
-    const int* const TLC = (const int*)(sl + PB.lay.tl_cnt);
-    uint32_t* const BF = (uint32_t*)(sl + PB.lay.bflags);
-    const TaskMeta* const TM = (const TaskMeta*)(sl + PB.lay.tm);
-    const BlockMeta* const BM = (const BlockMeta*)(sl + PB.lay.bm);
-    const TaskMeta* const BT = PB.base_tasks;
-    const BlockMeta* const BB = PB.base_blocks;
-    const int nbt_ = nbt, nbb_ = nbb, S_ = S, ms = mainsp, nl = nleaves, elem = PB.elem;
+#define HOT_ARR(type, field) ((type*)(sl + PB.lay.field))
+#define VV HOT_ARR(double, valid)
+#define T HOT_ARR(TState, ts)
+#define SU HOT_ARR(const int, succs)
+#define LF HOT_ARR(const int, leaf)
+#define PO HOT_ARR(int, pool)
+#define PR HOT_ARR(double, pool_rel)
+#define PK HOT_ARR(double, pool_key)
+#define RI HOT_ARR(int, gs_a)
+#define RK HOT_ARR(double, ready_key)
+#define RS HOT_ARR(int, ready)
+#define TLC HOT_ARR(const int, tl_cnt)
+#define BF HOT_ARR(uint32_t, bflags)
+#define TM HOT_ARR(const TaskMeta, tm)
+#define BM HOT_ARR(const BlockMeta, bm)
+#define BT (PB.base_tasks)
+#define BB (PB.base_blocks)
+    // problem-wide scalars are read from constant memory at each use
+#define nbt_ PB.n_base_tasks
+#define nbb_ PB.n_base_blocks
+#define S_ PB.S
+#define ms PB.main_space
+#define elem PB.elem
+#define sel PB.selection
+#define waits (PB.selection == SEL_RP || PB.selection == SEL_FP)
+#define pl (PB.ordering == ORD_PL)
+    const int nl = nleaves;
     const bool fst = fast;
-    const int sel = PB.selection;
-    const bool waits = sel == SEL_RP || sel == SEL_FP;
     auto Vr = [&](int b, int s) -> double& { return VV[(size_t)b * S_ + s]; };
     auto taskm = [&](int id) -> TaskMeta { return id < nbt_ ? BT[id] : TM[id - nbt_]; };
     auto tileof = [&](int b) -> int { return b < nbb_ ? BB[b].tile : BM[b - nbb_].tile; };
@@ -2001,6 +2011,31 @@ struct Engine {
     makespan = mk;
     ahash += ah;
     xhash += xh;
+#undef HOT_ARR
+#undef nbt_
+#undef nbb_
+#undef S_
+#undef ms
+#undef elem
+#undef sel
+#undef waits
+#undef pl
+#undef VV
+#undef T
+#undef SU
+#undef LF
+#undef PO
+#undef PR
+#undef PK
+#undef RI
+#undef RK
+#undef RS
+#undef TLC
+#undef BF
+#undef TM
+#undef BM
+#undef BT
+#undef BB
   }
 
   // =========================================================================
