@@ -1852,9 +1852,91 @@ struct Engine {
         } else {
           if (sel == SEL_EFTP) {
             bool noroute = false;
+#if defined(__CUDACC__)
+            // Warp-parallel est_transfer_ready (sim.cpp:762-793): lane (k, sp)
+            // owns block k of the working set in space sp.  One round trip
+            // loads every V(b_k, sp); ballots give each block's valid-space
+            // mask; the per-link accumulators of the reference's `acc` map are
+            // rebuilt in order from the (<= 2) earlier blocks of the same space
+            // by shuffles; a segmented max gives the estimate per space.
+            {
+              const unsigned FULL = 0xffffffffu;
+              const int lane = wp.lane();
+              const int Sx = S_;
+              const int k = lane / Sx, sp = lane - k * Sx;
+              const bool act = k < nw;
+              const int b = k == 0 ? w[0] : (k == 1 ? w[1] : (k == 2 ? w[2] : w[3]));
+              const double v = act ? Vr(b, sp) : ABSENT;
+              const unsigned vm = __ballot_sync(FULL, act && v != ABSENT);
+              const unsigned mymask = act ? (vm >> (k * Sx)) & ((1u << Sx) - 1u) : 0u;
+              int src = -1;
+              if (act && v == ABSENT) {
+                if (ms != sp && ((mymask >> ms) & 1u)) {
+                  src = ms;
+                } else {
+                  const unsigned o = mymask & ~(1u << ms) & ~(1u << sp);
+                  if (o) src = ctz32(o);
+                }
+              }
+              const double vsrc = __shfl_sync(FULL, v, src >= 0 ? k * Sx + src : lane);
+              int l0 = -1, l1 = -1, nh = 0;
+              double c0 = 0.0, c1 = 0.0;
+              if (src >= 0) {
+                nh = PB.route_n[src * MAXS + sp];
+                if (nh == 0) noroute = true;
+                const double nbytes = (double)bytesof(b);
+                if (nh >= 1) {
+                  l0 = PB.route_l[src * MAXS + sp][0];
+                  c0 = PB.link_lat[l0] + nbytes / PB.link_bw[l0];
+                }
+                if (nh >= 2) {
+                  l1 = PB.route_l[src * MAXS + sp][1];
+                  c1 = PB.link_lat[l1] + nbytes / PB.link_bw[l1];
+                }
+              }
+              double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+              for (int kp = 0; kp < 3; ++kp) {  // earlier blocks of this space, in order
+                const int from = kp * Sx + sp < 32 ? kp * Sx + sp : lane;
+                const int pl0 = __shfl_sync(FULL, l0, from), pl1 = __shfl_sync(FULL, l1, from);
+                const double pc0 = __shfl_sync(FULL, c0, from), pc1 = __shfl_sync(FULL, c1, from);
+                if (kp < k) {
+                  if (l0 >= 0 && pl0 == l0) acc0 += pc0;
+                  if (l0 >= 0 && pl1 == l0) acc0 += pc1;
+                  if (l1 >= 0 && pl0 == l1) acc1 += pc0;
+                  if (l1 >= 0 && pl1 == l1) acc1 += pc1;
+                }
+              }
+              double val = 0.0;
+              if (act) {
+                if (v != ABSENT) {
+                  val = v;
+                } else if (src >= 0 && nh > 0) {
+                  double tarr = dmax(tnow, vsrc);
+                  acc0 += c0;
+                  tarr += acc0;
+                  if (nh == 2) {
+                    acc1 += c1;
+                    tarr += acc1;
+                  }
+                  val = tarr;
+                }
+              }
+              double e = val;  // est(sp) = max(0, max_k val(k, sp)), held by lane sp
+#pragma unroll
+              for (int kp = 1; kp < 3; ++kp) {
+                const int from = kp * Sx + lane < 32 ? kp * Sx + lane : lane;
+                const double o = __shfl_sync(FULL, val, from);
+                if (lane < Sx && kp < nw) e = dmax(e, o);
+              }
+              estp.own(0) = __shfl_sync(FULL, e, pspace.own(0));
+            }
+            if (wp.any(noroute)) return fail(ST_NO_ROUTE);
+#else
             NOUNROLL for (int sp = wp.lane(); sp < S_; sp += WP::W) est.own(sp) = eft_space_h(sp, w, nw, noroute);
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
             estp.gather(est, pspace);  // estimate of each processor's space
+#endif
           }
           double a = ABSENT, b2 = 0.0;
           int id = -1;

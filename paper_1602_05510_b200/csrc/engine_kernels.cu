@@ -36,7 +36,7 @@ struct WarpBest {
 
 constexpr int WARPS_PER_BLOCK = 4;
 #ifndef HESP_MIN_BLOCKS
-#define HESP_MIN_BLOCKS 8
+#define HESP_MIN_BLOCKS 16
 #endif
 
 // The problem tables live in constant memory (hx::c_problem, engine.h):
