@@ -160,6 +160,8 @@ int main(int argc, char** argv) {
   hx::HostProblem hp = hx::build_problem(hplat, hmodel, hs, wl);
   hp.p.base_tasks = hp.base_tasks.data();
   hp.p.base_blocks = hp.base_blocks.data();
+  hp.p.base_preds = hp.base_preds.data();
+  hp.p.base_plist = hp.base_plist.data();
   const hx::SlotLayout L = hp.p.lay;
   std::vector<uint8_t> slot(L.total);
   hx::Small sm{};

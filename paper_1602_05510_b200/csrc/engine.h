@@ -820,27 +820,64 @@ struct Engine {
     }
   }
 
+  // Predecessor list of leaf j: candidate arena (off >= 0) or, for base tasks
+  // whose tiles have no sub-blocks, the shared base table (off = ~index).
+  HX const int32_t* pred_list(int j) const {
+    const int off = t_poff()[j];
+    return off >= 0 ? preds() + off : PB.base_plist + ~off;
+  }
+
   // Dependences (E2): per cell, last writer + readers since that write.
-  // For each leaf() j in program order: reads -> pred last writer, join
-  // readers; writes -> preds() last writer and all readers, become writer.
+  // E5: a base task whose tiles all lack sub-blocks sees the
+  // base tiling's exact accessor history on them (a partitioned accessor
+  // would have created sub-blocks), so its predecessors are the base
+  // predecessors precomputed on the host; only tasks touching subdivided
+  // tiles run the cell tracking, in program order.
   HXN void build_deps() {
     int rn_used = 0;
     nedges = 0;
-    NOUNROLL for (int li = 0; li < nleaves && !status; ++li) {
-      const int j = leaf()[li];
+    // ---- pass 0 (parallel): classify leaves, take base preds for the fast ones
+    int nslow = 0;
+    int* const slow = gs_b();
+    NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
+      const int li = base + wp.lane();
+      bool isslow = false;
+      int j = -1;
+      if (li < nleaves) {
+        j = leaf()[li];
+        const TaskMeta t = task(j);
+        int kt = 0;
+        bool fastj = j < nbt;
+        NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
+          bool dup = false;
+          for (int q = 0; q < k; ++q) dup |= t.blk[q] == t.blk[k];
+          kt += !dup;
+          if (fastj && tl_cnt()[tile_of(t.blk[k])] != 0) fastj = false;
+        }
+        sum_k += kt;
+        if (fastj) {
+          const BasePreds& bp = PB.base_preds[j];
+          t_poff()[j] = ~bp.uoff;
+          t_pcnt()[j] = bp.ucnt;
+          ts()[j].missing = bp.ucnt;
+        }
+        isslow = !fastj;
+      }
+      const unsigned m = wp.ballot(isslow);
+      if (isslow) slow[nslow + popc32(m & wp.lt())] = j;
+      nslow += popc32(m);
+    }
+    wp.sync();
+#if defined(__CUDACC__)
+    sum_k = wp.sumi(sum_k);
+#endif
+    // ---- pass A (serial in program order): cell tracking for the slow leaves
+    NOUNROLL for (int si = 0; si < nslow && !status; ++si) {
+      const int j = slow[si];
       const TaskMeta t = task(j);
       const int wb = t.blk[t.nrd];
       int npb = 0;
-      {
-        int kt = 0;
-        NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
-          bool dup = false;
-          NOUNROLL for (int q = 0; q < k; ++q)
-            if (t.blk[q] == t.blk[k]) dup = true;
-          kt += !dup;
-        }
-        sum_k += kt;
-      }
+      int slot = 0;
       // distinct blocks, read-only ones first in read order, then the write
       NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
         const int b = t.blk[k];
@@ -850,6 +887,18 @@ struct Engine {
           if (t.blk[q] == b && q < t.nrd) dup = true;
         if (dup && k < t.nrd) continue;
         const bool writes = (k == t.nrd);
+        const int myslot = slot++;
+        if (j < nbt && tl_cnt()[tile_of(b)] == 0) {
+          // unsubdivided tile of a base task: its base contribution (E5)
+          const BasePreds& bp = PB.base_preds[j];
+          const int off = bp.soff[myslot], cnt = bp.scnt[myslot];
+          NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W)
+            if (npb + q < PB.maxpb) pbuf()[npb + q] = PB.base_plist[off + q];
+          npb += cnt;
+          wp.sync();
+          if (npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
+          continue;
+        }
         int tt, r0, r1, c0, c1;
         cell_range(b, tt, r0, r1, c0, c1);
         const int nc = tl_ncb()[tt] - 1;
@@ -907,7 +956,7 @@ struct Engine {
         }
         if (rn_used > PB.maxrn || npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
       }
-      // dedup -> preds() CSR
+      // dedup -> preds arena
       int m = 0;
       NOUNROLL for (int base = 0; base < npb; base += WP::W) {
         const int q = base + wp.lane();
@@ -939,11 +988,22 @@ struct Engine {
       nedges += m;
     }
     if (status) return;
-    // successors CSR from the preds() lists
+    // ---- pass B (parallel): successors CSR from all predecessor lists
     NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].scnt = 0;
     wp.sync();
-    NOUNROLL for (int e = wp.lane(); e < nedges; e += WP::W) wp.atomic_add(&ts()[preds()[e]].scnt, 1);
+    int total = 0;
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) {
+      const int j = leaf()[li];
+      const int32_t* pl_ = pred_list(j);
+      const int cnt = t_pcnt()[j];
+      total += cnt;
+      NOUNROLL for (int q = 0; q < cnt; ++q) wp.atomic_add(&ts()[pl_[q]].scnt, 1);
+    }
     wp.sync();
+#if defined(__CUDACC__)
+    total = wp.sumi(total);
+#endif
+    nedges = total;  // all edges, base-table and arena alike
     int run = 0;
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
@@ -962,16 +1022,18 @@ struct Engine {
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
-    NOUNROLL for (int li = 0; li < nleaves; ++li) {  // fill (per dst; order within a list is irrelevant)
+    if (run > PB.maxedges) return fail(ST_ENGINE_LIMIT);
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) {  // order within a list is irrelevant
       const int j = leaf()[li];
-      const int off = t_poff()[j], cnt = t_pcnt()[j];
-      NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
-        const int p = preds()[off + q];
+      const int32_t* pl_ = pred_list(j);
+      const int cnt = t_pcnt()[j];
+      NOUNROLL for (int q = 0; q < cnt; ++q) {
+        const int p = pl_[q];
         const int pos = wp.atomic_add(&ts()[p].scnt, 1);
         succs()[ts()[p].soff + pos] = j;
       }
-      wp.sync();
     }
+    wp.sync();
   }
 
   // critical_times (sim.cpp:92-115): ct = avg + max(0, max_succ ct), reverse
@@ -983,9 +1045,10 @@ struct Engine {
       const int j = leaf()[li];
       const TaskMeta t = task(j);
       const double c = PB.ctavg[t.kind][t.bidx] + ts()[j].rel;
-      const int off = t_poff()[j], cnt = t_pcnt()[j];
+      const int32_t* pl_ = pred_list(j);
+      const int cnt = t_pcnt()[j];
       NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
-        const int p = preds()[off + q];
+        const int p = pl_[q];
         ts()[p].rel = dmax(ts()[p].rel, c);
       }
       if (wp.lane() == 0) ts()[j].ct = c;

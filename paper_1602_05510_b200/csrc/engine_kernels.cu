@@ -210,6 +210,8 @@ struct hesp_engine {
   HostProblem hp;
   Problem* d_problem = nullptr;
   TaskMeta* d_base_tasks = nullptr;
+  BasePreds* d_base_preds = nullptr;
+  int32_t* d_base_plist = nullptr;
   BlockMeta* d_base_blocks = nullptr;
   SlotLayout L{};
   uint8_t* d_scratch = nullptr;
@@ -374,8 +376,15 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   if ((c = cudaMalloc(&e->d_base_blocks, nb * sizeof(BlockMeta))) != cudaSuccess) return fail(c, "malloc");
   cudaMemcpy(e->d_base_tasks, e->hp.base_tasks.data(), nt * sizeof(TaskMeta), cudaMemcpyHostToDevice);
   cudaMemcpy(e->d_base_blocks, e->hp.base_blocks.data(), nb * sizeof(BlockMeta), cudaMemcpyHostToDevice);
+  const size_t npr = e->hp.base_preds.size(), npl = e->hp.base_plist.size();
+  if ((c = cudaMalloc(&e->d_base_preds, npr * sizeof(BasePreds))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMalloc(&e->d_base_plist, npl * sizeof(int32_t))) != cudaSuccess) return fail(c, "malloc");
+  cudaMemcpy(e->d_base_preds, e->hp.base_preds.data(), npr * sizeof(BasePreds), cudaMemcpyHostToDevice);
+  cudaMemcpy(e->d_base_plist, e->hp.base_plist.data(), npl * sizeof(int32_t), cudaMemcpyHostToDevice);
   p.base_tasks = e->d_base_tasks;
   p.base_blocks = e->d_base_blocks;
+  p.base_preds = e->d_base_preds;
+  p.base_plist = e->d_base_plist;
   p.lay = slot_layout(p);
   e->L = p.lay;
   if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
@@ -397,6 +406,8 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_problem);
   cudaFree(e->d_base_tasks);
   cudaFree(e->d_base_blocks);
+  cudaFree(e->d_base_preds);
+  cudaFree(e->d_base_plist);
   cudaFree(e->d_scratch);
   cudaFree(e->d_wbest);
   cudaFree(e->d_best);

@@ -65,6 +65,13 @@ struct TState {
   int32_t flag;     // committed
 };
 
+// Host-precomputed predecessors of a base task (E5): the deduplicated union
+// and the per-block-slot contributions, as offsets into Problem::base_plist.
+struct BasePreds {
+  int32_t uoff, ucnt;
+  int32_t soff[3], scnt[3];
+};
+
 struct PartEntry {
   int32_t task, child0, nchild, leaves;
 };
@@ -112,6 +119,8 @@ struct Problem {
   // ---- base graph (shared by every candidate) ----
   const TaskMeta* base_tasks;    // [n_base_tasks]
   const BlockMeta* base_blocks;  // [n_base_blocks]
+  const BasePreds* base_preds;   // [n_base_tasks]
+  const int32_t* base_plist;
   // ---- per-candidate slot layout (byte offsets, identical for every slot) ----
   SlotLayout lay;
 };

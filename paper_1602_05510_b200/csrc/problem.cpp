@@ -275,6 +275,55 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
     hp.base_blocks.push_back(root_b);
     for (int id = 1; id < eng.nblocks; ++id) hp.base_blocks.push_back(eng.bm()[id - 1]);
   }
+  // ---------------- base predecessors (E5) ----------------
+  // The engine's per-cell last-writer/readers tracking run once over the base
+  // tiling, where every tile is a single cell.  Slot order = the engine's
+  // processing order: read-only blocks in read order, then the write.
+  {
+    const int nt = static_cast<int>(hp.base_tasks.size());
+    const int nb = static_cast<int>(hp.base_blocks.size());
+    std::vector<int> writer(nb, -1);
+    std::vector<std::vector<int>> readers(nb);
+    hp.base_preds.assign(nt, BasePreds{});
+    for (int j = 1; j < nt; ++j) {
+      const TaskMeta& t = hp.base_tasks[j];
+      const int wb = t.blk[t.nrd];
+      std::vector<int> uni;
+      int slot = 0;
+      BasePreds bp{};
+      for (int k = 0; k <= t.nrd; ++k) {
+        const int b = t.blk[k];
+        if (k < t.nrd && b == wb) continue;
+        bool dup = false;
+        for (int q = 0; q < k; ++q)
+          if (t.blk[q] == b && q < t.nrd) dup = true;
+        if (dup && k < t.nrd) continue;
+        const bool writes = k == t.nrd;
+        std::vector<int> lst;
+        if (writer[b] >= 0 && writer[b] != j) lst.push_back(writer[b]);
+        if (!writes) {
+          readers[b].push_back(j);
+        } else {
+          for (auto it = readers[b].rbegin(); it != readers[b].rend(); ++it)
+            if (*it != j) lst.push_back(*it);
+          writer[b] = j;
+          readers[b].clear();
+        }
+        if (slot >= 3) bad("base task with more than 3 distinct blocks");
+        bp.soff[slot] = static_cast<int>(hp.base_plist.size());
+        bp.scnt[slot] = static_cast<int>(lst.size());
+        hp.base_plist.insert(hp.base_plist.end(), lst.begin(), lst.end());
+        for (int x : lst)
+          if (std::find(uni.begin(), uni.end(), x) == uni.end()) uni.push_back(x);
+        ++slot;
+      }
+      bp.uoff = static_cast<int>(hp.base_plist.size());
+      bp.ucnt = static_cast<int>(uni.size());
+      hp.base_plist.insert(hp.base_plist.end(), uni.begin(), uni.end());
+      hp.base_preds[j] = bp;
+    }
+    if (hp.base_plist.empty()) hp.base_plist.push_back(0);
+  }
   p.n_base_tasks = static_cast<int>(hp.base_tasks.size());
   p.n_base_blocks = static_cast<int>(hp.base_blocks.size());
   p.n_base_leaves = p.n_base_tasks - 1;

@@ -15,6 +15,8 @@ struct HostProblem {
   Problem p{};
   std::vector<TaskMeta> base_tasks;
   std::vector<BlockMeta> base_blocks;
+  std::vector<BasePreds> base_preds;
+  std::vector<int32_t> base_plist;
 };
 
 // Validates (Platform::validate, platform.cpp:91-138; PerfModel::analytic,
