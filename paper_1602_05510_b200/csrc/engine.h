@@ -1583,6 +1583,19 @@ struct Engine {
         if (nonroot + (q == mainsp ? bbytes(0) : 0) > PB.cap[q]) ok = false;
       fast = ok;
     }
+    switch (PB.selection) {
+      case SEL_EFTP: return fast ? sim_loop<SEL_EFTP, true>() : sim_loop<SEL_EFTP, false>();
+      case SEL_EITP: return fast ? sim_loop<SEL_EITP, true>() : sim_loop<SEL_EITP, false>();
+      case SEL_FP: return fast ? sim_loop<SEL_FP, true>() : sim_loop<SEL_FP, false>();
+      default: return fast ? sim_loop<SEL_RP, true>() : sim_loop<SEL_RP, false>();
+    }
+  }
+
+  // The loop proper, specialised on the selection policy and on E4 (no
+  // eviction possible) so one batch executes one compact instantiation.
+  template <int SELT, bool FASTT>
+  HXN void sim_loop() {
+    const int P = PB.P;
     // init_memory (sim.cpp:323-339): root materialised in main, every block
     // valid in main at t=0 (views into the root data)
     NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
@@ -1629,11 +1642,11 @@ struct Engine {
 #define S_ PB.S
 #define ms PB.main_space
 #define elem PB.elem
-#define sel PB.selection
-#define waits (PB.selection == SEL_RP || PB.selection == SEL_FP)
+#define sel SELT
+#define waits (SELT == SEL_RP || SELT == SEL_FP)
 #define pl (PB.ordering == ORD_PL)
     const int nl = nleaves;
-    const bool fst = fast;
+    constexpr bool fst = FASTT;
     auto Vr = [&](int b, int s) -> double& { return VV[(size_t)b * S_ + s]; };
     auto taskm = [&](int id) -> TaskMeta { return id < nbt_ ? BT[id] : TM[id - nbt_]; };
     auto tileof = [&](int b) -> int { return b < nbb_ ? BB[b].tile : BM[b - nbb_].tile; };
