@@ -236,16 +236,10 @@ def main():
     stream.synchronize()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
+    from paper_1602_05510_b200.dist import global_best as _gb
+
     def global_best(b):
-        if world == 1:
-            return b.makespan, b.index
-        bits = np.float64(b.makespan).view(np.int64) if b.index >= 0 else np.iinfo(np.int64).max
-        t = torch.tensor([int(bits)], dtype=torch.int64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        idx = b.index if (b.index >= 0 and int(bits) == int(t.item())) else np.iinfo(np.int64).max
-        u = torch.tensor([int(idx)], dtype=torch.int64, device="cuda")
-        dist.all_reduce(u, op=dist.ReduceOp.MIN)
-        return float(np.int64(t.item()).view(np.float64)), int(u.item())
+        return _gb(b.makespan, b.index, device="cuda")
 
     for s in range(args.warmup):
         b = eng.eval_descs_device(descs[s].data_ptr(), B, firsts[s], outs.data_ptr(), stream.cuda_stream)

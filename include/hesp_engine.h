@@ -164,6 +164,13 @@ int hesp_generate_device(hesp_engine* e, uint64_t first_index, uint64_t count,
 int hesp_generate_host(const hesp_engine* e, uint64_t first_index, uint64_t count,
                        hesp_cand_desc* descs);
 
+/* Pure host generator (no engine, no device): descriptors of candidates
+ * first..first+count-1 for a workload whose base tiling has n_base leaves
+ * of side base_b (s_base_snapped = n / base_b).  Same code as the device
+ * generator (include/hesp_workload.h). */
+int hesp_generate_batch(const hesp_gen_config* gen, int32_t s_base_snapped, int32_t n_base, int64_t base_b,
+                        uint64_t first_index, uint64_t count, hesp_cand_desc* descs);
+
 /* Per-task schedule of one candidate: for every task id < cap, proc/start/end
  * (proc = -1 for non-leaf or unscheduled ids).  Returns the outcome status. */
 int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, int32_t* proc,

@@ -65,6 +65,7 @@ int main(int argc, char** argv) {
     else if (k == "--seed") gen.seed = std::stoull(v(), nullptr, 0);
     else if (k == "--kmax") gen.k_max = std::stoi(v());
     else if (k == "--maxdepth") gen.max_depth = std::stoi(v());
+    else if (k == "--min-block") gen.min_block = std::stoll(v());
     else if (k == "--s-choices") {
       std::string s = v();
       gen.n_s_choices = 0;

@@ -544,6 +544,13 @@ int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, in
   return ok ? o.status : HESP_E_CUDA;
 }
 
+int hesp_generate_batch(const hesp_gen_config* gen, int32_t s_base_snapped, int32_t n_base, int64_t base_b,
+                        uint64_t first_index, uint64_t count, hesp_cand_desc* descs) {
+  if (!gen || !descs) return HESP_E_INVALID;
+  for (uint64_t i = 0; i < count; ++i) hesp_generate(gen, s_base_snapped, n_base, base_b, first_index + i, &descs[i]);
+  return HESP_OK;
+}
+
 int hesp_generate_host(const hesp_engine* e, uint64_t first_index, uint64_t count, hesp_cand_desc* descs) {
   if (!e || !descs) return HESP_E_INVALID;
   const Problem& p = e->hp.p;

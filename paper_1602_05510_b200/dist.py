@@ -1,0 +1,48 @@
+"""Cross-GPU plumbing for candidate sharding.
+
+Candidates are independent, so G ranks take disjoint index
+ranges and the only exchange is the final winner: an exact lexicographic
+argmin of (makespan, global index) over ranks, done as two 8-byte MIN
+all-reduces (NCCL over NVLink on GPUs; gloo in the CPU tests):
+
+  1. MIN over the order-preserving int64 view of each rank's best makespan
+     (positive IEEE doubles order like their bit patterns);
+  2. MIN over the index among ranks whose makespan equals the global one.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+NONE = np.iinfo(np.int64).max
+
+
+def shard(total: int, world: int, rank: int, first: int = 0) -> tuple[int, int]:
+    """[begin, end) of rank's contiguous share of `total` candidates starting at `first`."""
+    base, rem = divmod(total, world)
+    begin = first + rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def makespan_key(makespan: float, index: int) -> int:
+    """int64 order key of a rank-local best (NONE when the rank found no valid candidate)."""
+    if index < 0:
+        return NONE
+    return int(np.float64(makespan).view(np.int64))
+
+
+def global_best(makespan: float, index: int, device="cpu", group=None) -> tuple[float, int]:
+    """Exact (makespan, lowest index) argmin across all ranks of `group`."""
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return (makespan, index) if index >= 0 else (float("nan"), -1)
+    key = makespan_key(makespan, index)
+    t = torch.tensor([key], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    gkey = int(t.item())
+    if gkey == NONE:
+        return float("nan"), -1
+    mine = index if key == gkey else NONE
+    u = torch.tensor([mine], dtype=torch.int64, device=device)
+    dist.all_reduce(u, op=dist.ReduceOp.MIN, group=group)
+    return float(np.int64(gkey).view(np.float64)), int(u.item())

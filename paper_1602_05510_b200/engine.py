@@ -110,7 +110,8 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 136
 
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
-    "hesp_generate_device", "hesp_generate_host", "hesp_eval_detail", "hesp_engine_get_info",
+    "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
+    "hesp_engine_get_info",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -135,6 +136,8 @@ def load_library(path: str = LIB) -> C.CDLL:
                                            C.POINTER(Best), C.c_void_p]
     lib.hesp_generate_device.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p]
     lib.hesp_generate_host.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p]
+    lib.hesp_generate_batch.argtypes = [C.POINTER(GenConfig), C.c_int32, C.c_int32, C.c_int64, C.c_uint64,
+                                        C.c_uint64, C.c_void_p]
     lib.hesp_eval_detail.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.POINTER(Outcome)]
     lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
@@ -319,6 +322,18 @@ class BatchEngine:
         d = np.zeros(count, DESC_DTYPE)
         self._check(self.lib.hesp_generate_host(self.h, first, count, d.ctypes.data), "generate_host")
         return d
+
+
+def generate_batch(workload: "Workload", n_base: int, base_b: int, first: int, count: int) -> np.ndarray:
+    """Host generator (hesp_generate_batch): no engine or GPU needed."""
+    lib = load_library()
+    sc = (C.c_int32 * 4)(*(list(workload.s_choices) + [0] * (4 - len(workload.s_choices))))
+    g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block, len(workload.s_choices), sc)
+    d = np.zeros(count, DESC_DTYPE)
+    rc = lib.hesp_generate_batch(C.byref(g), workload.n // base_b, n_base, base_b, first, count, d.ctypes.data)
+    if rc != 0:
+        raise RuntimeError("hesp_generate_batch failed")
+    return d
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,142 @@
+"""CPU-only tests (no GPU): golden fixtures, the C ABI surface, the candidate
+generator, host-side sharding, and -- where oracle/_ref is built (build() runs
+`make -C oracle` when /root/reference exists) -- the unmodified reference
+reproducing the committed goldens and the engine's width-1 host build
+matching the reference candidate by candidate."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from golden_io import read_golden
+from paper_1602_05510_b200.configs import C2, PARITY, harness_args
+from paper_1602_05510_b200.dist import shard
+from paper_1602_05510_b200.engine import EXPORTS, FIXTURES, Workload, generate_batch, load_library
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "oracle", "_ref")
+HARNESS = os.path.join(REF, "ref_harness")
+ENGINE_CHECK = os.path.join(REF, "engine_check")
+
+# hesp::Err ordinals + 1 that a valid generator must never provoke
+GEN_ERRORS = {1 + 1: "Validation", 1 + 7: "NotALeaf", 1 + 8: "IndivisibleGrain", 100: "foreign exception"}
+
+
+@pytest.mark.parametrize("name", sorted(PARITY))
+def test_golden_fixture_shape(name):
+    p, count = PARITY[name]
+    g = read_golden(name)
+    assert len(g) == count
+    assert list(g["index"]) == list(range(count))
+    assert not np.isin(g["status"], list(GEN_ERRORS)).any(), "generator emitted an op the reference rejected"
+    ok = g[g["status"] == 0]
+    bad = g[g["status"] != 0]
+    assert (ok["makespan"] > 0).all() and (ok["n_leaves"] > 0).all()
+    assert (bad["makespan"] == 0).all() and (bad["assign_hash"] == 0).all()
+
+
+def test_goldens_exercise_every_path():
+    """The fixture set covers errors, eviction, intersections, every policy."""
+    statuses = set()
+    for name in PARITY:
+        statuses |= set(read_golden(name)["status"].tolist())
+    assert 0 in statuses and 20 in statuses  # ok and CoherenceError
+    assert sum(1 for n in PARITY if n.startswith("policy_")) == 24
+
+
+def test_library_exports_every_declared_symbol():
+    lib = load_library()
+    with open(os.path.join(ROOT, "include", "hesp_engine.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"\b(hesp_[a-z_]+)\s*\(", hdr))
+    declared -= {"hesp_engine"}
+    assert declared, "no declarations parsed"
+    for sym in sorted(declared):
+        getattr(lib, sym)  # raises AttributeError if not exported
+    assert set(EXPORTS) <= declared
+
+
+def test_status_names():
+    lib = load_library()
+    assert lib.hesp_status_name(0) == b"ok"
+    assert lib.hesp_status_name(20) == b"CoherenceError"
+    assert lib.hesp_status_name(14) == b"CapacityInfeasible"
+    assert lib.hesp_status_name(201) == b"EngineLimit"
+
+
+def c2_workload():
+    p = C2
+    return Workload(p["n"], p["elem"], p["s_base"], p["seed"], p["k_max"], p["max_depth"], p["min_block"],
+                    p["s_choices"])
+
+
+def test_generator_is_deterministic_and_bounded():
+    wl = c2_workload()
+    a = generate_batch(wl, 816, 1024, 0, 4096)
+    b = generate_batch(wl, 816, 1024, 0, 4096)
+    assert a.tobytes() == b.tobytes()
+    assert (a["n_ops"] >= 0).all() and (a["n_ops"] <= wl.k_max).all()
+    # all K in [0, k_max] occur, and ops address existing task ids with allowed s
+    assert set(a["n_ops"].tolist()) == set(range(wl.k_max + 1))
+    for d in a[:512]:
+        n = int(d["n_ops"])
+        ops = d["ops"][:n]
+        assert set(ops[:, 1].tolist()) <= set(wl.s_choices)
+        assert (ops[:, 0] >= 1).all()
+        assert (d["ops"][n:, 0] == -1).all()
+    # a different seed gives a different stream
+    wl2 = c2_workload()
+    wl2.seed = 2
+    c = generate_batch(wl2, 816, 1024, 0, 4096)
+    assert a.tobytes() != c.tobytes()
+    # an index range is a slice of a longer one
+    d = generate_batch(wl, 816, 1024, 100, 50)
+    assert d.tobytes() == a[100:150].tobytes()
+
+
+@pytest.mark.parametrize("total,world", [(100_000, 1), (100_000, 8), (10, 3), (7, 8)])
+def test_shard_partitions_the_index_range(total, world):
+    seen = []
+    for r in range(world):
+        b, e = shard(total, world, r, first=5)
+        assert 0 <= e - b <= total // world + 1
+        seen.extend(range(b, e))
+    assert seen == list(range(5, 5 + total))
+
+
+def _records(path):
+    from golden_io import read_golden as rg
+    return rg(path)
+
+
+REF_PRESETS = ["c1", "c3", "policy_PL_EFT-P_WB", "policy_FCFS_R-P_WA", "evict_wb", "sect_cpugpu", "table"]
+
+
+@pytest.mark.skipif(not os.path.exists(HARNESS), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("name", REF_PRESETS)
+def test_reference_reproduces_goldens(name, tmp_path):
+    p, count = PARITY[name]
+    k = min(count, 6)
+    out = tmp_path / f"{name}.bin"
+    subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--first", "0", "--count", str(k), "--threads",
+                    str(os.cpu_count()), "--out", str(out), "--quiet"], check=True)
+    got = _records(str(out))
+    want = read_golden(name)[:k]
+    assert got.tobytes() == want.tobytes()
+
+
+CHECK_PRESETS = ["c3", "policy_PL_EFT-P_WB", "policy_FCFS_EIT-P_WT", "policy_PL_F-P_WA", "policy_FCFS_R-P_WB",
+                 "evict_wb", "evict_wa", "sect_cpugpu", "sect_biglittle", "deep_biglittle", "table"]
+
+
+@pytest.mark.skipif(not os.path.exists(ENGINE_CHECK), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("name", CHECK_PRESETS)
+def test_host_engine_matches_reference(name):
+    """Engine<HostWarp> (the engine source at width 1) vs the reference library."""
+    p, count = PARITY[name]
+    r = subprocess.run([ENGINE_CHECK, *harness_args(p, FIXTURES), "--first", "0", "--count", str(min(count, 8))],
+                       capture_output=True, text=True, timeout=600)
+    assert "mismatches 0" in r.stdout, r.stdout[-2000:]
+    assert r.returncode == 0
