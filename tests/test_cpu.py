@@ -140,3 +140,12 @@ def test_host_engine_matches_reference(name):
                        capture_output=True, text=True, timeout=600)
     assert "mismatches 0" in r.stdout, r.stdout[-2000:]
     assert r.returncode == 0
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
+def test_reference_side_bridge_compiles(tmp_path):
+    """include/hesp_b200_bridge.hpp compiles against the reference's own hesp:: types."""
+    tu = tmp_path / "tu.cpp"
+    tu.write_text('#include "hesp_b200_bridge.hpp"\nint main() { return 0; }\n')
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-I",
+                    "/root/reference/proj/include", str(tu)], check=True)
