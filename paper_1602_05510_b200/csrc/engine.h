@@ -41,6 +41,12 @@
 
 namespace hx {
 
+#if !defined(__CUDACC__)
+struct int4 {
+  int x, y, z, w;
+};
+#endif
+
 #if defined(__CUDACC__)
 // The device problem lives in constant memory (engine_kernels.cu uploads it
 // before every launch); device code names it statically so no lane ever
@@ -228,6 +234,8 @@ struct Engine {
   HX int32_t* t_poff() const { return (int32_t*)(slot + PB.lay.t_poff); }
   HX int32_t* t_pcnt() const { return (int32_t*)(slot + PB.lay.t_pcnt); }
   HX int32_t* leaf() const { return (int32_t*)(slot + PB.lay.leaf); }
+  // per-task working set: 3 block ids in id order + count (built in build_deps)
+  HX int4* wsb() const { return (int4*)(slot + PB.lay.wsb); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -846,6 +854,16 @@ struct Engine {
       if (li < nleaves) {
         j = leaf()[li];
         const TaskMeta t = task(j);
+        {
+          int w[4];
+          const int nw = working_set(t, w);
+          int4 ws;
+          ws.x = w[0];
+          ws.y = nw > 1 ? w[1] : -1;
+          ws.z = nw > 2 ? w[2] : -1;
+          ws.w = nw;
+          wsb()[j] = ws;
+        }
         int kt = 0;
         bool fastj = j < nbt;
         NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
@@ -1556,6 +1574,30 @@ struct Engine {
 
   HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
 
+  // WT / WA write-back of a task's output to main (sim.cpp:631-656).
+  HXN void write_back(int out, int s, double end) {
+    const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
+    if (status) return;
+    pin(s, out, arr);
+    materialize<false>(out, mainsp, arr);
+    if (status) return;
+    if (PB.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
+      if (!fast) {
+        set_flag(out, 1u << s, false);
+        add_used(s, -bbytes(out));
+        setLU(out, s, 0.0);
+      }
+      V(out, s) = ABSENT;
+      const int tt = out == 0 ? -1 : tile_of(out);
+      if (!(tt > 0 && tl_cnt()[tt] == 0)) {
+        const Region ro = reg(out);
+        for_scope(tt, [&](int x) {
+          if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
+        });
+      }
+    }
+  }
+
   // The event loop (sim.cpp:704-834) with Engine::commit (sim.cpp:592-668)
   // inlined.  Everything the loop touches per task -- array bases, clocks,
   // pool size, hashes, makespan -- is copied into registers first (lanes own
@@ -1892,8 +1934,9 @@ struct Engine {
         const int j = RS[done];
         const TaskMeta t = taskm(j);
         const double rel = T[j].rel;
-        int w[4];
-        const int nw = working_set(t, w);
+        const int4 ws4 = HOT_ARR(const int4, wsb)[j];
+        const int w[4] = {ws4.x, ws4.y, ws4.z, -1};
+        const int nw = ws4.w;
         int p = -1;
         // ---------------- processor selection (sim.cpp:136-192) ----------------
         if (waits) {
@@ -2096,29 +2139,10 @@ struct Engine {
           if (PB.caching == CACHE_WB) {
             if (!fst) set_flag(out, 1u << (8 + s), true);
           } else {
-            const double arr = xfer(out, bytesof(out), s, ms, end);
+            cold_in();
+            write_back(out, s, end);  // WT / WA (cold: the headline policy is WB)
+            cold_out();
             if (st) return fail(st);
-            pin(s, out, arr);
-            if (!fst) {
-              reserve_bytes<false>(out, ms, arr);
-              if (status) return;
-            }
-            validate(out, ms, arr);
-            if (PB.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
-              if (!fst) {
-                set_flag(out, 1u << s, false);
-                add_used(s, -bytesof(out));
-                setLU(out, s, 0.0);
-              }
-              Vr(out, s) = ABSENT;
-              const int tt = out == 0 ? -1 : tileof(out);
-              if (!(tt > 0 && TLC[tt] == 0)) {
-                const Region ro = reg(out);
-                for_scope(tt, [&](int x) {
-                  if (inside(x, out, tt, ro)) V(x, s) = ABSENT;
-                });
-              }
-            }
           }
         }
         // release successors (sim.cpp:660-667): running max of pred ends;

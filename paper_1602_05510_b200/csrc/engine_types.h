@@ -78,7 +78,7 @@ struct PartEntry {
 
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
-  size_t tm, ts, t_poff, t_pcnt, leaf;
+  size_t tm, ts, t_poff, t_pcnt, leaf, wsb;
   size_t bm, bflags, valid, lastu, pinu;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
@@ -153,6 +153,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.t_poff = take(4 * T);
   L.t_pcnt = take(4 * T);
   L.leaf = take(4 * T);
+  L.wsb = take(16 * T);
   L.bm = take(sizeof(BlockMeta) * B);
   L.bflags = take(4 * B);
   L.valid = take(8 * B * S);
