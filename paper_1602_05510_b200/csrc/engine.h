@@ -81,6 +81,7 @@ struct HostWarp {
   int maxi(int v) const { return v; }
   // lexicographic argmin of (a, b, id); lanes with id < 0 do not participate
   void argmin3(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
+  void argmin_lane(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
   int atomic_add(int* p, int v) const {
     int o = *p;
     *p += v;
@@ -156,6 +157,34 @@ struct DevWarp {
         id = i2;
       }
     }
+  }
+  // Lexicographic argmin of (a, b, lane) over lanes with id == lane >= 0,
+  // for a, b >= 0: IEEE order of non-negative doubles is the unsigned order of
+  // their bits, so two 32-bit redux.sync minima per key plus ballots replace
+  // five rounds of three-key shuffles.
+  __device__ __forceinline__ void argmin_lane(double& a, double& b, int& id) const {
+    const bool v = id >= 0;
+    const unsigned long long ka = v ? (unsigned long long)__double_as_longlong(a) : ~0ULL;
+    const unsigned ha = (unsigned)(ka >> 32), la = (unsigned)ka;
+    const unsigned mh = __reduce_min_sync(FULL, ha);
+    const unsigned ml = __reduce_min_sync(FULL, ha == mh ? la : 0xffffffffu);
+    unsigned cand = __ballot_sync(FULL, v && ha == mh && la == ml);
+    if (cand & (cand - 1)) {  // tie on a: minimise b among the tied lanes
+      const bool c = (cand >> lane()) & 1u;
+      const unsigned long long kb = c ? (unsigned long long)__double_as_longlong(b) : ~0ULL;
+      const unsigned hb = (unsigned)(kb >> 32), lb = (unsigned)kb;
+      const unsigned mhb = __reduce_min_sync(FULL, hb);
+      const unsigned mlb = __reduce_min_sync(FULL, hb == mhb ? lb : 0xffffffffu);
+      cand = __ballot_sync(FULL, c && hb == mhb && lb == mlb);
+    }
+    if (cand == 0) {
+      id = -1;
+      return;
+    }
+    const int w = __ffs((int)cand) - 1;
+    a = __shfl_sync(FULL, a, w);
+    b = __shfl_sync(FULL, b, w);
+    id = w;
   }
   __device__ __forceinline__ int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
   struct LaneD {
@@ -1965,7 +1994,7 @@ struct Engine {
                 id = q;
               }
             }
-            wp.argmin3(a, b2, id);
+            wp.argmin_lane(a, b2, id);
             p = id;
           }
         } else {
@@ -2003,7 +2032,8 @@ struct Engine {
               if (src >= 0) {
                 nh = PB.route_n[src * MAXS + sp];
                 if (nh == 0) noroute = true;
-                const double nbytes = (double)bytesof(b);
+                // every block of a task has the task's side (graph.cpp:303-307)
+                const double nbytes = (double)((long long)t.b * t.b * elem);
                 if (nh >= 1) {
                   l0 = PB.route_l[src * MAXS + sp][0];
                   c0 = PB.link_lat[l0] + nbytes / PB.link_bw[l0];
@@ -2074,7 +2104,7 @@ struct Engine {
               id = q;
             }
           }
-          wp.argmin3(a, b2, id);
+          wp.argmin_lane(a, b2, id);
           p = id;
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
