@@ -258,6 +258,7 @@ struct Engine {
   Small* sm;
   // slot arrays: offsets from the (constant-memory) problem, no per-lane pointer copies
   uint8_t* slot;
+  HX SlotHeader* hdr() const { return (SlotHeader*)(slot + PB.lay.hdr); }
   HX TaskMeta* tm() const { return (TaskMeta*)(slot + PB.lay.tm); }
   HX TState* ts() const { return (TState*)(slot + PB.lay.ts); }
   HX int32_t* t_poff() const { return (int32_t*)(slot + PB.lay.t_poff); }
@@ -1373,7 +1374,7 @@ struct Engine {
         if (covered) {
           if (have) {
             if (mode == 0) return 1;
-            if (nout >= PB.maxgs) {
+            if (nout >= PB.maxgr) {
               fail(ST_ENGINE_LIMIT);
               return 0;
             }
@@ -1390,7 +1391,7 @@ struct Engine {
       }
       if (have) {
         if (mode == 0) return 1;
-        if (nout >= PB.maxgs) {
+        if (nout >= PB.maxgr) {
           fail(ST_ENGINE_LIMIT);
           return 0;
         }
@@ -1461,6 +1462,10 @@ struct Engine {
     wp.sync();
     double arrival = 0.0;
     int ncov = 0;
+    if (np > PB.maxgr) {
+      fail(ST_ENGINE_LIMIT);
+      return 0.0;
+    }
     NOUNROLL for (int k = 0; k < np; ++k) {
       const int piece = gs_reg2()[k].row;
       const Region pr = reg(piece);
@@ -2274,18 +2279,47 @@ struct Engine {
     }
   }
 
-  HXN Outcome run(const hesp_cand_desc& d) {
+  // Build phase: base tiling + ops -> leaves, dependences; state left in the slot.
+  HXN void build(const hesp_cand_desc& d) {
     reset_to_base();
     NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
-    Outcome o;
-    o.n_leaves = 0;
     sum_k = 0;
+    nleaves = 0;
+    nedges = 0;
     if (!status) build_tiles();
     if (!status) build_order();
-    o.n_leaves = status ? 0 : nleaves;
+    const int n_out = status ? 0 : nleaves;
     if (!status) build_cells();
     if (!status) build_deps();
+    if (wp.lane() == 0) {
+      SlotHeader h;
+      h.status = status;
+      h.ntasks = ntasks;
+      h.nblocks = nblocks;
+      h.nleaves = nleaves;
+      h.nedges = nedges;
+      h.sum_k = sum_k;
+      h.n_leaves_out = n_out;
+      h.pad = 0;
+      *hdr() = h;
+    }
+    wp.sync();
+  }
+
+  // Simulate phase on a slot left by build().
+  HXN Outcome sim_slot() {
+    const SlotHeader h = *hdr();
+    status = h.status;
+    ntasks = h.ntasks;
+    nblocks = h.nblocks;
+    nleaves = h.nleaves;
+    nedges = h.nedges;
+    sum_k = h.sum_k;
+    makespan = 0.0;
+    ahash = xhash = 0;
     if (!status) simulate();
+    Outcome o;
+    o.n_leaves = h.n_leaves_out;
     o.status = status;
     o.makespan = status ? 0.0 : makespan;
     o.assign_hash = status ? 0 : ahash;
@@ -2293,6 +2327,11 @@ struct Engine {
     o.sum_k = sum_k;
     o.n_edges = nedges;
     return o;
+  }
+
+  HXN Outcome run(const hesp_cand_desc& d) {
+    build(d);
+    return sim_slot();
   }
 };
 

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -111,6 +112,79 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
     b.edges = s_edges;
     wbest[gw] = b;
   }
+}
+
+// Phase-split evaluation (chunked): every resident warp of a launch runs the
+// same phase, so the instruction working set is one phase's code.
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
+    build_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
+                 unsigned long long count, uint8_t* slots, unsigned long long* counter) {
+  __shared__ Small smem[WARPS_PER_BLOCK];
+  __shared__ hesp_cand_desc sdesc[WARPS_PER_BLOCK];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const Problem& pb = c_problem;
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1ULL);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= count) break;
+    hesp_cand_desc& d = sdesc[wib];
+    if (descs) {
+      const int32_t* src = (const int32_t*)(descs + k);
+      int32_t* dst = (int32_t*)&d;
+      for (int i = lane; i < (int)(sizeof(hesp_cand_desc) / 4); i += 32) dst[i] = src[i];
+    } else if (lane == 0) {
+      generate_desc(first_index + k, &d);
+    }
+    __syncwarp();
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    eng.build(d);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
+    sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
+               WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter) {
+  __shared__ Small smem[WARPS_PER_BLOCK];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
+  const Problem& pb = c_problem;
+  WarpBest b{0.0, -1, 0, 0, 0, 0, 0};
+  if (accumulate) b = wbest[gw];
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1ULL);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= count) break;
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    const Outcome o = eng.sim_slot();
+    if (lane == 0 && out) {
+      hesp_outcome r;
+      r.status = o.status;
+      r.n_leaves = o.n_leaves;
+      r.makespan = o.makespan;
+      r.assign_hash = o.assign_hash;
+      r.xfer_hash = o.xfer_hash;
+      out[k] = r;
+    }
+    ++b.n_eval;
+    b.leaves += o.n_leaves;
+    b.k += o.sum_k;
+    b.edges += o.n_edges;
+    if (o.status == 0) {
+      ++b.n_ok;
+      const long long gi = (long long)(first_index + k);
+      if (b.index < 0 || o.makespan < b.makespan || (o.makespan == b.makespan && gi < b.index)) {
+        b.makespan = o.makespan;
+        b.index = gi;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) wbest[gw] = b;
 }
 
 __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* __restrict__ best) {
@@ -229,6 +303,10 @@ struct hesp_engine {
   size_t h_cap = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
+  // phase-split mode (HESP_SPLIT=1): per-candidate slots for one chunk
+  bool split = false;
+  uint8_t* d_cslots = nullptr;
+  unsigned long long chunk = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
@@ -261,8 +339,37 @@ bool grow_host(hesp_engine* e, size_t n) {
   return true;
 }
 
+int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
+                 hesp_outcome* d_out, cudaStream_t st) {
+  if (!e->d_cslots) {
+    if (!ck(cudaMalloc(&e->d_cslots, (size_t)e->chunk * e->L.total), "malloc chunk slots")) return HESP_E_CUDA;
+  }
+  if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
+          "problem -> constant"))
+    return HESP_E_CUDA;
+  cudaEventRecord(e->ev0, st);
+  int acc = 0;
+  for (uint64_t c0 = 0; c0 < count || (count == 0 && c0 == 0); c0 += e->chunk) {
+    const uint64_t n = count - c0 < e->chunk ? count - c0 : e->chunk;
+    cudaMemsetAsync(e->d_counter, 0, 2 * sizeof(unsigned long long), st);
+    build_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs ? d_descs + c0 : nullptr, first + c0, n,
+                                                                 e->d_cslots, e->d_counter);
+    sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
+                                                               e->d_wbest, acc, e->d_cslots, e->d_counter + 1);
+    e->launches += 2;
+    acc = 1;
+    if (count == 0) break;
+  }
+  cudaEventRecord(e->ev1, st);
+  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
+  e->launches += 1;
+  if (!ck(cudaGetLastError(), "split launch")) return HESP_E_CUDA;
+  return HESP_OK;
+}
+
 int launch_eval(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
                 hesp_outcome* d_out, cudaStream_t st) {
+  if (e->split) return launch_split(e, d_descs, first, count, d_out, st);
   if (!ck(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned long long), st), "memset counter"))
     return HESP_E_CUDA;
   if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
@@ -393,7 +500,13 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     return fail(c, "malloc scratch");
   if ((c = cudaMalloc(&e->d_wbest, (size_t)e->n_slots * sizeof(WarpBest))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
-  if ((c = cudaMalloc(&e->d_counter, sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
+  if ((c = cudaMalloc(&e->d_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
+  {
+    const char* sp = getenv("HESP_SPLIT");
+    e->split = sp && sp[0] == '1';
+    const char* ch = getenv("HESP_CHUNK");
+    e->chunk = ch ? strtoull(ch, nullptr, 10) : 65536ULL;
+  }
   if ((c = cudaMallocHost(&e->h_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc host");
   if ((c = cudaEventCreate(&e->ev0)) != cudaSuccess) return fail(c, "event");
   if ((c = cudaEventCreate(&e->ev1)) != cudaSuccess) return fail(c, "event");
@@ -409,6 +522,7 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_base_preds);
   cudaFree(e->d_base_plist);
   cudaFree(e->d_scratch);
+  cudaFree(e->d_cslots);
   cudaFree(e->d_wbest);
   cudaFree(e->d_best);
   cudaFree(e->d_counter);

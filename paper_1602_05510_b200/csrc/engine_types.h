@@ -72,17 +72,22 @@ struct BasePreds {
   int32_t soff[3], scnt[3];
 };
 
+// Per-candidate state carried from the build kernel to the simulate kernel.
+struct SlotHeader {
+  int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, pad;
+};
+
 struct PartEntry {
   int32_t task, child0, nchild, leaves;
 };
 
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
-  size_t tm, ts, t_poff, t_pcnt, leaf, wsb;
+  size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
   size_t bm, bflags, valid, lastu, pinu;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
-  size_t gs_a, gs_b, gs_reg, gs_reg2;
+  size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
   size_t total;
 };
 
@@ -115,7 +120,7 @@ struct Problem {
   int32_t ordering, selection, caching;
   uint64_t sched_seed;
   // ---- capacities of the per-candidate slot ----
-  int32_t maxt, maxb, maxbnd, maxcells, maxrn, maxedges, maxpb, maxgs;
+  int32_t maxt, maxb, maxbnd, maxcells, maxrn, maxedges, maxpb, maxgs, maxgr;
   // ---- base graph (shared by every candidate) ----
   const TaskMeta* base_tasks;    // [n_base_tasks]
   const BlockMeta* base_blocks;  // [n_base_blocks]
@@ -148,6 +153,7 @@ inline SlotLayout slot_layout(const Problem& p) {
     return at;
   };
   const size_t T = (size_t)p.maxt, B = (size_t)p.maxb, S = (size_t)p.S, NB = (size_t)p.n_base_blocks;
+  L.hdr = take(sizeof(SlotHeader));
   L.tm = take(sizeof(TaskMeta) * T);
   L.ts = take(sizeof(TState) * T);
   L.t_poff = take(4 * T);
@@ -180,8 +186,8 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.pbuf = take(4 * (size_t)p.maxpb);
   L.gs_a = take(4 * (size_t)p.maxgs);
   L.gs_b = take(4 * (size_t)p.maxgs);
-  L.gs_reg = take(sizeof(Region) * (size_t)p.maxgs);
-  L.gs_reg2 = take(sizeof(Region) * (size_t)p.maxgs);
+  L.gs_reg = take(sizeof(Region) * (size_t)p.maxgr);
+  L.gs_reg2 = take(sizeof(Region) * (size_t)p.maxgr);
   L.total = align_up(o, 256);
   return L;
 }

@@ -263,6 +263,7 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
     bp.maxedges = 16;
     bp.maxpb = 16;
     bp.maxgs = bp.maxb + 8;
+    bp.maxgr = bp.maxb + 8;
     bp.lay = slot_layout(bp);
     std::vector<uint8_t> slot(bp.lay.total);
     Small sm{};
@@ -338,10 +339,14 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   p.maxb = p.n_base_blocks + K * 5 * smax * smax + 64;
   p.maxcells = p.n_base_blocks + K * 3 * 256 + 256;
   p.maxbnd = 4 * p.maxb + 4 * p.n_base_blocks + 64;
-  p.maxrn = 8 * p.maxt + 4 * p.maxcells;
-  p.maxedges = 12 * p.maxt;
+  // reader nodes and arena edges only arise for tasks touching subdivided
+  // tiles (E5); overflow of any cap is reported as ST_ENGINE_LIMIT, never
+  // silently truncated
+  p.maxrn = 2 * p.maxt + p.maxcells;
+  p.maxedges = 8 * p.maxt;
   p.maxpb = 4096;
   p.maxgs = std::max(p.maxt, 4 * p.maxb + 8);
+  p.maxgr = p.maxb + 64;
   p.lay = slot_layout(p);
   return hp;
 }
