@@ -118,7 +118,9 @@ typedef struct {
   int64_t sum_leaves; /* leaf tasks of all expanded DAGs */
   int64_t sum_k;      /* sum over leaves of distinct blocks accessed */
   int64_t sum_edges;  /* dependence edges generated */
-  double kernel_ms;   /* CUDA-event duration of the evaluation kernel (same stream) */
+  double kernel_ms;   /* CUDA-event duration of all evaluation kernels of the call (same stream) */
+  double build_ms;    /* of which build kernels (phase-split mode) */
+  double sim_ms;      /* of which simulate kernels (phase-split mode) */
 } hesp_best;
 
 enum {
@@ -182,6 +184,7 @@ typedef struct {
   int32_t n_base_tasks, n_base_blocks, n_slots, sm_count;
   int64_t slot_bytes;
   int32_t warps_per_block, blocks_per_sm;
+  int64_t chunk;   /* candidates per build/simulate chunk (0 = fused kernel) */
 } hesp_engine_info;
 int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info);
 

@@ -230,7 +230,7 @@ __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* _
   __syncthreads();
   if (threadIdx.x == 0) {
     const int nw = (blockDim.x + 31) >> 5;
-    hesp_best r{0.0, -1, 0, 0, 0, 0, 0, 0.0};
+    hesp_best r{0.0, -1, 0, 0, 0, 0, 0, 0.0, 0.0, 0.0};
     for (int i = 0; i < nw; ++i) {
       r.n_ok += sok[i];
       r.n_evaluated += sev[i];
@@ -304,10 +304,14 @@ struct hesp_engine {
   cudaStream_t stream = nullptr;
   long long launches = 0;
   // phase-split mode (HESP_SPLIT=1): per-candidate slots for one chunk
-  bool split = false;
+  bool split = true;
   uint8_t* d_cslots = nullptr;
-  unsigned long long chunk = 0;
+  unsigned long long chunk = 0;      // max candidates per chunk (memory budget)
+  unsigned long long cslots_n = 0;   // slots currently allocated
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  static constexpr int NEV = 64;     // per-chunk kernel timing (build, sim)
+  cudaEvent_t evc[NEV][4] = {};
+  int nev_used = 0;
 };
 
 namespace {
@@ -341,21 +345,34 @@ bool grow_host(hesp_engine* e, size_t n) {
 
 int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
                  hesp_outcome* d_out, cudaStream_t st) {
-  if (!e->d_cslots) {
-    if (!ck(cudaMalloc(&e->d_cslots, (size_t)e->chunk * e->L.total), "malloc chunk slots")) return HESP_E_CUDA;
+  const unsigned long long need = count < e->chunk ? (count ? count : 1) : e->chunk;
+  if (need > e->cslots_n) {
+    if (e->d_cslots) cudaFree(e->d_cslots);
+    e->d_cslots = nullptr;
+    e->cslots_n = 0;
+    if (!ck(cudaMalloc(&e->d_cslots, (size_t)need * e->L.total), "malloc chunk slots")) return HESP_E_CUDA;
+    e->cslots_n = need;
   }
+  const unsigned long long chunk = e->cslots_n;
   if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
           "problem -> constant"))
     return HESP_E_CUDA;
   cudaEventRecord(e->ev0, st);
+  e->nev_used = 0;
   int acc = 0;
-  for (uint64_t c0 = 0; c0 < count || (count == 0 && c0 == 0); c0 += e->chunk) {
-    const uint64_t n = count - c0 < e->chunk ? count - c0 : e->chunk;
+  for (uint64_t c0 = 0; c0 < count || (count == 0 && c0 == 0); c0 += chunk) {
+    const uint64_t n = count - c0 < chunk ? count - c0 : chunk;
     cudaMemsetAsync(e->d_counter, 0, 2 * sizeof(unsigned long long), st);
+    const int ci = (int)(c0 / chunk);
+    const bool timed = ci < hesp_engine::NEV;
+    if (timed) cudaEventRecord(e->evc[ci][0], st);
     build_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs ? d_descs + c0 : nullptr, first + c0, n,
                                                                  e->d_cslots, e->d_counter);
+    if (timed) cudaEventRecord(e->evc[ci][1], st);
     sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
                                                                e->d_wbest, acc, e->d_cslots, e->d_counter + 1);
+    if (timed) cudaEventRecord(e->evc[ci][2], st);
+    e->nev_used = ci + 1 < hesp_engine::NEV ? ci + 1 : hesp_engine::NEV;
     e->launches += 2;
     acc = 1;
     if (count == 0) break;
@@ -394,6 +411,17 @@ int finish_best(hesp_engine* e, hesp_best* best, cudaStream_t st) {
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e->ev0, e->ev1);
   best->kernel_ms = ms;
+  best->build_ms = 0.0;
+  best->sim_ms = 0.0;
+  if (e->split) {
+    for (int i = 0; i < e->nev_used; ++i) {
+      float b = 0.f, m = 0.f;
+      cudaEventElapsedTime(&b, e->evc[i][0], e->evc[i][1]);
+      cudaEventElapsedTime(&m, e->evc[i][1], e->evc[i][2]);
+      best->build_ms += b;
+      best->sim_ms += m;
+    }
+  }
   return HESP_OK;
 }
 
@@ -496,20 +524,33 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   e->L = p.lay;
   if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
   cudaMemcpy(e->d_problem, &p, sizeof(Problem), cudaMemcpyHostToDevice);
-  if ((c = cudaMalloc(&e->d_scratch, (size_t)e->n_slots * e->L.total)) != cudaSuccess)
-    return fail(c, "malloc scratch");
   if ((c = cudaMalloc(&e->d_wbest, (size_t)e->n_slots * sizeof(WarpBest))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
   {
+    // Phase-split evaluation (build kernel, then simulate kernel, per chunk)
+    // is the default; HESP_SPLIT=0 selects the fused single kernel.
     const char* sp = getenv("HESP_SPLIT");
-    e->split = sp && sp[0] == '1';
+    e->split = !(sp && sp[0] == '0');
+    // Chunk = candidates whose slots are resident at once: up to 65536,
+    // bounded by ~35% of free device memory.
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    unsigned long long cap = (unsigned long long)(0.35 * (double)free_b) / (unsigned long long)e->L.total;
     const char* ch = getenv("HESP_CHUNK");
-    e->chunk = ch ? strtoull(ch, nullptr, 10) : 65536ULL;
+    unsigned long long want = ch ? strtoull(ch, nullptr, 10) : 65536ULL;
+    if (cap < 1024) cap = 1024;
+    e->chunk = want < cap ? want : cap;
   }
+  // per-warp slots only for the fused kernel; one slot for hesp_eval_detail otherwise
+  if ((c = cudaMalloc(&e->d_scratch, (size_t)(e->split ? 1 : e->n_slots) * e->L.total)) != cudaSuccess)
+    return fail(c, "malloc scratch");
   if ((c = cudaMallocHost(&e->h_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc host");
   if ((c = cudaEventCreate(&e->ev0)) != cudaSuccess) return fail(c, "event");
   if ((c = cudaEventCreate(&e->ev1)) != cudaSuccess) return fail(c, "event");
+  for (int i = 0; i < hesp_engine::NEV; ++i)
+    for (int j = 0; j < 3; ++j)
+      if ((c = cudaEventCreate(&e->evc[i][j])) != cudaSuccess) return fail(c, "event");
   e->hp.p = p;
   return e;
 }
@@ -533,6 +574,9 @@ void hesp_engine_destroy(hesp_engine* e) {
   if (e->h_out) cudaFreeHost(e->h_out);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  for (int i = 0; i < hesp_engine::NEV; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (e->evc[i][j]) cudaEventDestroy(e->evc[i][j]);
   if (e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }
@@ -547,6 +591,7 @@ int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info) {
   info->slot_bytes = (int64_t)e->L.total;
   info->warps_per_block = WARPS_PER_BLOCK;
   info->blocks_per_sm = e->blocks_per_sm;
+  info->chunk = e->split ? (int64_t)e->chunk : 0;
   return HESP_OK;
 }
 

@@ -92,14 +92,15 @@ class Outcome(C.Structure):
 class Best(C.Structure):
     _fields_ = [("makespan", C.c_double), ("index", C.c_int64), ("n_ok", C.c_int64),
                 ("n_evaluated", C.c_int64), ("sum_leaves", C.c_int64), ("sum_k", C.c_int64),
-                ("sum_edges", C.c_int64), ("kernel_ms", C.c_double)]
+                ("sum_edges", C.c_int64), ("kernel_ms", C.c_double), ("build_ms", C.c_double),
+                ("sim_ms", C.c_double)]
 
 
 class EngineInfo(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("n_base_tasks", C.c_int32),
                 ("n_base_blocks", C.c_int32), ("n_slots", C.c_int32), ("sm_count", C.c_int32),
                 ("slot_bytes", C.c_int64), ("warps_per_block", C.c_int32),
-                ("blocks_per_sm", C.c_int32)]
+                ("blocks_per_sm", C.c_int32), ("chunk", C.c_int64)]
 
 
 OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
