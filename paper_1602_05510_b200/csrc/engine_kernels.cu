@@ -345,7 +345,9 @@ bool grow_host(hesp_engine* e, size_t n) {
 
 int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
                  hesp_outcome* d_out, cudaStream_t st) {
-  const unsigned long long need = count < e->chunk ? (count ? count : 1) : e->chunk;
+  // equal-size chunks under the memory cap: each chunk pays one load-balance tail
+  const unsigned long long nchunks = count ? (count + e->chunk - 1) / e->chunk : 1;
+  const unsigned long long need = count ? (count + nchunks - 1) / nchunks : 1;
   if (need > e->cslots_n) {
     if (e->d_cslots) cudaFree(e->d_cslots);
     e->d_cslots = nullptr;
