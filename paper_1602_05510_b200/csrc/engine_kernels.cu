@@ -1,10 +1,13 @@
 // engine_kernels.cu — sm_100a kernels and the C ABI (include/hesp_engine.h).
 //
-// K1 eval_kernel: persistent warps; each warp pulls candidate indices from a
-//    global atomic counter, generates (or loads) the descriptor, expands the
-//    DAG, simulates the schedule in its private scratch slot and writes a
-//    32-byte outcome.  Candidates vary ~10x in cost (early CoherenceError vs a
-//    full 1.3k-task schedule), hence dynamic pulling instead of a static split.
+// K1 per chunk of candidates, two persistent kernels (one warp per candidate,
+//    indices pulled from a global atomic counter -- candidates vary ~10x in
+//    cost: early CoherenceError vs a full 1.3k-task schedule):
+//    build_kernel: generate/load the descriptor, expand the DAG, dependences;
+//    sim_kernel:   the event loop, 32-byte outcome, per-warp best.
+//    Splitting the phases keeps every resident warp in the same code
+//    (instruction-fetch stalls 52% -> ~25%) and lets each phase have its own
+//    register budget.
 // K2 reduce_best: grid-level argmin of (makespan, index) over status == 0.
 // The multi-GPU min-reduce over NVLink (K3) lives in the host driver
 // (paper_1602_05510_b200/engine.py) on 16 bytes per rank.
@@ -36,8 +39,14 @@ struct WarpBest {
 };
 
 constexpr int WARPS_PER_BLOCK = 4;
-#ifndef HESP_MIN_BLOCKS
-#define HESP_MIN_BLOCKS 16
+// Register budgets (min resident CTAs of 4 warps per SM): the build phase
+// is latency-bound with a small live set (16 CTAs = 64 warps, 32 regs); the
+// event loop keeps ~60 values live and spills below 64 registers.
+#ifndef HESP_BUILD_MIN_BLOCKS
+#define HESP_BUILD_MIN_BLOCKS 16
+#endif
+#ifndef HESP_SIM_MIN_BLOCKS
+#define HESP_SIM_MIN_BLOCKS 8
 #endif
 
 // The problem tables live in constant memory (hx::c_problem, engine.h):
@@ -49,74 +58,9 @@ __device__ __noinline__ void generate_desc(unsigned long long index, hesp_cand_d
                 index, d);
 }
 
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
-    eval_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
-                unsigned long long count, hesp_outcome* __restrict__ out, WarpBest* __restrict__ wbest,
-                uint8_t* scratch, unsigned long long* counter) {
-  __shared__ Small smem[WARPS_PER_BLOCK];
-  __shared__ hesp_cand_desc sdesc[WARPS_PER_BLOCK];
-  const int wib = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
-  const Problem& pb = c_problem;
-  uint8_t* slot = scratch + (size_t)gw * pb.lay.total;
-  double best_mk = 0.0;
-  long long best_idx = -1, n_ok = 0, n_eval = 0, s_leaves = 0, s_k = 0, s_edges = 0;
-  for (;;) {
-    unsigned long long k = 0;
-    if (lane == 0) k = atomicAdd(counter, 1ULL);
-    k = __shfl_sync(0xffffffffu, k, 0);
-    if (k >= count) break;
-    hesp_cand_desc& d = sdesc[wib];
-    if (descs) {
-      const int32_t* src = (const int32_t*)(descs + k);
-      int32_t* dst = (int32_t*)&d;
-      for (int i = lane; i < (int)(sizeof(hesp_cand_desc) / 4); i += 32) dst[i] = src[i];
-    } else if (lane == 0) {
-      generate_desc(first_index + k, &d);
-    }
-    __syncwarp();
-    Engine<DevWarp> eng(DevWarp{}, pb, slot, &smem[wib]);
-    const Outcome o = eng.run(d);
-    __syncwarp();
-    if (lane == 0 && out) {
-      hesp_outcome r;
-      r.status = o.status;
-      r.n_leaves = o.n_leaves;
-      r.makespan = o.makespan;
-      r.assign_hash = o.assign_hash;
-      r.xfer_hash = o.xfer_hash;
-      out[k] = r;
-    }
-    ++n_eval;
-    s_leaves += o.n_leaves;
-    s_k += o.sum_k;
-    s_edges += o.n_edges;
-    if (o.status == 0) {
-      ++n_ok;
-      const long long gi = (long long)(first_index + k);
-      if (best_idx < 0 || o.makespan < best_mk || (o.makespan == best_mk && gi < best_idx)) {
-        best_mk = o.makespan;
-        best_idx = gi;
-      }
-    }
-  }
-  if (lane == 0) {
-    WarpBest b;
-    b.makespan = best_mk;
-    b.index = best_idx;
-    b.n_ok = n_ok;
-    b.n_eval = n_eval;
-    b.leaves = s_leaves;
-    b.k = s_k;
-    b.edges = s_edges;
-    wbest[gw] = b;
-  }
-}
-
 // Phase-split evaluation (chunked): every resident warp of a launch runs the
 // same phase, so the instruction working set is one phase's code.
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     build_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
                  unsigned long long count, uint8_t* slots, unsigned long long* counter) {
   __shared__ Small smem[WARPS_PER_BLOCK];
@@ -144,7 +88,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
   }
 }
 
-__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_MIN_BLOCKS)
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
                WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter) {
   __shared__ Small smem[WARPS_PER_BLOCK];
@@ -289,7 +233,8 @@ struct hesp_engine {
   BlockMeta* d_base_blocks = nullptr;
   SlotLayout L{};
   uint8_t* d_scratch = nullptr;
-  int n_slots = 0, n_blocks = 0, sm_count = 0, blocks_per_sm = 0;
+  int n_slots = 0, n_blocks = 0, sm_count = 0, blocks_per_sm = 0;  // sim kernel grid
+  int n_build_blocks = 0;
   WarpBest* d_wbest = nullptr;
   hesp_best* d_best = nullptr;
   hesp_best* h_best = nullptr;  // pinned
@@ -368,7 +313,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     const int ci = (int)(c0 / chunk);
     const bool timed = ci < hesp_engine::NEV;
     if (timed) cudaEventRecord(e->evc[ci][0], st);
-    build_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs ? d_descs + c0 : nullptr, first + c0, n,
+    build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs ? d_descs + c0 : nullptr, first + c0, n,
                                                                  e->d_cslots, e->d_counter);
     if (timed) cudaEventRecord(e->evc[ci][1], st);
     sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
@@ -388,20 +333,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
 
 int launch_eval(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
                 hesp_outcome* d_out, cudaStream_t st) {
-  if (e->split) return launch_split(e, d_descs, first, count, d_out, st);
-  if (!ck(cudaMemsetAsync(e->d_counter, 0, sizeof(unsigned long long), st), "memset counter"))
-    return HESP_E_CUDA;
-  if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
-          "problem -> constant"))
-    return HESP_E_CUDA;
-  cudaEventRecord(e->ev0, st);
-  eval_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs, first, count, d_out, e->d_wbest,
-                                                            e->d_scratch, e->d_counter);
-  cudaEventRecord(e->ev1, st);
-  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
-  e->launches += 2;
-  if (!ck(cudaGetLastError(), "eval launch")) return HESP_E_CUDA;
-  return HESP_OK;
+  return launch_split(e, d_descs, first, count, d_out, st);
 }
 
 int finish_best(hesp_engine* e, hesp_best* best, cudaStream_t st) {
@@ -502,7 +434,11 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     return fail(c, "stream");
   e->sm_count = prop.multiProcessorCount;
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, eval_kernel, WARPS_PER_BLOCK * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sim_kernel, WARPS_PER_BLOCK * 32, 0);
+  int bbps = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bbps, build_kernel, WARPS_PER_BLOCK * 32, 0);
+  if (bbps < 1) bbps = 1;
+  e->n_build_blocks = prop.multiProcessorCount * bbps;
   if (bps < 1) bps = 1;
   e->blocks_per_sm = bps;
   e->n_blocks = e->sm_count * bps;
@@ -530,10 +466,7 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
   {
-    // Phase-split evaluation (build kernel, then simulate kernel, per chunk)
-    // is the default; HESP_SPLIT=0 selects the fused single kernel.
-    const char* sp = getenv("HESP_SPLIT");
-    e->split = !(sp && sp[0] == '0');
+    e->split = true;
     // Chunk = candidates whose slots are resident at once: up to 65536,
     // bounded by ~35% of free device memory.
     size_t free_b = 0, total_b = 0;
