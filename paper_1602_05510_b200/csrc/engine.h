@@ -264,8 +264,8 @@ struct Engine {
   HX int32_t* t_poff() const { return (int32_t*)(slot + PB.lay.t_poff); }
   HX int32_t* t_pcnt() const { return (int32_t*)(slot + PB.lay.t_pcnt); }
   HX int32_t* leaf() const { return (int32_t*)(slot + PB.lay.leaf); }
-  // per-task working set: 3 block ids in id order + count (built in build_deps)
-  HX int4* wsb() const { return (int4*)(slot + PB.lay.wsb); }
+  // per-task event-loop record (built in build_deps)
+  HX STask* wsb() const { return (STask*)(slot + PB.lay.wsb); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -887,11 +887,15 @@ struct Engine {
         {
           int w[4];
           const int nw = working_set(t, w);
-          int4 ws;
-          ws.x = w[0];
-          ws.y = nw > 1 ? w[1] : -1;
-          ws.z = nw > 2 ? w[2] : -1;
-          ws.w = nw;
+          STask ws;
+          ws.ws0 = w[0];
+          ws.ws1 = nw > 1 ? w[1] : -1;
+          ws.ws2 = nw > 2 ? w[2] : -1;
+          ws.nw = nw;
+          ws.out = t.blk[t.nrd];
+          ws.kb = (int)t.kind | ((int)t.bidx << 8);
+          ws.b = t.b;
+          ws.pad = 0;
           wsb()[j] = ws;
         }
         int kt = 0;
@@ -1723,7 +1727,7 @@ struct Engine {
 #define pl (PB.ordering == ORD_PL)
     const int nl = nleaves;
     constexpr bool fst = FASTT;
-    auto Vr = [&](int b, int s) -> double& { return VV[(size_t)b * S_ + s]; };
+    auto Vr = [&](int b, int s) -> double& { return VV[b * S_ + s]; };
     auto taskm = [&](int id) -> TaskMeta { return id < nbt_ ? BT[id] : TM[id - nbt_]; };
     auto tileof = [&](int b) -> int { return b < nbb_ ? BB[b].tile : BM[b - nbb_].tile; };
     auto bytesof = [&](int b) -> long long {
@@ -1774,6 +1778,9 @@ struct Engine {
       ptype.own(q) = q < P ? PB.proc_type[q] : 0;
       pspace.own(q) = q < P ? PB.proc_space[q] : 0;
     }
+#if defined(__CUDACC__)
+    const int eft_k = wp.lane() / S_, eft_sp = wp.lane() - (wp.lane() / S_) * S_;  // lane = (block, space)
+#endif
     rng = PB.sched_seed;
     double tnow = 0.0, mk = 0.0;
     uint64_t ah = 0, xh = 0;
@@ -1781,7 +1788,7 @@ struct Engine {
     now = 0.0;
 
     // plan_transfer (sim.cpp:468-499) on lane-owned link clocks
-    auto xfer = [&](int blk, long long nbytes, int src, int dst, double data_ready) -> double {
+    auto xfer = [&](int blk, long long nbytes, int bi, int src, int dst, double data_ready) -> double {
       const int nh = PB.route_n[src * MAXS + dst];
       if (nh == 0) {
         st = ST_NO_ROUTE;
@@ -1791,7 +1798,7 @@ struct Engine {
       NOUNROLL for (int h = 0; h < nh; ++h) {
         const int l = PB.route_l[src * MAXS + dst][h];
         const double s0 = dmax(lf.get(l), rdy);
-        const double en = s0 + PB.link_lat[l] + (double)nbytes / PB.link_bw[l];
+        const double en = s0 + PB.link_lat[l] + PB.hopq[l][bi];  // (s0 + lat) + bytes/bw
         lf.set(l, en);
         rdy = en;
         if (h == 0) start0 = s0;
@@ -1822,7 +1829,7 @@ struct Engine {
       }
     };
     // acquire (sim.cpp:501-519)
-    auto acquire_h = [&](int b, int s) -> double {
+    auto acquire_h = [&](int b, int s, int bi, long long nbytes) -> double {
       const double v = Vr(b, s);
       if (v != ABSENT) {
         if (!fst) LU(b, s) = dmax(LU(b, s), tnow);
@@ -1830,7 +1837,7 @@ struct Engine {
       }
       const int src = srcsp(b, s);
       if (src >= 0) {
-        const double arr = xfer(b, bytesof(b), src, s, Vr(b, src));
+        const double arr = xfer(b, nbytes, bi, src, s, Vr(b, src));
         if (st) return 0.0;
         if (!fst) {
           pin(src, b, arr);
@@ -1966,11 +1973,12 @@ struct Engine {
       int done = 0;
       NOUNROLL for (; done < nr; ++done) {
         const int j = RS[done];
-        const TaskMeta t = taskm(j);
+        const STask tk = HOT_ARR(const STask, wsb)[j];
+        const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
         const double rel = T[j].rel;
-        const int4 ws4 = HOT_ARR(const int4, wsb)[j];
-        const int w[4] = {ws4.x, ws4.y, ws4.z, -1};
-        const int nw = ws4.w;
+        const int w[4] = {tk.ws0, tk.ws1, tk.ws2, -1};
+        const int nw = tk.nw;
+        const long long tbytes = (long long)tk.b * tk.b * elem;  // every block of a task has its side
         int p = -1;
         // ---------------- processor selection (sim.cpp:136-192) ----------------
         if (waits) {
@@ -1993,7 +2001,7 @@ struct Engine {
             int id = -1;
             NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
               if (!((idle_mask >> q) & 1u)) continue;
-              const double tt = PB.ttime[t.kind][t.bidx][ptype.own(q)];
+              const double tt = PB.ttime[tkind][tbidx][ptype.own(q)];
               if (id < 0 || tt < a) {
                 a = tt;
                 id = q;
@@ -2016,7 +2024,7 @@ struct Engine {
               const unsigned FULL = 0xffffffffu;
               const int lane = wp.lane();
               const int Sx = S_;
-              const int k = lane / Sx, sp = lane - k * Sx;
+              const int k = eft_k, sp = eft_sp;
               const bool act = k < nw;
               const int b = k == 0 ? w[0] : (k == 1 ? w[1] : (k == 2 ? w[2] : w[3]));
               const double v = act ? Vr(b, sp) : ABSENT;
@@ -2037,15 +2045,15 @@ struct Engine {
               if (src >= 0) {
                 nh = PB.route_n[src * MAXS + sp];
                 if (nh == 0) noroute = true;
-                // every block of a task has the task's side (graph.cpp:303-307)
-                const double nbytes = (double)((long long)t.b * t.b * elem);
+                // every block of a task has the task's side (graph.cpp:303-307):
+                // hop cost lat + bytes/bw precomputed per (link, side)
                 if (nh >= 1) {
                   l0 = PB.route_l[src * MAXS + sp][0];
-                  c0 = PB.link_lat[l0] + nbytes / PB.link_bw[l0];
+                  c0 = PB.hopc[l0][tbidx];
                 }
                 if (nh >= 2) {
                   l1 = PB.route_l[src * MAXS + sp][1];
-                  c1 = PB.link_lat[l1] + nbytes / PB.link_bw[l1];
+                  c1 = PB.hopc[l1][tbidx];
                 }
               }
               double acc0 = 0.0, acc1 = 0.0;
@@ -2098,7 +2106,7 @@ struct Engine {
             const double nf = pf.own(q);
             double qa, qb = 0.0;
             if (sel == SEL_EFTP) {
-              qa = dmax(dmax(nf, rel), estp.own(q)) + PB.ttime[t.kind][t.bidx][ptype.own(q)];
+              qa = dmax(dmax(nf, rel), estp.own(q)) + PB.ttime[tkind][tbidx][ptype.own(q)];
               qb = nf;
             } else {
               qa = nf;  // EIT-P
@@ -2124,7 +2132,7 @@ struct Engine {
         double inputs = 0.0;
         double saved[4];
         NOUNROLL for (int k = 0; k < nw; ++k) {
-          const double a = acquire_h(w[k], s);
+          const double a = acquire_h(w[k], s, tbidx, tbytes);
           if (st) return fail(st);
           inputs = dmax(inputs, a);
           if (!fst) {
@@ -2132,7 +2140,7 @@ struct Engine {
             setPIN(w[k], s, HOLD);
           }
         }
-        const int out = t.blk[t.nrd];
+        const int out = tk.out;
         if (!fst) {
           cold_in();
           reserve_bytes(out, s, tnow);
@@ -2140,7 +2148,7 @@ struct Engine {
           if (st) return fail(st);
         }
         const double start = dmax(dmax(pf.get(p), rel), inputs);
-        const double end = start + PB.ttime[t.kind][t.bidx][type];
+        const double end = start + PB.ttime[tkind][tbidx][type];
         if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
         pf.set(p, end);
         ah += hesp_assign_term(j, p, dbits(start), dbits(end));

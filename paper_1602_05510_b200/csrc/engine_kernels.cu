@@ -46,7 +46,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 #define HESP_BUILD_MIN_BLOCKS 16
 #endif
 #ifndef HESP_SIM_MIN_BLOCKS
-#define HESP_SIM_MIN_BLOCKS 8
+#define HESP_SIM_MIN_BLOCKS 12
 #endif
 
 // The problem tables live in constant memory (hx::c_problem, engine.h):

@@ -72,6 +72,13 @@ struct BasePreds {
   int32_t soff[3], scnt[3];
 };
 
+// Per-task record of the event loop (built once per candidate): sorted
+// working set, output block, kind | bidx << 8, block side.
+struct STask {
+  int32_t ws0, ws1, ws2, nw;
+  int32_t out, kb, b, pad;
+};
+
 // Per-candidate state carried from the build kernel to the simulate kernel.
 struct SlotHeader {
   int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, pad;
@@ -106,6 +113,11 @@ struct Problem {
   double ttime[4][MAXBV][MAXTYPES];  // task_time(kind, b, type)
   double ctavg[4][MAXBV];            // critical_times' per-task mean over processors (sim.cpp:96-106)
   uint8_t known[4][MAXTYPES];        // PerfModel::knows
+  // per (link, block side): bytes/bw and lat + bytes/bw of moving one block,
+  // the same IEEE operations as transfer_time/plan_transfer (platform.cpp:207,
+  // sim.cpp:486, 785-787), so the device never divides on the hot path
+  double hopq[MAXL][MAXBV];
+  double hopc[MAXL][MAXBV];
   // ---- workload ----
   int64_t n;
   int32_t elem;
@@ -159,7 +171,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.t_poff = take(4 * T);
   L.t_pcnt = take(4 * T);
   L.leaf = take(4 * T);
-  L.wsb = take(16 * T);
+  L.wsb = take(sizeof(STask) * T);
   L.bm = take(sizeof(BlockMeta) * B);
   L.bflags = take(4 * B);
   L.valid = take(8 * B * S);

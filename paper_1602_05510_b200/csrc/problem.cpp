@@ -235,6 +235,13 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
     }
   }
 
+  for (int l = 0; l < p.L; ++l)
+    for (int i = 0; i < p.nbv; ++i) {
+      const long long bytes = p.bval[i] * p.bval[i] * wl.elem_size;
+      p.hopq[l][i] = static_cast<double>(bytes) / p.link_bw[l];
+      p.hopc[l][i] = p.link_lat[l] + static_cast<double>(bytes) / p.link_bw[l];
+    }
+
   // ---------------- base tiling via the width-1 engine ----------------
   {
     Problem bp = p;
