@@ -266,6 +266,9 @@ struct Engine {
   HX int32_t* leaf() const { return (int32_t*)(slot + PB.lay.leaf); }
   // per-task event-loop record (built in build_deps)
   HX STask* wsb() const { return (STask*)(slot + PB.lay.wsb); }
+  HX int4* bcell() const { return (int4*)(slot + PB.lay.bcell); }      // cell range per block
+  HX uint16_t* rht() const { return (uint16_t*)(slot + PB.lay.rht); }  // region hash of new blocks
+  HX uint8_t* pmark() const { return (uint8_t*)(slot + PB.lay.pmark); }  // 1 + partition entry per task id
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -347,6 +350,8 @@ struct Engine {
       if (sm->part[i].task == task) return i;
     return -1;
   }
+  // O(1) variant once pmark() is filled (build_order onwards)
+  HX int part_of(int task) const { return (int)pmark()[task] - 1; }
   HX int bidx_of(long long b) const {
     NOUNROLL for (int i = 0; i < PB.nbv; ++i)
       if (PB.bval[i] == b) return i;
@@ -360,6 +365,13 @@ struct Engine {
   // Existing block with exactly region r (DataDag::find_by_region).  t >= 0:
   // r lies inside base tile t, so only the root, the tile and the tile's
   // blocks can match.  t < 0 (base build): every block.
+  static HX unsigned rhash(const Region& r) {
+    unsigned h = (unsigned)r.row * 0x9E3779B1u ^ (unsigned)r.col * 0x85EBCA77u ^ (unsigned)r.rows * 0xC2B2AE3Du;
+    h ^= h >> 15;
+    return h * 0x27D4EB2Fu;
+  }
+  HX bool rht_usable() const { return nblocks - nbb < RHT / 2; }
+
   HXN int find_block(const Region& r, int t) {
     if (t < 0) {
       int found = -1;
@@ -376,6 +388,15 @@ struct Engine {
     }
     if (rsame(reg(0), r)) return 0;
     if (rsame(reg(t), r)) return t;
+    if (rht_usable()) {  // open addressing over the candidate's own blocks
+      unsigned i = rhash(r) & (RHT - 1);
+      NOUNROLL for (;;) {
+        const int e = rht()[i];
+        if (e == 0xffff) return -1;
+        if (rsame(bm()[e].r, r)) return nbb + e;
+        i = (i + 1) & (RHT - 1);
+      }
+    }
     NOUNROLL for (int base = nbb; base < nblocks; base += WP::W) {
       const int b = base + wp.lane();
       const bool hit = b < nblocks && bm()[b - nbb].tile == t && rsame(bm()[b - nbb].r, r);
@@ -398,6 +419,11 @@ struct Engine {
     m.isint = isint ? 1 : 0;
     m.pad = 0;
     if (wp.lane() == 0) bm()[id - nbb] = m;
+    if (t >= 0 && id - nbb < RHT / 2) {
+      unsigned i = rhash(r) & (RHT - 1);
+      while (rht()[i] != 0xffff) i = (i + 1) & (RHT - 1);
+      if (wp.lane() == 0) rht()[i] = (uint16_t)(id - nbb);
+    }
     wp.sync();
     return id;
   }
@@ -673,12 +699,17 @@ struct Engine {
   // Leaf program order: lexicographic seq, i.e. depth-first over clusters
   // with members in emission order (graph.cpp:552-562).
   HXN void build_order() {
+    NOUNROLL for (int i = wp.lane(); i < ntasks; i += WP::W) pmark()[i] = 0;
+    wp.sync();
+    if (wp.lane() == 0)
+      for (int i = 0; i < npart; ++i) pmark()[sm->part[i].task] = (uint8_t)(i + 1);
+    wp.sync();
     // subtree leaf() counts, innermost partitions last in op order
     NOUNROLL for (int i = npart - 1; i >= 0; --i) {
       const PartEntry pe = sm->part[i];
       int cnt = 0;
       NOUNROLL for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
-        const int pi = part_index(c);
+        const int pi = part_of(c);
         cnt += pi >= 0 ? sm->part[pi].leaves : 1;
       }
       if (wp.lane() == 0) sm->part[i].leaves = cnt;
@@ -687,7 +718,7 @@ struct Engine {
     // explicit stack of (first child, count, output position)
     int sf[MAXPART], sc[MAXPART], sp[MAXPART];
     int top = 0;
-    const int r = part_index(0);
+    const int r = part_of(0);
     if (r < 0) {  // unpartitioned root: a single leaf()
       if (wp.lane() == 0) leaf()[0] = 0;
       wp.sync();
@@ -707,7 +738,7 @@ struct Engine {
         const int k = base + wp.lane();
         int pi = -1, sz = 0;
         if (k < c) {
-          pi = part_index(f + k);
+          pi = part_of(f + k);
           sz = pi >= 0 ? sm->part[pi].leaves : 1;
         }
         int incl = sz;
@@ -829,6 +860,23 @@ struct Engine {
         tl_coff()[t] = nc_used;
       }
       wp.sync();
+      // cell rectangle of the tile and of each of its blocks, once
+      NOUNROLL for (int k = wp.lane(); k < cnt + 1; k += WP::W) {
+        const int b = k == 0 ? t : tl_ids()[tl_head()[t] + k - 1];
+        const Region rg = reg(b);
+        int4 cr;
+        cr.x = cr.y = cr.z = cr.w = 0;
+        NOUNROLL for (int q = 0; q < nr; ++q) {
+          if (rows[q] == rg.row) cr.x = q;
+          if (rows[q] == rg.row + rg.rows) cr.y = q;
+        }
+        NOUNROLL for (int q = 0; q < nc; ++q) {
+          if (rows[nr + q] == rg.col) cr.z = q;
+          if (rows[nr + q] == rg.col + rg.cols) cr.w = q;
+        }
+        bcell()[b] = cr;
+      }
+      wp.sync();
       nb_used += nr + nc;
       nc_used += ncell;
     }
@@ -843,19 +891,11 @@ struct Engine {
       r1 = c1 = 1;
       return;
     }
-    const int nr = tl_nrb()[t], nc = tl_ncb()[t];
-    const Region r = reg(b);
-    const int* rows = bnd() + off;
-    const int* cols = rows + nr;
-    r0 = r1 = c0 = c1 = 0;
-    NOUNROLL for (int k = 0; k < nr; ++k) {
-      if (rows[k] == r.row) r0 = k;
-      if (rows[k] == r.row + r.rows) r1 = k;
-    }
-    NOUNROLL for (int k = 0; k < nc; ++k) {
-      if (cols[k] == r.col) c0 = k;
-      if (cols[k] == r.col + r.cols) c1 = k;
-    }
+    const int4 cr = bcell()[b];  // precomputed in build_cells
+    r0 = cr.x;
+    r1 = cr.y;
+    c0 = cr.z;
+    c1 = cr.w;
   }
 
   // Predecessor list of leaf j: candidate arena (off >= 0) or, for base tasks
@@ -2269,6 +2309,8 @@ struct Engine {
 
   // Starts from the base tiling (root + base cluster, shared tables).
   HXN void reset_to_base() {
+    NOUNROLL for (int i = wp.lane(); i < RHT / 2; i += WP::W) ((uint32_t*)rht())[i] = 0xffffffffu;
+    wp.sync();
     status = 0;
     ntasks = nbt;
     nblocks = nbb;
