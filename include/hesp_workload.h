@@ -226,24 +226,25 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
 
 /* Order-independent result hashes (sum of mixed terms, wrapping).  Both the
  * oracle harness and the engine fold every assignment / transfer record of a
- * schedule into these, so equality means bit-identical records.  Two
- * splitmix finaliser rounds per record keep them cheap on the device. */
+ * schedule into these, so equality means bit-identical records.  One
+ * splitmix finaliser round per record over a rotation/xor combination of
+ * every field keeps them cheap on the device. */
+HESP_HD uint64_t hesp_rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
 HESP_HD uint64_t hesp_assign_term(int32_t task, int32_t proc, uint64_t start_bits,
                                   uint64_t end_bits) {
-  const uint64_t h = hesp_mix64(((uint64_t)(uint32_t)task << 32) ^ (uint64_t)(uint32_t)proc ^
-                                (start_bits * 0x9e3779b97f4a7c15ULL));
-  return hesp_mix64(h ^ end_bits);
+  return hesp_mix64((start_bits + hesp_rotl64(end_bits, 21)) ^
+                    (((uint64_t)(uint32_t)task << 32) | (uint64_t)(uint32_t)proc));
 }
 
 HESP_HD uint64_t hesp_xfer_term(int32_t block, int32_t src_space, int32_t dst_space, int64_t bytes,
                                 uint64_t start_bits, uint64_t end_bits, int64_t frow, int64_t fcol,
                                 int64_t frows, int64_t fcols) {
-  const uint64_t h = hesp_mix64(((uint64_t)(uint32_t)block << 24) ^ ((uint64_t)(uint32_t)src_space << 16) ^
-                                ((uint64_t)(uint32_t)dst_space << 8) ^ ((uint64_t)bytes * 0xc2b2ae3d27d4eb4fULL) ^
-                                start_bits);
-  const uint64_t f = ((uint64_t)frow << 32 ^ (uint64_t)fcol) * 0x165667b19e3779f9ULL ^
-                     ((uint64_t)frows << 32 ^ (uint64_t)fcols);
-  return hesp_mix64(h ^ (end_bits * 0x9e3779b97f4a7c15ULL) ^ f);
+  const uint64_t id = ((uint64_t)(uint32_t)block << 24) ^ ((uint64_t)(uint32_t)src_space << 16) ^
+                      ((uint64_t)(uint32_t)dst_space << 8);
+  const uint64_t f = hesp_rotl64(((uint64_t)frow << 32) ^ (uint64_t)(uint32_t)fcol, 7) ^
+                     hesp_rotl64(((uint64_t)frows << 32) ^ (uint64_t)(uint32_t)fcols, 29);
+  return hesp_mix64((start_bits + hesp_rotl64(end_bits, 21)) ^ hesp_rotl64((uint64_t)bytes, 40) ^ id ^ f);
 }
 
 #ifdef __cplusplus

@@ -1131,20 +1131,39 @@ struct Engine {
   // critical_times (sim.cpp:92-115): ct = avg + max(0, max_succ ct), reverse
   // program order; pushed to preds() so each pred sees all its successors.
   HXN void build_ct() {
-    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].rel = 0.0;  // .rel holds best_succ here
+    // ct(j) = avg(j) + max(0, max over successors ct(s)); successors lie later
+    // in program order.  Chunks of 32 leaves from the end: a lane finalises
+    // its task once every successor's ct is known (-1 = not yet), so a chunk
+    // needs as many rounds as its longest internal successor chain.
+    NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].ct = -1.0;
     wp.sync();
-    NOUNROLL for (int li = nleaves - 1; li >= 0; --li) {
-      const int j = leaf()[li];
-      const TaskMeta t = task(j);
-      const double c = PB.ctavg[t.kind][t.bidx] + ts()[j].rel;
-      const int32_t* pl_ = pred_list(j);
-      const int cnt = t_pcnt()[j];
-      NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) {
-        const int p = pl_[q];
-        ts()[p].rel = dmax(ts()[p].rel, c);
+    NOUNROLL for (int hi = nleaves; hi > 0; hi -= WP::W) {
+      const int li = hi - WP::W + wp.lane();
+      bool todo = li >= 0;
+      int j = -1;
+      double avg = 0.0;
+      if (todo) {
+        j = leaf()[li];
+        const int kb = wsb()[j].kb;
+        avg = PB.ctavg[kb & 0xff][kb >> 8];
       }
-      if (wp.lane() == 0) ts()[j].ct = c;
-      wp.sync();
+      NOUNROLL while (wp.any(todo)) {
+        if (todo) {
+          const TState& tj = ts()[j];
+          double best = 0.0;
+          bool ready = true;
+          NOUNROLL for (int q = 0; q < tj.scnt; ++q) {
+            const double c = ts()[succs()[tj.soff + q]].ct;
+            if (c < 0.0) ready = false;
+            best = dmax(best, c);
+          }
+          if (ready) {
+            ts()[j].ct = avg + best;
+            todo = false;
+          }
+        }
+        wp.sync();
+      }
     }
   }
 
