@@ -42,7 +42,7 @@ struct Record {
 static_assert(sizeof(Record) == 40, "record layout");
 
 struct Args {
-  std::string platform, model, out, detail_out;
+  std::string platform, model, out, detail_out, descs;
   bool model_csv = false;
   int64_t n = 16384;
   int elem = 4;
@@ -84,11 +84,14 @@ struct Ctx {
   int32_t s_base_snapped;
 };
 
+std::vector<hesp_cand_desc> g_descs;  // --descs: explicit candidates (index = position)
+
 Record evaluate(const Ctx& c, uint64_t index, hesp::SimResult* keep, hesp::TaskGraph** keep_graph) {
   Record r{};
   r.index = index;
   hesp_cand_desc d;
-  hesp_generate(&c.a->gen, c.s_base_snapped, c.n_base, c.base_b, index, &d);
+  if (!g_descs.empty()) d = g_descs.at(index);
+  else hesp_generate(&c.a->gen, c.s_base_snapped, c.n_base, c.base_b, index, &d);
   try {
     auto g = hesp::TaskGraph::root_cholesky(c.a->n, c.a->elem);
     g.partition_task(0, 1.0 / c.a->s_base, c.a->gen.min_block);
@@ -179,12 +182,20 @@ int main(int argc, char** argv) {
     else if (k == "--detail") a.detail = std::atol(v());
     else if (k == "--detail-out") a.detail_out = v();
     else if (k == "--quiet") a.quiet = true;
+    else if (k == "--descs") a.descs = v();
     else {
       std::fprintf(stderr, "unknown argument %s\n", k.c_str());
       return 2;
     }
   }
   if (a.threads <= 0) a.threads = static_cast<int>(std::thread::hardware_concurrency());
+  if (!a.descs.empty()) {
+    std::ifstream f(a.descs, std::ios::binary);
+    hesp_cand_desc d;
+    while (f.read(reinterpret_cast<char*>(&d), sizeof d)) g_descs.push_back(d);
+    a.first = 0;
+    a.count = g_descs.size();
+  }
 
   const auto plat = hesp::Platform::from_json(slurp(a.platform));
   const auto model = a.model_csv ? hesp::PerfModel::from_table_csv(slurp(a.model))
@@ -210,7 +221,8 @@ int main(int argc, char** argv) {
     Record r = evaluate(c, static_cast<uint64_t>(a.detail), &res, &g);
     FILE* f = a.detail_out.empty() ? stdout : std::fopen(a.detail_out.c_str(), "w");
     hesp_cand_desc d;
-    hesp_generate(&a.gen, c.s_base_snapped, c.n_base, c.base_b, r.index, &d);
+    if (!g_descs.empty()) d = g_descs.at(r.index);
+    else hesp_generate(&a.gen, c.s_base_snapped, c.n_base, c.base_b, r.index, &d);
     std::fprintf(f, "index %llu status %d leaves %d makespan %.17g bits %016llx ah %016llx xh %016llx\n",
                  (unsigned long long)r.index, r.status, r.n_leaves, r.makespan,
                  (unsigned long long)bits(r.makespan), (unsigned long long)r.assign_hash,

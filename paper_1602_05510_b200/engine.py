@@ -319,6 +319,19 @@ class BatchEngine:
         self._check(self.lib.hesp_generate_device(self.h, first, count, C.c_void_p(descs_ptr),
                                                   C.c_void_p(stream) if stream else None), "generate_device")
 
+    def eval_detail(self, desc: np.ndarray, cap: int):
+        """Per-task (proc, start, end) of one candidate (proc -1 = not a scheduled leaf)."""
+        desc = np.ascontiguousarray(desc, DESC_DTYPE).reshape(1)
+        proc = np.full(cap, -1, np.int32)
+        start = np.zeros(cap, np.float64)
+        end = np.zeros(cap, np.float64)
+        o = Outcome()
+        rc = self.lib.hesp_eval_detail(self.h, desc.ctypes.data, cap, proc.ctypes.data, start.ctypes.data,
+                                       end.ctypes.data, C.byref(o))
+        if rc < 0:
+            self._check(rc, "eval_detail")
+        return o, proc, start, end
+
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)
         self._check(self.lib.hesp_generate_host(self.h, first, count, d.ctypes.data), "generate_host")

@@ -26,11 +26,94 @@ from paper_1602_05510_b200.engine import FIXTURES  # noqa: E402
 
 HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
 
+# Hand-built candidates on the C2 base tiling (n=16384, 16x16 tiles of 1024; base
+# task ids 1..816 in CHOL loop order: 1 CHOL(0,0), 2..16 TRSM(i,0), 17 SYRK(1,0),
+# 18 GEMM(2,1,0), ...).  Statuses cover the reference's partition_task errors
+# (graph.cpp:457-481): NotALeaf, Validation (unknown id, p not in (0,1)),
+# IndivisibleGrain; plus tile-count snapping, a 16-way split, a 5-deep chain,
+# 16 ops, and every kind partitioned.
+EXPLICIT_OPS = [
+    [],                                             # base tiling only
+    [(0, 2)],                                       # root already partitioned -> NotALeaf
+    [(5000, 2)],                                    # no such task -> Validation
+    [(1, 1)],                                       # p = 1 -> Validation
+    [(1, 0)],                                       # p = inf -> Validation
+    [(1, -2)],                                      # p < 0 -> Validation
+    [(1, 3)],                                       # snaps to 2
+    [(1, 5)],                                       # snaps to 4
+    [(1, 16)],                                      # 816-task sub-Cholesky of 64-tiles
+    [(1, 1000)],                                    # snaps to 16
+    [(1, 2), (817, 2), (821, 2), (825, 2), (829, 2)],  # 1024->512->256->128->64 -> IndivisibleGrain
+    [(1, 2), (817, 2), (821, 2), (825, 2)],         # deepest valid chain (depth 5)
+    [(2, 2), (2, 2)],                               # second split of the same task -> NotALeaf
+    [(t, 2) for t in range(1, 17)],                 # 16 ops
+    [(18, 4), (17, 2), (2, 4), (1, 2)],             # GEMM, SYRK, TRSM, CHOL
+    [(18, 4), (818, 2), (900, 2), (17, 4)],          # sub-tasks of sub-tasks, mixed sides
+]
+# n=6144 base (8x8 tiles of 768): mixing s=3 (256) and s=2 (384) on overlapping
+# operands creates intersection descriptors (graph.cpp:197-210).
+SECT_OPS = [
+    [(1, 3), (2, 2)],
+    [(2, 2), (1, 3), (3, 3)],
+    [(1, 2), (2, 3), (9, 3), (10, 2)],
+    [(1, 3), (2, 2), (4, 3), (5, 2), (9, 2)],
+]
+EXPLICIT = {
+    "explicit_c2": ("c2", EXPLICIT_OPS),
+    "explicit_c3": ("c3", EXPLICIT_OPS),
+    "explicit_sect": ("sect_cpugpu", SECT_OPS),
+}
+# (preset, candidate index, explicit descs file or None)
+DETAIL = {
+    "detail_c2_1": ("c2", 1, None),
+    "detail_explicit_c2_14": ("c2", 14, "explicit_c2"),
+    "detail_evict_wb_0": ("evict_wb", 0, None),
+}
+
+
+def write_descs(path, ops_lists):
+    import numpy as np
+    from paper_1602_05510_b200.engine import DESC_DTYPE, MAX_OPS
+    d = np.zeros(len(ops_lists), DESC_DTYPE)
+    d["ops"][:] = -1
+    d["ops"][:, :, 1] = 0
+    for i, ops in enumerate(ops_lists):
+        d[i]["n_ops"] = len(ops)
+        for k, (t, s) in enumerate(ops):
+            d[i]["ops"][k] = (t, s)
+    d.tofile(path)
+
 
 def main(names):
     if not os.path.exists(HARNESS):
         subprocess.run(["make", "-C", os.path.join(ROOT, "oracle")], check=True)
-    for name in names or sorted(PARITY):
+    # explicit descriptors: error paths and edge cases the generator never emits
+    for name, (preset_name, ops_lists) in EXPLICIT.items():
+        if names and name not in names:
+            continue
+        p, _ = PARITY[preset_name]
+        dpath = os.path.join(HERE, f"{name}.descs")
+        write_descs(dpath, ops_lists)
+        out = os.path.join(HERE, f"{name}.bin")
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--descs", dpath, "--threads",
+                            str(os.cpu_count()), "--out", out], check=True, capture_output=True, text=True)
+        print(name, r.stdout.strip())
+    # per-task schedules of a few candidates (hesp_eval_detail parity)
+    for name, (preset_name, idx, descs_name) in DETAIL.items():
+        if names and name not in names:
+            continue
+        p, _ = PARITY[preset_name]
+        args = [HARNESS, *harness_args(p, FIXTURES), "--detail", str(idx), "--detail-out",
+                os.path.join(HERE, f"{name}.txt")]
+        if descs_name:
+            args += ["--descs", os.path.join(HERE, f"{descs_name}.descs")]
+        subprocess.run(args, check=True)
+        path = os.path.join(HERE, f"{name}.txt")
+        keep = [l for l in open(path) if l.startswith(("index", "ops", "A "))]
+        with open(path, "w") as f:
+            f.writelines(keep)
+        print(name, "detail written")
+    for name in [n for n in (names or sorted(PARITY)) if n in PARITY]:
         p, count = PARITY[name]
         out = os.path.join(HERE, f"{name}.bin")
         cmd = [HARNESS, *harness_args(p, FIXTURES), "--first", "0", "--count", str(count),

@@ -50,3 +50,55 @@ def test_descs_path_matches_generated(lib):
     out2, b2 = eng.eval_generated(0, count)
     assert np.array_equal(out1, out2)
     assert (b1.makespan, b1.index) == (b2.makespan, b2.index)
+
+
+EXPLICIT = {"explicit_c2": "c2", "explicit_c3": "c3", "explicit_sect": "sect_cpugpu"}
+
+
+@pytest.mark.parametrize("name", sorted(EXPLICIT))
+def test_explicit_descriptor_parity(lib, name):
+    """Hand-built candidates (error statuses, snapping, deep chains, 16 ops,
+    intersections) through the host-buffer ABI path, vs the reference."""
+    from golden_io import GOLDEN_DIR
+    from paper_1602_05510_b200.engine import DESC_DTYPE
+    import os
+    p, _ = PARITY[EXPLICIT[name]]
+    descs = np.fromfile(os.path.join(GOLDEN_DIR, f"{name}.descs"), DESC_DTYPE)
+    g = read_golden(name)
+    eng = make_engine(p)
+    out, best = eng.eval_descs(descs, first=0)
+    bad = compare(out, g)
+    assert not bad, "\n".join(bad[:10])
+
+
+DETAIL = {"detail_c2_1": ("c2", None), "detail_explicit_c2_14": ("c2", "explicit_c2"),
+          "detail_evict_wb_0": ("evict_wb", None)}
+
+
+@pytest.mark.parametrize("name", sorted(DETAIL))
+def test_per_task_schedule_parity(lib, name):
+    """hesp_eval_detail: every leaf's processor, start and end bits equal the
+    reference SimResult::assignments."""
+    import os
+    from golden_io import GOLDEN_DIR
+    from paper_1602_05510_b200.engine import DESC_DTYPE
+    preset, descs_name = DETAIL[name]
+    p, _ = PARITY[preset]
+    lines = open(os.path.join(GOLDEN_DIR, f"{name}.txt")).read().splitlines()
+    idx = int(lines[0].split()[1])
+    want = {}
+    for l in lines:
+        if l.startswith("A "):
+            f = l.split()
+            want[int(f[1])] = (int(f[2]), int(f[5], 16), int(f[6], 16))
+    eng = make_engine(p)
+    if descs_name:
+        desc = np.fromfile(os.path.join(GOLDEN_DIR, f"{descs_name}.descs"), DESC_DTYPE)[idx]
+    else:
+        desc = eng.generate_host(idx, 1)[0]
+    cap = max(want) + 64
+    o, proc, start, end = eng.eval_detail(desc, cap)
+    assert o.status == 0
+    got = {t: (int(proc[t]), int(np.float64(start[t]).view(np.uint64)), int(np.float64(end[t]).view(np.uint64)))
+           for t in range(cap) if proc[t] >= 0}
+    assert got == want
