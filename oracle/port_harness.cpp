@@ -31,7 +31,7 @@ int kind_of(const std::string& k) { return k == "CHOL" ? 0 : k == "TRSM" ? 1 : k
 }  // namespace
 
 int main(int argc, char** argv) {
-  std::string platform, model, out, ordering = "PL", selection = "EFT-P", caching = "WB";
+  std::string platform, model, out, descs_path, ordering = "PL", selection = "EFT-P", caching = "WB";
   bool csv = false;
   long long n = 16384, first = 0, count = 10;
   int elem = 4, s_base = 16, threads = 1;
@@ -73,6 +73,7 @@ int main(int argc, char** argv) {
     else if (k == "--time-limit") time_limit = std::stod(v());
     else if (k == "--out") out = v();
     else if (k == "--quiet") {}
+    else if (k == "--descs") descs_path = v();
     else {
       std::fprintf(stderr, "unknown argument %s\n", k.c_str());
       return 2;
@@ -120,6 +121,14 @@ int main(int argc, char** argv) {
   const long long s0 = hesp_snap_tiles(n, s_base, gen.min_block);
   const long long base_b = n / s0;
   const int n_base = hesp_member_count(HESP_CHOL, static_cast<int>(s0));
+  std::vector<hesp_cand_desc> explicit_descs;
+  if (!descs_path.empty()) {
+    std::ifstream f(descs_path, std::ios::binary);
+    hesp_cand_desc d;
+    while (f.read(reinterpret_cast<char*>(&d), sizeof d)) explicit_descs.push_back(d);
+    first = 0;
+    count = static_cast<long long>(explicit_descs.size());
+  }
   std::vector<Record> recs(count);
   std::vector<char> done(count, 0);
   std::atomic<long long> next{0};
@@ -131,7 +140,8 @@ int main(int argc, char** argv) {
       const long long k = next++;
       if (k >= count) return;
       hesp_cand_desc d;
-      hesp_generate(&gen, static_cast<int>(s0), n_base, base_b, first + k, &d);
+      if (!explicit_descs.empty()) d = explicit_descs[k];
+      else hesp_generate(&gen, static_cast<int>(s0), n_base, base_b, first + k, &d);
       const port::Result r = port::evaluate(plat, mdl, sched, n, elem, s_base, d);
       recs[k] = Record{static_cast<uint64_t>(first + k), r.status, r.leaves, r.status ? 0.0 : r.makespan,
                        r.status ? 0 : r.ahash, r.status ? 0 : r.xhash};

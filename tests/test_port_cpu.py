@@ -28,3 +28,14 @@ def test_port_matches_goldens(name, tmp_path):
     got = read_golden(str(out))
     want = read_golden(name)[:k]
     assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.skipif(not os.path.exists(PORT), reason="oracle/_ref/port_harness not built")
+@pytest.mark.parametrize("name,preset", [("explicit_c2", "c2"), ("explicit_c3", "c3"), ("explicit_sect", "sect_cpugpu")])
+def test_port_matches_explicit_goldens(name, preset, tmp_path):
+    from golden_io import GOLDEN_DIR
+    p, _ = PARITY[preset]
+    out = tmp_path / "port.bin"
+    subprocess.run([PORT, *harness_args(p, FIXTURES), "--descs", os.path.join(GOLDEN_DIR, f"{name}.descs"),
+                    "--threads", str(os.cpu_count()), "--out", str(out)], check=True, capture_output=True, timeout=600)
+    assert read_golden(str(out)).tobytes() == read_golden(name).tobytes()
