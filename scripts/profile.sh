@@ -1,7 +1,7 @@
 #!/bin/bash
 # Profiling recipe (B200_PROFILING.md) for the engine's kernels; run under gpurun.
 # usage: scripts/profile.sh <tag>
-TAG=${1:-r02}
+TAG=${1:-r03}
 mkdir -p gpurun_out
 # 1) clean bench line (not under a profiler)
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
