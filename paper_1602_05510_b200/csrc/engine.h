@@ -2085,7 +2085,7 @@ struct Engine {
               const int Sx = S_;
               const int k = eft_k, sp = eft_sp;
               const bool act = k < nw;
-              const int b = k == 0 ? w[0] : (k == 1 ? w[1] : (k == 2 ? w[2] : w[3]));
+              const int b = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
               const double v = act ? Vr(b, sp) : ABSENT;
               const unsigned vm = __ballot_sync(FULL, act && v != ABSENT);
               const unsigned mymask = act ? (vm >> (k * Sx)) & ((1u << Sx) - 1u) : 0u;
@@ -2116,8 +2116,11 @@ struct Engine {
                 }
               }
               double acc0 = 0.0, acc1 = 0.0;
+              // rebuild only if some lane transfers; only nw-1 earlier blocks exist
+              const int rounds = __any_sync(FULL, src >= 0) ? nw - 1 : 0;
 #pragma unroll
-              for (int kp = 0; kp < 3; ++kp) {  // earlier blocks of this space, in order
+              for (int kp = 0; kp < 2; ++kp) {  // earlier blocks of this space, in order
+                if (kp >= rounds) break;
                 const int from = kp * Sx + sp < 32 ? kp * Sx + sp : lane;
                 const int pl0 = __shfl_sync(FULL, l0, from), pl1 = __shfl_sync(FULL, l1, from);
                 const double pc0 = __shfl_sync(FULL, c0, from), pc1 = __shfl_sync(FULL, c1, from);
@@ -2189,14 +2192,17 @@ struct Engine {
           if (wset > PB.cap[s]) return fail(ST_CAPACITY);
         }
         double inputs = 0.0;
-        double saved[4];
-        NOUNROLL for (int k = 0; k < nw; ++k) {
-          const double a = acquire_h(w[k], s, tbidx, tbytes);
+        double saved[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {  // working set in id order (<= 3 blocks, kept in registers)
+          if (k >= nw) break;
+          const int wb = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
+          const double a = acquire_h(wb, s, tbidx, tbytes);
           if (st) return fail(st);
           inputs = dmax(inputs, a);
           if (!fst) {
-            saved[k] = PIN(w[k], s);
-            setPIN(w[k], s, HOLD);
+            saved[k] = PIN(wb, s);
+            setPIN(wb, s, HOLD);
           }
         }
         const int out = tk.out;
@@ -2217,8 +2223,11 @@ struct Engine {
           tr_end[j] = end;
         }
         mk = dmax(mk, end);
-        if (!fst)
-          NOUNROLL for (int k = 0; k < nw; ++k) setPIN(w[k], s, dmax(saved[k], end));
+        if (!fst) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            if (k < nw) setPIN(k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2), s, dmax(saved[k], end));
+        }
         // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
         // validate out and its descendants here, valid[out] = end
         {
