@@ -2193,9 +2193,7 @@ struct Engine {
         }
         double inputs = 0.0;
         double saved[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {  // working set in id order (<= 3 blocks, kept in registers)
-          if (k >= nw) break;
+        NOUNROLL for (int k = 0; k < nw; ++k) {  // working set in id order (<= 3 blocks, registers)
           const int wb = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
           const double a = acquire_h(wb, s, tbidx, tbytes);
           if (st) return fail(st);
