@@ -251,7 +251,7 @@ struct Small {
 // ---------------------------------------------------------------------------
 // Engine
 
-template <class WP>
+template <class WP, bool TRACE = false>
 struct Engine {
   WP wp;
   const Problem* pbp;
@@ -352,6 +352,12 @@ struct Engine {
   }
   // O(1) variant once pmark() is filled (build_order onwards)
   HX int part_of(int task) const { return (int)pmark()[task] - 1; }
+  // base tile with no sub-blocks: its invalidation cone is {root, itself}
+  // and it has no descendants (E1)
+  HX bool simple_tile(int b) const {
+    const int tt = b == 0 ? -1 : tile_of(b);
+    return tt > 0 && tl_cnt()[tt] == 0;
+  }
   HX int bidx_of(long long b) const {
     NOUNROLL for (int i = 0; i < PB.nbv; ++i)
       if (PB.bval[i] == b) return i;
@@ -935,7 +941,15 @@ struct Engine {
           ws.out = t.blk[t.nrd];
           ws.kb = (int)t.kind | ((int)t.bidx << 8);
           ws.b = t.b;
-          ws.pad = 0;
+          // static per-block facts the event loop would otherwise look up per
+          // commit: bit k = working-set block k is a base tile with no
+          // sub-blocks (no descendants, no intersections), bit 3 = the same
+          // for the output block (tile membership is fixed after the build)
+          int fl = 0;
+          NOUNROLL for (int k = 0; k < nw; ++k)
+            if (simple_tile(w[k])) fl |= 1 << k;
+          if (simple_tile(ws.out)) fl |= 8;
+          ws.pad = fl;
           wsb()[j] = ws;
         }
         int kt = 0;
@@ -1878,9 +1892,8 @@ struct Engine {
       st = status;
     };
     // validate_from on the hot path: an unsubdivided tile has no descendants
-    auto validate = [&](int b, int s, double at) {
-      const int tt = b == 0 ? -1 : tileof(b);
-      if (fst && tt > 0 && TLC[tt] == 0) {
+    auto validate = [&](int b, int s, double at, bool simple) {
+      if (fst && simple) {
         double& v = Vr(b, s);
         if (v > at) v = at;
       } else {
@@ -1888,7 +1901,7 @@ struct Engine {
       }
     };
     // acquire (sim.cpp:501-519)
-    auto acquire_h = [&](int b, int s, int bi, long long nbytes) -> double {
+    auto acquire_h = [&](int b, int s, int bi, long long nbytes, bool simple) -> double {
       const double v = Vr(b, s);
       if (v != ABSENT) {
         if (!fst) LU(b, s) = dmax(LU(b, s), tnow);
@@ -1905,7 +1918,7 @@ struct Engine {
           cold_out();
           if (st) return 0.0;
         }
-        validate(b, s, arr);
+        validate(b, s, arr, simple);
         return arr;
       }
       cold_in();
@@ -2033,8 +2046,8 @@ struct Engine {
       NOUNROLL for (; done < nr; ++done) {
         const int j = RS[done];
         const STask tk = HOT_ARR(const STask, wsb)[j];
-        const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
         const double rel = T[j].rel;
+        const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
         const int w[4] = {tk.ws0, tk.ws1, tk.ws2, -1};
         const int nw = tk.nw;
         const long long tbytes = (long long)tk.b * tk.b * elem;  // every block of a task has its side
@@ -2195,7 +2208,7 @@ struct Engine {
         double saved[3] = {0.0, 0.0, 0.0};
         NOUNROLL for (int k = 0; k < nw; ++k) {  // working set in id order (<= 3 blocks, registers)
           const int wb = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
-          const double a = acquire_h(wb, s, tbidx, tbytes);
+          const double a = acquire_h(wb, s, tbidx, tbytes, (tk.pad >> k) & 1);
           if (st) return fail(st);
           inputs = dmax(inputs, a);
           if (!fst) {
@@ -2215,7 +2228,7 @@ struct Engine {
         if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
         pf.set(p, end);
         ah += hesp_assign_term(j, p, dbits(start), dbits(end));
-        if (tr_proc && j < tr_cap && wp.lane() == 0) {
+        if (TRACE && j < tr_cap && wp.lane() == 0) {
           tr_proc[j] = p;
           tr_start[j] = start;
           tr_end[j] = end;
@@ -2229,8 +2242,7 @@ struct Engine {
         // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
         // validate out and its descendants here, valid[out] = end
         {
-          const int tt = out == 0 ? -1 : tileof(out);
-          if (fst && tt > 0 && TLC[tt] == 0) {  // cone = {root, tile}, no descendants
+          if (fst && (tk.pad & 8)) {  // cone = {root, tile}, no descendants
             NOUNROLL for (int q = wp.lane(); q < S_; q += WP::W)
               if (q != s) {
                 Vr(0, q) = ABSENT;

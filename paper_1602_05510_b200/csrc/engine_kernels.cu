@@ -206,7 +206,7 @@ __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* 
   __shared__ hesp_cand_desc sd;
   if (threadIdx.x == 0) sd = *desc;
   __syncwarp();
-  Engine<DevWarp> eng(DevWarp{}, c_problem, slot, &smem);
+  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &smem);
   eng.tr_proc = proc;
   eng.tr_start = start;
   eng.tr_end = end;
