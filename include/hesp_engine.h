@@ -127,7 +127,8 @@ enum {
   HESP_OK = 0,
   HESP_E_INVALID = -1, /* bad argument / platform / model (message in hesp_last_error) */
   HESP_E_CUDA = -2,    /* CUDA runtime failure */
-  HESP_E_NODEV = -3    /* no usable sm_100 device */
+  HESP_E_NODEV = -3,   /* no usable sm_100 device */
+  HESP_E_LIMIT = -4    /* a caller-provided trace array is too small (counts report the need) */
 };
 
 typedef struct hesp_engine hesp_engine;
@@ -177,6 +178,88 @@ int hesp_generate_batch(const hesp_gen_config* gen, int32_t s_base_snapped, int3
  * (proc = -1 for non-leaf or unscheduled ids).  Returns the outcome status. */
 int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, int32_t* proc,
                      double* start, double* end, hesp_outcome* out);
+
+/* ---------------------------------------------------------------------------
+ * Full trace of one candidate: the complete
+ * hesp::SimResult of simulate() (sim.hpp:77-88) -- assignments, transfers
+ * with their routes, time-ordered events, residency log, idle_avg -- plus
+ * compute_load_trace (sim.cpp:975-991) and the SimResult summary metrics.
+ * The schedule is simulated on the device (one warp, full residency
+ * bookkeeping); the host only orders the device logs the way Engine::run
+ * does (sim.cpp:813-831) and derives the reference's post-passes
+ * (compute_idle_avgs sim.cpp:670-702, busy_time/avg_load sim.cpp:78-87,
+ * LoadTrace::integral sim.cpp:71-76). */
+typedef struct {
+  int32_t task, proc;
+  double start, end;
+  double idle_avg;   /* SimResult::idle_avg[task] */
+} hesp_assignment;
+
+typedef struct {
+  int32_t block, src_space, dst_space, n_hops;
+  int64_t bytes;
+  double start, end;
+  int32_t has_fragment, frag_row, frag_col, frag_rows, frag_cols, pad;
+  int32_t hop_src[2], hop_dst[2];  /* TransferRec::route */
+  double hop_start[2], hop_end[2]; /* per-hop times (the Xfer events) */
+} hesp_transfer;
+
+typedef struct {
+  double time;
+  int32_t space, block;
+  int64_t delta_bytes;
+} hesp_residency;
+
+enum { HESP_EV_TASK_START = 0, HESP_EV_TASK_END = 1, HESP_EV_XFER_START = 2, HESP_EV_XFER_END = 3 };
+/* EventRec (sim.hpp:34-39) with its strings kept structured: subject is
+ * "T<id>:<KIND>:b<b>" (task events) or "B<id>" (transfer events); resource is
+ * the processor id or the link "src->dst". */
+typedef struct {
+  int32_t kind;
+  int32_t id;         /* task id or block id */
+  int32_t task_kind;  /* hesp TaskKind ordinal (task events) */
+  int32_t res_a;      /* processor id, or link source space */
+  int32_t res_b;      /* link destination space (transfer events), else -1 */
+  int32_t pad;
+  int64_t b;          /* task block side (task events) */
+  double time;
+} hesp_event;
+
+typedef struct {
+  double time;
+  int32_t active, pad;
+} hesp_load_step;
+
+typedef struct {
+  /* in: caller arrays and their capacities (entries) */
+  int32_t cap_assign, cap_xfer, cap_res, cap_events, cap_steps;
+  int32_t pad0;
+  hesp_assignment* assignments; /* task-id order (SimResult::assignments map order) */
+  hesp_transfer* transfers;     /* Engine::run order: (start, block), stable */
+  hesp_residency* residency;    /* (time, space, delta desc, block), stable */
+  hesp_event* events;           /* (time, kind, resource, subject), stable */
+  hesp_load_step* steps;        /* LoadTrace::steps */
+  /* out: counts (also set, with HESP_E_LIMIT, when an array is too small) */
+  int32_t n_assign, n_xfer, n_res, n_events, n_steps;
+  int32_t pad1;
+  hesp_outcome outcome;         /* status, leaves, makespan, the two hashes */
+  double busy_time, avg_load, load_integral;
+} hesp_trace;
+
+/* Simulates one candidate with full tracing.  Returns the candidate status
+ * (0 = ok, else 1 + Err ordinal; the arrays are filled only when 0), or a
+ * negative HESP_E_* code.  The candidate's graph is kept in the handle for
+ * hesp_verify_trace. */
+int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* trace);
+
+/* verify_schedule (sim.cpp:857-973) of a trace (possibly edited by the
+ * caller) against the graph of the candidate last passed to
+ * hesp_eval_trace: per-processor overlap, dependence order over the reduced
+ * edge list, read coherence, capacity.  Writes the violation messages,
+ * '\n'-separated and NUL-terminated, into buf (truncated to cap bytes) and
+ * their count into *n_violations.  Returns HESP_OK or HESP_E_INVALID. */
+int hesp_verify_trace(const hesp_engine* e, const hesp_trace* trace, char* buf, size_t cap,
+                      int32_t* n_violations);
 
 /* Engine facts: kernel launches issued so far, base tiling sizes, slots. */
 typedef struct {

@@ -55,6 +55,10 @@ struct Args {
   double time_limit = 0;  // seconds; 0 = none
   long detail = -1;
   bool quiet = false;
+  long trace = -1;  // --trace: full SimResult dump (JSON) of one candidate
+  std::string trace_out;
+  int shift_task = -1;  // --shift-task T --shift-by X: move T's interval by -X before verify
+  double shift_by = 0;
 };
 
 std::string slurp(const std::string& path) {
@@ -139,6 +143,80 @@ bool parse_int_list(const char* s, hesp_gen_config* g) {
   return g->n_s_choices > 0;
 }
 
+// Full SimResult of one candidate as JSON, doubles as 16-hex-digit bit
+// patterns, in the reference's own container orders (sim.cpp:813-832), plus
+// compute_load_trace, the summary metrics and verify_schedule's messages.
+void dump_trace(FILE* f, const Record& r, hesp::SimResult& res, const hesp::TaskGraph* g, const hesp::Platform& plat,
+                const Args& a) {
+  auto hx = [](double x) {
+    char b[24];
+    std::snprintf(b, sizeof b, "\"%016llx\"", (unsigned long long)bits(x));
+    return std::string(b);
+  };
+  auto q = [](const std::string& x) { return "\"" + x + "\""; };
+  std::fprintf(f, "{\"index\": %llu, \"status\": %d, \"leaves\": %d, \"makespan\": %s",
+               (unsigned long long)r.index, r.status, r.n_leaves, hx(r.makespan).c_str());
+  if (r.status != 0 || !g) {
+    std::fprintf(f, "}\n");
+    return;
+  }
+  std::fprintf(f, ",\n\"assignments\": [");
+  bool first = true;
+  for (const auto& [id, x] : res.assignments) {
+    std::fprintf(f, "%s[%d, %d, %s, %s, %s]", first ? "" : ", ", x.task, x.proc, hx(x.start).c_str(),
+                 hx(x.end).c_str(), hx(res.idle_avg.at(id)).c_str());
+    first = false;
+  }
+  std::fprintf(f, "],\n\"transfers\": [");
+  first = true;
+  for (const auto& x : res.transfers) {
+    std::string fr = "null", route = "[";
+    if (x.fragment)
+      fr = "[" + std::to_string(x.fragment->row) + ", " + std::to_string(x.fragment->col) + ", " +
+           std::to_string(x.fragment->rows) + ", " + std::to_string(x.fragment->cols) + "]";
+    for (size_t h = 0; h < x.route.size(); ++h)
+      route += (h ? ", [" : "[") + std::to_string(x.route[h].first) + ", " + std::to_string(x.route[h].second) + "]";
+    route += "]";
+    std::fprintf(f, "%s[%d, %d, %d, %lld, %s, %s, %s, %s]", first ? "" : ", ", x.block, x.route.front().first,
+                 x.dst_space, (long long)x.bytes, hx(x.start).c_str(), hx(x.end).c_str(), fr.c_str(), route.c_str());
+    first = false;
+  }
+  std::fprintf(f, "],\n\"events\": [");
+  first = true;
+  for (const auto& e : res.events) {
+    std::fprintf(f, "%s[%d, %s, %s, %s]", first ? "" : ", ", static_cast<int>(e.kind), hx(e.time).c_str(),
+                 q(e.subject).c_str(), q(e.resource).c_str());
+    first = false;
+  }
+  std::fprintf(f, "],\n\"residency\": [");
+  first = true;
+  for (const auto& c : res.residency_log) {
+    std::fprintf(f, "%s[%s, %d, %lld, %d]", first ? "" : ", ", hx(c.time).c_str(), c.space, (long long)c.delta_bytes,
+                 c.block);
+    first = false;
+  }
+  const auto lt = hesp::compute_load_trace(res, plat);
+  std::fprintf(f, "],\n\"load\": [");
+  first = true;
+  for (const auto& [t, n] : lt.steps) {
+    std::fprintf(f, "%s[%s, %d]", first ? "" : ", ", hx(t).c_str(), n);
+    first = false;
+  }
+  std::fprintf(f, "],\n\"busy\": %s, \"avg_load\": %s, \"integral\": %s", hx(res.busy_time()).c_str(),
+               hx(res.avg_load(plat.processor_count())).c_str(), hx(lt.integral()).c_str());
+  if (a.shift_task >= 0) {
+    auto it = res.assignments.find(a.shift_task);
+    if (it != res.assignments.end()) {
+      it->second.start -= a.shift_by;
+      it->second.end -= a.shift_by;
+    }
+  }
+  const auto v = hesp::verify_schedule(res, *g, plat);
+  std::fprintf(f, ",\n\"violations\": [");
+  for (size_t i = 0; i < v.size(); ++i) std::fprintf(f, "%s%s", i ? ", " : "", q(v[i]).c_str());
+  std::fprintf(f, "]}\n");
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -183,6 +261,10 @@ int main(int argc, char** argv) {
     else if (k == "--detail-out") a.detail_out = v();
     else if (k == "--quiet") a.quiet = true;
     else if (k == "--descs") a.descs = v();
+    else if (k == "--trace") a.trace = std::atol(v());
+    else if (k == "--trace-out") a.trace_out = v();
+    else if (k == "--shift-task") a.shift_task = std::atoi(v());
+    else if (k == "--shift-by") a.shift_by = std::atof(v());
     else {
       std::fprintf(stderr, "unknown argument %s\n", k.c_str());
       return 2;
@@ -215,6 +297,16 @@ int main(int argc, char** argv) {
     c.s_base_snapped = static_cast<int32_t>(a.n / c.base_b);
   }
 
+  if (a.trace >= 0) {
+    hesp::SimResult res;
+    hesp::TaskGraph* g = nullptr;
+    Record r = evaluate(c, static_cast<uint64_t>(a.trace), &res, &g);
+    FILE* f = a.trace_out.empty() ? stdout : std::fopen(a.trace_out.c_str(), "w");
+    dump_trace(f, r, res, g, plat, a);
+    if (f != stdout) std::fclose(f);
+    delete g;
+    return 0;
+  }
   if (a.detail >= 0) {
     hesp::SimResult res;
     hesp::TaskGraph* g = nullptr;

@@ -16,8 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhesp_b200.so")
 
-SOURCES = ["engine_kernels.cu", "problem.cpp"]
-HEADERS = ["engine.h", "engine_types.h", "problem.h"]
+SOURCES = ["engine_kernels.cu", "problem.cpp", "trace.cpp"]
+HEADERS = ["engine.h", "engine_types.h", "problem.h", "trace.h"]
 
 
 def _nvcc() -> str:

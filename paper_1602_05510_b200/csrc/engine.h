@@ -321,6 +321,65 @@ struct Engine {
   int32_t* tr_proc = nullptr;
   double *tr_start = nullptr, *tr_end = nullptr;
   int32_t tr_cap = 0;
+  TraceBufs* tb = nullptr;  // full-trace sinks (TRACE only)
+
+  // ---- full-trace logging (compiled out unless TRACE) ----
+  HX void log_res(double t, int s, long long delta, int b) {  // one lane calls
+    if constexpr (TRACE) {
+      if (!tb) return;
+      const int k = atomic_slot(&tb->nr);
+      if (k < tb->rcap) {
+        ResLog r;
+        r.time = t;
+        r.space = s;
+        r.block = b;
+        r.delta = delta;
+        tb->r[k] = r;
+      } else {
+        tb->overflow = 1;
+      }
+    }
+  }
+  HX void log_xfer(int blk, const Region* frag, long long bytes, int src, int dst, double start0, double end,
+                   int nh, const double* hs, const double* he) {  // uniform: lane 0 writes
+    if constexpr (TRACE) {
+      if (!tb) return;
+      if (wp.lane() == 0) {
+        const int k = tb->nx++;
+        if (k < tb->xcap) {
+          XferLog x;
+          x.block = blk;
+          x.src = src;
+          x.dst = dst;
+          x.nh = nh;
+          x.bytes = bytes;
+          x.start = start0;
+          x.end = end;
+          x.has_frag = frag ? 1 : 0;
+          x.frow = frag ? frag->row : 0;
+          x.fcol = frag ? frag->col : 0;
+          x.frows = frag ? frag->rows : 0;
+          x.fcols = frag ? frag->cols : 0;
+          x.pad = 0;
+          for (int h = 0; h < 2; ++h) {
+            x.hs[h] = h < nh ? hs[h] : 0.0;
+            x.he[h] = h < nh ? he[h] : 0.0;
+          }
+          tb->x[k] = x;
+        } else {
+          tb->overflow = 1;
+        }
+      }
+      wp.sync();
+    }
+  }
+  HX int atomic_slot(int32_t* c) const {
+#if defined(__CUDACC__)
+    return atomicAdd(c, 1);
+#else
+    return (*c)++;
+#endif
+  }
 
   HX Engine(WP w, const Problem& p, uint8_t* slot_, Small* s) : wp(w), pbp(&p), sm(s), slot(slot_) {
     nbt = p.n_base_tasks;
@@ -1220,6 +1279,7 @@ struct Engine {
     }
     double rdy = dmax(data_ready, tnow);
     double start0 = 0.0;
+    double hs[2] = {0.0, 0.0}, he[2] = {0.0, 0.0};
     NOUNROLL for (int h = 0; h < nh; ++h) {
       const int l = PB.route_l[src * MAXS + dst][h];
       const double st = dmax(sm->link_free[l], rdy);
@@ -1227,8 +1287,13 @@ struct Engine {
       sm->link_free[l] = en;
       rdy = en;
       if (h == 0) start0 = st;
+      if (TRACE && h < 2) {
+        hs[h] = st;
+        he[h] = en;
+      }
     }
     if (!(rdy > now)) fail(ST_ENGINE_INVARIANT);
+    log_xfer(blk, frag, bytes, src, dst, start0, rdy, nh, hs, he);
     if (frag)
       xhash += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), frag->row, frag->col,
                               frag->rows, frag->cols);
@@ -1322,6 +1387,7 @@ struct Engine {
       set_flag(victim, 1u << s, false);
       setV(victim, s, ABSENT);
       add_used(s, -vbytes);
+      if (TRACE && wp.lane() == 0) log_res(at, s, -vbytes, victim);
       setLU(victim, s, 0.0);
       if (s != mainsp) {
         // views lose their backing when no materialised block covers them
@@ -1354,6 +1420,7 @@ struct Engine {
     if (status) return;
     set_flag(b, 1u << s, true);
     add_used(s, bytes);
+    if (TRACE && wp.lane() == 0) log_res(at, s, bytes, b);
     setLU(b, s, at);
   }
 
@@ -1594,7 +1661,7 @@ struct Engine {
   // invalidate_elsewhere (sim.cpp:574-590) over the invalidation cone
   // (sim.cpp:204-212), which by E1 is: blocks inside b, plus blocks strictly
   // containing some block inside b.
-  HXN void invalidate_elsewhere(int b, int ws) {
+  HXN void invalidate_elsewhere(int b, int ws, double at) {
     const int t = b == 0 ? -1 : tile_of(b);
     const Region rb = reg(b);
     long long freed[MAXS];
@@ -1626,6 +1693,7 @@ struct Engine {
         if ((f >> q) & 1u) {
           freed[q] += rbytes(rx);
           LU(x, q) = 0.0;
+          if (TRACE) log_res(at, q, -rbytes(rx), x);
         }
         V(x, q) = ABSENT;
       }
@@ -1696,6 +1764,7 @@ struct Engine {
       if (!fast) {
         set_flag(out, 1u << s, false);
         add_used(s, -bbytes(out));
+        if (TRACE && wp.lane() == 0) log_res(arr, s, -bbytes(out), out);
         setLU(out, s, 0.0);
       }
       V(out, s) = ABSENT;
@@ -1734,7 +1803,7 @@ struct Engine {
       bool ok = true;
       NOUNROLL for (int q = 0; q < S; ++q)
         if (nonroot + (q == mainsp ? bbytes(0) : 0) > PB.cap[q]) ok = false;
-      fast = ok;
+      fast = ok && !TRACE;  // the trace keeps full residency bookkeeping
     }
     switch (PB.selection) {
       case SEL_EFTP: return fast ? sim_loop<SEL_EFTP, true>() : sim_loop<SEL_EFTP, false>();
@@ -1762,6 +1831,7 @@ struct Engine {
       bflags()[x] = x == 0 ? (1u << mainsp) : 0u;
     }
     NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
+    if (TRACE && wp.lane() == 0) log_res(0.0, mainsp, bbytes(0), 0);  // init_memory (sim.cpp:333)
     wp.sync();
     if (sm->used[mainsp] > PB.cap[mainsp]) return fail(ST_CAPACITY);
     if (PB.ordering == ORD_PL) build_ct();
@@ -1868,6 +1938,7 @@ struct Engine {
         return 0.0;
       }
       double rdy = dmax(data_ready, tnow), start0 = 0.0;
+      double hs[2] = {0.0, 0.0}, he[2] = {0.0, 0.0};
       NOUNROLL for (int h = 0; h < nh; ++h) {
         const int l = PB.route_l[src * MAXS + dst][h];
         const double s0 = dmax(lf.get(l), rdy);
@@ -1875,8 +1946,13 @@ struct Engine {
         lf.set(l, en);
         rdy = en;
         if (h == 0) start0 = s0;
+        if (TRACE && h < 2) {
+          hs[h] = s0;
+          he[h] = en;
+        }
       }
       if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
+      if (TRACE) log_xfer(blk, nullptr, nbytes, src, dst, start0, rdy, nh, hs, he);
       xh += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
       return rdy;
     };
@@ -2250,7 +2326,7 @@ struct Engine {
               }
             wp.sync();
           } else {
-            invalidate_elsewhere(out, s);
+            invalidate_elsewhere(out, s, start);
             validate_from(out, s, end);
           }
           Vr(out, s) = end;
@@ -2419,7 +2495,51 @@ struct Engine {
 
   HXN Outcome run(const hesp_cand_desc& d) {
     build(d);
+    if constexpr (TRACE) export_graph();
     return sim_slot();
+  }
+
+  // Trace mode: the candidate's leaves (program order), their reads/writes,
+  // predecessor lists and every block's region, for verify_schedule.
+  HXN void export_graph() {
+    if (!tb || status) return;
+    const int nl = nleaves, nb = nblocks;
+    if (nl > tb->leaf_cap || nb > tb->block_cap) {
+      if (wp.lane() == 0) tb->overflow = 1;
+      wp.sync();
+      return;
+    }
+    int np = 0;
+    NOUNROLL for (int li = 0; li < nl; ++li) np += t_pcnt()[leaf()[li]];
+    if (np > tb->pred_cap) {
+      if (wp.lane() == 0) tb->overflow = 1;
+      wp.sync();
+      return;
+    }
+    int off = 0;
+    NOUNROLL for (int li = 0; li < nl; ++li) {
+      const int j = leaf()[li];
+      const int cnt = t_pcnt()[j];
+      const int32_t* pl_ = pred_list(j);
+      NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W) tb->lpreds[off + q] = pl_[q];
+      if (wp.lane() == 0) {
+        tb->leaves[li] = j;
+        tb->lmeta[li] = task(j);
+        tb->lpoff[li] = off;
+        tb->lpcnt[li] = cnt;
+      }
+      off += cnt;
+    }
+    NOUNROLL for (int b = wp.lane(); b < nb; b += WP::W) {
+      tb->bregion[b] = reg(b);
+      tb->bisint[b] = bmeta(b).isint;
+    }
+    if (wp.lane() == 0) {
+      tb->nleaves = nl;
+      tb->npreds = np;
+      tb->nblocks = nb;
+    }
+    wp.sync();
   }
 };
 

@@ -23,6 +23,7 @@
 #include "engine.h"
 #include "hesp_engine.h"
 #include "problem.h"
+#include "trace.h"
 
 using namespace hx;
 
@@ -201,7 +202,7 @@ __global__ void gen_kernel(unsigned long long first, unsigned long long count, h
 }
 
 __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* slot, int32_t cap, int32_t* proc,
-                              double* start, double* end, hesp_outcome* out) {
+                              double* start, double* end, hesp_outcome* out, TraceBufs* tb) {
   __shared__ Small smem;
   __shared__ hesp_cand_desc sd;
   if (threadIdx.x == 0) sd = *desc;
@@ -211,6 +212,7 @@ __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* 
   eng.tr_start = start;
   eng.tr_end = end;
   eng.tr_cap = cap;
+  eng.tb = tb;
   const Outcome o = eng.run(sd);
   if (threadIdx.x == 0) {
     out->status = o.status;
@@ -257,6 +259,7 @@ struct hesp_engine {
   static constexpr int NEV = 64;     // per-chunk kernel timing (build, sim)
   cudaEvent_t evc[NEV][4] = {};
   int nev_used = 0;
+  hx::TraceGraph last_graph;  // candidate of the last hesp_eval_trace (for hesp_verify_trace)
 };
 
 namespace {
@@ -359,6 +362,20 @@ int finish_best(hesp_engine* e, hesp_best* best, cudaStream_t st) {
   return HESP_OK;
 }
 
+}  // namespace
+
+namespace {
+template <class T>
+bool dalloc(T** p, size_t n, std::vector<void*>& owned) {
+  if (!ck(cudaMalloc((void**)p, (n ? n : 1) * sizeof(T)), "cudaMalloc trace")) return false;
+  owned.push_back(*p);
+  return true;
+}
+template <class T>
+bool d2h(std::vector<T>& v, const T* d, size_t n) {
+  v.resize(n);
+  return !n || ck(cudaMemcpy(v.data(), d, n * sizeof(T), cudaMemcpyDeviceToHost), "trace D2H");
+}
 }  // namespace
 
 extern "C" {
@@ -618,7 +635,7 @@ int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, in
     cudaMemset(ds, 0, n * 8);
     cudaMemset(de, 0, n * 8);
     cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, e->stream);
-    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, cap, dp, ds, de, dout);
+    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, cap, dp, ds, de, dout, nullptr);
     e->launches += 1;
     ok = ck(cudaStreamSynchronize(e->stream), "detail");
   }
@@ -636,6 +653,100 @@ int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, in
   cudaFree(de);
   cudaFree(dout);
   return ok ? o.status : HESP_E_CUDA;
+}
+
+int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) {
+  if (!e || !desc || !tr) return HESP_E_INVALID;
+  if (tr->cap_assign < 0 || tr->cap_xfer < 0 || tr->cap_res < 0 || tr->cap_events < 0 || tr->cap_steps < 0)
+    return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  e->last_graph = hx::TraceGraph{};
+  const Problem& P = e->hp.p;
+  const int T = P.maxt, B = P.maxb;
+  // device log capacities: transfers and residency changes per task are few
+  // (<= 3 acquires + write-back + flushes); gathers add fragments
+  const int xcap = 16 * T + 1024, rcap = 32 * T + 1024;
+  std::vector<void*> owned;
+  hesp_cand_desc* dd = nullptr;
+  int32_t* dp = nullptr;
+  double *ds = nullptr, *de = nullptr;
+  hesp_outcome* dout = nullptr;
+  XferLog* dx = nullptr;
+  ResLog* dr = nullptr;
+  TraceBufs* dtb = nullptr;
+  TraceBufs tb{};
+  bool ok = dalloc(&dd, 1, owned) && dalloc(&dp, T, owned) && dalloc(&ds, T, owned) && dalloc(&de, T, owned) &&
+            dalloc(&dout, 1, owned) && dalloc(&dx, xcap, owned) && dalloc(&dr, rcap, owned) &&
+            dalloc(&tb.leaves, T, owned) && dalloc(&tb.lmeta, T, owned) && dalloc(&tb.lpoff, T, owned) &&
+            dalloc(&tb.lpcnt, T, owned) && dalloc(&tb.lpreds, P.maxedges, owned) && dalloc(&tb.bregion, B, owned) &&
+            dalloc(&tb.bisint, B, owned) && dalloc(&dtb, 1, owned);
+  hesp_outcome o{};
+  hx::TraceLogs logs;
+  TraceBufs hb{};
+  if (ok) {
+    tb.x = dx;
+    tb.r = dr;
+    tb.xcap = xcap;
+    tb.rcap = rcap;
+    tb.leaf_cap = T;
+    tb.pred_cap = P.maxedges;
+    tb.block_cap = B;
+    cudaMemcpy(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice);
+    cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
+    cudaMemset(dp, 0xff, (size_t)T * 4);
+    cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, e->stream);
+    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, T, dp, ds, de, dout, dtb);
+    e->launches += 1;
+    ok = ck(cudaStreamSynchronize(e->stream), "trace kernel") &&
+         ck(cudaMemcpy(&o, dout, sizeof(o), cudaMemcpyDeviceToHost), "trace D2H") &&
+         ck(cudaMemcpy(&hb, dtb, sizeof(hb), cudaMemcpyDeviceToHost), "trace D2H");
+  }
+  if (ok && hb.overflow) {
+    g_last_error = "trace buffers overflowed";
+    ok = false;
+  }
+  if (ok && o.status == 0) {
+    hx::TraceGraph& g = e->last_graph;
+    ok = d2h(logs.proc, dp, T) && d2h(logs.start, ds, T) && d2h(logs.end, de, T) &&
+         d2h(logs.xfers, dx, (size_t)hb.nx) && d2h(logs.res, dr, (size_t)hb.nr) &&
+         d2h(g.leaves, tb.leaves, (size_t)hb.nleaves) && d2h(g.meta, tb.lmeta, (size_t)hb.nleaves) &&
+         d2h(g.poff, tb.lpoff, (size_t)hb.nleaves) && d2h(g.pcnt, tb.lpcnt, (size_t)hb.nleaves) &&
+         d2h(g.preds, tb.lpreds, (size_t)hb.npreds) && d2h(g.bregion, tb.bregion, (size_t)hb.nblocks) &&
+         d2h(g.bisint, tb.bisint, (size_t)hb.nblocks);
+    g.valid = ok;
+  }
+  for (void* q : owned) cudaFree(q);
+  if (!ok) return o.status ? o.status : HESP_E_CUDA;
+  tr->outcome = o;
+  tr->n_assign = tr->n_xfer = tr->n_res = tr->n_events = tr->n_steps = 0;
+  tr->busy_time = tr->avg_load = tr->load_integral = 0.0;
+  if (o.status != 0) return o.status;
+  const int r = hx::finish_trace(P, e->last_graph, logs, tr);
+  if (r != HESP_OK) {
+    g_last_error = "trace arrays too small (see the hesp_trace counts)";
+    return r;
+  }
+  return 0;
+}
+
+int hesp_verify_trace(const hesp_engine* e, const hesp_trace* tr, char* buf, size_t cap, int32_t* n_violations) {
+  if (!e || !tr || !e->last_graph.valid) {
+    g_last_error = "hesp_verify_trace needs a successful hesp_eval_trace first";
+    return HESP_E_INVALID;
+  }
+  const auto v = hx::verify_trace(e->hp.p, e->last_graph, *tr);
+  if (n_violations) *n_violations = (int32_t)v.size();
+  if (buf && cap) {
+    std::string all;
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (i) all += '\n';
+      all += v[i];
+    }
+    const size_t n = all.size() < cap - 1 ? all.size() : cap - 1;
+    std::memcpy(buf, all.data(), n);
+    buf[n] = 0;
+  }
+  return HESP_OK;
 }
 
 int hesp_generate_batch(const hesp_gen_config* gen, int32_t s_base_snapped, int32_t n_base, int64_t base_b,

@@ -143,6 +143,42 @@ struct Problem {
   SlotLayout lay;
 };
 
+// ---- full-trace mode (Engine<..., TRACE = true>, hesp_eval_trace) ----
+// One transfer as plan_transfer records it (sim.cpp:468-499), in emission
+// order, with the per-hop times the reference turns into Xfer events.
+struct XferLog {
+  int32_t block, src, dst, nh;
+  int64_t bytes;
+  double start, end;
+  int32_t has_frag, frow, fcol, frows, fcols, pad;
+  double hs[2], he[2];
+};
+// One residency change (sim.cpp ResidencyChange), in emission order.
+struct ResLog {
+  double time;
+  int32_t space, block;
+  int64_t delta;
+};
+// Device-side sinks of the trace kernel (one candidate).  Counters are
+// advanced by the owning warp; overflow is reported, never written past.
+struct TraceBufs {
+  XferLog* x;
+  ResLog* r;
+  int32_t xcap, rcap;
+  int32_t nx, nr;
+  // graph of the traced candidate (for verify_schedule on the host)
+  int32_t* leaves;   // program order
+  TaskMeta* lmeta;   // per leaf
+  int32_t* lpoff;    // per leaf: offset/count into lpreds
+  int32_t* lpcnt;
+  int32_t* lpreds;
+  Region* bregion;   // per block id
+  int32_t* bisint;
+  int32_t leaf_cap, pred_cap, block_cap;
+  int32_t nleaves, npreds, nblocks;
+  int32_t overflow;
+};
+
 // Per-candidate result record (also the golden-record payload).
 struct Outcome {
   int32_t status;

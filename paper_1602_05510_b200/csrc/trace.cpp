@@ -1,0 +1,402 @@
+// trace.cpp — host post-passes of the full-trace path (see trace.h).
+//
+// The schedule itself comes from the device (Engine<DevWarp, true>); this
+// file only reproduces what the reference does with its SimResult after the
+// event loop, in the same IEEE operation order:
+//   ordering of events / residency log / transfers   sim.cpp:813-831
+//   compute_idle_avgs                                sim.cpp:670-702
+//   busy_time, avg_load, LoadTrace::integral         sim.cpp:71-87
+//   compute_load_trace                               sim.cpp:975-991
+//   verify_schedule                                  sim.cpp:857-973
+#include "trace.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdint>
+#include <map>
+#include <string>
+#include <unordered_map>
+
+namespace hx {
+namespace {
+
+const char* kind_name(int k) {  // to_string(TaskKind), platform.cpp:39-47
+  switch (k) {
+    case 0: return "CHOL";
+    case 1: return "TRSM";
+    case 2: return "SYRK";
+    case 3: return "GEMM";
+  }
+  return "?";
+}
+
+struct R64 {
+  int64_t row, col, rows, cols;
+};
+R64 r64(const Region& r) { return {r.row, r.col, r.rows, r.cols}; }
+bool contains(const R64& o, const R64& i) {  // graph.cpp:34-38
+  return i.row >= o.row && i.col >= o.col && i.row + i.rows <= o.row + o.rows && i.col + i.cols <= o.col + o.cols;
+}
+bool overlap(const R64& a, const R64& b) {  // graph.cpp:40-43
+  return a.row < b.row + b.rows && b.row < a.row + a.rows && a.col < b.col + b.cols && b.col < a.col + a.cols;
+}
+
+struct Ev {
+  hesp_event e;
+  std::string resource, subject;
+};
+
+void hop_link(const Problem& p, int src, int dst, int h, int32_t* hs, int32_t* hd) {
+  const int l = p.route_l[src * MAXS + dst][h];
+  *hs = p.link_src[l];
+  *hd = p.link_dst[l];
+}
+
+// (start, +1) / (end, -1) deltas of the assignments, sorted (sim.cpp:672-677, 977-982)
+std::vector<std::pair<double, int>> deltas_of(const hesp_trace& tr) {
+  std::vector<std::pair<double, int>> d;
+  d.reserve(2 * (size_t)tr.n_assign);
+  for (int i = 0; i < tr.n_assign; ++i) {
+    d.push_back({tr.assignments[i].start, +1});
+    d.push_back({tr.assignments[i].end, -1});
+  }
+  std::sort(d.begin(), d.end());
+  return d;
+}
+
+}  // namespace
+
+int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr) {
+  (void)g;
+  // assignments in task-id order (std::map order of SimResult::assignments)
+  int na = 0;
+  for (size_t id = 0; id < logs.proc.size(); ++id) na += logs.proc[id] >= 0;
+  // transfers: stable by (start, block) over emission order
+  std::vector<XferLog> xs = logs.xfers;
+  std::stable_sort(xs.begin(), xs.end(), [](const XferLog& a, const XferLog& b) {
+    if (a.start != b.start) return a.start < b.start;
+    return a.block < b.block;
+  });
+  std::vector<ResLog> rs = logs.res;
+  std::stable_sort(rs.begin(), rs.end(), [](const ResLog& a, const ResLog& b) {
+    if (a.time != b.time) return a.time < b.time;
+    if (a.space != b.space) return a.space < b.space;
+    if (a.delta != b.delta) return a.delta > b.delta;
+    return a.block < b.block;
+  });
+  int nhops = 0;
+  for (const auto& x : xs) nhops += x.nh;
+  const int nev = 2 * na + 2 * nhops;
+  tr->n_assign = na;
+  tr->n_xfer = (int32_t)xs.size();
+  tr->n_res = (int32_t)rs.size();
+  tr->n_events = nev;
+  // load steps need the assignments first; their count is bounded by 2*na
+  if (na > tr->cap_assign || (int)xs.size() > tr->cap_xfer || (int)rs.size() > tr->cap_res ||
+      nev > tr->cap_events || 2 * na > tr->cap_steps) {
+    tr->n_steps = 2 * na;
+    return HESP_E_LIMIT;
+  }
+  {
+    int k = 0;
+    for (size_t id = 0; id < logs.proc.size(); ++id) {
+      if (logs.proc[id] < 0) continue;
+      hesp_assignment& a = tr->assignments[k++];
+      a.task = (int32_t)id;
+      a.proc = logs.proc[id];
+      a.start = logs.start[id];
+      a.end = logs.end[id];
+      a.idle_avg = 0.0;
+    }
+  }
+  for (size_t i = 0; i < xs.size(); ++i) {
+    const XferLog& x = xs[i];
+    hesp_transfer& t = tr->transfers[i];
+    t.block = x.block;
+    t.src_space = x.src;
+    t.dst_space = x.dst;
+    t.n_hops = x.nh;
+    t.bytes = x.bytes;
+    t.start = x.start;
+    t.end = x.end;
+    t.has_fragment = x.has_frag;
+    t.frag_row = x.frow;
+    t.frag_col = x.fcol;
+    t.frag_rows = x.frows;
+    t.frag_cols = x.fcols;
+    t.pad = 0;
+    for (int h = 0; h < 2; ++h) {
+      t.hop_src[h] = t.hop_dst[h] = -1;
+      t.hop_start[h] = t.hop_end[h] = 0.0;
+      if (h < x.nh) {
+        hop_link(p, x.src, x.dst, h, &t.hop_src[h], &t.hop_dst[h]);
+        t.hop_start[h] = x.hs[h];
+        t.hop_end[h] = x.he[h];
+      }
+    }
+  }
+  for (size_t i = 0; i < rs.size(); ++i) {
+    tr->residency[i].time = rs[i].time;
+    tr->residency[i].space = rs[i].space;
+    tr->residency[i].block = rs[i].block;
+    tr->residency[i].delta_bytes = rs[i].delta;
+  }
+  // events: every field is part of the sort key, so records that tie are
+  // identical and the emission order does not matter
+  {
+    std::vector<Ev> ev;
+    ev.reserve(nev);
+    std::unordered_map<int, int> li;  // task id -> leaf index
+    for (size_t k = 0; k < g.leaves.size(); ++k) li[g.leaves[k]] = (int)k;
+    for (int i = 0; i < na; ++i) {
+      const hesp_assignment& a = tr->assignments[i];
+      const auto it = li.find(a.task);
+      const TaskMeta m = it != li.end() ? g.meta[it->second] : TaskMeta{};
+      std::string subj = "T" + std::to_string(a.task) + ":" + kind_name(m.kind) + ":b" + std::to_string(m.b);
+      std::string res = std::to_string(a.proc);
+      for (int k = 0; k < 2; ++k) {
+        Ev e{};
+        e.e.kind = k == 0 ? HESP_EV_TASK_START : HESP_EV_TASK_END;
+        e.e.id = a.task;
+        e.e.task_kind = m.kind;
+        e.e.res_a = a.proc;
+        e.e.res_b = -1;
+        e.e.b = m.b;
+        e.e.time = k == 0 ? a.start : a.end;
+        e.resource = res;
+        e.subject = subj;
+        ev.push_back(e);
+      }
+    }
+    for (const auto& x : xs) {
+      for (int h = 0; h < x.nh; ++h) {
+        int32_t hs, hd;
+        hop_link(p, x.src, x.dst, h, &hs, &hd);
+        for (int k = 0; k < 2; ++k) {
+          Ev e{};
+          e.e.kind = k == 0 ? HESP_EV_XFER_START : HESP_EV_XFER_END;
+          e.e.id = x.block;
+          e.e.task_kind = -1;
+          e.e.res_a = hs;
+          e.e.res_b = hd;
+          e.e.b = 0;
+          e.e.time = k == 0 ? x.hs[h] : x.he[h];
+          e.resource = std::to_string(hs) + "->" + std::to_string(hd);
+          e.subject = "B" + std::to_string(x.block);
+          ev.push_back(e);
+        }
+      }
+    }
+    std::stable_sort(ev.begin(), ev.end(), [](const Ev& a, const Ev& b) {
+      if (a.e.time != b.e.time) return a.e.time < b.e.time;
+      if (a.e.kind != b.e.kind) return a.e.kind < b.e.kind;
+      if (a.resource != b.resource) return a.resource < b.resource;
+      return a.subject < b.subject;
+    });
+    for (size_t i = 0; i < ev.size(); ++i) tr->events[i] = ev[i].e;
+  }
+  // compute_idle_avgs (sim.cpp:670-702)
+  const int P = p.P;
+  const auto d = deltas_of(*tr);
+  std::vector<double> times;
+  std::vector<int> active;
+  {
+    int cur = 0;
+    for (size_t i = 0; i < d.size();) {
+      const double t = d[i].first;
+      while (i < d.size() && d[i].first == t) cur += d[i++].second;
+      times.push_back(t);
+      active.push_back(cur);
+    }
+  }
+  std::vector<double> cum(times.size(), 0.0);
+  for (size_t i = 1; i < times.size(); ++i) cum[i] = cum[i - 1] + (P - active[i - 1]) * (times[i] - times[i - 1]);
+  auto idle_up_to = [&](double t) {
+    auto it = std::upper_bound(times.begin(), times.end(), t);
+    if (it == times.begin()) return 0.0;
+    const size_t k = (size_t)(it - times.begin()) - 1;
+    return cum[k] + (P - active[k]) * (t - times[k]);
+  };
+  for (int i = 0; i < na; ++i) {
+    hesp_assignment& a = tr->assignments[i];
+    const double dur = a.end - a.start;
+    a.idle_avg = dur > 0 ? (idle_up_to(a.end) - idle_up_to(a.start)) / dur : 0.0;
+  }
+  // compute_load_trace (sim.cpp:975-991): same grouping as above
+  tr->n_steps = (int32_t)times.size();
+  for (size_t i = 0; i < times.size(); ++i) {
+    tr->steps[i].time = times[i];
+    tr->steps[i].active = active[i];
+    tr->steps[i].pad = 0;
+  }
+  // SimResult::busy_time / avg_load, LoadTrace::integral (sim.cpp:71-87)
+  double busy = 0;
+  for (int i = 0; i < na; ++i) busy += tr->assignments[i].end - tr->assignments[i].start;
+  tr->busy_time = busy;
+  const double mk = tr->outcome.makespan;
+  tr->avg_load = (mk <= 0 || P < 1) ? 0.0 : busy / (P * mk);
+  double integral = 0;
+  for (size_t i = 0; i + 1 < times.size(); ++i) integral += active[i] * (times[i + 1] - times[i]);
+  tr->load_integral = integral;
+  return HESP_OK;
+}
+
+std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr) {
+  std::vector<std::string> violations;
+  const double eps = 1e-9 * std::max(1.0, tr.outcome.makespan);
+  const int main_space = p.main_space;
+  std::map<int, hesp_assignment> asg;  // SimResult::assignments
+  for (int i = 0; i < tr.n_assign; ++i) asg[tr.assignments[i].task] = tr.assignments[i];
+  std::unordered_map<int, int> li;
+  for (size_t k = 0; k < g.leaves.size(); ++k) li[g.leaves[k]] = (int)k;
+
+  // (a) per-processor intervals disjoint
+  std::map<int, std::vector<hesp_assignment>> per_proc;
+  for (const auto& [id, a] : asg) per_proc[a.proc].push_back(a);
+  for (auto& [proc, list] : per_proc) {
+    std::sort(list.begin(), list.end(),
+              [](const hesp_assignment& x, const hesp_assignment& y) { return x.start < y.start; });
+    for (size_t i = 1; i < list.size(); ++i)
+      if (list[i].start < list[i - 1].end - eps)
+        violations.push_back("processor " + std::to_string(proc) + ": tasks " + std::to_string(list[i - 1].task) +
+                             " and " + std::to_string(list[i].task) + " overlap");
+  }
+
+  // (b) dependence ordering over TaskGraph::edges(): the transitive reduction
+  // of the dependence relation in (src rank, dst rank) program order
+  // (graph.cpp:684-726).  The device's predecessor lists carry the same
+  // closure (E2), so the reduction is the reference's edge list.
+  {
+    const int n = (int)g.leaves.size();
+    std::vector<std::vector<int>> direct(n);
+    for (int v = 0; v < n; ++v)
+      for (int q = 0; q < g.pcnt[v]; ++q) {
+        const auto it = li.find(g.preds[g.poff[v] + q]);
+        if (it != li.end()) direct[it->second].push_back(v);
+      }
+    for (auto& d : direct) {
+      std::sort(d.begin(), d.end());
+      d.erase(std::unique(d.begin(), d.end()), d.end());
+    }
+    const size_t words = ((size_t)n + 63) / 64;
+    std::vector<uint64_t> reach((size_t)n * words, 0);
+    for (int u = n - 1; u >= 0; --u) {
+      uint64_t* row = &reach[(size_t)u * words];
+      for (int v : direct[u]) {
+        row[v / 64] |= 1ull << (v % 64);
+        const uint64_t* vrow = &reach[(size_t)v * words];
+        for (size_t w = 0; w < words; ++w) row[w] |= vrow[w];
+      }
+    }
+    auto bit = [&](int node, int target) { return (reach[(size_t)node * words + target / 64] >> (target % 64)) & 1u; };
+    for (int u = 0; u < n; ++u)
+      for (int v : direct[u]) {
+        bool redundant = false;
+        for (int w : direct[u]) {
+          if (w == v) continue;
+          if (bit(w, v)) {
+            redundant = true;
+            break;
+          }
+        }
+        if (redundant) continue;
+        const int src = g.leaves[u], dst = g.leaves[v];
+        auto si = asg.find(src), di = asg.find(dst);
+        if (si == asg.end() || di == asg.end()) {
+          violations.push_back("edge endpoint not scheduled");
+          continue;
+        }
+        if (di->second.start < si->second.end - eps)
+          violations.push_back("edge " + std::to_string(src) + "->" + std::to_string(dst) +
+                               " violated: dst starts before src ends");
+      }
+  }
+
+  // (c) read coherence (sim.cpp:897-959)
+  struct WriteEvt {
+    double end;
+    int space;
+    R64 region;
+  };
+  std::vector<WriteEvt> writes;
+  for (const auto& [id, a] : asg) {
+    const auto it = li.find(id);
+    if (it == li.end()) continue;
+    const TaskMeta& m = g.meta[it->second];
+    writes.push_back({a.end, p.proc_space[a.proc], r64(g.bregion[m.blk[m.nrd]])});
+  }
+  for (const auto& [id, a] : asg) {
+    const auto it = li.find(id);
+    if (it == li.end()) continue;
+    const TaskMeta& m = g.meta[it->second];
+    const int space = p.proc_space[a.proc];
+    for (int k = 0; k < m.nrd; ++k) {
+      const int rblk = m.blk[k];
+      const R64 rreg = r64(g.bregion[rblk]);
+      std::vector<int64_t> xv{rreg.col, rreg.col + rreg.cols};
+      std::vector<int64_t> yv{rreg.row, rreg.row + rreg.rows};
+      for (const auto& w : writes) {
+        if (!overlap(w.region, rreg)) continue;
+        xv.push_back(std::clamp(w.region.col, rreg.col, rreg.col + rreg.cols));
+        xv.push_back(std::clamp(w.region.col + w.region.cols, rreg.col, rreg.col + rreg.cols));
+        yv.push_back(std::clamp(w.region.row, rreg.row, rreg.row + rreg.rows));
+        yv.push_back(std::clamp(w.region.row + w.region.rows, rreg.row, rreg.row + rreg.rows));
+      }
+      std::sort(xv.begin(), xv.end());
+      xv.erase(std::unique(xv.begin(), xv.end()), xv.end());
+      std::sort(yv.begin(), yv.end());
+      yv.erase(std::unique(yv.begin(), yv.end()), yv.end());
+      bool fail_read = false;
+      for (size_t yi = 0; yi + 1 < yv.size() && !fail_read; ++yi)
+        for (size_t xi = 0; xi + 1 < xv.size() && !fail_read; ++xi) {
+          const R64 cell{yv[yi], xv[xi], yv[yi + 1] - yv[yi], xv[xi + 1] - xv[xi]};
+          double w_end = -1;
+          int w_space = main_space;
+          for (const auto& w : writes) {
+            if (w.end > a.start + eps) continue;
+            if (!contains(w.region, cell)) continue;
+            if (w.end > w_end) {
+              w_end = w.end;
+              w_space = w.space;
+            }
+          }
+          bool ok = false;
+          if (w_end >= 0 && w_space == space) ok = true;
+          if (!ok && w_end < 0 && space == main_space) ok = true;
+          if (!ok) {
+            const double lower = std::max(w_end, 0.0);
+            for (int xi2 = 0; xi2 < tr.n_xfer; ++xi2) {
+              const hesp_transfer& x = tr.transfers[xi2];
+              if (x.dst_space != space) continue;
+              const R64 xr = x.has_fragment ? R64{x.frag_row, x.frag_col, x.frag_rows, x.frag_cols}
+                                            : r64(g.bregion[x.block]);
+              if (!contains(xr, cell)) continue;
+              if (x.end <= a.start + eps && x.end >= lower - eps) {
+                ok = true;
+                break;
+              }
+            }
+          }
+          if (!ok) {
+            violations.push_back("task " + std::to_string(id) + " reads block " + std::to_string(rblk) +
+                                 " in space " + std::to_string(space) + " without a fresh local copy");
+            fail_read = true;
+          }
+        }
+    }
+  }
+
+  // (d) capacity respected at every residency change
+  std::map<int, int64_t> used;
+  for (int i = 0; i < tr.n_res; ++i) {
+    const hesp_residency& rc = tr.residency[i];
+    used[rc.space] += rc.delta_bytes;
+    if (used[rc.space] > p.cap[rc.space])
+      violations.push_back("space " + std::to_string(rc.space) + " exceeds capacity at t=" + std::to_string(rc.time));
+    if (used[rc.space] < 0)
+      violations.push_back("space " + std::to_string(rc.space) + " under-run at t=" + std::to_string(rc.time));
+  }
+  return violations;
+}
+
+}  // namespace hx

@@ -1,0 +1,38 @@
+// trace.h — host side of the full-trace path (hesp_eval_trace /
+// hesp_verify_trace): orders the device logs of one simulated candidate the
+// way the reference's Engine::run does and derives its post-passes.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "engine_types.h"
+#include "hesp_engine.h"
+
+namespace hx {
+
+// Graph of the traced candidate, exported by the device (TraceBufs).
+struct TraceGraph {
+  std::vector<int32_t> leaves;  // program order
+  std::vector<TaskMeta> meta;   // per leaf
+  std::vector<int32_t> poff, pcnt, preds;
+  std::vector<Region> bregion;
+  std::vector<int32_t> bisint;
+  bool valid = false;
+};
+
+// Device logs of one traced candidate, as copied back.
+struct TraceLogs {
+  std::vector<int32_t> proc;  // by task id (-1: not a scheduled leaf)
+  std::vector<double> start, end;
+  std::vector<XferLog> xfers;  // emission order
+  std::vector<ResLog> res;     // emission order (ties are identical records)
+};
+
+// Fills the caller's hesp_trace arrays; HESP_OK or HESP_E_LIMIT.
+int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr);
+
+// verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph.
+std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr);
+
+}  // namespace hx

@@ -103,6 +103,60 @@ class EngineInfo(C.Structure):
                 ("blocks_per_sm", C.c_int32), ("chunk", C.c_int64)]
 
 
+ASSIGN_DTYPE = np.dtype([("task", "<i4"), ("proc", "<i4"), ("start", "<f8"), ("end", "<f8"),
+                         ("idle_avg", "<f8")])
+XFER_DTYPE = np.dtype([("block", "<i4"), ("src_space", "<i4"), ("dst_space", "<i4"), ("n_hops", "<i4"),
+                       ("bytes", "<i8"), ("start", "<f8"), ("end", "<f8"), ("has_fragment", "<i4"),
+                       ("frag", "<i4", (4,)), ("pad", "<i4"), ("hop_src", "<i4", (2,)), ("hop_dst", "<i4", (2,)),
+                       ("hop_start", "<f8", (2,)), ("hop_end", "<f8", (2,))])
+RES_DTYPE = np.dtype([("time", "<f8"), ("space", "<i4"), ("block", "<i4"), ("delta_bytes", "<i8")])
+EVENT_DTYPE = np.dtype([("kind", "<i4"), ("id", "<i4"), ("task_kind", "<i4"), ("res_a", "<i4"), ("res_b", "<i4"),
+                        ("pad", "<i4"), ("b", "<i8"), ("time", "<f8")])
+STEP_DTYPE = np.dtype([("time", "<f8"), ("active", "<i4"), ("pad", "<i4")])
+EVENT_KINDS = ("TaskStart", "TaskEnd", "XferStart", "XferEnd")
+KIND_NAMES = ("CHOL", "TRSM", "SYRK", "GEMM")
+
+
+class TraceC(C.Structure):
+    _fields_ = [("cap_assign", C.c_int32), ("cap_xfer", C.c_int32), ("cap_res", C.c_int32),
+                ("cap_events", C.c_int32), ("cap_steps", C.c_int32), ("pad0", C.c_int32),
+                ("assignments", C.c_void_p), ("transfers", C.c_void_p), ("residency", C.c_void_p),
+                ("events", C.c_void_p), ("steps", C.c_void_p),
+                ("n_assign", C.c_int32), ("n_xfer", C.c_int32), ("n_res", C.c_int32), ("n_events", C.c_int32),
+                ("n_steps", C.c_int32), ("pad1", C.c_int32), ("outcome", Outcome),
+                ("busy_time", C.c_double), ("avg_load", C.c_double), ("load_integral", C.c_double)]
+
+
+@dataclass
+class Trace:
+    """hesp::SimResult of one candidate (+ compute_load_trace), from hesp_eval_trace."""
+    status: int
+    n_leaves: int
+    makespan: float
+    assignments: np.ndarray  # ASSIGN_DTYPE, task-id order
+    transfers: np.ndarray    # XFER_DTYPE, SimResult::transfers order
+    events: np.ndarray       # EVENT_DTYPE, SimResult::events order
+    residency: np.ndarray    # RES_DTYPE, SimResult::residency_log order
+    steps: np.ndarray        # STEP_DTYPE, LoadTrace::steps
+    busy_time: float = 0.0
+    avg_load: float = 0.0
+    load_integral: float = 0.0
+
+    def event_strings(self) -> list[tuple[str, float, str, str]]:
+        """(kind, time, subject, resource) exactly as the reference's EventRec strings."""
+        out = []
+        for e in self.events:
+            k = int(e["kind"])
+            if k < 2:
+                subj = f"T{int(e['id'])}:{KIND_NAMES[int(e['task_kind'])]}:b{int(e['b'])}"
+                res = str(int(e["res_a"]))
+            else:
+                subj = f"B{int(e['id'])}"
+                res = f"{int(e['res_a'])}->{int(e['res_b'])}"
+            out.append((EVENT_KINDS[k], float(e["time"]), subj, res))
+        return out
+
+
 OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
                           ("assign_hash", "<u8"), ("xfer_hash", "<u8")])
 assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 32
@@ -112,7 +166,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 136
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -142,6 +196,9 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_eval_detail.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.POINTER(Outcome)]
     lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
+    lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
+    lib.hesp_verify_trace.argtypes = [C.c_void_p, C.POINTER(TraceC), C.c_char_p, C.c_size_t,
+                                      C.POINTER(C.c_int32)]
     lib.hesp_engine_destroy.argtypes = [C.c_void_p]
     lib.hesp_last_error.restype = C.c_char_p
     lib.hesp_status_name.restype = C.c_char_p
@@ -331,6 +388,43 @@ class BatchEngine:
         if rc < 0:
             self._check(rc, "eval_detail")
         return o, proc, start, end
+
+    def eval_trace(self, desc: np.ndarray, caps: tuple[int, int, int, int, int] | None = None) -> Trace:
+        """Full SimResult of one candidate (hesp_eval_trace).  Arrays grow on HESP_E_LIMIT."""
+        desc = np.ascontiguousarray(desc, DESC_DTYPE).reshape(1)
+        na, nx, nr, ne, ns = caps or (4096, 8192, 16384, 32768, 8192)
+        for _ in range(3):
+            arrs = (np.zeros(na, ASSIGN_DTYPE), np.zeros(nx, XFER_DTYPE), np.zeros(nr, RES_DTYPE),
+                    np.zeros(ne, EVENT_DTYPE), np.zeros(ns, STEP_DTYPE))
+            t = TraceC(na, nx, nr, ne, ns, 0, *[a.ctypes.data for a in arrs])
+            rc = self.lib.hesp_eval_trace(self.h, desc.ctypes.data, C.byref(t))
+            if rc == -4:  # HESP_E_LIMIT: the counts say what is needed
+                na, nx, nr, ne, ns = (max(na, t.n_assign), max(nx, t.n_xfer), max(nr, t.n_res),
+                                      max(ne, t.n_events), max(ns, t.n_steps))
+                continue
+            if rc < 0:
+                self._check(rc, "eval_trace")
+            self._last_trace = (t, arrs)
+            a, x, r, e, st = arrs
+            return Trace(int(t.outcome.status), int(t.outcome.n_leaves), float(t.outcome.makespan),
+                         a[:t.n_assign].copy(), x[:t.n_xfer].copy(), e[:t.n_events].copy(), r[:t.n_res].copy(),
+                         st[:t.n_steps].copy(), float(t.busy_time), float(t.avg_load), float(t.load_integral))
+        raise RuntimeError("eval_trace: could not size the trace arrays")
+
+    def verify_trace(self, trace: Trace) -> list[str]:
+        """verify_schedule of `trace` (possibly edited) against the graph of the last eval_trace."""
+        a = np.ascontiguousarray(trace.assignments)
+        x = np.ascontiguousarray(trace.transfers)
+        r = np.ascontiguousarray(trace.residency)
+        t = TraceC(len(a), len(x), len(r), 0, 0, 0, a.ctypes.data, x.ctypes.data, r.ctypes.data, None, None,
+                   len(a), len(x), len(r), 0, 0, 0)
+        t.outcome.status = trace.status
+        t.outcome.makespan = trace.makespan
+        buf = C.create_string_buffer(1 << 22)
+        n = C.c_int32(0)
+        self._check(self.lib.hesp_verify_trace(self.h, C.byref(t), buf, len(buf), C.byref(n)), "verify_trace")
+        text = buf.value.decode()
+        return text.split("\n") if n.value else []
 
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)

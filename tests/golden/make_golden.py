@@ -70,6 +70,56 @@ DETAIL = {
     "detail_evict_wb_0": ("evict_wb", 0, None),
 }
 
+# Full SimResult traces (hesp_eval_trace parity):
+# name -> (preset, candidate index).  Chosen to cover transfers over two-hop
+# routes, gather fragments (sect_cpugpu 0, policy WA 10), eviction with the
+# reference's own capacity violations (evict_*), write-through/around, R-P,
+# single-space platforms and a tabulated model.
+TRACES = {
+    "c1_0": ("c1", 0), "c2_1": ("c2", 1), "c3_2": ("c3", 2), "table_1": ("table", 1),
+    "evict_wb_0": ("evict_wb", 0), "evict_wt_1": ("evict_wt", 1), "evict_wa_0": ("evict_wa", 0),
+    "sect_cpugpu_0": ("sect_cpugpu", 0), "deep_biglittle_1": ("deep_biglittle", 1),
+    "policy_PL_EFT-P_WA_10": ("policy_PL_EFT-P_WA", 10), "policy_FCFS_R-P_WT_5": ("policy_FCFS_R-P_WT", 5),
+}
+# verify_schedule on edited schedules: (trace, task to move, seconds earlier)
+SHIFTS = {
+    "c2_1_early": ("c2_1", 400, 0.02),
+    "c2_1_late": ("c2_1", 400, -0.02),
+    "evict_wb_0_early": ("evict_wb_0", 30, 0.005),
+    "sect_cpugpu_0_late": ("sect_cpugpu_0", 20, -0.01),
+}
+
+
+def write_traces(names):
+    import gzip
+    import json
+    for name, (preset_name, idx) in TRACES.items():
+        if names and f"trace_{name}" not in names:
+            continue
+        p, _ = PARITY[preset_name]
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx)], check=True,
+                           capture_output=True, text=True)
+        d = json.loads(r.stdout)
+        d["preset"] = preset_name
+        with gzip.open(os.path.join(HERE, f"trace_{name}.json.gz"), "wt") as f:
+            json.dump(d, f, separators=(",", ":"))
+        print("trace", name, len(d["assignments"]), "tasks", len(d["transfers"]), "transfers")
+    for name, (tname, task_rank, by) in SHIFTS.items():
+        if names and f"shift_{name}" not in names:
+            continue
+        preset_name, idx = TRACES[tname]
+        p, _ = PARITY[preset_name]
+        base = json.loads(subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx)], check=True,
+                                         capture_output=True, text=True).stdout)
+        task = base["assignments"][task_rank][0]
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx), "--shift-task", str(task),
+                            "--shift-by", repr(by)], check=True, capture_output=True, text=True)
+        d = json.loads(r.stdout)
+        out = {"trace": tname, "task": task, "shift_by": by, "violations": d["violations"]}
+        with open(os.path.join(HERE, f"shift_{name}.json"), "w") as f:
+            json.dump(out, f, indent=0)
+        print("shift", name, len(d["violations"]), "violations")
+
 
 def write_descs(path, ops_lists):
     import numpy as np
@@ -113,6 +163,7 @@ def main(names):
         with open(path, "w") as f:
             f.writelines(keep)
         print(name, "detail written")
+    write_traces(names)
     for name in [n for n in (names or sorted(PARITY)) if n in PARITY]:
         p, count = PARITY[name]
         out = os.path.join(HERE, f"{name}.bin")

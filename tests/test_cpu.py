@@ -3,6 +3,7 @@ generator, host-side sharding, and -- where oracle/_ref is built (build() runs
 `make -C oracle` when /root/reference exists) -- the unmodified reference
 reproducing the committed goldens and the engine's width-1 host build
 matching the reference candidate by candidate."""
+import json
 import os
 import re
 import subprocess
@@ -149,3 +150,47 @@ def test_reference_side_bridge_compiles(tmp_path):
     tu.write_text('#include "hesp_b200_bridge.hpp"\nint main() { return 0; }\n')
     subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-I",
                     "/root/reference/proj/include", str(tu)], check=True)
+
+
+# ---- full-trace goldens ----
+from trace_io import TRACE_NAMES, fbits, hbits, read_trace  # noqa: E402
+
+
+@pytest.mark.parametrize("name", TRACE_NAMES)
+def test_trace_golden_post_passes(name):
+    """The trace goldens are self-consistent with a plain restatement of the
+    reference's post-passes (compute_load_trace sim.cpp:975-991,
+    compute_idle_avgs sim.cpp:670-702, busy_time sim.cpp:78-82)."""
+    g = read_trace(name)
+    P = len(json.load(open(os.path.join(FIXTURES, PARITY[g["preset"]][0]["platform"])))["processors"])
+    asg = [(a[0], a[1], fbits(a[2]), fbits(a[3]), fbits(a[4])) for a in g["assignments"]]
+    deltas = sorted([(s, 1) for _, _, s, _, _ in asg] + [(e, -1) for _, _, _, e, _ in asg])
+    times, active, cur, i = [], [], 0, 0
+    while i < len(deltas):
+        t = deltas[i][0]
+        while i < len(deltas) and deltas[i][0] == t:
+            cur += deltas[i][1]
+            i += 1
+        times.append(t)
+        active.append(cur)
+    assert [[hbits(t), n] for t, n in zip(times, active)] == g["load"]
+    cum = [0.0] * len(times)
+    for k in range(1, len(times)):
+        cum[k] = cum[k - 1] + (P - active[k - 1]) * (times[k] - times[k - 1])
+    import bisect
+
+    def idle_up_to(t):
+        k = bisect.bisect_right(times, t)
+        if k == 0:
+            return 0.0
+        k -= 1
+        return cum[k] + (P - active[k]) * (t - times[k])
+    for task, _, s, e, idle in asg:
+        dur = e - s
+        want = (idle_up_to(e) - idle_up_to(s)) / dur if dur > 0 else 0.0
+        assert hbits(want) == hbits(idle), task
+    busy = 0.0
+    for _, _, s, e, _ in asg:
+        busy += e - s
+    assert hbits(busy) == g["busy"]
+    assert len(g["events"]) == 2 * len(asg) + 2 * sum(len(x[7]) for x in g["transfers"])
