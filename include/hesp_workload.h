@@ -1,11 +1,12 @@
 /* hesp_workload.h — the synthetic candidate workload shared by every arm.
  *
- * A candidate is a sequence of partition operations applied, after the base
- * tiling, to a root tiled-Cholesky task:
+ * A candidate is a sequence of partition (and optionally merge) operations
+ * applied, after the base tiling, to a root tiled-Cholesky task:
  *
  *     g = TaskGraph::root_cholesky(n, elem)                  graph.cpp:397
  *     g.partition_task(0, 1.0 / s_base, min_block)           graph.cpp:456  (base tiling)
  *     for op in desc.ops: g.partition_task(op.task, 1.0 / op.s, min_block)
+ *                         (or g.merge_cluster(op.task) when merge_mask bit is set)
  *
  * The reference has no candidate generator (its solver is declared only,
  * solver.hpp:57-86), so this header *defines* the workload of BASELINE.json's
@@ -43,13 +44,16 @@ enum { HESP_CHOL = 0, HESP_TRSM = 1, HESP_SYRK = 2, HESP_GEMM = 3 };
 #define HESP_MAX_OPS 16
 
 typedef struct {
-  int32_t task; /* reference task id (must be a leaf when applied) */
+  int32_t task; /* reference task id (must be a leaf when applied); cluster id for a merge */
   int32_t s;    /* requested tile count; applied as p = 1.0 / s   */
 } hesp_op;
 
 typedef struct {
   int32_t n_ops;
-  int32_t reserved;
+  int32_t merge_mask; /* bit k set: ops[k] is TaskGraph::merge_cluster(ops[k].task)
+                         (graph.cpp:521-534) instead of a partition; a
+                         repartition_cluster (graph.cpp:536-539) is a merge
+                         followed by a partition of the restored parent */
   hesp_op ops[HESP_MAX_OPS];
 } hesp_cand_desc; /* 136 bytes */
 
@@ -60,6 +64,8 @@ typedef struct {
   int64_t min_block; /* grain; also partition_task's min_block       */
   int32_t n_s_choices;
   int32_t s_choices[4];
+  int32_t merge_pct; /* per op: % chance of merging a random innermost
+                        non-base cluster instead (0 = partitions only) */
 } hesp_gen_config;
 
 /* splitmix64, identical to hesp::Rng::next (sim.cpp:59-65). */
@@ -152,6 +158,7 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
     int32_t first, count;
     int64_t b;
     int32_t depth, pkind, s;
+    int32_t parent, dead; /* partitioned task; merged away */
   } rg[HESP_MAX_OPS + 1];
   int32_t removed[HESP_MAX_OPS];
   int32_t nr = 1, nrem = 0, nops = 0;
@@ -164,10 +171,44 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
   rg[0].depth = 1;
   rg[0].pkind = HESP_CHOL;
   rg[0].s = s_base;
+  rg[0].parent = 0;
+  rg[0].dead = 0;
   int32_t next_id = 1 + n_base;
+  int32_t mask = 0;
   HESP_NOUNROLL for (int32_t op = 0; op < K; ++op) {
+    if (cfg->merge_pct > 0) {
+      /* innermost live clusters created by earlier ops (never the base one) */
+      int32_t ninner = 0;
+      HESP_NOUNROLL for (int32_t r = 1; r < nr; ++r) {
+        int32_t inner = !rg[r].dead;
+        HESP_NOUNROLL for (int32_t q = 0; q < nrem && inner; ++q)
+          if (removed[q] >= rg[r].first && removed[q] < rg[r].first + rg[r].count) inner = 0;
+        ninner += inner;
+      }
+      if (ninner > 0 && (int32_t)(hesp_splitmix_next(&st) % 100u) < cfg->merge_pct) {
+        int32_t k = (int32_t)(hesp_splitmix_next(&st) % (uint64_t)ninner), c = -1;
+        HESP_NOUNROLL for (int32_t r = 1; r < nr && c < 0; ++r) {
+          int32_t inner = !rg[r].dead;
+          HESP_NOUNROLL for (int32_t q = 0; q < nrem && inner; ++q)
+            if (removed[q] >= rg[r].first && removed[q] < rg[r].first + rg[r].count) inner = 0;
+          if (inner && k-- == 0) c = r;
+        }
+        out->ops[nops].task = c; /* cluster ids follow partition order: base = 0 */
+        out->ops[nops].s = 0;
+        mask |= 1 << nops;
+        ++nops;
+        rg[c].dead = 1;
+        /* the restored parent is a leaf again */
+        int32_t w = 0;
+        HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
+          if (removed[q] != rg[c].parent) removed[w++] = removed[q];
+        nrem = w;
+        continue;
+      }
+    }
     uint64_t total = 0;
     HESP_NOUNROLL for (int32_t r = 0; r < nr; ++r) {
+      if (rg[r].dead) continue;
       if (!(rg[r].b / 2 >= cfg->min_block && rg[r].depth < cfg->max_depth)) continue;
       int32_t live = rg[r].count;
       HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
@@ -178,6 +219,7 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
     uint64_t pick = hesp_splitmix_next(&st) % total;
     int32_t id = -1, rsel = -1;
     HESP_NOUNROLL for (int32_t r = 0; r < nr && id < 0; ++r) {
+      if (rg[r].dead) continue;
       if (!(rg[r].b / 2 >= cfg->min_block && rg[r].depth < cfg->max_depth)) continue;
       int32_t live = rg[r].count;
       HESP_NOUNROLL for (int32_t q = 0; q < nrem; ++q)
@@ -213,11 +255,13 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
     rg[nr].depth = rg[rsel].depth + 1;
     rg[nr].pkind = kind;
     rg[nr].s = (int32_t)s;
+    rg[nr].parent = id;
+    rg[nr].dead = 0;
     ++nr;
     next_id += cnt;
   }
   out->n_ops = nops;
-  out->reserved = 0;
+  out->merge_mask = mask;
   HESP_NOUNROLL for (int32_t r = nops; r < HESP_MAX_OPS; ++r) {
     out->ops[r].task = -1;
     out->ops[r].s = 0;

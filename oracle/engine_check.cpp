@@ -76,6 +76,7 @@ int main(int argc, char** argv) {
     else if (k == "--selection") selection = v();
     else if (k == "--caching") caching = v();
     else if (k == "--sched-seed") sseed = std::stoull(v());
+    else if (k == "--merge-pct") gen.merge_pct = std::stoi(v());
     else if (k == "--first") first = std::stoull(v());
     else if (k == "--count") count = std::stoull(v());
     else if (k == "--verbose") verbose = std::stoi(v());
@@ -190,7 +191,10 @@ int main(int argc, char** argv) {
     try {
       auto g = hesp::TaskGraph::root_cholesky(n, elem);
       g.partition_task(0, 1.0 / s_base, gen.min_block);
-      for (int k = 0; k < d.n_ops; ++k) g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, gen.min_block);
+      for (int k = 0; k < d.n_ops; ++k) {
+        if ((d.merge_mask >> k) & 1) g.merge_cluster(d.ops[k].task);
+        else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, gen.min_block);
+      }
       rleaves = (int)g.leaf_tasks().size();
       res = hesp::simulate(g, rplat, rmodel, rcfg);
       rmk = res.makespan;

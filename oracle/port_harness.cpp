@@ -67,6 +67,13 @@ int main(int argc, char** argv) {
     else if (k == "--selection") selection = v();
     else if (k == "--caching") caching = v();
     else if (k == "--sched-seed") sched.seed = std::stoull(v());
+    else if (k == "--merge-pct") {
+      gen.merge_pct = std::stoi(v());
+      if (gen.merge_pct) {
+        std::fprintf(stderr, "port_harness: merge ops are not restated in oracle/port (partitions only)\n");
+        return 2;
+      }
+    }
     else if (k == "--first") first = std::stoll(v());
     else if (k == "--count") count = std::stoll(v());
     else if (k == "--threads") threads = std::stoi(v());

@@ -99,8 +99,10 @@ Record evaluate(const Ctx& c, uint64_t index, hesp::SimResult* keep, hesp::TaskG
   try {
     auto g = hesp::TaskGraph::root_cholesky(c.a->n, c.a->elem);
     g.partition_task(0, 1.0 / c.a->s_base, c.a->gen.min_block);
-    for (int k = 0; k < d.n_ops; ++k)
-      g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, c.a->gen.min_block);
+    for (int k = 0; k < d.n_ops; ++k) {
+      if ((d.merge_mask >> k) & 1) g.merge_cluster(d.ops[k].task);  // graph.cpp:521-534
+      else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, c.a->gen.min_block);
+    }
     r.n_leaves = static_cast<int32_t>(g.leaf_tasks().size());
     auto res = hesp::simulate(g, *c.plat, *c.model, c.cfg);
     r.makespan = res.makespan;
@@ -252,6 +254,7 @@ int main(int argc, char** argv) {
     else if (k == "--selection") a.selection = v();
     else if (k == "--caching") a.caching = v();
     else if (k == "--sched-seed") a.sched_seed = std::strtoull(v(), nullptr, 0);
+    else if (k == "--merge-pct") a.gen.merge_pct = std::atoi(v());
     else if (k == "--first") a.first = std::strtoull(v(), nullptr, 0);
     else if (k == "--count") a.count = std::strtoull(v(), nullptr, 0);
     else if (k == "--threads") a.threads = std::atoi(v());
@@ -320,7 +323,8 @@ int main(int argc, char** argv) {
                  (unsigned long long)bits(r.makespan), (unsigned long long)r.assign_hash,
                  (unsigned long long)r.xfer_hash);
     std::fprintf(f, "ops");
-    for (int k = 0; k < d.n_ops; ++k) std::fprintf(f, " %d/%d", d.ops[k].task, d.ops[k].s);
+    for (int k = 0; k < d.n_ops; ++k)
+      std::fprintf(f, (d.merge_mask >> k) & 1 ? " m%d" : " %d/%d", d.ops[k].task, d.ops[k].s);
     std::fprintf(f, "\n");
     if (g) {
       for (const auto& [id, blk] : g->data().blocks())

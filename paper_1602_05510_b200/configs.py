@@ -16,10 +16,11 @@ BIGLITTLE = ("platform_biglittle.json", "model_biglittle.json")
 
 
 def preset(fix, n, elem, s_base, k_max, max_depth=3, s_choices=(2, 4), seed=1,
-           ordering="PL", selection="EFT-P", caching="WB", sched_seed=0, min_block=64):
+           ordering="PL", selection="EFT-P", caching="WB", sched_seed=0, min_block=64, merge_pct=0):
     return dict(platform=fix[0], model=fix[1], n=n, elem=elem, s_base=s_base, k_max=k_max,
                 max_depth=max_depth, s_choices=tuple(s_choices), seed=seed, ordering=ordering,
-                selection=selection, caching=caching, sched_seed=sched_seed, min_block=min_block)
+                selection=selection, caching=caching, sched_seed=sched_seed, min_block=min_block,
+                merge_pct=merge_pct)
 
 
 # BASELINE.json configs
@@ -48,6 +49,11 @@ PARITY = {
     "deep_biglittle": (preset(BIGLITTLE, 8192, 8, 8, 12, max_depth=4, seed=12, selection="R-P",
                               sched_seed=77), 48),
 }
+# merge ops (TaskGraph::merge_cluster) mixed into the random partitionings
+PARITY["merge_c2"] = (preset(CPUGPU, 16384, 4, 16, 12, seed=21, merge_pct=35), 64)
+PARITY["merge_evict"] = (preset(CPUGPU_EVICT, 16384, 4, 16, 10, seed=22, merge_pct=30), 24)
+PARITY["merge_c3"] = (preset(BIGLITTLE, 8192, 8, 16, 10, seed=23, merge_pct=40, ordering="FCFS",
+                             selection="F-P"), 32)
 for o, s, c in itertools.product(("FCFS", "PL"), ("R-P", "F-P", "EIT-P", "EFT-P"), ("WT", "WB", "WA")):
     PARITY[f"policy_{o}_{s}_{c}"] = (preset(CPUGPU, 4096, 4, 8, 8, seed=7, ordering=o, selection=s, caching=c,
                                             sched_seed=5), 24)
@@ -63,7 +69,7 @@ def harness_args(p: dict, fixtures_dir: str) -> list[str]:
             "--seed", str(p["seed"]), "--kmax", str(p["k_max"]), "--maxdepth", str(p["max_depth"]),
             "--min-block", str(p["min_block"]), "--s-choices", ",".join(map(str, p["s_choices"])),
             "--ordering", p["ordering"], "--selection", p["selection"], "--caching", p["caching"],
-            "--sched-seed", str(p["sched_seed"])]
+            "--sched-seed", str(p["sched_seed"]), "--merge-pct", str(p.get("merge_pct", 0))]
 
 
 def make_engine(p: dict, device: int = 0):
@@ -73,5 +79,5 @@ def make_engine(p: dict, device: int = 0):
     model = load_model(p["model"])
     sched = SchedConfig(p["ordering"], p["selection"], p["caching"], p["sched_seed"], p["min_block"])
     wl = Workload(p["n"], p["elem"], p["s_base"], p["seed"], p["k_max"], p["max_depth"], p["min_block"],
-                  p["s_choices"])
+                  p["s_choices"], p.get("merge_pct", 0))
     return BatchEngine(plat, model, sched, wl, device)

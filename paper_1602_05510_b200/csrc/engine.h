@@ -269,6 +269,7 @@ struct Engine {
   HX int4* bcell() const { return (int4*)(slot + PB.lay.bcell); }      // cell range per block
   HX uint16_t* rht() const { return (uint16_t*)(slot + PB.lay.rht); }  // region hash of new blocks
   HX uint8_t* pmark() const { return (uint8_t*)(slot + PB.lay.pmark); }  // 1 + partition entry per task id
+  HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - nbb
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -483,7 +484,10 @@ struct Engine {
     m.next = -1;
     m.isint = isint ? 1 : 0;
     m.pad = 0;
-    if (wp.lane() == 0) bm()[id - nbb] = m;
+    if (wp.lane() == 0) {
+      bm()[id - nbb] = m;
+      bref()[id - nbb] = 0;
+    }
     if (t >= 0 && id - nbb < RHT / 2) {
       unsigned i = rhash(r) & (RHT - 1);
       while (rht()[i] != 0xffff) i = (i + 1) & (RHT - 1);
@@ -580,7 +584,61 @@ struct Engine {
     }
     m.bidx = (int8_t)bi;
     const int id = ntasks++;
-    if (wp.lane() == 0) tm()[id - nbt] = m;
+    if (wp.lane() == 0) {
+      tm()[id - nbt] = m;
+      NOUNROLL for (int k = 0; k <= nr; ++k)
+        if (m.blk[k] >= nbb) ++bref()[m.blk[k] - nbb];
+    }
+    wp.sync();
+  }
+
+  // merged-away task (member of a dead cluster): no longer in tasks_
+  HX bool dead_task(int id) const {
+    NOUNROLL for (int i = 0; i < npart; ++i) {
+      const PartEntry pe = sm->part[i];
+      if (pe.task < 0 && id >= pe.child0 && id < pe.child0 + pe.nchild) return true;
+    }
+    return false;
+  }
+  static HX bool dead_region(const Region& r) { return r.rows == 0; }
+
+  // TaskGraph::merge_cluster (graph.cpp:521-534) with
+  // DataDag::prune_unreferenced (graph.cpp:214-266): the members leave the
+  // graph (their ids stay consumed), the parent is a leaf again, and every
+  // candidate block no remaining task references is removed -- here by
+  // giving it an empty region, which no geometric query (find, overlap,
+  // containment, scopes) can match.  Intersection descriptors are pruned by
+  // their DataDag parent links, which E1 does not model after a prune; a
+  // merge while any intersection block exists reports ST_ENGINE_LIMIT, as
+  // does merging the base cluster (the base tiling is shared by the batch).
+  HXN void apply_merge(int c) {
+    if (c < 0 || c >= npart || sm->part[c].task < 0) return fail(ST_UNKNOWN_CLUSTER);
+    const PartEntry pe = sm->part[c];
+    NOUNROLL for (int m = pe.child0; m < pe.child0 + pe.nchild; ++m)
+      if (part_index(m) >= 0) return fail(ST_NESTED_CLUSTER);
+    if (c == 0 || pe.child0 < nbt) return fail(ST_ENGINE_LIMIT);
+    bool sect = false;
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
+      const BlockMeta& o = bm()[b - nbb];
+      if (o.isint && !dead_region(o.r)) sect = true;
+    }
+    if (wp.any(sect)) return fail(ST_ENGINE_LIMIT);
+    NOUNROLL for (int m = pe.child0 + wp.lane(); m < pe.child0 + pe.nchild; m += WP::W) {
+      const TaskMeta t = tm()[m - nbt];
+      NOUNROLL for (int k = 0; k <= t.nrd; ++k)
+        if (t.blk[k] >= nbb) wp.atomic_add(&bref()[t.blk[k] - nbb], -1);
+    }
+    wp.sync();
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
+      BlockMeta& o = bm()[b - nbb];
+      if (!o.isint && bref()[b - nbb] == 0 && !dead_region(o.r)) {
+        o.r.row = -1;
+        o.r.col = -1;
+        o.r.rows = 0;
+        o.r.cols = 0;
+      }
+    }
+    if (wp.lane() == 0) sm->part[c].task = -2 - pe.task;
     wp.sync();
   }
 
@@ -588,6 +646,7 @@ struct Engine {
   // enumerate_partition loop nests (graph.cpp:301-392).
   HXN void apply_op(int task_id, int s_req) {
     if (task_id < 0 || task_id >= ntasks) return fail(ST_VALIDATION);
+    if (task_id >= nbt && dead_task(task_id)) return fail(ST_VALIDATION);  // merged away: unknown task
     if (part_index(task_id) >= 0) return fail(ST_NOT_A_LEAF);
     const double p = 1.0 / (double)s_req;
     if (!(p > 0.0 && p < 1.0)) return fail(ST_VALIDATION);
@@ -732,7 +791,8 @@ struct Engine {
   HXN void build_tiles() {
     NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt()[i] = 0;
     wp.sync();
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) wp.atomic_add(&tl_cnt()[bm()[b - nbb].tile], 1);
+    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W)
+      if (!dead_region(bm()[b - nbb].r)) wp.atomic_add(&tl_cnt()[bm()[b - nbb].tile], 1);
     wp.sync();
     // exclusive scan over base tiles
     int run = 0;
@@ -753,6 +813,7 @@ struct Engine {
     NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb()[i] = 0;  // fill cursor
     wp.sync();
     NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
+      if (dead_region(bm()[b - nbb].r)) continue;
       const int t = bm()[b - nbb].tile;
       const int pos = wp.atomic_add(&tl_ncb()[t], 1);
       tl_ids()[tl_head()[t] + pos] = b;
@@ -767,11 +828,13 @@ struct Engine {
     NOUNROLL for (int i = wp.lane(); i < ntasks; i += WP::W) pmark()[i] = 0;
     wp.sync();
     if (wp.lane() == 0)
-      for (int i = 0; i < npart; ++i) pmark()[sm->part[i].task] = (uint8_t)(i + 1);
+      for (int i = 0; i < npart; ++i)
+        if (sm->part[i].task >= 0) pmark()[sm->part[i].task] = (uint8_t)(i + 1);
     wp.sync();
     // subtree leaf() counts, innermost partitions last in op order
     NOUNROLL for (int i = npart - 1; i >= 0; --i) {
       const PartEntry pe = sm->part[i];
+      if (pe.task < 0) continue;  // merged away
       int cnt = 0;
       NOUNROLL for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
         const int pi = part_of(c);
@@ -2446,7 +2509,10 @@ struct Engine {
   // Build phase: base tiling + ops -> leaves, dependences; state left in the slot.
   HXN void build(const hesp_cand_desc& d) {
     reset_to_base();
-    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) apply_op(d.ops[k].task, d.ops[k].s);
+    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
+      if ((d.merge_mask >> k) & 1) apply_merge(d.ops[k].task);
+      else apply_op(d.ops[k].task, d.ops[k].s);
+    }
     sum_k = 0;
     nleaves = 0;
     nedges = 0;

@@ -24,6 +24,8 @@ enum : int32_t {
   ST_NO_ROUTE = 1 + 5,
   ST_NOT_A_LEAF = 1 + 7,
   ST_INDIVISIBLE = 1 + 8,
+  ST_NESTED_CLUSTER = 1 + 10,
+  ST_UNKNOWN_CLUSTER = 1 + 11,
   ST_MODEL_MISS = 1 + 12,
   ST_CAPACITY = 1 + 13,
   ST_NO_PROCESSORS = 1 + 14,
@@ -85,6 +87,8 @@ struct SlotHeader {
   int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, pad;
 };
 
+// One cluster (TaskCluster, graph.hpp:103-108); index = cluster id.  A merged
+// cluster keeps its entry (ids are never reused) with task = -2 - parent.
 struct PartEntry {
   int32_t task, child0, nchild, leaves;
 };
@@ -92,7 +96,7 @@ struct PartEntry {
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
   size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
-  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark;
+  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
@@ -214,6 +218,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.bcell = take(16 * B);
   L.rht = take(2 * (size_t)RHT);
   L.pmark = take(T);
+  L.bref = take(4 * B);  // task references per candidate block (merge pruning)
   L.valid = take(8 * B * S);
   L.lastu = take(8 * B * S);
   L.pinu = take(8 * B * S);

@@ -69,7 +69,8 @@ class SchedConfigC(C.Structure):
 
 class GenConfig(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("k_max", C.c_int32), ("max_depth", C.c_int32),
-                ("min_block", C.c_int64), ("n_s_choices", C.c_int32), ("s_choices", C.c_int32 * 4)]
+                ("min_block", C.c_int64), ("n_s_choices", C.c_int32), ("s_choices", C.c_int32 * 4),
+                ("merge_pct", C.c_int32)]
 
 
 class WorkloadC(C.Structure):
@@ -81,7 +82,7 @@ class Op(C.Structure):
 
 
 class CandDesc(C.Structure):
-    _fields_ = [("n_ops", C.c_int32), ("reserved", C.c_int32), ("ops", Op * MAX_OPS)]
+    _fields_ = [("n_ops", C.c_int32), ("merge_mask", C.c_int32), ("ops", Op * MAX_OPS)]
 
 
 class Outcome(C.Structure):
@@ -160,7 +161,7 @@ class Trace:
 OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
                           ("assign_hash", "<u8"), ("xfer_hash", "<u8")])
 assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 32
-DESC_DTYPE = np.dtype([("n_ops", "<i4"), ("reserved", "<i4"), ("ops", "<i4", (MAX_OPS, 2))])
+DESC_DTYPE = np.dtype([("n_ops", "<i4"), ("merge_mask", "<i4"), ("ops", "<i4", (MAX_OPS, 2))])
 assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 136
 
 EXPORTS = [
@@ -303,6 +304,7 @@ class Workload:
     max_depth: int = 3
     min_block: int = 64
     s_choices: tuple = (2, 4)
+    merge_pct: int = 0
 
 
 class BatchEngine:
@@ -318,7 +320,7 @@ class BatchEngine:
                                 0, sched.seed, sched.min_block)
         sc = (C.c_int32 * 4)(*(list(workload.s_choices) + [0] * (4 - len(workload.s_choices))))
         g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block,
-                      len(workload.s_choices), sc)
+                      len(workload.s_choices), sc, workload.merge_pct)
         self._wc = WorkloadC(workload.n, workload.elem_size, workload.s_base, g)
         self._keep = keep
         h = self.lib.hesp_engine_create(device, C.byref(self._pc), C.byref(self._mc), C.byref(self._sc),
@@ -436,7 +438,8 @@ def generate_batch(workload: "Workload", n_base: int, base_b: int, first: int, c
     """Host generator (hesp_generate_batch): no engine or GPU needed."""
     lib = load_library()
     sc = (C.c_int32 * 4)(*(list(workload.s_choices) + [0] * (4 - len(workload.s_choices))))
-    g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block, len(workload.s_choices), sc)
+    g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block, len(workload.s_choices), sc,
+                  workload.merge_pct)
     d = np.zeros(count, DESC_DTYPE)
     rc = lib.hesp_generate_batch(C.byref(g), workload.n // base_b, n_base, base_b, first, count, d.ctypes.data)
     if rc != 0:

@@ -58,7 +58,24 @@ SECT_OPS = [
     [(1, 2), (2, 3), (9, 3), (10, 2)],
     [(1, 3), (2, 2), (4, 3), (5, 2), (9, 2)],
 ]
+# merge_cluster / repartition on the C2 base (cluster ids follow partition
+# order, base = 0): ("m", c) merges cluster c.  Base task 18 = GEMM(2,1,0),
+# 17 = SYRK(1,0), 2 = TRSM(1,0); a s=2 split of a CHOL/TRSM/SYRK/GEMM base
+# task makes 4/6/6/8 members starting at id 817.
+MERGE_OPS = [
+    [(18, 2), ("m", 1)],                            # partition then merge: back to the base tiling
+    [(18, 2), ("m", 1), (18, 4)],                   # repartition_cluster(1, 1/4)
+    [(18, 2), ("m", 1), (18, 2)],                   # re-partition to the same s: fresh ids
+    [(18, 2), (817, 2), ("m", 1)],                  # member partitioned -> NestedCluster
+    [(18, 2), (817, 2), ("m", 2), ("m", 1)],        # innermost first, then the parent cluster
+    [("m", 1)],                                     # no such cluster -> UnknownCluster
+    [(18, 2), ("m", 1), ("m", 1)],                  # merged twice -> UnknownCluster
+    [(18, 2), ("m", 1), (817, 2)],                  # partition a merged-away task -> Validation
+    [(1, 2), (2, 2), (17, 4), ("m", 2), (18, 2), ("m", 1)],  # interleaved, shared blocks survive
+    [(2, 4), (17, 2), ("m", 1), (3, 2), ("m", 3), (2, 2)],
+]
 EXPLICIT = {
+    "explicit_merge_c2": ("c2", MERGE_OPS),
     "explicit_c2": ("c2", EXPLICIT_OPS),
     "explicit_c3": ("c3", EXPLICIT_OPS),
     "explicit_sect": ("sect_cpugpu", SECT_OPS),
@@ -130,7 +147,11 @@ def write_descs(path, ops_lists):
     for i, ops in enumerate(ops_lists):
         d[i]["n_ops"] = len(ops)
         for k, (t, s) in enumerate(ops):
-            d[i]["ops"][k] = (t, s)
+            if t == "m":  # merge_cluster(s)
+                d[i]["ops"][k] = (s, 0)
+                d[i]["merge_mask"] |= 1 << k
+            else:
+                d[i]["ops"][k] = (t, s)
     d.tofile(path)
 
 

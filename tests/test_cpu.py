@@ -129,7 +129,8 @@ def test_reference_reproduces_goldens(name, tmp_path):
 
 
 CHECK_PRESETS = ["c3", "policy_PL_EFT-P_WB", "policy_FCFS_EIT-P_WT", "policy_PL_F-P_WA", "policy_FCFS_R-P_WB",
-                 "evict_wb", "evict_wa", "sect_cpugpu", "sect_biglittle", "deep_biglittle", "table"]
+                 "evict_wb", "evict_wa", "sect_cpugpu", "sect_biglittle", "deep_biglittle", "table", "merge_c2",
+                 "merge_evict", "merge_c3"]
 
 
 @pytest.mark.skipif(not os.path.exists(ENGINE_CHECK), reason="oracle/_ref not built (needs /root/reference)")
