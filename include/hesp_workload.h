@@ -6,7 +6,7 @@
  *     g = TaskGraph::root_cholesky(n, elem)                  graph.cpp:397
  *     g.partition_task(0, 1.0 / s_base, min_block)           graph.cpp:456  (base tiling)
  *     for op in desc.ops: g.partition_task(op.task, 1.0 / op.s, min_block)
- *                         (or g.merge_cluster(op.task) when merge_mask bit is set)
+ *                         (or g.merge_cluster(op.task) when op.s == HESP_OP_MERGE)
  *
  * The reference has no candidate generator (its solver is declared only,
  * solver.hpp:57-86), so this header *defines* the workload of BASELINE.json's
@@ -41,25 +41,27 @@ extern "C" {
 /* TaskKind ordinals, platform.hpp:15 */
 enum { HESP_CHOL = 0, HESP_TRSM = 1, HESP_SYRK = 2, HESP_GEMM = 3 };
 
-#define HESP_MAX_OPS 16
+#define HESP_MAX_OPS 64     /* operations per candidate (solver chains append one per iteration) */
+#define HESP_GEN_MAX_OPS 16 /* bound on the generator's k_max */
+/* op.s value marking TaskGraph::merge_cluster(op.task) (graph.cpp:521-534);
+ * repartition_cluster (graph.cpp:536-539) is a merge followed by a partition
+ * of the restored parent. */
+#define HESP_OP_MERGE ((int32_t)0x80000000)
 
 typedef struct {
   int32_t task; /* reference task id (must be a leaf when applied); cluster id for a merge */
-  int32_t s;    /* requested tile count; applied as p = 1.0 / s   */
+  int32_t s;    /* requested tile count, applied as p = 1.0 / s; HESP_OP_MERGE = merge */
 } hesp_op;
 
 typedef struct {
   int32_t n_ops;
-  int32_t merge_mask; /* bit k set: ops[k] is TaskGraph::merge_cluster(ops[k].task)
-                         (graph.cpp:521-534) instead of a partition; a
-                         repartition_cluster (graph.cpp:536-539) is a merge
-                         followed by a partition of the restored parent */
+  int32_t reserved;
   hesp_op ops[HESP_MAX_OPS];
-} hesp_cand_desc; /* 136 bytes */
+} hesp_cand_desc; /* 520 bytes */
 
 typedef struct {
   uint64_t seed;
-  int32_t k_max;     /* K ~ U[0, k_max], k_max <= HESP_MAX_OPS       */
+  int32_t k_max;     /* K ~ U[0, k_max], k_max <= HESP_GEN_MAX_OPS   */
   int32_t max_depth; /* leaves with depth < max_depth are eligible    */
   int64_t min_block; /* grain; also partition_task's min_block       */
   int32_t n_s_choices;
@@ -159,11 +161,11 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
     int64_t b;
     int32_t depth, pkind, s;
     int32_t parent, dead; /* partitioned task; merged away */
-  } rg[HESP_MAX_OPS + 1];
-  int32_t removed[HESP_MAX_OPS];
+  } rg[HESP_GEN_MAX_OPS + 1];
+  int32_t removed[HESP_GEN_MAX_OPS];
   int32_t nr = 1, nrem = 0, nops = 0;
   uint64_t st = cfg->seed ^ index;
-  const int32_t kmax = cfg->k_max < HESP_MAX_OPS ? cfg->k_max : HESP_MAX_OPS;
+  const int32_t kmax = cfg->k_max < HESP_GEN_MAX_OPS ? cfg->k_max : HESP_GEN_MAX_OPS;
   const int32_t K = (int32_t)(hesp_splitmix_next(&st) % (uint64_t)(kmax + 1));
   rg[0].first = 1;
   rg[0].count = n_base;
@@ -174,7 +176,6 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
   rg[0].parent = 0;
   rg[0].dead = 0;
   int32_t next_id = 1 + n_base;
-  int32_t mask = 0;
   HESP_NOUNROLL for (int32_t op = 0; op < K; ++op) {
     if (cfg->merge_pct > 0) {
       /* innermost live clusters created by earlier ops (never the base one) */
@@ -194,8 +195,7 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
           if (inner && k-- == 0) c = r;
         }
         out->ops[nops].task = c; /* cluster ids follow partition order: base = 0 */
-        out->ops[nops].s = 0;
-        mask |= 1 << nops;
+        out->ops[nops].s = HESP_OP_MERGE;
         ++nops;
         rg[c].dead = 1;
         /* the restored parent is a leaf again */
@@ -261,7 +261,7 @@ HESP_HD void hesp_generate(const hesp_gen_config* cfg, int32_t s_base, int32_t n
     next_id += cnt;
   }
   out->n_ops = nops;
-  out->merge_mask = mask;
+  out->reserved = 0;
   HESP_NOUNROLL for (int32_t r = nops; r < HESP_MAX_OPS; ++r) {
     out->ops[r].task = -1;
     out->ops[r].s = 0;

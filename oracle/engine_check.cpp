@@ -192,7 +192,7 @@ int main(int argc, char** argv) {
       auto g = hesp::TaskGraph::root_cholesky(n, elem);
       g.partition_task(0, 1.0 / s_base, gen.min_block);
       for (int k = 0; k < d.n_ops; ++k) {
-        if ((d.merge_mask >> k) & 1) g.merge_cluster(d.ops[k].task);
+        if (d.ops[k].s == HESP_OP_MERGE) g.merge_cluster(d.ops[k].task);
         else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, gen.min_block);
       }
       rleaves = (int)g.leaf_tasks().size();

@@ -100,7 +100,7 @@ Record evaluate(const Ctx& c, uint64_t index, hesp::SimResult* keep, hesp::TaskG
     auto g = hesp::TaskGraph::root_cholesky(c.a->n, c.a->elem);
     g.partition_task(0, 1.0 / c.a->s_base, c.a->gen.min_block);
     for (int k = 0; k < d.n_ops; ++k) {
-      if ((d.merge_mask >> k) & 1) g.merge_cluster(d.ops[k].task);  // graph.cpp:521-534
+      if (d.ops[k].s == HESP_OP_MERGE) g.merge_cluster(d.ops[k].task);  // graph.cpp:521-534
       else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, c.a->gen.min_block);
     }
     r.n_leaves = static_cast<int32_t>(g.leaf_tasks().size());
@@ -324,7 +324,8 @@ int main(int argc, char** argv) {
                  (unsigned long long)r.xfer_hash);
     std::fprintf(f, "ops");
     for (int k = 0; k < d.n_ops; ++k)
-      std::fprintf(f, (d.merge_mask >> k) & 1 ? " m%d" : " %d/%d", d.ops[k].task, d.ops[k].s);
+      if (d.ops[k].s == HESP_OP_MERGE) std::fprintf(f, " m%d", d.ops[k].task);
+      else std::fprintf(f, " %d/%d", d.ops[k].task, d.ops[k].s);
     std::fprintf(f, "\n");
     if (g) {
       for (const auto& [id, blk] : g->data().blocks())

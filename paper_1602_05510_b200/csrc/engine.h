@@ -243,7 +243,6 @@ struct Small {
   double link_free[MAXL];
   long long used[MAXS];
   double est[MAXS];
-  PartEntry part[MAXPART];
   int32_t tmp_i[64];
   double tmp_d[8];
 };
@@ -270,6 +269,8 @@ struct Engine {
   HX uint16_t* rht() const { return (uint16_t*)(slot + PB.lay.rht); }  // region hash of new blocks
   HX uint8_t* pmark() const { return (uint8_t*)(slot + PB.lay.pmark); }  // 1 + partition entry per task id
   HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - nbb
+  HX PartEntry* part() const { return (PartEntry*)(slot + PB.lay.part); }  // clusters, by id
+  HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -407,7 +408,7 @@ struct Engine {
   HX bool is_dirty(int b, int s) const { return (bflags()[b] >> (8 + s)) & 1u; }
   HX int part_index(int task) const {
     NOUNROLL for (int i = 0; i < npart; ++i)
-      if (sm->part[i].task == task) return i;
+      if (part()[i].task == task) return i;
     return -1;
   }
   // O(1) variant once pmark() is filled (build_order onwards)
@@ -595,7 +596,7 @@ struct Engine {
   // merged-away task (member of a dead cluster): no longer in tasks_
   HX bool dead_task(int id) const {
     NOUNROLL for (int i = 0; i < npart; ++i) {
-      const PartEntry pe = sm->part[i];
+      const PartEntry pe = part()[i];
       if (pe.task < 0 && id >= pe.child0 && id < pe.child0 + pe.nchild) return true;
     }
     return false;
@@ -612,8 +613,8 @@ struct Engine {
   // merge while any intersection block exists reports ST_ENGINE_LIMIT, as
   // does merging the base cluster (the base tiling is shared by the batch).
   HXN void apply_merge(int c) {
-    if (c < 0 || c >= npart || sm->part[c].task < 0) return fail(ST_UNKNOWN_CLUSTER);
-    const PartEntry pe = sm->part[c];
+    if (c < 0 || c >= npart || part()[c].task < 0) return fail(ST_UNKNOWN_CLUSTER);
+    const PartEntry pe = part()[c];
     NOUNROLL for (int m = pe.child0; m < pe.child0 + pe.nchild; ++m)
       if (part_index(m) >= 0) return fail(ST_NESTED_CLUSTER);
     if (c == 0 || pe.child0 < nbt) return fail(ST_ENGINE_LIMIT);
@@ -638,7 +639,7 @@ struct Engine {
         o.r.cols = 0;
       }
     }
-    if (wp.lane() == 0) sm->part[c].task = -2 - pe.task;
+    if (wp.lane() == 0) part()[c].task = -2 - pe.task;
     wp.sync();
   }
 
@@ -773,10 +774,10 @@ struct Engine {
     }
     if (status) return;
     if (wp.lane() == 0) {
-      sm->part[npart].task = task_id;
-      sm->part[npart].child0 = child0;
-      sm->part[npart].nchild = ntasks - child0;
-      sm->part[npart].leaves = 0;
+      part()[npart].task = task_id;
+      part()[npart].child0 = child0;
+      part()[npart].nchild = ntasks - child0;
+      part()[npart].leaves = 0;
     }
     wp.sync();
     ++npart;
@@ -829,22 +830,25 @@ struct Engine {
     wp.sync();
     if (wp.lane() == 0)
       for (int i = 0; i < npart; ++i)
-        if (sm->part[i].task >= 0) pmark()[sm->part[i].task] = (uint8_t)(i + 1);
+        if (part()[i].task >= 0) pmark()[part()[i].task] = (uint8_t)(i + 1);
     wp.sync();
     // subtree leaf() counts, innermost partitions last in op order
     NOUNROLL for (int i = npart - 1; i >= 0; --i) {
-      const PartEntry pe = sm->part[i];
+      const PartEntry pe = part()[i];
       if (pe.task < 0) continue;  // merged away
       int cnt = 0;
       NOUNROLL for (int c = pe.child0; c < pe.child0 + pe.nchild; ++c) {
         const int pi = part_of(c);
-        cnt += pi >= 0 ? sm->part[pi].leaves : 1;
+        cnt += pi >= 0 ? part()[pi].leaves : 1;
       }
-      if (wp.lane() == 0) sm->part[i].leaves = cnt;
+      if (wp.lane() == 0) part()[i].leaves = cnt;
       wp.sync();
     }
     // explicit stack of (first child, count, output position)
-    int sf[MAXPART], sc[MAXPART], sp[MAXPART];
+    // pending sibling subtrees: at most one entry per cluster (slot scratch)
+    int* const sf = dstack();
+    int* const sc = sf + MAXPART;
+    int* const sp = sc + MAXPART;
     int top = 0;
     const int r = part_of(0);
     if (r < 0) {  // unpartitioned root: a single leaf()
@@ -853,12 +857,15 @@ struct Engine {
       nleaves = 1;
       return;
     }
-    sf[0] = sm->part[r].child0;
-    sc[0] = sm->part[r].nchild;
-    sp[0] = 0;
+    if (wp.lane() == 0) {
+      sf[0] = part()[r].child0;
+      sc[0] = part()[r].nchild;
+      sp[0] = 0;
+    }
     top = 1;
-    nleaves = sm->part[r].leaves;
+    nleaves = part()[r].leaves;
     while (top > 0) {
+      wp.sync();
       --top;
       const int f = sf[top], c = sc[top];
       int pos = sp[top];
@@ -867,7 +874,7 @@ struct Engine {
         int pi = -1, sz = 0;
         if (k < c) {
           pi = part_of(f + k);
-          sz = pi >= 0 ? sm->part[pi].leaves : 1;
+          sz = pi >= 0 ? part()[pi].leaves : 1;
         }
         int incl = sz;
 #if defined(__CUDACC__)
@@ -883,12 +890,12 @@ struct Engine {
           const int ln = ctz32(mm);
           const int q = wp.bcast(pi, ln);
           const int qp = wp.bcast(my, ln);
-          if (top < MAXPART) {
-            sf[top] = sm->part[q].child0;
-            sc[top] = sm->part[q].nchild;
+          if (top < MAXPART && wp.lane() == 0) {
+            sf[top] = part()[q].child0;
+            sc[top] = part()[q].nchild;
             sp[top] = qp;
-            ++top;
           }
+          ++top;
         }
         pos += wp.bcast(incl, WP::W - 1);
       }
@@ -2496,10 +2503,10 @@ struct Engine {
     ahash = xhash = 0;
     if (nbt > 1) {  // the base op partitioned the root into tasks 1..nbt-1
       if (wp.lane() == 0) {
-        sm->part[0].task = 0;
-        sm->part[0].child0 = 1;
-        sm->part[0].nchild = nbt - 1;
-        sm->part[0].leaves = 0;
+        part()[0].task = 0;
+        part()[0].child0 = 1;
+        part()[0].nchild = nbt - 1;
+        part()[0].leaves = 0;
       }
       wp.sync();
       npart = 1;
@@ -2510,7 +2517,7 @@ struct Engine {
   HXN void build(const hesp_cand_desc& d) {
     reset_to_base();
     NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
-      if ((d.merge_mask >> k) & 1) apply_merge(d.ops[k].task);
+      if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
       else apply_op(d.ops[k].task, d.ops[k].s);
     }
     sum_k = 0;

@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     if (k >= count) break;
     hesp_cand_desc& d = sdesc[wib];
     if (descs) {
+      // header + the used ops only (descriptors are mostly short)
       const int32_t* src = (const int32_t*)(descs + k);
       int32_t* dst = (int32_t*)&d;
-      for (int i = lane; i < (int)(sizeof(hesp_cand_desc) / 4); i += 32) dst[i] = src[i];
+      const int n_ops = __shfl_sync(0xffffffffu, lane == 0 ? src[0] : 0, 0);
+      const int words = 2 + 2 * (n_ops < HESP_MAX_OPS ? (n_ops > 0 ? n_ops : 0) : HESP_MAX_OPS);
+      for (int i = lane; i < words; i += 32) dst[i] = src[i];
     } else if (lane == 0) {
       generate_desc(first_index + k, &d);
     }

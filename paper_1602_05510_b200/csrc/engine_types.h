@@ -14,7 +14,7 @@ constexpr int MAXS = 8;       // memory spaces
 constexpr int MAXL = 32;      // directed links
 constexpr int MAXTYPES = 8;   // processor types
 constexpr int MAXBV = 48;     // distinct block sides with tabulated times
-constexpr int MAXPART = HESP_MAX_OPS + 2;
+constexpr int MAXPART = HESP_MAX_OPS + 2;  // clusters per candidate (slot array)
 constexpr int RHT = 2048;  // per-candidate region hash (new blocks), 16-bit ids
 
 // Status codes: 0 ok, 1 + hesp::Err ordinal (errors.hpp:10-32), engine codes >= 200.
@@ -96,7 +96,7 @@ struct PartEntry {
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
   size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
-  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref;
+  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
@@ -219,6 +219,8 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.rht = take(2 * (size_t)RHT);
   L.pmark = take(T);
   L.bref = take(4 * B);  // task references per candidate block (merge pruning)
+  L.part = take(sizeof(PartEntry) * MAXPART);
+  L.dstack = take(3 * 4 * (size_t)MAXPART);
   L.valid = take(8 * B * S);
   L.lastu = take(8 * B * S);
   L.pinu = take(8 * B * S);

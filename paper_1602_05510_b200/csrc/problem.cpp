@@ -182,7 +182,7 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   if (wl.elem_size < 1) bad("element size must be >= 1");
   if (wl.n >= (1LL << 30)) bad("matrix side must be < 2^30");
   if (wl.s_base < 2) bad("s_base must be >= 2");
-  if (wl.gen.k_max < 0 || wl.gen.k_max > HESP_MAX_OPS) bad("k_max must lie in [0, 16]");
+  if (wl.gen.k_max < 0 || wl.gen.k_max > HESP_GEN_MAX_OPS) bad("k_max must lie in [0, 16]");
   if (wl.gen.n_s_choices < 1 || wl.gen.n_s_choices > 4) bad("1..4 s choices");
   if (sched.min_block != wl.gen.min_block) bad("sched.min_block must equal gen.min_block");
   p.n = wl.n;

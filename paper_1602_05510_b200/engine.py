@@ -24,7 +24,8 @@ ORDERING = {"FCFS": 0, "PL": 1}
 SELECTION = {"R-P": 0, "F-P": 1, "EIT-P": 2, "EFT-P": 3}
 CACHING = {"WT": 0, "WB": 1, "WA": 2}
 
-MAX_OPS = 16
+MAX_OPS = 64
+OP_MERGE = -(1 << 31)  # hesp_op.s of a merge_cluster op (HESP_OP_MERGE)
 
 
 class Space(C.Structure):
@@ -82,7 +83,7 @@ class Op(C.Structure):
 
 
 class CandDesc(C.Structure):
-    _fields_ = [("n_ops", C.c_int32), ("merge_mask", C.c_int32), ("ops", Op * MAX_OPS)]
+    _fields_ = [("n_ops", C.c_int32), ("reserved", C.c_int32), ("ops", Op * MAX_OPS)]
 
 
 class Outcome(C.Structure):
@@ -161,8 +162,8 @@ class Trace:
 OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
                           ("assign_hash", "<u8"), ("xfer_hash", "<u8")])
 assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 32
-DESC_DTYPE = np.dtype([("n_ops", "<i4"), ("merge_mask", "<i4"), ("ops", "<i4", (MAX_OPS, 2))])
-assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 136
+DESC_DTYPE = np.dtype([("n_ops", "<i4"), ("reserved", "<i4"), ("ops", "<i4", (MAX_OPS, 2))])
+assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",

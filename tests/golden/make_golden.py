@@ -140,7 +140,7 @@ def write_traces(names):
 
 def write_descs(path, ops_lists):
     import numpy as np
-    from paper_1602_05510_b200.engine import DESC_DTYPE, MAX_OPS
+    from paper_1602_05510_b200.engine import DESC_DTYPE, MAX_OPS, OP_MERGE
     d = np.zeros(len(ops_lists), DESC_DTYPE)
     d["ops"][:] = -1
     d["ops"][:, :, 1] = 0
@@ -148,8 +148,7 @@ def write_descs(path, ops_lists):
         d[i]["n_ops"] = len(ops)
         for k, (t, s) in enumerate(ops):
             if t == "m":  # merge_cluster(s)
-                d[i]["ops"][k] = (s, 0)
-                d[i]["merge_mask"] |= 1 << k
+                d[i]["ops"][k] = (s, OP_MERGE)
             else:
                 d[i]["ops"][k] = (t, s)
     d.tofile(path)

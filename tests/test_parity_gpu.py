@@ -34,7 +34,7 @@ def test_device_generator_matches_host(lib):
     p, _ = PARITY["c2"]
     eng = make_engine(p)
     n = 4096
-    buf = torch.empty(n * 136, dtype=torch.uint8, device="cuda")
+    buf = torch.empty(n * 520, dtype=torch.uint8, device="cuda")
     eng.generate_device(1000, n, buf.data_ptr())
     torch.cuda.synchronize()
     dev = buf.cpu().numpy().tobytes()
