@@ -261,6 +261,62 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* trac
 int hesp_verify_trace(const hesp_engine* e, const hesp_trace* trace, char* buf, size_t cap,
                       int32_t* n_violations);
 
+/* ---------------------------------------------------------------------------
+ * Iterative schedule/partition solver (the reference
+ * declares it only: solver.hpp:57-86, semantics SPEC.md:410-461).  A chain
+ * state is a candidate descriptor (base tiling + partition/merge ops).  Each
+ * iteration simulates the state on the device with the full trace (idle_avg
+ * per task), records its metrics, collects and scores candidates exactly as
+ * SPEC's collect_candidates / score_candidate / choose_p define them, then
+ * evaluates EVERY candidate mutation in one device batch and keeps only the
+ * ones whose graph simulates (status 0) before select_candidate (Hard: max
+ * score, first in candidate order on ties; Soft: score-proportional draw
+ * from hesp::Rng).  DESIGN.md §10 states the decisions the SPEC leaves open. */
+enum { HESP_SEL_ALL = 0, HESP_SEL_CP = 1, HESP_SEL_SHALLOW = 2 };
+enum { HESP_SAMPLE_HARD = 0, HESP_SAMPLE_SOFT = 1 };
+enum { HESP_ACT_NONE = -1, HESP_ACT_PARTITION = 0, HESP_ACT_MERGE = 1, HESP_ACT_REPARTITION = 2 };
+
+typedef struct {              /* SolverConfig, solver.hpp:20-28 */
+  int32_t iterations;
+  int32_t task_selection;     /* HESP_SEL_* */
+  int32_t sampling;           /* HESP_SAMPLE_* */
+  int32_t k_max;
+  uint64_t seed;
+  int64_t min_block;
+  double overhead_factor;
+} hesp_solver_config;
+
+typedef struct {              /* IterationRecord, solver.hpp:42-49 */
+  int32_t iteration;
+  int32_t action;             /* HESP_ACT_* applied at the end of the round */
+  int32_t target;             /* leaf task id or cluster id */
+  int32_t n_candidates;       /* collected (score > 0, within the op budget) */
+  int32_t n_valid;            /* of which simulate on the device */
+  int32_t dag_depth;
+  int64_t d;                  /* characteristic block side of the target */
+  double p;                   /* partition parameter of the applied candidate (1 = merge) */
+  double score;
+  double makespan;
+  double avg_block_side;      /* flop-weighted mean leaf block side */
+  double avg_load_pct;
+} hesp_solver_iteration;
+
+typedef struct {
+  int32_t cap_history;        /* in: entries of history (>= iterations) */
+  int32_t n_history;
+  hesp_solver_iteration* history;
+  hesp_cand_desc best;        /* best state found (min makespan, earliest iteration) */
+  double best_makespan;
+  int32_t best_iteration;
+  int32_t pad;
+  int64_t n_simulated;        /* device simulations issued (states + candidate batches) */
+} hesp_solver_result;
+
+/* Runs solve() from `initial` (NULL = the base tiling).  Returns 0, the
+ * status of a failing initial state, or a negative HESP_E_* code. */
+int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfg,
+               hesp_solver_result* out);
+
 /* Engine facts: kernel launches issued so far, base tiling sizes, slots. */
 typedef struct {
   int64_t kernel_launches;

@@ -13,7 +13,9 @@
 // makespan bits, and order-independent hashes of every Assignment and
 // TransferRec (include/hesp_workload.h), so a single 40-byte record pins the
 // whole schedule bit-for-bit.
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -59,6 +61,13 @@ struct Args {
   std::string trace_out;
   int shift_task = -1;  // --shift-task T --shift-by X: move T's interval by -X before verify
   double shift_by = 0;
+  // --solve N: the SPEC solver restated over the reference
+  // TaskGraph/simulate, for hesp_solve parity
+  int solve = -1;
+  std::string solve_sel = "All", solve_samp = "Hard";
+  int solve_kmax = 8;
+  uint64_t solve_seed = 0;
+  double overhead = 1.1;
 };
 
 std::string slurp(const std::string& path) {
@@ -219,6 +228,223 @@ void dump_trace(FILE* f, const Record& r, hesp::SimResult& res, const hesp::Task
   std::fprintf(f, "]}\n");
 }
 
+// ---------------------------------------------------------------------------
+// Solver oracle.  TEST INFRASTRUCTURE: the declared-only solver
+// (solver.hpp:57-86) restated from SPEC.md:410-461 with the decisions of
+// DESIGN.md §10, driving the UNMODIFIED reference TaskGraph (partition_task,
+// merge_cluster, repartition_cluster) and simulate().
+struct OCand {
+  int action;  // 0 partition, 1 merge, 2 repartition
+  int target, parent;
+  int64_t k;
+  double score;
+  int64_t d;
+};
+
+int64_t o_snap(int64_t d, int64_t k, int64_t mb) {  // TaskGraph::snap_tiling
+  return hesp::TaskGraph::snap_tiling(d, k, mb);
+}
+
+void run_solve(const Ctx& c, FILE* f) {
+  const Args& a = *c.a;
+  const hesp::Platform& plat = *c.plat;
+  const hesp::PerfModel& model = *c.model;
+  const int64_t mb = a.gen.min_block;
+  const int sel = a.solve_sel == "CP" ? 1 : a.solve_sel == "Shallow" ? 2 : 0;
+  const bool soft = a.solve_samp == "Soft";
+  hesp::Rng rng(a.solve_seed);
+  auto g = hesp::TaskGraph::root_cholesky(a.n, a.elem);
+  g.partition_task(0, 1.0 / a.s_base, mb);
+  auto choose_k = [&](double idle, int64_t d) -> int64_t {
+    if (d < 2 * mb) return 0;
+    const int64_t lim = std::min<int64_t>(a.solve_kmax, d / mb);
+    int64_t k = (int64_t)std::ceil(std::sqrt(idle + 1.0)) + 1;
+    k = std::max<int64_t>(2, std::min(k, lim));
+    return o_snap(d, k, mb);
+  };
+  auto w_sub = [&](const hesp::Task& t, int64_t k, const std::string& type, double* w) {
+    std::vector<hesp::Region> rr;
+    for (int r : t.reads)
+      if (std::find(t.writes.begin(), t.writes.end(), r) == t.writes.end()) rr.push_back(g.data().block(r).region);
+    const auto specs = hesp::enumerate_partition(t.kind, rr, g.data().block(t.writes.front()).region, k);
+    double sum = 0;
+    for (const auto& sp : specs) {
+      if (!model.knows(sp.kind, type)) return false;
+      sum += model.task_time(sp.kind, sp.write.rows, type);
+    }
+    *w = sum;
+    return true;
+  };
+  std::fprintf(f, "{\"history\": [");
+  double best = 0;
+  int best_it = -1;
+  for (int it = 0; it < a.solve; ++it) {
+    hesp::SimResult res;
+    try {
+      res = hesp::simulate(g, plat, model, c.cfg);
+    } catch (const hesp::Error& e) {
+      std::fprintf(f, "], \"status\": %d}\n", 1 + static_cast<int>(e.code()));
+      return;
+    }
+    int depth = 0;
+    double num = 0, den = 0;
+    for (const auto& [id, t] : g.tasks()) {
+      if (!t.is_leaf()) continue;
+      depth = std::max(depth, g.task_depth(id));
+      const double fl = hesp::task_flops(t.kind, t.b);
+      num += fl * (double)t.b;
+      den += fl;
+    }
+    const double avgb = den > 0 ? num / den : 0.0;
+    const double load = 100.0 * res.avg_load(plat.processor_count());
+    if (best_it < 0 || res.makespan < best) {
+      best = res.makespan;
+      best_it = it;
+    }
+    int action = -1, target = -1, ncand = 0, nvalid = 0;
+    int64_t dd = 0;
+    double pp = 0, sc = 0;
+    if (it + 1 < a.solve) {
+      std::vector<int> tasks;
+      if (sel == 0) {
+        for (const auto& [id, x] : res.assignments) tasks.push_back(id);
+      } else if (sel == 2) {
+        int dmin = 1 << 30;
+        for (const auto& [id, x] : res.assignments) dmin = std::min(dmin, g.task_depth(id));
+        for (const auto& [id, x] : res.assignments)
+          if (g.task_depth(id) == dmin) tasks.push_back(id);
+      } else {
+        int cur = -1;
+        for (const auto& [id, x] : res.assignments)
+          if (cur < 0 || x.end > res.assignments.at(cur).end) cur = id;
+        while (cur >= 0) {
+          tasks.push_back(cur);
+          int nxt = -1;
+          for (int pr : g.preds(cur))
+            if (nxt < 0 || res.assignments.at(pr).end > res.assignments.at(nxt).end) nxt = pr;
+          cur = nxt;
+        }
+        std::sort(tasks.begin(), tasks.end());
+      }
+      std::vector<OCand> cands;
+      for (int id : tasks) {
+        const auto& x = res.assignments.at(id);
+        const auto& t = g.task(id);
+        const double idle = res.idle_avg.at(id);
+        const int64_t k = choose_k(idle, t.b);
+        if (k == 0) continue;
+        double w;
+        if (!w_sub(t, k, plat.type_name(x.proc), &w)) continue;
+        const double est = a.overhead * w / std::min(idle + 1.0, (double)k);
+        const double score = std::max(0.0, (x.end - x.start) - est);
+        if (score > 0) cands.push_back({0, id, id, k, score, t.b});
+      }
+      for (int cid : g.innermost_clusters()) {
+        if (cid == 0) continue;  // the base cluster stays
+        const auto& cl = g.cluster(cid);
+        double lo = 0, hi = 0, isum = 0;
+        bool first = true;
+        for (int m : cl.members) {
+          const auto& x = res.assignments.at(m);
+          if (first || x.start < lo) lo = x.start;
+          if (first || x.end > hi) hi = x.end;
+          first = false;
+          isum += res.idle_avg.at(m);
+        }
+        const auto& par = g.task(cl.parent_task);
+        double tmin = 0;
+        std::string tbest;
+        bool have = false;
+        for (const auto& ty : plat.types()) {
+          if (!model.knows(par.kind, ty.name)) continue;
+          const double tt = model.task_time(par.kind, par.b, ty.name);
+          if (!have || tt < tmin) {
+            tmin = tt;
+            tbest = ty.name;
+            have = true;
+          }
+        }
+        if (!have) continue;
+        const double span = hi - lo;
+        const double merge = std::max(0.0, span - tmin);
+        if (merge > 0) cands.push_back({1, cid, cl.parent_task, 0, merge, par.b});
+        const double ic = isum / (double)cl.members.size();
+        const int64_t k = choose_k(ic, par.b);
+        const int64_t kc = par.b / g.task(cl.members.front()).b;
+        double w;
+        if (k == 0 || k == kc || !w_sub(par, k, tbest, &w)) continue;
+        const double est = a.overhead * w / std::min(ic + 1.0, (double)k);
+        const double rep = merge + std::max(0.0, span - est);
+        if (rep > 0) cands.push_back({2, cid, cl.parent_task, k, rep, par.b});
+      }
+      ncand = (int)cands.size();
+      auto mutated = [&](const OCand& x) {
+        hesp::TaskGraph h = g;
+        if (x.action == 0) h.partition_task(x.target, 1.0 / (double)x.k, mb);
+        else if (x.action == 1) h.merge_cluster(x.target);
+        else h.repartition_cluster(x.target, 1.0 / (double)x.k, mb);
+        return h;
+      };
+      std::vector<char> ok(cands.size(), 0);
+      {
+        std::atomic<size_t> next{0};
+        auto worker = [&]() {
+          for (;;) {
+            const size_t i = next.fetch_add(1);
+            if (i >= cands.size()) return;
+            try {
+              auto h = mutated(cands[i]);
+              hesp::simulate(h, plat, model, c.cfg);
+              ok[i] = 1;
+            } catch (const std::exception&) {
+            }
+          }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 0; t < std::max(1, a.threads); ++t) pool.emplace_back(worker);
+        for (auto& t : pool) t.join();
+      }
+      std::vector<OCand> valid;
+      for (size_t i = 0; i < cands.size(); ++i)
+        if (ok[i]) valid.push_back(cands[i]);
+      nvalid = (int)valid.size();
+      if (!valid.empty()) {
+        size_t pick = 0;
+        if (!soft) {
+          for (size_t i = 1; i < valid.size(); ++i)
+            if (valid[i].score > valid[pick].score) pick = i;
+        } else {
+          double total = 0;
+          for (const auto& x : valid) total += x.score;
+          const double u = rng.uniform() * total;
+          double acc = 0;
+          pick = valid.size() - 1;
+          for (size_t i = 0; i < valid.size(); ++i) {
+            acc += valid[i].score;
+            if (u < acc) {
+              pick = i;
+              break;
+            }
+          }
+        }
+        const OCand& x = valid[pick];
+        action = x.action;
+        target = x.target;
+        dd = x.d;
+        pp = x.action == 1 ? 1.0 : 1.0 / (double)x.k;
+        sc = x.score;
+        g = mutated(x);
+      }
+    }
+    std::fprintf(f, "%s[%d, %d, %d, %d, %d, %d, %lld, \"%016llx\", \"%016llx\", \"%016llx\", \"%016llx\", \"%016llx\"]",
+                 it ? ", " : "", it, action, target, ncand, nvalid, depth, (long long)dd, (unsigned long long)bits(pp),
+                 (unsigned long long)bits(sc), (unsigned long long)bits(res.makespan), (unsigned long long)bits(avgb),
+                 (unsigned long long)bits(load));
+  }
+  std::fprintf(f, "], \"status\": 0, \"best\": \"%016llx\", \"best_iteration\": %d}\n",
+               (unsigned long long)bits(best), best_it);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -265,6 +491,12 @@ int main(int argc, char** argv) {
     else if (k == "--quiet") a.quiet = true;
     else if (k == "--descs") a.descs = v();
     else if (k == "--trace") a.trace = std::atol(v());
+    else if (k == "--solve") a.solve = std::atoi(v());
+    else if (k == "--solve-selection") a.solve_sel = v();
+    else if (k == "--solve-sampling") a.solve_samp = v();
+    else if (k == "--solve-kmax") a.solve_kmax = std::atoi(v());
+    else if (k == "--solve-seed") a.solve_seed = std::strtoull(v(), nullptr, 0);
+    else if (k == "--overhead") a.overhead = std::atof(v());
     else if (k == "--trace-out") a.trace_out = v();
     else if (k == "--shift-task") a.shift_task = std::atoi(v());
     else if (k == "--shift-by") a.shift_by = std::atof(v());
@@ -300,6 +532,12 @@ int main(int argc, char** argv) {
     c.s_base_snapped = static_cast<int32_t>(a.n / c.base_b);
   }
 
+  if (a.solve >= 0) {
+    FILE* f = a.trace_out.empty() ? stdout : std::fopen(a.trace_out.c_str(), "w");
+    run_solve(c, f);
+    if (f != stdout) std::fclose(f);
+    return 0;
+  }
   if (a.trace >= 0) {
     hesp::SimResult res;
     hesp::TaskGraph* g = nullptr;

@@ -2607,10 +2607,16 @@ struct Engine {
       tb->bregion[b] = reg(b);
       tb->bisint[b] = bmeta(b).isint;
     }
+    NOUNROLL for (int c = wp.lane(); c < npart; c += WP::W) tb->parts[c] = part()[c];
+    if (ntasks <= tb->task_cap)
+      NOUNROLL for (int j = wp.lane(); j < ntasks; j += WP::W) tb->tmeta[j] = task(j);
     if (wp.lane() == 0) {
       tb->nleaves = nl;
       tb->npreds = np;
       tb->nblocks = nb;
+      tb->nparts = npart;
+      tb->ntasks = ntasks;
+      if (ntasks > tb->task_cap) tb->overflow = 1;
     }
     wp.sync();
   }

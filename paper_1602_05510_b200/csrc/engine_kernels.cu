@@ -682,7 +682,8 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
             dalloc(&dout, 1, owned) && dalloc(&dx, xcap, owned) && dalloc(&dr, rcap, owned) &&
             dalloc(&tb.leaves, T, owned) && dalloc(&tb.lmeta, T, owned) && dalloc(&tb.lpoff, T, owned) &&
             dalloc(&tb.lpcnt, T, owned) && dalloc(&tb.lpreds, P.maxedges, owned) && dalloc(&tb.bregion, B, owned) &&
-            dalloc(&tb.bisint, B, owned) && dalloc(&dtb, 1, owned);
+            dalloc(&tb.bisint, B, owned) && dalloc(&tb.parts, MAXPART, owned) && dalloc(&tb.tmeta, T, owned) &&
+            dalloc(&dtb, 1, owned);
   hesp_outcome o{};
   hx::TraceLogs logs;
   TraceBufs hb{};
@@ -694,6 +695,7 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
     tb.leaf_cap = T;
     tb.pred_cap = P.maxedges;
     tb.block_cap = B;
+    tb.task_cap = T;
     cudaMemcpy(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice);
     cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
     cudaMemset(dp, 0xff, (size_t)T * 4);
@@ -715,7 +717,8 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
          d2h(g.leaves, tb.leaves, (size_t)hb.nleaves) && d2h(g.meta, tb.lmeta, (size_t)hb.nleaves) &&
          d2h(g.poff, tb.lpoff, (size_t)hb.nleaves) && d2h(g.pcnt, tb.lpcnt, (size_t)hb.nleaves) &&
          d2h(g.preds, tb.lpreds, (size_t)hb.npreds) && d2h(g.bregion, tb.bregion, (size_t)hb.nblocks) &&
-         d2h(g.bisint, tb.bisint, (size_t)hb.nblocks);
+         d2h(g.bisint, tb.bisint, (size_t)hb.nblocks) && d2h(g.parts, tb.parts, (size_t)hb.nparts) &&
+         d2h(g.tmeta, tb.tmeta, (size_t)hb.ntasks);
     g.valid = ok;
   }
   for (void* q : owned) cudaFree(q);
@@ -731,6 +734,13 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
   }
   return 0;
 }
+
+}  // extern "C"
+
+const hx::Problem& hesp_engine_problem(const hesp_engine* e) { return e->hp.p; }
+const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e) { return e->last_graph; }
+
+extern "C" {
 
 int hesp_verify_trace(const hesp_engine* e, const hesp_trace* tr, char* buf, size_t cap, int32_t* n_violations) {
   if (!e || !tr || !e->last_graph.valid) {

@@ -87,11 +87,7 @@ struct SlotHeader {
   int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, pad;
 };
 
-// One cluster (TaskCluster, graph.hpp:103-108); index = cluster id.  A merged
-// cluster keeps its entry (ids are never reused) with task = -2 - parent.
-struct PartEntry {
-  int32_t task, child0, nchild, leaves;
-};
+
 
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
@@ -147,6 +143,12 @@ struct Problem {
   SlotLayout lay;
 };
 
+// One cluster (TaskCluster, graph.hpp:103-108); index = cluster id.  A merged
+// cluster keeps its entry (ids are never reused) with task = -2 - parent.
+struct PartEntry {
+  int32_t task, child0, nchild, leaves;
+};
+
 // ---- full-trace mode (Engine<..., TRACE = true>, hesp_eval_trace) ----
 // One transfer as plan_transfer records it (sim.cpp:468-499), in emission
 // order, with the per-hop times the reference turns into Xfer events.
@@ -178,6 +180,9 @@ struct TraceBufs {
   int32_t* lpreds;
   Region* bregion;   // per block id
   int32_t* bisint;
+  PartEntry* parts;  // clusters by id (MAXPART)
+  TaskMeta* tmeta;   // every task id < ntasks (leaf or not; merged-away ones too)
+  int32_t nparts, ntasks, task_cap, pad_;
   int32_t leaf_cap, pred_cap, block_cap;
   int32_t nleaves, npreds, nblocks;
   int32_t overflow;

@@ -203,7 +203,7 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   if (s0 == 0) bad("base tiling: no tiling of the root with tiles >= min_block");
   std::vector<long long> bvals{wl.n};
   std::vector<long long> frontier{wl.n / s0};
-  std::set<int> reqs{2, 3, 4};
+  std::set<int> reqs{2, 3, 4, 5, 6, 7, 8};  // generator choices and the solver's choose_p range
   for (int i = 0; i < wl.gen.n_s_choices; ++i) reqs.insert(wl.gen.s_choices[i]);
   while (!frontier.empty()) {
     const long long b = frontier.back();

@@ -1,0 +1,342 @@
+// solver.cpp — hesp_solve: the iterative schedule/partition solver
+// (SURVEY.md §8f row f1).  The reference declares it only (solver.hpp:57-86);
+// its semantics are SPEC.md:410-461, restated here with the decisions the
+// SPEC leaves open written down in DESIGN.md §10.
+//
+// Per iteration (SPEC solve):
+//   simulate the state          device, full trace (hesp_eval_trace): idle_avg
+//   record IterationRecord      makespan, DAG depth, flop-weighted side, load
+//   collect_candidates          SPEC.md:420-427 (All / CP / Shallow + innermost clusters)
+//   score_candidate, choose_p   SPEC.md:428-440, solver.hpp:51-66
+//   validity filter             every candidate mutation in ONE device batch
+//                               (hesp_eval_descs); failing graphs are dropped
+//   select_candidate            SPEC.md:441-446 (Hard / Soft with hesp::Rng)
+//   apply                       append the op(s) to the state's descriptor
+// The host side only does the per-candidate arithmetic (one pass over the
+// leaves); every schedule is simulated by the sm_100a engine.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "hesp_engine.h"
+#include "trace.h"
+
+namespace {
+
+using hx::PartEntry;
+using hx::Problem;
+using hx::TaskMeta;
+using hx::TraceGraph;
+
+struct Rng {  // hesp::Rng (sim.cpp:59-69)
+  uint64_t s;
+  uint64_t next() { return hesp_splitmix_next(&s); }
+  double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+};
+
+struct Cand {
+  int action;  // HESP_ACT_*
+  int target;  // leaf task id / cluster id
+  int parent;  // restored parent (merge / repartition)
+  int k;       // tiles of the partition (0 for a merge)
+  double score;
+  int64_t d;
+};
+
+double task_flops(int kind, int64_t b) {  // platform.cpp:57-66
+  const double bd = (double)b;
+  switch (kind) {
+    case HESP_CHOL: return bd * bd * bd / 3.0;
+    case HESP_TRSM: return bd * bd * bd;
+    case HESP_SYRK: return bd * bd * bd;
+    default: return 2.0 * bd * bd * bd;
+  }
+}
+
+// TaskGraph::snap_tiling (graph.cpp:450-454): largest s <= k dividing d with d/s >= min_block
+int64_t snap_tiling(int64_t d, int64_t k, int64_t min_block) {
+  for (int64_t s = k; s >= 2; --s)
+    if (d % s == 0 && d / s >= min_block) return s;
+  return 0;
+}
+
+struct Ctx {
+  const Problem& p;
+  const hesp_solver_config& cfg;
+  // PerfModel::task_time through the engine's host table (every side the
+  // engine can create is tabulated); false = no model for it
+  bool ttime(int kind, int64_t b, int type, double* t) const {
+    for (int i = 0; i < p.nbv; ++i)
+      if (p.bval[i] == b) {
+        if (!p.known[kind][type]) return false;
+        *t = p.ttime[kind][i][type];
+        return true;
+      }
+    return false;
+  }
+  // choose_p (solver.hpp:59-62): k = clamp(ceil(sqrt(I+1)) + 1, 2, min(k_max, d/min_block)),
+  // snapped down to a divisor grid; 0 = GrainTooSmall / no grid
+  int64_t choose_k(double idle, int64_t d) const {
+    if (d < 2 * cfg.min_block) return 0;
+    const int64_t lim = std::min<int64_t>(cfg.k_max, d / cfg.min_block);
+    int64_t k = (int64_t)std::ceil(std::sqrt(idle + 1.0)) + 1;
+    k = std::max<int64_t>(2, std::min(k, lim));
+    return snap_tiling(d, k, cfg.min_block);
+  }
+  // W_sub: sum of the would-be sub-task times on one processor type, in emission order
+  bool w_sub(int kind, int64_t d, int64_t k, int type, double* w) const {
+    double sum = 0;
+    const int cnt = hesp_member_count(kind, (int32_t)k);
+    for (int m = 0; m < cnt; ++m) {
+      double t;
+      if (!ttime(hesp_member_kind(kind, (int32_t)k, m), d / k, type, &t)) return false;
+      sum += t;
+    }
+    *w = sum;
+    return true;
+  }
+};
+
+}  // namespace
+
+extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfgp,
+                          hesp_solver_result* out) {
+  if (!e || !cfgp || !out || cfgp->iterations < 0 || cfgp->k_max < 2 || cfgp->overhead_factor < 1.0 ||
+      cfgp->min_block < 1 || cfgp->task_selection < 0 || cfgp->task_selection > 2 || cfgp->sampling < 0 ||
+      cfgp->sampling > 1)
+    return HESP_E_INVALID;
+  if (out->cap_history < cfgp->iterations || (!out->history && cfgp->iterations > 0)) return HESP_E_INVALID;
+  const Problem& P = hesp_engine_problem(e);
+  const hesp_solver_config cfg = *cfgp;
+  Ctx cx{P, cfg};
+  Rng rng{cfg.seed};
+  hesp_cand_desc cur;
+  std::memset(&cur, 0, sizeof cur);
+  if (initial) cur = *initial;
+  out->n_history = 0;
+  out->best_makespan = 0;
+  out->best_iteration = -1;
+  out->n_simulated = 0;
+  std::memset(&out->best, 0, sizeof out->best);
+  // trace arrays, grown on HESP_E_LIMIT
+  std::vector<hesp_assignment> A(4096);
+  std::vector<hesp_transfer> X(8192);
+  std::vector<hesp_residency> R(16384);
+  std::vector<hesp_event> E(32768);
+  std::vector<hesp_load_step> S(8192);
+  std::vector<hesp_cand_desc> batch;
+  std::vector<hesp_outcome> outc;
+  for (int it = 0; it < cfg.iterations; ++it) {
+    hesp_trace tr{};
+    int rc;
+    for (;;) {
+      tr = hesp_trace{};
+      tr.cap_assign = (int32_t)A.size();
+      tr.cap_xfer = (int32_t)X.size();
+      tr.cap_res = (int32_t)R.size();
+      tr.cap_events = (int32_t)E.size();
+      tr.cap_steps = (int32_t)S.size();
+      tr.assignments = A.data();
+      tr.transfers = X.data();
+      tr.residency = R.data();
+      tr.events = E.data();
+      tr.steps = S.data();
+      rc = hesp_eval_trace(e, &cur, &tr);
+      if (rc != HESP_E_LIMIT) break;
+      A.resize(std::max<size_t>(A.size(), tr.n_assign));
+      X.resize(std::max<size_t>(X.size(), tr.n_xfer));
+      R.resize(std::max<size_t>(R.size(), tr.n_res));
+      E.resize(std::max<size_t>(E.size(), tr.n_events));
+      S.resize(std::max<size_t>(S.size(), tr.n_steps));
+    }
+    ++out->n_simulated;
+    if (rc != 0) return rc;  // only the initial state can fail (mutations are filtered)
+    const TraceGraph& g = hesp_engine_last_graph(e);
+    const double makespan = tr.outcome.makespan;
+    // ---- graph facts: clusters, membership, depth ----
+    std::map<int, int> cluster_of;   // member task -> live cluster id
+    std::map<int, int> parent_of;    // partitioned task -> live cluster id
+    for (int c = 0; c < (int)g.parts.size(); ++c) {
+      const PartEntry& pe = g.parts[c];
+      if (pe.task < 0) continue;
+      parent_of[pe.task] = c;
+      for (int m = pe.child0; m < pe.child0 + pe.nchild; ++m) cluster_of[m] = c;
+    }
+    auto depth_of = [&](int t) {  // TaskGraph::task_depth (graph.cpp:564-572)
+      int d = 0;
+      for (auto it2 = cluster_of.find(t); it2 != cluster_of.end(); it2 = cluster_of.find(g.parts[it2->second].task))
+        ++d;
+      return d;
+    };
+    std::map<int, const hesp_assignment*> asg;  // leaf task id -> assignment
+    for (int i = 0; i < tr.n_assign; ++i) asg[A[i].task] = &A[i];
+    // ---- IterationRecord metrics ----
+    hesp_solver_iteration rec{};
+    rec.iteration = it;
+    rec.action = HESP_ACT_NONE;
+    rec.target = -1;
+    rec.makespan = makespan;
+    int depth = 0;
+    double num = 0, den = 0;
+    for (const auto& [id, a] : asg) {  // task-id order
+      (void)a;
+      depth = std::max(depth, depth_of(id));
+      const TaskMeta& m = g.tmeta[id];
+      const double f = task_flops(m.kind, m.b);
+      num += f * (double)m.b;
+      den += f;
+    }
+    rec.dag_depth = depth;
+    rec.avg_block_side = den > 0 ? num / den : 0.0;
+    rec.avg_load_pct = 100.0 * tr.avg_load;
+    if (out->best_iteration < 0 || makespan < out->best_makespan) {
+      out->best_makespan = makespan;
+      out->best_iteration = it;
+      out->best = cur;
+    }
+    if (it + 1 == cfg.iterations) {  // the last round's mutation could never be simulated
+      out->history[out->n_history++] = rec;
+      break;
+    }
+    // ---- collect_candidates ----
+    std::vector<Cand> cands;
+    std::vector<int> tasks;  // selected leaves, id order
+    if (cfg.task_selection == HESP_SEL_ALL) {
+      for (const auto& [id, a] : asg) tasks.push_back(id);
+    } else if (cfg.task_selection == HESP_SEL_SHALLOW) {
+      int dmin = 1 << 30;
+      for (const auto& [id, a] : asg) dmin = std::min(dmin, depth_of(id));
+      for (const auto& [id, a] : asg)
+        if (depth_of(id) == dmin) tasks.push_back(id);
+    } else {  // CP: realized longest path, backtracked by latest-ending predecessor
+      std::map<int, int> li;
+      for (size_t k = 0; k < g.leaves.size(); ++k) li[g.leaves[k]] = (int)k;
+      int curt = -1;
+      for (const auto& [id, a] : asg)
+        if (curt < 0 || a->end > asg[curt]->end) curt = id;
+      while (curt >= 0) {
+        tasks.push_back(curt);
+        const int l = li[curt];
+        int nxt = -1;
+        for (int q = 0; q < g.pcnt[l]; ++q) {
+          const int pr = g.preds[g.poff[l] + q];
+          if (!asg.count(pr)) continue;
+          if (nxt < 0 || asg[pr]->end > asg[nxt]->end || (asg[pr]->end == asg[nxt]->end && pr < nxt)) nxt = pr;
+        }
+        curt = nxt;
+      }
+      std::sort(tasks.begin(), tasks.end());
+    }
+    for (int id : tasks) {  // Partition(p) of a scheduled leaf
+      const hesp_assignment& a = *asg[id];
+      const TaskMeta& m = g.tmeta[id];
+      const int64_t k = cx.choose_k(a.idle_avg, m.b);
+      if (k == 0) continue;
+      double w;
+      if (!cx.w_sub(m.kind, m.b, k, P.proc_type[a.proc], &w)) continue;
+      const double est = cfg.overhead_factor * w / std::min(a.idle_avg + 1.0, (double)k);
+      const double score = std::max(0.0, (a.end - a.start) - est);
+      if (score > 0) cands.push_back({HESP_ACT_PARTITION, id, id, (int)k, score, m.b});
+    }
+    for (int c = 1; c < (int)g.parts.size(); ++c) {  // innermost clusters (not the base one)
+      const PartEntry& pe = g.parts[c];
+      if (pe.task < 0) continue;
+      bool flat = true;
+      double lo = 0, hi = 0, isum = 0;
+      for (int mm = pe.child0; mm < pe.child0 + pe.nchild && flat; ++mm) {
+        auto f = asg.find(mm);
+        if (f == asg.end()) {
+          flat = false;
+          break;
+        }
+        const hesp_assignment& a = *f->second;
+        if (mm == pe.child0 || a.start < lo) lo = a.start;
+        if (mm == pe.child0 || a.end > hi) hi = a.end;
+        isum += a.idle_avg;
+      }
+      if (!flat) continue;
+      const TaskMeta& par = g.tmeta[pe.task];
+      double tmin = 0;
+      int tbest = -1;
+      for (int ty = 0; ty < P.n_types; ++ty) {
+        double t;
+        if (!cx.ttime(par.kind, par.b, ty, &t)) continue;
+        if (tbest < 0 || t < tmin) {
+          tmin = t;
+          tbest = ty;
+        }
+      }
+      if (tbest < 0) continue;
+      const double span = hi - lo;
+      const double merge = std::max(0.0, span - tmin);
+      if (merge > 0) cands.push_back({HESP_ACT_MERGE, c, pe.task, 0, merge, par.b});
+      const double ic = isum / (double)pe.nchild;
+      const int64_t k = cx.choose_k(ic, par.b);
+      const int64_t kc = par.b / g.tmeta[pe.child0].b;
+      double w;
+      if (k == 0 || k == kc || !cx.w_sub(par.kind, par.b, k, tbest, &w)) continue;
+      const double est = cfg.overhead_factor * w / std::min(ic + 1.0, (double)k);
+      const double rep = merge + std::max(0.0, span - est);
+      if (rep > 0) cands.push_back({HESP_ACT_REPARTITION, c, pe.task, (int)k, rep, par.b});
+    }
+    // op budget of the descriptor
+    cands.erase(std::remove_if(cands.begin(), cands.end(),
+                               [&](const Cand& c) {
+                                 return cur.n_ops + (c.action == HESP_ACT_REPARTITION ? 2 : 1) > HESP_MAX_OPS;
+                               }),
+                cands.end());
+    rec.n_candidates = (int32_t)cands.size();
+    // ---- validity filter: every mutation in one device batch ----
+    auto mutate = [&](const Cand& c) {
+      hesp_cand_desc d = cur;
+      if (c.action != HESP_ACT_PARTITION) d.ops[d.n_ops++] = hesp_op{c.target, HESP_OP_MERGE};
+      if (c.action != HESP_ACT_MERGE) d.ops[d.n_ops++] = hesp_op{c.parent, c.k};
+      return d;
+    };
+    std::vector<Cand> valid;
+    if (!cands.empty()) {
+      batch.resize(cands.size());
+      outc.resize(cands.size());
+      for (size_t i = 0; i < cands.size(); ++i) batch[i] = mutate(cands[i]);
+      hesp_best b{};
+      const int r = hesp_eval_descs(e, batch.data(), batch.size(), 0, outc.data(), &b);
+      if (r != 0) return r;
+      out->n_simulated += (int64_t)cands.size();
+      for (size_t i = 0; i < cands.size(); ++i)
+        if (outc[i].status == 0) valid.push_back(cands[i]);
+    }
+    rec.n_valid = (int32_t)valid.size();
+    if (!valid.empty()) {
+      // ---- select_candidate ----
+      size_t pick = 0;
+      if (cfg.sampling == HESP_SAMPLE_HARD) {
+        for (size_t i = 1; i < valid.size(); ++i)
+          if (valid[i].score > valid[pick].score) pick = i;
+      } else {
+        double total = 0;
+        for (const auto& c : valid) total += c.score;
+        const double u = rng.uniform() * total;
+        double acc = 0;
+        pick = valid.size() - 1;
+        for (size_t i = 0; i < valid.size(); ++i) {
+          acc += valid[i].score;
+          if (u < acc) {
+            pick = i;
+            break;
+          }
+        }
+      }
+      const Cand& c = valid[pick];
+      rec.action = c.action;
+      rec.target = c.target;
+      rec.d = c.d;
+      rec.p = c.action == HESP_ACT_MERGE ? 1.0 : 1.0 / (double)c.k;
+      rec.score = c.score;
+      cur = mutate(c);
+    }
+    out->history[out->n_history++] = rec;
+  }
+  return 0;
+}

@@ -18,6 +18,8 @@ struct TraceGraph {
   std::vector<int32_t> poff, pcnt, preds;
   std::vector<Region> bregion;
   std::vector<int32_t> bisint;
+  std::vector<PartEntry> parts;  // clusters by id; merged ones have task < 0
+  std::vector<TaskMeta> tmeta;   // by task id
   bool valid = false;
 };
 
@@ -34,5 +36,13 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
 
 // verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph.
 std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr);
+
+}  // namespace hx
+
+// engine internals the host-side solver reads (engine_kernels.cu)
+const hx::Problem& hesp_engine_problem(const hesp_engine* e);
+const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e);
+
+namespace hx {
 
 }  // namespace hx

@@ -119,6 +119,29 @@ EVENT_KINDS = ("TaskStart", "TaskEnd", "XferStart", "XferEnd")
 KIND_NAMES = ("CHOL", "TRSM", "SYRK", "GEMM")
 
 
+class SolverConfigC(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("task_selection", C.c_int32), ("sampling", C.c_int32),
+                ("k_max", C.c_int32), ("seed", C.c_uint64), ("min_block", C.c_int64),
+                ("overhead_factor", C.c_double)]
+
+
+SOLVER_ITER_DTYPE = np.dtype([("iteration", "<i4"), ("action", "<i4"), ("target", "<i4"), ("n_candidates", "<i4"),
+                              ("n_valid", "<i4"), ("dag_depth", "<i4"), ("d", "<i8"), ("p", "<f8"),
+                              ("score", "<f8"), ("makespan", "<f8"), ("avg_block_side", "<f8"),
+                              ("avg_load_pct", "<f8")])
+
+
+class SolverResultC(C.Structure):
+    _fields_ = [("cap_history", C.c_int32), ("n_history", C.c_int32), ("history", C.c_void_p),
+                ("best", CandDesc), ("best_makespan", C.c_double), ("best_iteration", C.c_int32),
+                ("pad", C.c_int32), ("n_simulated", C.c_int64)]
+
+
+TASK_SELECTION = {"All": 0, "CP": 1, "Shallow": 2}
+SAMPLING = {"Hard": 0, "Soft": 1}
+ACTIONS = {-1: None, 0: "Partition", 1: "Merge", 2: "Repartition"}
+
+
 class TraceC(C.Structure):
     _fields_ = [("cap_assign", C.c_int32), ("cap_xfer", C.c_int32), ("cap_res", C.c_int32),
                 ("cap_events", C.c_int32), ("cap_steps", C.c_int32), ("pad0", C.c_int32),
@@ -168,7 +191,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -199,6 +222,7 @@ def load_library(path: str = LIB) -> C.CDLL:
                                      C.c_void_p, C.POINTER(Outcome)]
     lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
+    lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
     lib.hesp_verify_trace.argtypes = [C.c_void_p, C.POINTER(TraceC), C.c_char_p, C.c_size_t,
                                       C.POINTER(C.c_int32)]
     lib.hesp_engine_destroy.argtypes = [C.c_void_p]
@@ -428,6 +452,28 @@ class BatchEngine:
         self._check(self.lib.hesp_verify_trace(self.h, C.byref(t), buf, len(buf), C.byref(n)), "verify_trace")
         text = buf.value.decode()
         return text.split("\n") if n.value else []
+
+    def solve(self, iterations: int = 50, task_selection: str = "All", sampling: str = "Soft", seed: int = 0,
+              k_max: int = 8, min_block: int = 64, overhead_factor: float = 1.1, initial: np.ndarray | None = None):
+        """SPEC solve() (hesp_solve): returns (history, best descriptor, best makespan, best iteration,
+        device simulations issued)."""
+        cfg = SolverConfigC(iterations, TASK_SELECTION[task_selection], SAMPLING[sampling], k_max, seed, min_block,
+                            overhead_factor)
+        hist = np.zeros(max(1, iterations), SOLVER_ITER_DTYPE)
+        res = SolverResultC()
+        res.cap_history = len(hist)
+        res.history = hist.ctypes.data
+        init = None
+        if initial is not None:
+            init = np.ascontiguousarray(initial, DESC_DTYPE).reshape(1)
+        rc = self.lib.hesp_solve(self.h, init.ctypes.data if init is not None else None, C.byref(cfg), C.byref(res))
+        if rc < 0:
+            self._check(rc, "solve")
+        if rc > 0:
+            raise RuntimeError(f"solve: initial state fails with status {rc} ({status_name(rc)})")
+        best = np.frombuffer(bytes(res.best), DESC_DTYPE)[0].copy()
+        return hist[:res.n_history].copy(), best, float(res.best_makespan), int(res.best_iteration), \
+            int(res.n_simulated)
 
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)

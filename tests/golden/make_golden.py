@@ -106,6 +106,32 @@ SHIFTS = {
     "sect_cpugpu_0_late": ("sect_cpugpu_0", 20, -0.01),
 }
 
+# SPEC solver runs (hesp_solve parity): name -> (preset, iterations, selection, sampling, seed)
+SOLVES = {
+    "small_all_hard": ("policy_PL_EFT-P_WB", 12, "All", "Hard", 0),
+    "small_cp_soft": ("policy_PL_EFT-P_WB", 12, "CP", "Soft", 3),
+    "small_shallow_soft": ("policy_PL_EFT-P_WB", 12, "Shallow", "Soft", 5),
+    "small_rp_all_soft": ("policy_FCFS_R-P_WB", 10, "All", "Soft", 9),
+    "c2_all_soft": ("c2", 5, "All", "Soft", 1),
+}
+
+
+def write_solves(names):
+    import json
+    for name, (preset_name, iters, sel, samp, seed) in SOLVES.items():
+        if names and f"solve_{name}" not in names:
+            continue
+        p, _ = PARITY[preset_name]
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--threads", str(os.cpu_count()), "--solve",
+                            str(iters), "--solve-selection", sel, "--solve-sampling", samp, "--solve-seed",
+                            str(seed)], check=True, capture_output=True, text=True)
+        d = json.loads(r.stdout)
+        d.update(preset=preset_name, iterations=iters, selection=sel, sampling=samp, seed=seed, k_max=8,
+                 overhead=1.1)
+        with open(os.path.join(HERE, f"solve_{name}.json"), "w") as f:
+            json.dump(d, f)
+        print("solve", name, [h[1] for h in d["history"]], "best it", d["best_iteration"])
+
 
 def write_traces(names):
     import gzip
@@ -184,6 +210,7 @@ def main(names):
             f.writelines(keep)
         print(name, "detail written")
     write_traces(names)
+    write_solves(names)
     for name in [n for n in (names or sorted(PARITY)) if n in PARITY]:
         p, count = PARITY[name]
         out = os.path.join(HERE, f"{name}.bin")
