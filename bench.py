@@ -153,6 +153,27 @@ def roofline(best_steps, kernel_ms, P, S, n_types, peak_gbs, peak_kind, traffic)
                      "bound — issue-slot and memory-latency evidence in profiles/")}
 
 
+def issue_roofline(config, value, sm_count, clk):
+    """Issue-slot view of the same step (the binding resource):
+    warp-instructions per candidate measured by ncu on this config
+    (profiles/ncu_issue.json, smsp__inst_executed.sum of build_kernel +
+    sim_kernel / candidates) x candidates/s, against SMs x 4 schedulers x the
+    SM clock sampled during the timed region."""
+    path = os.path.join(ROOT, "profiles", "ncu_issue.json")
+    if not os.path.exists(path) or not clk:
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    if d.get("config") != config:
+        return None
+    ipc = d["warp_inst_per_candidate"]
+    per_cand = sum(ipc.values())
+    peak = sm_count * 4 * clk["sm_mhz"] * 1e6
+    ach = per_cand * value
+    return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": round(ach / peak, 4),
+            "warp_inst_per_candidate": ipc, "source": "profiles/ncu_issue.json (" + d.get("source", "ncu") + ")"}
+
+
 def ncu_traffic(config, batch):
     path = os.path.join(ROOT, "profiles", "ncu_eval_kernel.json")
     if not os.path.exists(path):
@@ -319,6 +340,7 @@ def main():
                     "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64},
             "gpu_launches": int(launches),
             "roofline": rf,
+            "issue_roofline": issue_roofline(args.config, value, info.sm_count, clk),
             "cpu_baseline": cpu,
             "clocks": clk,
             "valid_fraction": n_ok / (B * args.steps),

@@ -102,3 +102,17 @@ def test_per_task_schedule_parity(lib, name):
     got = {t: (int(proc[t]), int(np.float64(start[t]).view(np.uint64)), int(np.float64(end[t]).view(np.uint64)))
            for t in range(cap) if proc[t] >= 0}
     assert got == want
+
+
+def test_search_driver_matches_batch_best(lib, capsys):
+    """paper_1602_05510_b200.search (the sharded C4/C5 driver, 1 rank here)
+    finds the same winner as one batch over the same index range, and its
+    winner trace verifies clean."""
+    import json
+    from paper_1602_05510_b200.search import main
+    main(["--config", "c2", "--candidates", "3000", "--batch", "1000", "--trace-winner"])
+    line = json.loads(capsys.readouterr().out.strip().splitlines()[-1])
+    p, _ = PARITY["c2"]
+    _, b = make_engine(p).eval_generated(0, 3000, outcomes=False)
+    assert line["best"]["index"] == b.index and line["best"]["makespan"] == b.makespan
+    assert line["valid"] == b.n_ok and line["winner_trace"]["verify_violations"] == 0
