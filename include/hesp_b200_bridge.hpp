@@ -6,16 +6,18 @@
 // PerfModel::analytic / PerfModel::tabulated (platform.hpp:118-121).
 // It maps those types field for field onto the C ABI (hesp_engine.h) and
 // turns ABI errors back into hesp::Error, so callers keep the reference's
-// error behaviour.  Candidates are partition-op sequences applied after
+// error behaviour.  Candidates are partition/merge-op sequences applied after
 // root_cholesky(n, elem) + partition_task(0, 1/s_base) (graph.hpp:119,136).
 //
 //   hesp::b200::BatchSimulator gpu(platform, analytic_entries, cfg, n, elem, s_base, gen);
 //   std::vector<hesp_outcome> out = gpu.evaluate(descs, &best);   // per-candidate status/makespan
+//   hesp::SimResult r = gpu.simulate(descs[best.index], elem);     // the winner's full SimResult
 //
 // Link with paper_1602_05510_b200/libhesp_b200.so; include paths: this
 // directory and the reference's proj/include.
 #pragma once
 
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 #include <tuple>
@@ -84,6 +86,100 @@ class BatchSimulator {
     if (out) out->resize(count);
     check(hesp_eval_generated(engine_, first, count, out ? out->data() : nullptr, &best));
     return best;
+  }
+
+  // The full hesp::SimResult of one candidate, simulated on the device
+  // (hesp_eval_trace): the value simulate(graph, platform, model, cfg)
+  // (sim.hpp:150-151) returns for the graph the descriptor describes, in the
+  // reference's own types and container orders.  Throws the reference's
+  // hesp::Error for a failing candidate.
+  SimResult simulate(const hesp_cand_desc& desc, int elem_size) {
+    std::vector<hesp_assignment> a(4096);
+    std::vector<hesp_transfer> x(8192);
+    std::vector<hesp_residency> r(16384);
+    std::vector<hesp_event> e(32768);
+    std::vector<hesp_load_step> st(8192);
+    hesp_trace t{};
+    int rc;
+    for (;;) {
+      t = hesp_trace{};
+      t.cap_assign = (int32_t)a.size();
+      t.cap_xfer = (int32_t)x.size();
+      t.cap_res = (int32_t)r.size();
+      t.cap_events = (int32_t)e.size();
+      t.cap_steps = (int32_t)st.size();
+      t.assignments = a.data();
+      t.transfers = x.data();
+      t.residency = r.data();
+      t.events = e.data();
+      t.steps = st.data();
+      rc = hesp_eval_trace(engine_, &desc, &t);
+      if (rc != HESP_E_LIMIT) break;
+      a.resize(std::max<size_t>(a.size(), t.n_assign));
+      x.resize(std::max<size_t>(x.size(), t.n_xfer));
+      r.resize(std::max<size_t>(r.size(), t.n_res));
+      e.resize(std::max<size_t>(e.size(), t.n_events));
+      st.resize(std::max<size_t>(st.size(), t.n_steps));
+    }
+    if (rc < 0) check(rc);
+    if (rc > 0) {
+      hesp_outcome o{};
+      o.status = rc;
+      rethrow(o);
+    }
+    static const char* kinds[] = {"CHOL", "TRSM", "SYRK", "GEMM"};
+    SimResult res;
+    res.makespan = t.outcome.makespan;
+    for (int i = 0; i < t.n_assign; ++i) {
+      res.assignments[a[i].task] = {a[i].task, a[i].proc, a[i].start, a[i].end};
+      res.idle_avg[a[i].task] = a[i].idle_avg;
+    }
+    for (int i = 0; i < t.n_xfer; ++i) {
+      TransferRec rec;
+      rec.block = x[i].block;
+      if (x[i].has_fragment)
+        rec.fragment = Region{x[i].frag_row, x[i].frag_col, x[i].frag_rows, x[i].frag_cols, elem_size};
+      for (int h = 0; h < x[i].n_hops; ++h) rec.route.emplace_back(x[i].hop_src[h], x[i].hop_dst[h]);
+      rec.start = x[i].start;
+      rec.end = x[i].end;
+      rec.bytes = x[i].bytes;
+      rec.dst_space = x[i].dst_space;
+      res.transfers.push_back(rec);
+    }
+    for (int i = 0; i < t.n_events; ++i) {
+      EventRec ev;
+      ev.kind = static_cast<EventRec::Kind>(e[i].kind);
+      ev.time = e[i].time;
+      if (e[i].kind <= HESP_EV_TASK_END) {
+        ev.subject = "T" + std::to_string(e[i].id) + ":" + kinds[e[i].task_kind] + ":b" + std::to_string(e[i].b);
+        ev.resource = std::to_string(e[i].res_a);
+      } else {
+        ev.subject = "B" + std::to_string(e[i].id);
+        ev.resource = std::to_string(e[i].res_a) + "->" + std::to_string(e[i].res_b);
+      }
+      res.events.push_back(std::move(ev));
+    }
+    for (int i = 0; i < t.n_res; ++i)
+      res.residency_log.push_back({r[i].time, r[i].space, r[i].delta_bytes, r[i].block});
+    return res;
+  }
+
+  // The iterative solver (hesp_solve; solver.hpp:83-84 semantics).
+  hesp_solver_result solve(const hesp_solver_config& cfg, std::vector<hesp_solver_iteration>& history,
+                           const hesp_cand_desc* initial = nullptr) {
+    history.resize(cfg.iterations > 0 ? cfg.iterations : 1);
+    hesp_solver_result out{};
+    out.cap_history = (int32_t)history.size();
+    out.history = history.data();
+    const int rc = hesp_solve(engine_, initial, &cfg, &out);
+    if (rc < 0) check(rc);
+    if (rc > 0) {
+      hesp_outcome o{};
+      o.status = rc;
+      rethrow(o);
+    }
+    history.resize(out.n_history);
+    return out;
   }
 
   // The reference's per-candidate exception, if any (errors.hpp:10-32).

@@ -1,0 +1,30 @@
+"""The reference-side C++ binding as a drop-in (include/hesp_b200_bridge.hpp):
+oracle/_ref/bridge_check builds the reference graph and runs the UNMODIFIED
+reference simulate() and, in the same process, BatchSimulator::simulate on the
+B200 engine; the two hesp::SimResult values must be identical field by field
+(assignments, idle_avg, transfers with routes/fragments, event strings,
+residency log), and the reference's own verify_schedule must say the same
+about both."""
+import os
+import subprocess
+
+import pytest
+
+from paper_1602_05510_b200.configs import PARITY, harness_args
+from paper_1602_05510_b200.engine import FIXTURES
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHECK = os.path.join(ROOT, "oracle", "_ref", "bridge_check")
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not os.path.exists(CHECK), reason="oracle/_ref/bridge_check not built")]
+
+
+@pytest.mark.parametrize("name,count", [("c2", 6), ("evict_wb", 4), ("evict_wa", 4), ("sect_cpugpu", 8),
+                                        ("table", 4), ("c3", 4), ("merge_c2", 8), ("policy_FCFS_R-P_WT", 8)])
+def test_bridge_simresult_identical_to_reference(lib, name, count):
+    p, _ = PARITY[name]
+    r = subprocess.run([CHECK, *harness_args(p, FIXTURES), "--count", str(count)], capture_output=True, text=True,
+                       timeout=900)
+    assert "mismatches 0" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
+    assert r.returncode == 0
