@@ -321,7 +321,7 @@ def main():
                       ncu_traffic(args.config, B))
         rf["build_kernel_ms_per_step"] = round(statistics.mean(build_ms), 4) if build_ms else None
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
             d, err = cpu_baseline(p, args.cpu_seconds)
             if d:
                 cpu = {"value": d["cand_per_s"], "unit": UNIT, "cores": d["threads"], "kind": "reference",
