@@ -13,6 +13,8 @@
 // (paper_1602_05510_b200/engine.py) on 16 bytes per rank.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -63,7 +65,8 @@ __device__ __noinline__ void generate_desc(unsigned long long index, hesp_cand_d
 // same phase, so the instruction working set is one phase's code.
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     build_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
-                 unsigned long long count, uint8_t* slots, unsigned long long* counter) {
+                 unsigned long long count, uint8_t* slots, unsigned long long* counter,
+                 const uint32_t* __restrict__ order) {
   __shared__ Small smem[WARPS_PER_BLOCK];
   __shared__ hesp_cand_desc sdesc[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
@@ -74,6 +77,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     if (lane == 0) k = atomicAdd(counter, 1ULL);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= count) break;
+    if (order) k = order[k];
     hesp_cand_desc& d = sdesc[wib];
     if (descs) {
       // header + the used ops only (descriptors are mostly short)
@@ -92,9 +96,40 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
   }
 }
 
+// Build-phase cost proxy from the descriptor alone: sum of s^3 over its
+// partition ops (the sub-task count of a GEMM split; merges add nothing).
+__global__ void order_keys_desc(const hesp_cand_desc* __restrict__ descs, unsigned long long count,
+                                uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const hesp_cand_desc* d = descs + k;
+  const int n = d->n_ops < HESP_MAX_OPS ? d->n_ops : HESP_MAX_OPS;
+  uint32_t c = 0;
+  for (int i = 0; i < n; ++i) {
+    const int s = d->ops[i].s;
+    if (s > 1 && s <= 64) c += (uint32_t)(s * s * s);
+  }
+  keys[k] = c;
+  vals[k] = (uint32_t)k;
+}
+
+// Longest-processing-time-first order for the simulate kernel: candidates
+// vary ~10x in cost, and a persistent kernel's tail is the last long
+// candidates; starting the largest expanded DAGs first shrinks it.  Key =
+// leaf count (0 for candidates whose build already failed).
+__global__ void order_keys(const uint8_t* __restrict__ slots, unsigned long long count, uint32_t* __restrict__ keys,
+                           uint32_t* __restrict__ vals) {
+  const unsigned long long k = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  const SlotHeader h = *(const SlotHeader*)(slots + k * c_problem.lay.total + c_problem.lay.hdr);
+  keys[k] = h.status ? 0u : (uint32_t)h.nleaves;
+  vals[k] = (uint32_t)k;
+}
+
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
-               WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter) {
+               WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter,
+               const uint32_t* __restrict__ order) {
   __shared__ Small smem[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -107,6 +142,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     if (lane == 0) k = atomicAdd(counter, 1ULL);
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= count) break;
+    if (order) k = order[k];
     Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
     const Outcome o = eng.sim_slot();
     if (lane == 0 && out) {
@@ -258,6 +294,11 @@ struct hesp_engine {
   uint8_t* d_cslots = nullptr;
   unsigned long long chunk = 0;      // max candidates per chunk (memory budget)
   unsigned long long cslots_n = 0;   // slots currently allocated
+  uint32_t* d_order = nullptr;       // LPT order: keys/vals in, keys/vals out (4 x cslots_n)
+  hesp_cand_desc* d_gen = nullptr;   // generated descriptors of one chunk (LPT on generated batches)
+  void* d_sort_tmp = nullptr;
+  size_t sort_tmp_bytes = 0;
+  bool lpt = true;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   static constexpr int NEV = 64;     // per-chunk kernel timing (build, sim)
   cudaEvent_t evc[NEV][4] = {};
@@ -305,6 +346,18 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     e->cslots_n = 0;
     if (!ck(cudaMalloc(&e->d_cslots, (size_t)need * e->L.total), "malloc chunk slots")) return HESP_E_CUDA;
     e->cslots_n = need;
+    if (e->d_order) cudaFree(e->d_order);
+    if (e->d_sort_tmp) cudaFree(e->d_sort_tmp);
+    if (e->d_gen) cudaFree(e->d_gen);
+    e->d_gen = nullptr;
+    e->d_order = nullptr;
+    e->d_sort_tmp = nullptr;
+    if (!ck(cudaMalloc(&e->d_order, 4 * sizeof(uint32_t) * need), "malloc order")) return HESP_E_CUDA;
+    e->sort_tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, e->sort_tmp_bytes, e->d_order, e->d_order + need,
+                                              e->d_order + 2 * need, e->d_order + 3 * need, (int)need, 0, 32, st);
+    if (!ck(cudaMalloc(&e->d_sort_tmp, e->sort_tmp_bytes ? e->sort_tmp_bytes : 1), "malloc sort tmp"))
+      return HESP_E_CUDA;
   }
   const unsigned long long chunk = e->cslots_n;
   if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
@@ -319,11 +372,44 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     const int ci = (int)(c0 / chunk);
     const bool timed = ci < hesp_engine::NEV;
     if (timed) cudaEventRecord(e->evc[ci][0], st);
-    build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_descs ? d_descs + c0 : nullptr, first + c0, n,
-                                                                 e->d_cslots, e->d_counter);
+    const hesp_cand_desc* cd = d_descs ? d_descs + c0 : nullptr;
+    if (e->lpt && !cd && n > 1) {  // generated candidates: materialise the descriptors to order them
+      if (!e->d_gen) {
+        if (!ck(cudaMalloc(&e->d_gen, chunk * sizeof(hesp_cand_desc)), "malloc gen descs")) return HESP_E_CUDA;
+      }
+      gen_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(first + c0, n, e->d_gen);
+      e->launches += 1;
+      cd = e->d_gen;
+    }
+    const uint32_t* border = nullptr;
+    if (e->lpt && cd && n > 1) {
+      uint32_t* kin = e->d_order;
+      uint32_t* kout = e->d_order + chunk;
+      uint32_t* vin = e->d_order + 2 * chunk;
+      uint32_t* vout = e->d_order + 3 * chunk;
+      order_keys_desc<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(cd, n, kin, vin);
+      size_t tb = e->sort_tmp_bytes;
+      cub::DeviceRadixSort::SortPairsDescending(e->d_sort_tmp, tb, kin, kout, vin, vout, (int)n, 0, 32, st);
+      border = vout;
+      e->launches += 1;
+    }
+    build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(cd, first + c0, n, e->d_cslots, e->d_counter,
+                                                                 border);
+    const uint32_t* order = nullptr;
+    if (e->lpt && n > 1) {
+      uint32_t* kin = e->d_order;
+      uint32_t* kout = e->d_order + chunk;
+      uint32_t* vin = e->d_order + 2 * chunk;
+      uint32_t* vout = e->d_order + 3 * chunk;
+      order_keys<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(e->d_cslots, n, kin, vin);
+      size_t tb = e->sort_tmp_bytes;
+      cub::DeviceRadixSort::SortPairsDescending(e->d_sort_tmp, tb, kin, kout, vin, vout, (int)n, 0, 32, st);
+      order = vout;
+      e->launches += 1;
+    }
     if (timed) cudaEventRecord(e->evc[ci][1], st);
     sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
-                                                               e->d_wbest, acc, e->d_cslots, e->d_counter + 1);
+                                                               e->d_wbest, acc, e->d_cslots, e->d_counter + 1, order);
     if (timed) cudaEventRecord(e->evc[ci][2], st);
     e->nev_used = ci + 1 < hesp_engine::NEV ? ci + 1 : hesp_engine::NEV;
     e->launches += 2;
@@ -491,9 +577,12 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     // bounded by ~35% of free device memory.
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    unsigned long long cap = (unsigned long long)(0.35 * (double)free_b) / (unsigned long long)e->L.total;
+    const char* mf = getenv("HESP_MEM_FRAC");
+    const double frac = mf ? atof(mf) : 0.6;
+    if (const char* l = getenv("HESP_LPT")) e->lpt = atoi(l) != 0;
+    unsigned long long cap = (unsigned long long)(frac * (double)free_b) / (unsigned long long)e->L.total;
     const char* ch = getenv("HESP_CHUNK");
-    unsigned long long want = ch ? strtoull(ch, nullptr, 10) : 65536ULL;
+    unsigned long long want = ch ? strtoull(ch, nullptr, 10) : 131072ULL;
     if (cap < 1024) cap = 1024;
     e->chunk = want < cap ? want : cap;
   }
@@ -519,6 +608,9 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_base_plist);
   cudaFree(e->d_scratch);
   cudaFree(e->d_cslots);
+  cudaFree(e->d_order);
+  cudaFree(e->d_sort_tmp);
+  cudaFree(e->d_gen);
   cudaFree(e->d_wbest);
   cudaFree(e->d_best);
   cudaFree(e->d_counter);
