@@ -245,6 +245,8 @@ struct Small {
   double est[MAXS];
   int32_t tmp_i[64];
   double tmp_d[8];
+  uint64_t ah, xh;  // event-loop result hashes (one copy per warp)
+  int32_t ptype[MAXP], pspace[MAXP];
 };
 
 // ---------------------------------------------------------------------------
@@ -1805,22 +1807,6 @@ struct Engine {
   using LaneD = typename WP::LaneD;
   using LaneI = typename WP::LaneI;
 
-  // Link clocks live in lane registers in the hot loop (lane l owns
-  // link_free[l]); cold member paths (gather, eviction flush) use the Small
-  // copy, so they are spilled around those calls.
-  HX void lf_spill(LaneD& lf) {
-    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) sm->link_free[i] = lf.own(i);
-    wp.sync();
-  }
-  HX void lf_load(LaneD& lf) {
-    wp.sync();
-    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) lf.own(i) = sm->link_free[i];
-  }
-
-
-
-
-
   HX uint64_t rng_next() { return hesp_splitmix_next(&rng); }
 
   // WT / WA write-back of a task's output to main (sim.cpp:631-656).
@@ -1981,22 +1967,35 @@ struct Engine {
     }
     wp.sync();
     // lane-owned clocks and processor attributes
-    LaneD pf, lf, est, estp;
-    LaneI ptype, pspace;
-    pf.fill(0.0);
-    lf.fill(0.0);
+    LaneD est, estp;
+    // processor clocks and attributes in the warp's Small, like the link clocks
+#define PF_OWN(q) sm->proc_free[q]
+#define PF_GET(p) sm->proc_free[p]
+#define PF_SET(p, v) (sm->proc_free[p] = (v))
+#define PTYPE(q) sm->ptype[q]
+#define PSPACE_OWN sm->pspace[wp.lane()]
+    NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) sm->proc_free[q] = 0.0;
     est.fill(0.0);
     estp.fill(0.0);
     NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) {
-      ptype.own(q) = q < P ? PB.proc_type[q] : 0;
-      pspace.own(q) = q < P ? PB.proc_space[q] : 0;
+      PTYPE(q) = q < P ? PB.proc_type[q] : 0;
+      sm->pspace[q] = q < P ? PB.proc_space[q] : 0;
     }
 #if defined(__CUDACC__)
     const int eft_k = wp.lane() / S_, eft_sp = wp.lane() - (wp.lane() / S_) * S_;  // lane = (block, space)
 #endif
     rng = PB.sched_seed;
     double tnow = 0.0, mk = 0.0;
-    uint64_t ah = 0, xh = 0;
+    // link clocks and the result hashes live in the warp's shared Small
+    // (uniform values: every lane stores the same value and reads its own
+    // store), which keeps them out of the register file the loop spills from
+    Small* const smw = sm;
+    smw->ah = 0;
+    smw->xh = 0;
+#define HAH smw->ah
+#define HXH smw->xh
+    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) smw->link_free[i] = 0.0;
+    wp.sync();
     int st = 0;  // status mirror for the hot loop
     now = 0.0;
 
@@ -2011,9 +2010,9 @@ struct Engine {
       double hs[2] = {0.0, 0.0}, he[2] = {0.0, 0.0};
       NOUNROLL for (int h = 0; h < nh; ++h) {
         const int l = PB.route_l[src * MAXS + dst][h];
-        const double s0 = dmax(lf.get(l), rdy);
+        const double s0 = dmax(smw->link_free[l], rdy);
         const double en = s0 + PB.link_lat[l] + PB.hopq[l][bi];  // (s0 + lat) + bytes/bw
-        lf.set(l, en);
+        smw->link_free[l] = en;  // uniform: every lane stores the same value and reads its own store
         rdy = en;
         if (h == 0) start0 = s0;
         if (TRACE && h < 2) {
@@ -2023,18 +2022,18 @@ struct Engine {
       }
       if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
       if (TRACE) log_xfer(blk, nullptr, nbytes, src, dst, start0, rdy, nh, hs, he);
-      xh += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      HXH += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
       return rdy;
     };
     // cold-call bracket: hand the uniform hot state to the member paths and back
     auto cold_in = [&]() {
-      lf_spill(lf);
-      xhash += xh;
-      xh = 0;
+      wp.sync();
+      xhash += HXH;
+      HXH = 0;
       status = st;
     };
     auto cold_out = [&]() {
-      lf_load(lf);
+      wp.sync();
       st = status;
     };
     // validate_from on the hot path: an unsubdivided tile has no descendants
@@ -2128,7 +2127,7 @@ struct Engine {
         }
         if (waits) {
           NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
-            const double f = pf.own(q);
+            const double f = PF_OWN(q);
             if (f > tnow && f < nx) nx = f;
           }
         }
@@ -2202,7 +2201,7 @@ struct Engine {
         if (waits) {
           unsigned idle_mask = 0;
           NOUNROLL for (int q = wp.lane(); q < P; q += WP::W)
-            if (pf.own(q) <= tnow) idle_mask |= 1u << q;
+            if (PF_OWN(q) <= tnow) idle_mask |= 1u << q;
 #if defined(__CUDACC__)
           idle_mask = __reduce_or_sync(0xffffffffu, idle_mask);
 #endif
@@ -2219,7 +2218,7 @@ struct Engine {
             int id = -1;
             NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
               if (!((idle_mask >> q) & 1u)) continue;
-              const double tt = PB.ttime[tkind][tbidx][ptype.own(q)];
+              const double tt = PB.ttime[tkind][tbidx][PTYPE(q)];
               if (id < 0 || tt < a) {
                 a = tt;
                 id = q;
@@ -2312,22 +2311,22 @@ struct Engine {
                 const double o = __shfl_sync(FULL, val, from);
                 if (lane < Sx && kp < nw) e = dmax(e, o);
               }
-              estp.own(0) = __shfl_sync(FULL, e, pspace.own(0));
+              estp.own(0) = __shfl_sync(FULL, e, PSPACE_OWN);
             }
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
 #else
             NOUNROLL for (int sp = wp.lane(); sp < S_; sp += WP::W) est.own(sp) = eft_space_h(sp, w, nw, noroute);
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
-            estp.gather(est, pspace);  // estimate of each processor's space
+            NOUNROLL for (int q = 0; q < P; ++q) estp.own(q) = est.get(sm->pspace[q]);  // estimate of each processor's space
 #endif
           }
           double a = ABSENT, b2 = 0.0;
           int id = -1;
           NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
-            const double nf = pf.own(q);
+            const double nf = PF_OWN(q);
             double qa, qb = 0.0;
             if (sel == SEL_EFTP) {
-              qa = dmax(dmax(nf, rel), estp.own(q)) + PB.ttime[tkind][tbidx][ptype.own(q)];
+              qa = dmax(dmax(nf, rel), estp.own(q)) + PB.ttime[tkind][tbidx][PTYPE(q)];
               qb = nf;
             } else {
               qa = nf;  // EIT-P
@@ -2369,11 +2368,11 @@ struct Engine {
           cold_out();
           if (st) return fail(st);
         }
-        const double start = dmax(dmax(pf.get(p), rel), inputs);
+        const double start = dmax(dmax(PF_GET(p), rel), inputs);
         const double end = start + PB.ttime[tkind][tbidx][type];
         if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
-        pf.set(p, end);
-        ah += hesp_assign_term(j, p, dbits(start), dbits(end));
+        PF_SET(p, end);
+        HAH += hesp_assign_term(j, p, dbits(start), dbits(end));
         if (TRACE && j < tr_cap && wp.lane() == 0) {
           tr_proc[j] = p;
           tr_start[j] = start;
@@ -2458,8 +2457,15 @@ struct Engine {
       }
     }
     makespan = mk;
-    ahash += ah;
-    xhash += xh;
+    ahash += HAH;
+    xhash += HXH;
+#undef HAH
+#undef HXH
+#undef PF_OWN
+#undef PF_GET
+#undef PF_SET
+#undef PTYPE
+#undef PSPACE_OWN
 #undef HOT_ARR
 #undef nbt_
 #undef nbb_
