@@ -49,6 +49,9 @@ PARITY = {
     "deep_biglittle": (preset(BIGLITTLE, 8192, 8, 8, 12, max_depth=4, seed=12, selection="R-P",
                               sched_seed=77), 48),
 }
+SERIAL = ("platform_serial.json", "model_biglittle.json")  # one big core: SPEC acceptance 6
+PARITY["serial"] = (preset(SERIAL, 4096, 8, 8, 8, seed=31, merge_pct=20), 24)
+
 # merge ops (TaskGraph::merge_cluster) mixed into the random partitionings
 PARITY["merge_c2"] = (preset(CPUGPU, 16384, 4, 16, 12, seed=21, merge_pct=35), 64)
 PARITY["merge_evict"] = (preset(CPUGPU_EVICT, 16384, 4, 16, 10, seed=22, merge_pct=30), 24)

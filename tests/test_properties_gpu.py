@@ -1,0 +1,87 @@
+"""Size-independent properties of the engine's schedules (SPEC.md acceptance
+criteria 1, 4, 5, 6), checked on the device output for many candidates --
+beyond the candidates the golden records pin."""
+import numpy as np
+import pytest
+
+from paper_1602_05510_b200.configs import PARITY, preset, make_engine, CPUGPU
+from paper_1602_05510_b200.engine import load_model
+
+pytestmark = pytest.mark.gpu
+
+
+def task_flops(kind, b):  # platform.cpp:57-66
+    bd = float(b)
+    return (bd * bd * bd / 3.0, bd * bd * bd, bd * bd * bd, 2.0 * bd * bd * bd)[kind]
+
+
+def analytic_time(model, kind, b, type_name):  # PerfModel::task_time, platform.cpp:351-357
+    from paper_1602_05510_b200.engine import KINDS
+    for k, t, peak, bh in model.analytic:
+        if KINDS[k] == kind and t == type_name:
+            eff = float(b) / (float(b) + bh)
+            return task_flops(kind, b) / (peak * eff)
+    raise KeyError((kind, type_name))
+
+
+@pytest.mark.parametrize("s", [2, 4, 8, 16])
+def test_task_count_law(lib, s):
+    """Criterion 1: a uniform s-tile Cholesky has s(s+1)(s+2)/6 tasks."""
+    eng = make_engine(preset(CPUGPU, 16384, 4, s, 0))
+    out, _ = eng.eval_generated(0, 1)
+    assert int(out[0]["status"]) == 0 and int(out[0]["n_leaves"]) == s * (s + 1) * (s + 2) // 6
+
+
+def test_serial_identity(lib):
+    """Criterion 6: on one processor the makespan is the plain sum of the task
+    times in commit order, exactly -- for random partitionings with merges."""
+    p, _ = PARITY["serial"]
+    eng = make_engine(p)
+    model = load_model(p["model"])
+    descs = eng.generate_host(0, 40)
+    for d in descs:
+        tr = eng.eval_trace(d)
+        if tr.status:
+            continue
+        order = np.argsort(tr.assignments["start"], kind="stable")
+        a = tr.assignments[order]
+        ev = {int(e["id"]): (int(e["task_kind"]), int(e["b"])) for e in tr.events if int(e["kind"]) == 0}
+        t = 0.0
+        for row in a:
+            assert row["start"] == t
+            kind, b = ev[int(row["task"])]
+            t = t + analytic_time(model, kind, b, "big")
+            assert row["end"] == t
+        assert tr.makespan == t
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "sect_cpugpu", "table", "merge_c2", "policy_FCFS_R-P_WT",
+                                  "policy_PL_F-P_WA", "deep_biglittle"])
+def test_schedules_verify_and_respect_work_bound(lib, name):
+    """Criteria 4 and 5: verify_schedule finds nothing, and the makespan is at
+    least the work bound sum_t min_type time(t) / P."""
+    p, _ = PARITY[name]
+    eng = make_engine(p)
+    model = load_model(p["model"])
+    import json
+    import os
+    from paper_1602_05510_b200.engine import FIXTURES
+    plat = json.load(open(os.path.join(FIXTURES, p["platform"])))
+    types = [t["name"] for t in plat["types"]]
+    P = len(plat["processors"])
+    descs = eng.generate_host(50_000, 16)
+    checked = 0
+    for d in descs:
+        tr = eng.eval_trace(d)
+        if tr.status:
+            continue
+        assert eng.verify_trace(tr) == []
+        if model.analytic is not None:
+            work = 0.0
+            for e in tr.events:
+                if int(e["kind"]) == 0:
+                    work += min(analytic_time(model, int(e["task_kind"]), int(e["b"]), ty) for ty in types)
+            assert tr.makespan * (1 + 1e-12) >= work / P
+        assert tr.busy_time <= P * tr.makespan * (1 + 1e-12)
+        checked += 1
+    assert checked > 0
