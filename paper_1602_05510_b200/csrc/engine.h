@@ -29,11 +29,13 @@
 #include "engine_types.h"
 
 #if defined(__CUDACC__)
+#define HHD __host__ __device__ inline  // width-1 warp policy methods
 #define HX __device__ __forceinline__   // tiny accessors
 #define HXN __device__ __noinline__     // engine phases: one copy each keeps the kernel i-cache sized
 #define NOUNROLL _Pragma("unroll 1")
 #else
 #include <cstring>
+#define HHD inline
 #define HX inline
 #define HXN inline
 #define NOUNROLL
@@ -64,25 +66,27 @@ constexpr double HOLD = 1.0e307;    // pinned for the commit in progress
 // ---------------------------------------------------------------------------
 // Warp policies
 
+// Width-1 policy: the host build, and on the device the thread-per-candidate
+// simulate kernel (every lane runs its own candidate).
 struct HostWarp {
   static constexpr int W = 1;
-  int lane() const { return 0; }
-  unsigned ballot(bool p) const { return p ? 1u : 0u; }
-  unsigned lt() const { return 0u; }
-  void sync() const {}
+  HHD int lane() const { return 0; }
+  HHD unsigned ballot(bool p) const { return p ? 1u : 0u; }
+  HHD unsigned lt() const { return 0u; }
+  HHD void sync() const {}
   template <class T>
-  T bcast(T v, int) const { return v; }
-  bool any(bool p) const { return p; }
-  int sumi(int v) const { return v; }
-  long long suml(long long v) const { return v; }
-  double maxd(double v) const { return v; }
-  double mind(double v) const { return v; }
-  int mini(int v) const { return v; }
-  int maxi(int v) const { return v; }
+  HHD T bcast(T v, int) const { return v; }
+  HHD bool any(bool p) const { return p; }
+  HHD int sumi(int v) const { return v; }
+  HHD long long suml(long long v) const { return v; }
+  HHD double maxd(double v) const { return v; }
+  HHD double mind(double v) const { return v; }
+  HHD int mini(int v) const { return v; }
+  HHD int maxi(int v) const { return v; }
   // lexicographic argmin of (a, b, id); lanes with id < 0 do not participate
-  void argmin3(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
-  void argmin_lane(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
-  int atomic_add(int* p, int v) const {
+  HHD void argmin3(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
+  HHD void argmin_lane(double& a, double& b, int& id) const { (void)a; (void)b; (void)id; }
+  HHD int atomic_add(int* p, int v) const {
     int o = *p;
     *p += v;
     return o;
@@ -90,21 +94,21 @@ struct HostWarp {
   // per-lane owned vectors (device: one register per lane; host: the array)
   struct LaneD {
     double a[32];
-    double get(int i) const { return a[i]; }
-    void set(int i, double x) { a[i] = x; }
-    double& own(int i) { return a[i]; }
-    void fill(double x) {
+    HHD double get(int i) const { return a[i]; }
+    HHD void set(int i, double x) { a[i] = x; }
+    HHD double& own(int i) { return a[i]; }
+    HHD void fill(double x) {
       for (double& v : a) v = x;
     }
     template <class I>
-    void gather(const LaneD& src, const I& idx) {  // a[i] = src[idx[i]]
+    HHD void gather(const LaneD& src, const I& idx) {  // a[i] = src[idx[i]]
       for (int i = 0; i < 32; ++i) a[i] = src.a[idx.a[i]];
     }
   };
   struct LaneI {
     int a[32];
-    int get(int i) const { return a[i]; }
-    int& own(int i) { return a[i]; }
+    HHD int get(int i) const { return a[i]; }
+    HHD int& own(int i) { return a[i]; }
   };
 };
 
@@ -248,6 +252,7 @@ struct Small {
   uint64_t ah, xh;  // event-loop result hashes (one copy per warp)
   int32_t ptype[MAXP], pspace[MAXP];
 };
+static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
 
 // ---------------------------------------------------------------------------
 // Engine
@@ -804,9 +809,11 @@ struct Engine {
       const int c = i < nbb ? tl_cnt()[i] : 0;
       int incl = c;
 #if defined(__CUDACC__)
-      NOUNROLL for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (wp.lane() >= o) incl += v;
+      if constexpr (WP::W > 1) {
+        NOUNROLL for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (wp.lane() >= o) incl += v;
+        }
       }
 #endif
       if (i < nbb) tl_head()[i] = run + incl - c;
@@ -880,9 +887,11 @@ struct Engine {
         }
         int incl = sz;
 #if defined(__CUDACC__)
-        NOUNROLL for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xffffffffu, incl, o);
-          if (wp.lane() >= o) incl += v;
+        if constexpr (WP::W > 1) {
+          NOUNROLL for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (wp.lane() >= o) incl += v;
+          }
         }
 #endif
         const int my = pos + incl - sz;
@@ -1105,9 +1114,7 @@ struct Engine {
       nslow += popc32(m);
     }
     wp.sync();
-#if defined(__CUDACC__)
     sum_k = wp.sumi(sum_k);
-#endif
     // ---- pass A (serial in program order): cell tracking for the slow leaves
     NOUNROLL for (int si = 0; si < nslow && !status; ++si) {
       const int j = slow[si];
@@ -1237,9 +1244,7 @@ struct Engine {
       NOUNROLL for (int q = 0; q < cnt; ++q) wp.atomic_add(&ts()[pl_[q]].scnt, 1);
     }
     wp.sync();
-#if defined(__CUDACC__)
     total = wp.sumi(total);
-#endif
     nedges = total;  // all edges, base-table and arena alike
     int run = 0;
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
@@ -1247,9 +1252,11 @@ struct Engine {
       const int c = li < nleaves ? ts()[leaf()[li]].scnt : 0;
       int incl = c;
 #if defined(__CUDACC__)
-      NOUNROLL for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (wp.lane() >= o) incl += v;
+      if constexpr (WP::W > 1) {
+        NOUNROLL for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (wp.lane() >= o) incl += v;
+        }
       }
 #endif
       if (li < nleaves) {
@@ -1983,6 +1990,8 @@ struct Engine {
     }
 #if defined(__CUDACC__)
     const int eft_k = wp.lane() / S_, eft_sp = wp.lane() - (wp.lane() / S_) * S_;  // lane = (block, space)
+    (void)eft_k;
+    (void)eft_sp;
 #endif
     rng = PB.sched_seed;
     double tnow = 0.0, mk = 0.0;
@@ -2203,7 +2212,7 @@ struct Engine {
           NOUNROLL for (int q = wp.lane(); q < P; q += WP::W)
             if (PF_OWN(q) <= tnow) idle_mask |= 1u << q;
 #if defined(__CUDACC__)
-          idle_mask = __reduce_or_sync(0xffffffffu, idle_mask);
+          if constexpr (WP::W > 1) idle_mask = __reduce_or_sync(0xffffffffu, idle_mask);
 #endif
           if (idle_mask == 0) break;  // R-P/F-P wait for a processor (sim.cpp:800-801)
           if (sel == SEL_RP) {
@@ -2231,6 +2240,7 @@ struct Engine {
           if (sel == SEL_EFTP) {
             bool noroute = false;
 #if defined(__CUDACC__)
+            if constexpr (WP::W > 1) {
             // Warp-parallel est_transfer_ready (sim.cpp:762-793): lane (k, sp)
             // owns block k of the working set in space sp.  One round trip
             // loads every V(b_k, sp); ballots give each block's valid-space
@@ -2314,11 +2324,13 @@ struct Engine {
               estp.own(0) = __shfl_sync(FULL, e, PSPACE_OWN);
             }
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
-#else
+            } else
+#endif
+            {  // one lane: the reference's loop, space by space
             NOUNROLL for (int sp = wp.lane(); sp < S_; sp += WP::W) est.own(sp) = eft_space_h(sp, w, nw, noroute);
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
             NOUNROLL for (int q = 0; q < P; ++q) estp.own(q) = est.get(sm->pspace[q]);  // estimate of each processor's space
-#endif
+            }
           }
           double a = ABSENT, b2 = 0.0;
           int id = -1;

@@ -171,6 +171,84 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
   if (lane == 0) wbest[gw] = b;
 }
 
+// Thread-per-candidate simulate kernel (HESP_SIM_THREAD=1): the same event
+// loop instantiated at width 1 (Engine<HostWarp>, the source the host build
+// verifies), one candidate per thread, the longest-first order keeping a
+// warp's candidates of similar size.  Small lives in the candidate's slot.
+#ifndef HESP_SIMT_MIN_BLOCKS
+#define HESP_SIMT_MIN_BLOCKS 8
+#endif
+constexpr int SIMT_THREADS = 128;
+
+__global__ void __launch_bounds__(SIMT_THREADS, HESP_SIMT_MIN_BLOCKS)
+    sim_thread_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
+                      WarpBest* __restrict__ wbest, uint8_t* slots, const uint32_t* __restrict__ order) {
+  const Problem& pb = c_problem;
+  const unsigned long long tid = blockIdx.x * (unsigned long long)SIMT_THREADS + threadIdx.x;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * SIMT_THREADS;
+  const long long gw = (long long)(tid >> 5);
+  WarpBest b{0.0, -1, 0, 0, 0, 0, 0};
+  for (unsigned long long i = tid; i < count; i += nthreads) {
+    const unsigned long long k = order ? order[i] : i;
+    uint8_t* slot = slots + (size_t)k * pb.lay.total;
+    Engine<HostWarp> eng(HostWarp{}, pb, slot, (Small*)(slot + pb.lay.small));
+    const Outcome o = eng.sim_slot();
+    if (out) {
+      hesp_outcome r;
+      r.status = o.status;
+      r.n_leaves = o.n_leaves;
+      r.makespan = o.makespan;
+      r.assign_hash = o.assign_hash;
+      r.xfer_hash = o.xfer_hash;
+      out[k] = r;
+    }
+    ++b.n_eval;
+    b.leaves += o.n_leaves;
+    b.k += o.sum_k;
+    b.edges += o.n_edges;
+    if (o.status == 0) {
+      ++b.n_ok;
+      const long long gi = (long long)(first_index + k);
+      if (b.index < 0 || o.makespan < b.makespan || (o.makespan == b.makespan && gi < b.index)) {
+        b.makespan = o.makespan;
+        b.index = gi;
+      }
+    }
+  }
+  // warp merge of the lanes' bests, folded into this warp's accumulator
+  for (int off = 16; off; off >>= 1) {
+    const double m2 = __shfl_xor_sync(0xffffffffu, b.makespan, off);
+    const long long i2 = __shfl_xor_sync(0xffffffffu, b.index, off);
+    b.n_ok += __shfl_xor_sync(0xffffffffu, b.n_ok, off);
+    b.n_eval += __shfl_xor_sync(0xffffffffu, b.n_eval, off);
+    b.leaves += __shfl_xor_sync(0xffffffffu, b.leaves, off);
+    b.k += __shfl_xor_sync(0xffffffffu, b.k, off);
+    b.edges += __shfl_xor_sync(0xffffffffu, b.edges, off);
+    if (i2 >= 0 && (b.index < 0 || m2 < b.makespan || (m2 == b.makespan && i2 < b.index))) {
+      b.makespan = m2;
+      b.index = i2;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    WarpBest a = wbest[gw];
+    a.n_ok += b.n_ok;
+    a.n_eval += b.n_eval;
+    a.leaves += b.leaves;
+    a.k += b.k;
+    a.edges += b.edges;
+    if (b.index >= 0 && (a.index < 0 || b.makespan < a.makespan || (b.makespan == a.makespan && b.index < a.index))) {
+      a.makespan = b.makespan;
+      a.index = b.index;
+    }
+    wbest[gw] = a;
+  }
+}
+
+__global__ void init_best(WarpBest* __restrict__ wb, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) wb[i] = WarpBest{0.0, -1, 0, 0, 0, 0, 0};
+}
+
 __global__ void reduce_best(const WarpBest* __restrict__ wb, int n, hesp_best* __restrict__ best) {
   __shared__ double smk[32];
   __shared__ long long sidx[32], sok[32], sev[32], sl[32], sk[32], se[32];
@@ -299,6 +377,9 @@ struct hesp_engine {
   void* d_sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
   bool lpt = true;
+  bool sim_thread = false;           // HESP_SIM_THREAD=1: thread-per-candidate simulate kernel
+  int n_simt_blocks = 0;
+  int n_wbest = 0;                   // entries of d_wbest (max of both simulate grids, in warps)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   static constexpr int NEV = 64;     // per-chunk kernel timing (build, sim)
   cudaEvent_t evc[NEV][4] = {};
@@ -366,6 +447,10 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
   cudaEventRecord(e->ev0, st);
   e->nev_used = 0;
   int acc = 0;
+  if (e->sim_thread) {  // the thread kernel always accumulates: start from empty per-warp bests
+    init_best<<<(e->n_wbest + 255) / 256, 256, 0, st>>>(e->d_wbest, e->n_wbest);
+    e->launches += 1;
+  }
   for (uint64_t c0 = 0; c0 < count || (count == 0 && c0 == 0); c0 += chunk) {
     const uint64_t n = count - c0 < chunk ? count - c0 : chunk;
     cudaMemsetAsync(e->d_counter, 0, 2 * sizeof(unsigned long long), st);
@@ -408,8 +493,12 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
       e->launches += 1;
     }
     if (timed) cudaEventRecord(e->evc[ci][1], st);
-    sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
-                                                               e->d_wbest, acc, e->d_cslots, e->d_counter + 1, order);
+    if (e->sim_thread)
+      sim_thread_kernel<<<e->n_simt_blocks, SIMT_THREADS, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
+                                                                   e->d_wbest, e->d_cslots, order);
+    else
+      sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
+                                                                 e->d_wbest, acc, e->d_cslots, e->d_counter + 1, order);
     if (timed) cudaEventRecord(e->evc[ci][2], st);
     e->nev_used = ci + 1 < hesp_engine::NEV ? ci + 1 : hesp_engine::NEV;
     e->launches += 2;
@@ -417,7 +506,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     if (count == 0) break;
   }
   cudaEventRecord(e->ev1, st);
-  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_slots, e->d_best);
+  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_wbest, e->d_best);
   e->launches += 1;
   if (!ck(cudaGetLastError(), "split launch")) return HESP_E_CUDA;
   return HESP_OK;
@@ -568,7 +657,16 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   e->L = p.lay;
   if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
   cudaMemcpy(e->d_problem, &p, sizeof(Problem), cudaMemcpyHostToDevice);
-  if ((c = cudaMalloc(&e->d_wbest, (size_t)e->n_slots * sizeof(WarpBest))) != cudaSuccess) return fail(c, "malloc");
+  {
+    if (const char* t = getenv("HESP_SIM_THREAD")) e->sim_thread = atoi(t) != 0;
+    int tb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, sim_thread_kernel, SIMT_THREADS, 0);
+    if (tb < 1) tb = 1;
+    e->n_simt_blocks = e->sm_count * tb;
+    const int simt_warps = e->n_simt_blocks * (SIMT_THREADS / 32);
+    e->n_wbest = e->n_slots > simt_warps ? e->n_slots : simt_warps;
+  }
+  if ((c = cudaMalloc(&e->d_wbest, (size_t)e->n_wbest * sizeof(WarpBest))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc");
   if ((c = cudaMalloc(&e->d_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
   {

@@ -15,6 +15,7 @@ constexpr int MAXL = 32;      // directed links
 constexpr int MAXTYPES = 8;   // processor types
 constexpr int MAXBV = 48;     // distinct block sides with tabulated times
 constexpr int MAXPART = HESP_MAX_OPS + 2;  // clusters per candidate (slot array)
+constexpr size_t SMALL_BYTES = 2048;       // >= sizeof(hx::Small) (engine.h asserts)
 constexpr int RHT = 2048;  // per-candidate region hash (new blocks), 16-bit ids
 
 // Status codes: 0 ok, 1 + hesp::Err ordinal (errors.hpp:10-32), engine codes >= 200.
@@ -92,7 +93,7 @@ struct SlotHeader {
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
   size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
-  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack;
+  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack, small;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
@@ -226,6 +227,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.bref = take(4 * B);  // task references per candidate block (merge pruning)
   L.part = take(sizeof(PartEntry) * MAXPART);
   L.dstack = take(3 * 4 * (size_t)MAXPART);
+  L.small = take(SMALL_BYTES);  // per-candidate Small of the thread-per-candidate simulate kernel
   L.valid = take(8 * B * S);
   L.lastu = take(8 * B * S);
   L.pinu = take(8 * B * S);
