@@ -210,6 +210,10 @@ typedef struct {
   int64_t delta_bytes;
 } hesp_residency;
 
+/* hesp_trace.flags: skip the transfer / residency / event logs (and their
+ * bookkeeping), e.g. for the solver, which reads only the assignments */
+#define HESP_TRACE_SCHEDULE_ONLY 1
+
 enum { HESP_EV_TASK_START = 0, HESP_EV_TASK_END = 1, HESP_EV_XFER_START = 2, HESP_EV_XFER_END = 3 };
 /* EventRec (sim.hpp:34-39) with its strings kept structured: subject is
  * "T<id>:<KIND>:b<b>" (task events) or "B<id>" (transfer events); resource is
@@ -233,7 +237,7 @@ typedef struct {
 typedef struct {
   /* in: caller arrays and their capacities (entries) */
   int32_t cap_assign, cap_xfer, cap_res, cap_events, cap_steps;
-  int32_t pad0;
+  int32_t flags;                /* HESP_TRACE_SCHEDULE_ONLY: assignments + idle_avg + load only */
   hesp_assignment* assignments; /* task-id order (SimResult::assignments map order) */
   hesp_transfer* transfers;     /* Engine::run order: (start, block), stable */
   hesp_residency* residency;    /* (time, space, delta desc, block), stable */

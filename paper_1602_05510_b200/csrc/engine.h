@@ -335,7 +335,7 @@ struct Engine {
   // ---- full-trace logging (compiled out unless TRACE) ----
   HX void log_res(double t, int s, long long delta, int b) {  // one lane calls
     if constexpr (TRACE) {
-      if (!tb) return;
+      if (!tb || tb->lite) return;
       const int k = atomic_slot(&tb->nr);
       if (k < tb->rcap) {
         ResLog r;
@@ -352,7 +352,7 @@ struct Engine {
   HX void log_xfer(int blk, const Region* frag, long long bytes, int src, int dst, double start0, double end,
                    int nh, const double* hs, const double* he) {  // uniform: lane 0 writes
     if constexpr (TRACE) {
-      if (!tb) return;
+      if (!tb || tb->lite) return;
       if (wp.lane() == 0) {
         const int k = tb->nx++;
         if (k < tb->xcap) {
@@ -1866,7 +1866,7 @@ struct Engine {
       bool ok = true;
       NOUNROLL for (int q = 0; q < S; ++q)
         if (nonroot + (q == mainsp ? bbytes(0) : 0) > PB.cap[q]) ok = false;
-      fast = ok && !TRACE;  // the trace keeps full residency bookkeeping
+      fast = ok && (!TRACE || (tb && tb->lite));  // the full trace keeps residency bookkeeping
     }
     switch (PB.selection) {
       case SEL_EFTP: return fast ? sim_loop<SEL_EFTP, true>() : sim_loop<SEL_EFTP, false>();

@@ -385,6 +385,13 @@ struct hesp_engine {
   cudaEvent_t evc[NEV][4] = {};
   int nev_used = 0;
   hx::TraceGraph last_graph;  // candidate of the last hesp_eval_trace (for hesp_verify_trace)
+  std::vector<void*> trace_bufs;  // device buffers of hesp_eval_trace, allocated on first use
+  TraceBufs trace_tb{};
+  TraceBufs* d_trace_tb = nullptr;
+  hesp_cand_desc* d_trace_desc = nullptr;
+  int32_t* d_trace_proc = nullptr;
+  double *d_trace_start = nullptr, *d_trace_end = nullptr;
+  hesp_outcome* d_trace_out = nullptr;
 };
 
 namespace {
@@ -709,6 +716,7 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_order);
   cudaFree(e->d_sort_tmp);
   cudaFree(e->d_gen);
+  for (void* q : e->trace_bufs) cudaFree(q);
   cudaFree(e->d_wbest);
   cudaFree(e->d_best);
   cudaFree(e->d_counter);
@@ -859,33 +867,43 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
   // device log capacities: transfers and residency changes per task are few
   // (<= 3 acquires + write-back + flushes); gathers add fragments
   const int xcap = 16 * T + 1024, rcap = 32 * T + 1024;
-  std::vector<void*> owned;
-  hesp_cand_desc* dd = nullptr;
-  int32_t* dp = nullptr;
-  double *ds = nullptr, *de = nullptr;
-  hesp_outcome* dout = nullptr;
-  XferLog* dx = nullptr;
-  ResLog* dr = nullptr;
-  TraceBufs* dtb = nullptr;
-  TraceBufs tb{};
-  bool ok = dalloc(&dd, 1, owned) && dalloc(&dp, T, owned) && dalloc(&ds, T, owned) && dalloc(&de, T, owned) &&
-            dalloc(&dout, 1, owned) && dalloc(&dx, xcap, owned) && dalloc(&dr, rcap, owned) &&
-            dalloc(&tb.leaves, T, owned) && dalloc(&tb.lmeta, T, owned) && dalloc(&tb.lpoff, T, owned) &&
-            dalloc(&tb.lpcnt, T, owned) && dalloc(&tb.lpreds, P.maxedges, owned) && dalloc(&tb.bregion, B, owned) &&
-            dalloc(&tb.bisint, B, owned) && dalloc(&tb.parts, MAXPART, owned) && dalloc(&tb.tmeta, T, owned) &&
-            dalloc(&dtb, 1, owned);
+  bool ok = true;
+  if (!e->d_trace_tb) {  // first trace on this handle: allocate once, reuse after
+    std::vector<void*>& owned = e->trace_bufs;
+    TraceBufs& tb0 = e->trace_tb;
+    ok = dalloc(&e->d_trace_desc, 1, owned) && dalloc(&e->d_trace_proc, T, owned) &&
+         dalloc(&e->d_trace_start, T, owned) && dalloc(&e->d_trace_end, T, owned) &&
+         dalloc(&e->d_trace_out, 1, owned) && dalloc(&tb0.x, xcap, owned) && dalloc(&tb0.r, rcap, owned) &&
+         dalloc(&tb0.leaves, T, owned) && dalloc(&tb0.lmeta, T, owned) && dalloc(&tb0.lpoff, T, owned) &&
+         dalloc(&tb0.lpcnt, T, owned) && dalloc(&tb0.lpreds, P.maxedges, owned) && dalloc(&tb0.bregion, B, owned) &&
+         dalloc(&tb0.bisint, B, owned) && dalloc(&tb0.parts, MAXPART, owned) && dalloc(&tb0.tmeta, T, owned) &&
+         dalloc(&e->d_trace_tb, 1, owned);
+    tb0.xcap = xcap;
+    tb0.rcap = rcap;
+    tb0.leaf_cap = T;
+    tb0.pred_cap = P.maxedges;
+    tb0.block_cap = B;
+    tb0.task_cap = T;
+    if (!ok) {
+      for (void* q : owned) cudaFree(q);
+      owned.clear();
+      e->d_trace_tb = nullptr;
+      return HESP_E_CUDA;
+    }
+  }
+  hesp_cand_desc* dd = e->d_trace_desc;
+  int32_t* dp = e->d_trace_proc;
+  double *ds = e->d_trace_start, *de = e->d_trace_end;
+  hesp_outcome* dout = e->d_trace_out;
+  TraceBufs* dtb = e->d_trace_tb;
+  TraceBufs tb = e->trace_tb;  // counters zero
+  tb.lite = (tr->flags & HESP_TRACE_SCHEDULE_ONLY) ? 1 : 0;
+  XferLog* dx = tb.x;
+  ResLog* dr = tb.r;
   hesp_outcome o{};
   hx::TraceLogs logs;
   TraceBufs hb{};
   if (ok) {
-    tb.x = dx;
-    tb.r = dr;
-    tb.xcap = xcap;
-    tb.rcap = rcap;
-    tb.leaf_cap = T;
-    tb.pred_cap = P.maxedges;
-    tb.block_cap = B;
-    tb.task_cap = T;
     cudaMemcpy(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice);
     cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
     cudaMemset(dp, 0xff, (size_t)T * 4);
@@ -911,13 +929,12 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
          d2h(g.tmeta, tb.tmeta, (size_t)hb.ntasks);
     g.valid = ok;
   }
-  for (void* q : owned) cudaFree(q);
   if (!ok) return o.status ? o.status : HESP_E_CUDA;
   tr->outcome = o;
   tr->n_assign = tr->n_xfer = tr->n_res = tr->n_events = tr->n_steps = 0;
   tr->busy_time = tr->avg_load = tr->load_integral = 0.0;
   if (o.status != 0) return o.status;
-  const int r = hx::finish_trace(P, e->last_graph, logs, tr);
+  const int r = hx::finish_trace(P, e->last_graph, logs, tr, tb.lite != 0);
   if (r != HESP_OK) {
     g_last_error = "trace arrays too small (see the hesp_trace counts)";
     return r;

@@ -187,6 +187,7 @@ struct TraceBufs {
   int32_t leaf_cap, pred_cap, block_cap;
   int32_t nleaves, npreds, nblocks;
   int32_t overflow;
+  int32_t lite;  // schedule only: keep the E4 fast path, no logs
 };
 
 // Per-candidate result record (also the golden-record payload).

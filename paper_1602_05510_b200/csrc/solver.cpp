@@ -143,6 +143,7 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
       tr.residency = R.data();
       tr.events = E.data();
       tr.steps = S.data();
+      tr.flags = HESP_TRACE_SCHEDULE_ONLY;
       rc = hesp_eval_trace(e, &cur, &tr);
       if (rc != HESP_E_LIMIT) break;
       A.resize(std::max<size_t>(A.size(), tr.n_assign));

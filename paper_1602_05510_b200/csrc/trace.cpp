@@ -66,18 +66,17 @@ std::vector<std::pair<double, int>> deltas_of(const hesp_trace& tr) {
 
 }  // namespace
 
-int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr) {
-  (void)g;
+int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr, bool schedule_only) {
   // assignments in task-id order (std::map order of SimResult::assignments)
   int na = 0;
   for (size_t id = 0; id < logs.proc.size(); ++id) na += logs.proc[id] >= 0;
   // transfers: stable by (start, block) over emission order
-  std::vector<XferLog> xs = logs.xfers;
+  std::vector<XferLog> xs = schedule_only ? std::vector<XferLog>{} : logs.xfers;
   std::stable_sort(xs.begin(), xs.end(), [](const XferLog& a, const XferLog& b) {
     if (a.start != b.start) return a.start < b.start;
     return a.block < b.block;
   });
-  std::vector<ResLog> rs = logs.res;
+  std::vector<ResLog> rs = schedule_only ? std::vector<ResLog>{} : logs.res;
   std::stable_sort(rs.begin(), rs.end(), [](const ResLog& a, const ResLog& b) {
     if (a.time != b.time) return a.time < b.time;
     if (a.space != b.space) return a.space < b.space;
@@ -86,7 +85,7 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
   });
   int nhops = 0;
   for (const auto& x : xs) nhops += x.nh;
-  const int nev = 2 * na + 2 * nhops;
+  const int nev = schedule_only ? 0 : 2 * na + 2 * nhops;
   tr->n_assign = na;
   tr->n_xfer = (int32_t)xs.size();
   tr->n_res = (int32_t)rs.size();
@@ -143,7 +142,7 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
   }
   // events: every field is part of the sort key, so records that tie are
   // identical and the emission order does not matter
-  {
+  if (!schedule_only) {
     std::vector<Ev> ev;
     ev.reserve(nev);
     std::unordered_map<int, int> li;  // task id -> leaf index

@@ -32,7 +32,8 @@ struct TraceLogs {
 };
 
 // Fills the caller's hesp_trace arrays; HESP_OK or HESP_E_LIMIT.
-int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr);
+int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr,
+                 bool schedule_only = false);
 
 // verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph.
 std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr);

@@ -144,7 +144,7 @@ ACTIONS = {-1: None, 0: "Partition", 1: "Merge", 2: "Repartition"}
 
 class TraceC(C.Structure):
     _fields_ = [("cap_assign", C.c_int32), ("cap_xfer", C.c_int32), ("cap_res", C.c_int32),
-                ("cap_events", C.c_int32), ("cap_steps", C.c_int32), ("pad0", C.c_int32),
+                ("cap_events", C.c_int32), ("cap_steps", C.c_int32), ("flags", C.c_int32),
                 ("assignments", C.c_void_p), ("transfers", C.c_void_p), ("residency", C.c_void_p),
                 ("events", C.c_void_p), ("steps", C.c_void_p),
                 ("n_assign", C.c_int32), ("n_xfer", C.c_int32), ("n_res", C.c_int32), ("n_events", C.c_int32),
