@@ -321,6 +321,15 @@ typedef struct {
 int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfg,
                hesp_solver_result* out);
 
+/* Cross-GPU winner: every rank passes its own batch
+ * best; on return `best` holds the exact lexicographic (makespan, lowest
+ * global index) argmin over all ranks of `nccl_comm` and the summed work
+ * counters.  Two int64 MIN all-reduces (positive doubles order like their
+ * bit patterns) + one int64 SUM, on the engine's stream, over the caller's
+ * communicator (an ncclComm_t created by any NCCL in the process, e.g.
+ * PyTorch's).  NCCL is resolved at run time (libnccl.so.2), not linked. */
+int hesp_min_reduce(hesp_engine* e, void* nccl_comm, hesp_best* best);
+
 /* Engine facts: kernel launches issued so far, base tiling sizes, slots. */
 typedef struct {
   int64_t kernel_launches;

@@ -34,7 +34,7 @@ def nvcc_command(out: str = LIB, verbose_ptxas: bool = False) -> list[str]:
         "-O3", "-lineinfo", "--fmad=false", "-std=c++17",
         "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
         "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-        "-shared", "-o", out,
+        "-shared", "-o", out, "-ldl",
     ]
     if verbose_ptxas:
         cmd += ["-Xptxas", "-v"]

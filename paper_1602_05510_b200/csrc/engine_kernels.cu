@@ -12,6 +12,7 @@
 // The multi-GPU min-reduce over NVLink (K3) lives in the host driver
 // (paper_1602_05510_b200/engine.py) on 16 bytes per rank.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -966,6 +967,98 @@ int hesp_verify_trace(const hesp_engine* e, const hesp_trace* tr, char* buf, siz
     std::memcpy(buf, all.data(), n);
     buf[n] = 0;
   }
+  return HESP_OK;
+}
+
+}  // extern "C"
+
+namespace {
+// NCCL entry points resolved at run time: the process's libnccl.so.2 (the one
+// that created the caller's communicator) or the system one.
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+typedef const char* (*nccl_errstr_fn)(int);
+struct NcclApi {
+  nccl_allreduce_fn allreduce = nullptr;
+  nccl_errstr_fn errstr = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      a.allreduce = (nccl_allreduce_fn)dlsym(h, "ncclAllReduce");
+      a.errstr = (nccl_errstr_fn)dlsym(h, "ncclGetErrorString");
+    }
+    a.ok = a.allreduce != nullptr;
+    return a;
+  }();
+  return api;
+}
+constexpr int NCCL_INT64 = 4, NCCL_SUM = 0, NCCL_MIN = 3;  // nccl.h ncclDataType_t / ncclRedOp_t
+
+__global__ void winner_keys(long long* buf) {  // buf[0] = makespan key, buf[1] = index (in/out)
+  // second round: keep the index only where this rank holds the global key
+  if (threadIdx.x == 0 && buf[2] != buf[0]) buf[1] = 0x7fffffffffffffffLL;
+}
+}  // namespace
+
+extern "C" {
+
+int hesp_min_reduce(hesp_engine* e, void* comm, hesp_best* best) {
+  if (!e || !comm || !best) return HESP_E_INVALID;
+  NcclApi& api = nccl_api();
+  if (!api.ok) {
+    g_last_error = "hesp_min_reduce: libnccl.so.2 not found";
+    return HESP_E_INVALID;
+  }
+  cudaSetDevice(e->device);
+  const long long NONE = 0x7fffffffffffffffLL;
+  long long h[10];
+  long long key;
+  std::memcpy(&key, &best->makespan, 8);
+  h[0] = best->index >= 0 ? key : NONE;   // global min key goes here
+  h[1] = best->index >= 0 ? best->index : NONE;
+  h[2] = h[0];                            // this rank's key (kept)
+  h[3] = best->n_ok;
+  h[4] = best->n_evaluated;
+  h[5] = best->sum_leaves;
+  h[6] = best->sum_k;
+  h[7] = best->sum_edges;
+  long long* d = nullptr;
+  if (!ck(cudaMalloc(&d, sizeof h), "malloc reduce")) return HESP_E_CUDA;
+  cudaStream_t st = e->stream;
+  int r = 0;
+  bool ok = ck(cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, st), "reduce H2D");
+  if (ok) r = api.allreduce(d, d, 1, NCCL_INT64, NCCL_MIN, comm, st);           // 1: min key
+  if (ok && r == 0) {
+    winner_keys<<<1, 32, 0, st>>>(d);                                         // index only on the holders
+    e->launches += 1;
+    r = api.allreduce(d + 1, d + 1, 1, NCCL_INT64, NCCL_MIN, comm, st);         // 2: lowest index
+  }
+  if (ok && r == 0) r = api.allreduce(d + 3, d + 3, 5, NCCL_INT64, NCCL_SUM, comm, st);  // counters
+  if (ok && r != 0) {
+    g_last_error = std::string("ncclAllReduce: ") + (api.errstr ? api.errstr(r) : "error");
+    ok = false;
+  }
+  ok = ok && ck(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st), "reduce D2H") &&
+       ck(cudaStreamSynchronize(st), "reduce sync");
+  cudaFree(d);
+  if (!ok) return r ? HESP_E_INVALID : HESP_E_CUDA;
+  if (h[0] == NONE) {
+    best->index = -1;
+    best->makespan = 0.0;
+  } else {
+    std::memcpy(&best->makespan, &h[0], 8);
+    best->index = h[1];
+  }
+  best->n_ok = h[3];
+  best->n_evaluated = h[4];
+  best->sum_leaves = h[5];
+  best->sum_k = h[6];
+  best->sum_edges = h[7];
   return HESP_OK;
 }
 

@@ -46,3 +46,28 @@ def global_best(makespan: float, index: int, device="cpu", group=None) -> tuple[
     u = torch.tensor([mine], dtype=torch.int64, device=device)
     dist.all_reduce(u, op=dist.ReduceOp.MIN, group=group)
     return float(np.int64(gkey).view(np.float64)), int(u.item())
+
+
+def nccl_comm_ptr(group=None) -> int:
+    """Raw ncclComm_t of a NCCL process group (0 if the communicator does not
+    exist yet: it is created by the group's first collective)."""
+    import torch
+    import torch.distributed as dist
+    pg = group or dist.group.WORLD
+    backend = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+    return int(backend._comm_ptr())
+
+
+def engine_global_best(eng, best, group=None):
+    """K3 through the engine's C ABI: hesp_min_reduce over the process group's
+    own NCCL communicator (NVLink/NVSwitch on one node).  Returns
+    (makespan, index) like global_best, plus the all-rank hesp_best."""
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return (best.makespan, best.index) if best.index >= 0 else (float("nan"), -1), best
+    comm = nccl_comm_ptr(group)
+    if not comm:
+        dist.barrier(group=group)  # creates the communicator
+        comm = nccl_comm_ptr(group)
+    g = eng.min_reduce(comm, best)
+    return (g.makespan, g.index) if g.index >= 0 else (float("nan"), -1), g

@@ -191,7 +191,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_min_reduce",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -223,6 +223,7 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
+    lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
     lib.hesp_verify_trace.argtypes = [C.c_void_p, C.POINTER(TraceC), C.c_char_p, C.c_size_t,
                                       C.POINTER(C.c_int32)]
     lib.hesp_engine_destroy.argtypes = [C.c_void_p]
@@ -474,6 +475,13 @@ class BatchEngine:
         best = np.frombuffer(bytes(res.best), DESC_DTYPE)[0].copy()
         return hist[:res.n_history].copy(), best, float(res.best_makespan), int(res.best_iteration), \
             int(res.n_simulated)
+
+    def min_reduce(self, nccl_comm: int, best: Best) -> Best:
+        """hesp_min_reduce: the exact cross-rank winner over an ncclComm_t (K3)."""
+        b = Best()
+        C.memmove(C.byref(b), C.byref(best), C.sizeof(Best))
+        self._check(self.lib.hesp_min_reduce(self.h, C.c_void_p(nccl_comm), C.byref(b)), "min_reduce")
+        return b
 
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)

@@ -7,7 +7,7 @@
 Each rank takes a disjoint, contiguous share of the candidate index range
 (`dist.shard`), generates and evaluates it on its own GPU in device batches
 (no descriptors cross PCIe), and keeps its best (makespan, index).  The only
-exchange is the final winner: `dist.global_best`, two 8-byte MIN all-reduces
+exchange is the final winner: `hesp_min_reduce` (C ABI), two 8-byte MIN all-reduces
 over NCCL.  Rank 0 prints one JSON line; with --trace-winner it re-simulates
 the winner with the full trace (hesp_eval_trace) and runs verify_schedule.
 """
@@ -33,7 +33,7 @@ def main(argv=None) -> int:
     import torch.distributed as dist
 
     from .configs import CONFIGS, PARITY, make_engine
-    from .dist import global_best, shard
+    from .dist import engine_global_best, shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -67,7 +67,10 @@ def main(argv=None) -> int:
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
         t = torch.cat([tmax, tsum])
     wall, ok_all, ev_all = float(t[0]), int(t[1]), int(t[2])
-    gmk, gidx = global_best(best_mk, best_idx, device="cuda")
+    from .engine import Best
+    mine = Best()
+    mine.makespan, mine.index = (best_mk, best_idx) if best_idx >= 0 else (0.0, -1)
+    (gmk, gidx), _ = engine_global_best(eng, mine)  # hesp_min_reduce over NCCL
     if rank == 0:
         line = {"config": args.config, "candidates": args.candidates, "n_gpus": world, "evaluated": ev_all,
                 "valid": ok_all, "seconds_max_over_ranks": wall, "schedules_per_s": ev_all / wall,

@@ -116,3 +116,54 @@ def test_search_driver_matches_batch_best(lib, capsys):
     _, b = make_engine(p).eval_generated(0, 3000, outcomes=False)
     assert line["best"]["index"] == b.index and line["best"]["makespan"] == b.makespan
     assert line["valid"] == b.n_ok and line["winner_trace"]["verify_violations"] == 0
+
+
+def test_min_reduce_over_nccl_single_rank(lib):
+    """hesp_min_reduce (the C-ABI cross-GPU winner, K3) over a real one-rank
+    NCCL communicator: the winner and the counters come back unchanged."""
+    import ctypes as C
+    import torch  # noqa: F401  (loads the process's libnccl.so.2, as in bench.py)
+    nccl = C.CDLL("libnccl.so.2")
+    comm = C.c_void_p()
+    dev = (C.c_int * 1)(0)
+    assert nccl.ncclCommInitAll(C.byref(comm), 1, dev) == 0
+    try:
+        p, _ = PARITY["c2"]
+        eng = make_engine(p)
+        _, b = eng.eval_generated(0, 64, outcomes=False)
+        r = eng.min_reduce(comm.value, b)
+        assert (r.makespan, r.index, r.n_ok, r.n_evaluated, r.sum_leaves) == \
+            (b.makespan, b.index, b.n_ok, b.n_evaluated, b.sum_leaves)
+        from paper_1602_05510_b200.engine import Best
+        empty = Best()
+        empty.index = -1
+        r2 = eng.min_reduce(comm.value, empty)
+        assert r2.index == -1
+    finally:
+        nccl.ncclCommDestroy(comm)
+
+
+def test_min_reduce_over_torch_process_group(lib):
+    """bench.py / search.py path at N>1, exercised at world size 1: the
+    communicator of a real NCCL process group handed to hesp_min_reduce."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_1602_05510_b200.dist import engine_global_best
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        dist.barrier()
+        p, _ = PARITY["c2"]
+        eng = make_engine(p)
+        _, b = eng.eval_generated(0, 64, outcomes=False)
+        from paper_1602_05510_b200.dist import nccl_comm_ptr
+        assert nccl_comm_ptr() != 0
+        g = eng.min_reduce(nccl_comm_ptr(), b)
+        assert (g.makespan, g.index, g.n_ok) == (b.makespan, b.index, b.n_ok)
+        (mk, idx), _ = engine_global_best(eng, b)
+        assert (mk, idx) == (b.makespan, b.index)
+    finally:
+        dist.destroy_process_group()
