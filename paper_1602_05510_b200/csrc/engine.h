@@ -278,6 +278,7 @@ struct Engine {
   HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - nbb
   HX PartEntry* part() const { return (PartEntry*)(slot + PB.lay.part); }  // clusters, by id
   HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
+  HX uint8_t* tmis() const { return (uint8_t*)(slot + PB.lay.tmis); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -505,6 +506,16 @@ struct Engine {
     return id;
   }
 
+  // r is a dyadic square of base tile t: side = tile side / 2^k at an offset
+  // that is a multiple of the side.  Two dyadic squares of one tile are
+  // nested or disjoint, never partially overlapping.
+  HX bool dyadic(const Region& r, int t) const {
+    const Region T = reg(t);
+    if (r.rows != r.cols || r.rows <= 0 || T.rows % r.rows) return false;
+    const int q = T.rows / r.rows;
+    return (q & (q - 1)) == 0 && (r.row - T.row) % r.rows == 0 && (r.col - T.col) % r.cols == 0;
+  }
+
   HXN int get_or_create(const Region& r, int t) {  // graph.cpp:191-212
     const int ex = find_block(r, t);
     if (ex >= 0) return ex;
@@ -512,7 +523,13 @@ struct Engine {
     if (id < 0) return -1;
     // Partial overlaps with existing non-intersection blocks get an
     // intersection descriptor (id order).  Inside tile t only the tile's own
-    // blocks can partially overlap r (root and tile contain it).
+    // blocks can partially overlap r (root and tile contain it), and none can
+    // while every block of the tile (r included) is dyadic: skip the scan.
+    if (t >= 0) {
+      if (dyadic(r, t) && !tmis()[t]) return id;
+      if (wp.lane() == 0) tmis()[t] = 1;
+      wp.sync();
+    }
     int nsect = 0;
     const int lo = t < 0 ? 0 : nbb;
     NOUNROLL for (int base = lo; base < id; base += WP::W) {
@@ -2511,6 +2528,7 @@ struct Engine {
 
   // Starts from the base tiling (root + base cluster, shared tables).
   HXN void reset_to_base() {
+    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tmis()[i] = 0;
     NOUNROLL for (int i = wp.lane(); i < RHT / 2; i += WP::W) ((uint32_t*)rht())[i] = 0xffffffffu;
     wp.sync();
     status = 0;
