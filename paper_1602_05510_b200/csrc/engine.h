@@ -279,6 +279,7 @@ struct Engine {
   HX PartEntry* part() const { return (PartEntry*)(slot + PB.lay.part); }  // clusters, by id
   HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
   HX uint8_t* tmis() const { return (uint8_t*)(slot + PB.lay.tmis); }
+  HX uint8_t* wrt() const { return (uint8_t*)(slot + PB.lay.wrt); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -1734,7 +1735,7 @@ struct Engine {
         const Region fr = gs_reg2()[f];
         bool hit = false;
         for_scope(t, [&](int x) {
-          if ((bflags()[x] >> 16) & 1u)
+          if (wrt()[x])
             if (roverlap(fr, reg(x))) hit = true;
         });
         bad = wp.any(hit);
@@ -1909,6 +1910,7 @@ struct Engine {
         }
       }
       bflags()[x] = x == 0 ? (1u << mainsp) : 0u;
+      wrt()[x] = 0;
     }
     NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
     if (TRACE && wp.lane() == 0) log_res(0.0, mainsp, bbytes(0), 0);  // init_memory (sim.cpp:333)
@@ -2429,7 +2431,7 @@ struct Engine {
           }
           Vr(out, s) = end;
         }
-        BF[out] |= 1u << 16;  // written (gather's coherence check)
+        HOT_ARR(uint8_t, wrt)[out] = 1;  // written (gather's coherence check): a plain store
         if (s != ms) {
           if (PB.caching == CACHE_WB) {
             if (!fst) set_flag(out, 1u << (8 + s), true);
