@@ -91,6 +91,11 @@ struct HostWarp {
     *p += v;
     return o;
   }
+  HHD int exch(int* p, int v) const {
+    int o = *p;
+    *p = v;
+    return o;
+  }
   // per-lane owned vectors (device: one register per lane; host: the array)
   struct LaneD {
     double a[32];
@@ -191,6 +196,7 @@ struct DevWarp {
     id = w;
   }
   __device__ __forceinline__ int atomic_add(int* p, int v) const { return atomicAdd(p, v); }
+  __device__ __forceinline__ int exch(int* p, int v) const { return atomicExch(p, v); }
   struct LaneD {
     double v;
     __device__ __forceinline__ double get(int i) const { return __shfl_sync(FULL, v, i); }
@@ -280,6 +286,7 @@ struct Engine {
   HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
   HX uint8_t* tmis() const { return (uint8_t*)(slot + PB.lay.tmis); }
   HX uint8_t* wrt() const { return (uint8_t*)(slot + PB.lay.wrt); }
+  HX int32_t* pmk() const { return (int32_t*)(slot + PB.lay.pmk); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
   HX double* valid() const { return (double*)(slot + PB.lay.valid); }
@@ -1078,6 +1085,8 @@ struct Engine {
   HXN void build_deps() {
     int rn_used = 0;
     nedges = 0;
+    NOUNROLL for (int i = wp.lane(); i < ntasks; i += WP::W) pmk()[i] = -1;
+    wp.sync();
     // ---- pass 0 (parallel): classify leaves, take base preds for the fast ones
     int nslow = 0;
     int* const slow = gs_b();
@@ -1167,10 +1176,16 @@ struct Engine {
         const int w = c1 - c0;
         const int ncells = (r1 - r0) * w;
         const int cbase = tl_coff()[tt];
+        const float rw = 1.0f / (float)w;  // q / w via a corrected float reciprocal (q < 2^20)
         NOUNROLL for (int base = 0; base < ncells; base += WP::W) {
           const int q = base + wp.lane();
           int cell = -1;
-          if (q < ncells) cell = cbase + (r0 + q / w) * nc + (c0 + q % w);
+          if (q < ncells) {
+            int rq = (int)((float)q * rw);
+            if (rq * w > q) --rq;
+            else if ((rq + 1) * w <= q) ++rq;
+            cell = cbase + (r0 + rq) * nc + (c0 + (q - rq * w));
+          }
           // last writer
           int wr = cell >= 0 ? c_writer()[cell] : -1;
           bool e = wr >= 0 && wr != j;
@@ -1226,12 +1241,9 @@ struct Engine {
         int v = -1;
         if (q < npb) {
           v = pbuf()[q];
-          keep = true;
-          NOUNROLL for (int z = 0; z < q; ++z)
-            if (pbuf()[z] == v) {
-              keep = false;
-              break;
-            }
+          // first claimant of predecessor v for task j keeps it (marks were
+          // cleared at the start of build_deps, so a stale j cannot match)
+          keep = wp.exch(&pmk()[v], j) != j;
         }
         const unsigned mk = wp.ballot(keep);
         if (keep) {
@@ -1978,7 +1990,6 @@ struct Engine {
         j = LF[li];
         TState& st = T[j];
         st.rel = 0.0;
-        st.flag = 0;
         z = st.missing == 0;
         key = pl ? st.ct : 0.0;
       }
@@ -2373,8 +2384,8 @@ struct Engine {
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
         // ---------------- commit (sim.cpp:592-668) ----------------
-        const int s = PB.proc_space[p];
-        const int type = PB.proc_type[p];
+        const int s = sm->pspace[p];
+        const int type = PTYPE(p);
         if (!fst) {
           long long wset = 0;
           NOUNROLL for (int k = 0; k < nw; ++k) wset += bytesof(w[k]);
@@ -2444,7 +2455,6 @@ struct Engine {
         }
         // release successors (sim.cpp:660-667): running max of pred ends;
         // released tasks enter the pool with release time and key inline
-        T[j].flag = 1;
         const int off = T[j].soff, cnt = T[j].scnt;
         int added = 0;
         NOUNROLL for (int base = 0; base < cnt; base += WP::W) {

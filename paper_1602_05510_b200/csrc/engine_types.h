@@ -66,7 +66,7 @@ struct TState {
   double ct;        // critical time (PL) / best successor ct while building
   int32_t missing;  // predecessors not yet committed
   int32_t soff, scnt;  // successor list (CSR)
-  int32_t flag;     // committed
+  int32_t pad;      // (a committed flag here cost a store per commit; nothing read it)
 };
 
 // Host-precomputed predecessors of a base task (E5): the deduplicated union
@@ -93,7 +93,7 @@ struct SlotHeader {
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
   size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
-  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack, small, tmis, wrt;
+  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack, small, tmis, wrt, pmk;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
@@ -231,6 +231,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.small = take(SMALL_BYTES);  // per-candidate Small of the thread-per-candidate simulate kernel
   L.tmis = take(NB);            // per base tile: holds a non-dyadic block (partial overlaps possible)
   L.wrt = take(B);              // per block: written since t=0 (gather's coherence check)
+  L.pmk = take(4 * T);          // per task: last task whose predecessor list took it (dedup)
   L.valid = take(8 * B * S);
   L.lastu = take(8 * B * S);
   L.pinu = take(8 * B * S);
