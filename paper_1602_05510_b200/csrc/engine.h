@@ -2066,6 +2066,7 @@ struct Engine {
     };
     // cold-call bracket: hand the uniform hot state to the member paths and back
     auto cold_in = [&]() {
+      now = tnow;
       wp.sync();
       xhash += HXH;
       HXH = 0;
@@ -2172,8 +2173,7 @@ struct Engine {
         }
         nx = wp.mind(nx);
         if (nx == ABSENT) return fail(ST_INTERNAL);  // scheduler stalled
-        tnow = nx;
-        now = nx;
+        tnow = nx;  // the member `now` is only read by the cold paths: set in cold_in
       }
       first = false;
       // ready = released, uncommitted, rel <= now, ordered FCFS (rel asc, id
