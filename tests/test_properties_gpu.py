@@ -85,3 +85,26 @@ def test_schedules_verify_and_respect_work_bound(lib, name):
         assert tr.busy_time <= P * tr.makespan * (1 + 1e-12)
         checked += 1
     assert checked > 0
+
+
+@pytest.mark.parametrize("name,count", [("c2", 20000), ("c4", 2000), ("evict_wa", 2000), ("sect_cpugpu", 5000),
+                                        ("merge_c2", 5000), ("policy_FCFS_R-P_WT", 5000)])
+def test_warp_and_scalar_engines_agree_at_scale(lib, name, count):
+    """Two independent device code paths over the same candidates: the
+    warp-parallel simulate kernel (lanes = processors, (block, space) EFT
+    lanes, redux argmins) and the width-1 thread-per-candidate kernel (the
+    reference's loops as written) must produce bit-identical outcome records
+    for every candidate -- a full-scale check beyond the golden sizes."""
+    import os
+    from paper_1602_05510_b200.configs import CONFIGS
+    p = (PARITY.get(name) or (CONFIGS[name.upper()], 0))[0]
+    warp = make_engine(p)
+    os.environ["HESP_SIM_THREAD"] = "1"
+    try:
+        scalar = make_engine(p)
+    finally:
+        del os.environ["HESP_SIM_THREAD"]
+    a, ba = warp.eval_generated(123_000, count)
+    b, bb = scalar.eval_generated(123_000, count)
+    assert a.tobytes() == b.tobytes()
+    assert (ba.makespan, ba.index, ba.n_ok) == (bb.makespan, bb.index, bb.n_ok)
