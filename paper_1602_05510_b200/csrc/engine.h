@@ -1921,7 +1921,7 @@ struct Engine {
           PIN(x, q) = NOPIN;
         }
       }
-      bflags()[x] = x == 0 ? (1u << mainsp) : 0u;
+      if (!fast) bflags()[x] = x == 0 ? (1u << mainsp) : 0u;  // read only by eviction bookkeeping
       wrt()[x] = 0;
     }
     NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
