@@ -316,6 +316,16 @@ typedef struct {
   int64_t n_simulated;        /* device simulations issued (states + candidate batches) */
 } hesp_solver_result;
 
+/* choose_p (solver.hpp:59-62): p = 1/k, k = clamp(ceil(sqrt(I+1)) + 1, 2,
+ * min(k_max, d/min_block)) snapped down to a divisor grid of d; 0.0 when
+ * d < 2*min_block or no grid exists (GrainTooSmall). */
+double hesp_choose_p(double idle_avg, int64_t d, int64_t min_block, int32_t k_max);
+
+/* select_candidate (solver.hpp:78-80): Hard = index of the maximum score
+ * (first on ties); Soft = score-proportional draw with hesp::Rng, whose
+ * splitmix64 state *rng_state advances.  -1 for an empty list. */
+int32_t hesp_select_candidate(const double* scores, int32_t n, int32_t sampling, uint64_t* rng_state);
+
 /* Runs solve() from `initial` (NULL = the base tiling).  Returns 0, the
  * status of a failing initial state, or a negative HESP_E_* code. */
 int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfg,

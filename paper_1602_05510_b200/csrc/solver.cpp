@@ -62,6 +62,16 @@ int64_t snap_tiling(int64_t d, int64_t k, int64_t min_block) {
   return 0;
 }
 
+// choose_p (solver.hpp:59-62) as a tile count: k = clamp(ceil(sqrt(I+1)) + 1,
+// 2, min(k_max, d/min_block)), snapped down to a divisor grid; 0 = GrainTooSmall
+int64_t choose_tiles(double idle, int64_t d, int64_t min_block, int64_t k_max) {
+  if (d < 2 * min_block) return 0;
+  const int64_t lim = std::min<int64_t>(k_max, d / min_block);
+  int64_t k = (int64_t)std::ceil(std::sqrt(idle + 1.0)) + 1;
+  k = std::max<int64_t>(2, std::min(k, lim));
+  return snap_tiling(d, k, min_block);
+}
+
 struct Ctx {
   const Problem& p;
   const hesp_solver_config& cfg;
@@ -76,15 +86,7 @@ struct Ctx {
       }
     return false;
   }
-  // choose_p (solver.hpp:59-62): k = clamp(ceil(sqrt(I+1)) + 1, 2, min(k_max, d/min_block)),
-  // snapped down to a divisor grid; 0 = GrainTooSmall / no grid
-  int64_t choose_k(double idle, int64_t d) const {
-    if (d < 2 * cfg.min_block) return 0;
-    const int64_t lim = std::min<int64_t>(cfg.k_max, d / cfg.min_block);
-    int64_t k = (int64_t)std::ceil(std::sqrt(idle + 1.0)) + 1;
-    k = std::max<int64_t>(2, std::min(k, lim));
-    return snap_tiling(d, k, cfg.min_block);
-  }
+  int64_t choose_k(double idle, int64_t d) const { return choose_tiles(idle, d, cfg.min_block, cfg.k_max); }
   // W_sub: sum of the would-be sub-task times on one processor type, in emission order
   bool w_sub(int kind, int64_t d, int64_t k, int type, double* w) const {
     double sum = 0;
@@ -99,7 +101,41 @@ struct Ctx {
   }
 };
 
+// select_candidate over scores in candidate order (shared by hesp_solve)
+size_t select_index(const double* sc, size_t n, int sampling, Rng& rng) {
+  size_t pick = 0;
+  if (sampling == HESP_SAMPLE_HARD) {
+    for (size_t i = 1; i < n; ++i)
+      if (sc[i] > sc[pick]) pick = i;
+    return pick;
+  }
+  double total = 0;
+  for (size_t i = 0; i < n; ++i) total += sc[i];
+  const double u = rng.uniform() * total;
+  double acc = 0;
+  pick = n - 1;
+  for (size_t i = 0; i < n; ++i) {
+    acc += sc[i];
+    if (u < acc) return i;
+  }
+  return pick;
+}
+
 }  // namespace
+
+extern "C" double hesp_choose_p(double idle_avg, int64_t d, int64_t min_block, int32_t k_max) {
+  if (k_max < 2 || min_block < 1) return 0.0;
+  const int64_t k = choose_tiles(idle_avg, d, min_block, k_max);
+  return k ? 1.0 / (double)k : 0.0;
+}
+
+extern "C" int32_t hesp_select_candidate(const double* scores, int32_t n, int32_t sampling, uint64_t* rng_state) {
+  if (n <= 0 || !scores || !rng_state) return -1;
+  Rng rng{*rng_state};
+  const size_t i = select_index(scores, (size_t)n, sampling, rng);
+  *rng_state = rng.s;
+  return (int32_t)i;
+}
 
 extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfgp,
                           hesp_solver_result* out) {
@@ -311,24 +347,9 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
     rec.n_valid = (int32_t)valid.size();
     if (!valid.empty()) {
       // ---- select_candidate ----
-      size_t pick = 0;
-      if (cfg.sampling == HESP_SAMPLE_HARD) {
-        for (size_t i = 1; i < valid.size(); ++i)
-          if (valid[i].score > valid[pick].score) pick = i;
-      } else {
-        double total = 0;
-        for (const auto& c : valid) total += c.score;
-        const double u = rng.uniform() * total;
-        double acc = 0;
-        pick = valid.size() - 1;
-        for (size_t i = 0; i < valid.size(); ++i) {
-          acc += valid[i].score;
-          if (u < acc) {
-            pick = i;
-            break;
-          }
-        }
-      }
+      std::vector<double> sc(valid.size());
+      for (size_t i = 0; i < valid.size(); ++i) sc[i] = valid[i].score;
+      const size_t pick = select_index(sc.data(), sc.size(), cfg.sampling, rng);
       const Cand& c = valid[pick];
       rec.action = c.action;
       rec.target = c.target;

@@ -191,7 +191,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_min_reduce",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -224,6 +224,10 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
     lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
+    lib.hesp_choose_p.restype = C.c_double
+    lib.hesp_choose_p.argtypes = [C.c_double, C.c_int64, C.c_int64, C.c_int32]
+    lib.hesp_select_candidate.restype = C.c_int32
+    lib.hesp_select_candidate.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
     lib.hesp_verify_trace.argtypes = [C.c_void_p, C.POINTER(TraceC), C.c_char_p, C.c_size_t,
                                       C.POINTER(C.c_int32)]
     lib.hesp_engine_destroy.argtypes = [C.c_void_p]

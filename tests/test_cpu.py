@@ -195,3 +195,33 @@ def test_trace_golden_post_passes(name):
         busy += e - s
     assert hbits(busy) == g["busy"]
     assert len(g["events"]) == 2 * len(asg) + 2 * sum(len(x[7]) for x in g["transfers"])
+
+
+# ---- solver primitives through the C ABI (no device needed) ----
+def test_choose_p_spec_examples():
+    """SPEC.md choose_p examples (I=0 -> p=0.5, I=8 -> 0.25, I=24 & k_max=4 -> 0.25),
+    GrainTooSmall, and snapping down to a divisor grid."""
+    lib = load_library()
+    assert lib.hesp_choose_p(0.0, 1024, 64, 8) == 0.5
+    assert lib.hesp_choose_p(8.0, 1024, 64, 8) == 0.25
+    assert lib.hesp_choose_p(24.0, 1024, 64, 4) == 0.25
+    assert lib.hesp_choose_p(0.0, 100, 64, 8) == 0.0          # d < 2*min_block
+    assert lib.hesp_choose_p(15.0, 768, 64, 8) == 1.0 / 4     # k = 5 -> snapped to 4 (768 % 5 != 0)
+    assert lib.hesp_choose_p(48.0, 768, 64, 8) == 1.0 / 8     # k = 8, 768/8 = 96
+
+
+def test_select_candidate_hard_and_soft_law():
+    """SPEC.md select_candidate: Hard = max score, first on ties; Soft draws
+    follow score / sum within +-0.01 over 1e5 draws (acceptance criterion 12)."""
+    import ctypes as C
+    lib = load_library()
+    st = C.c_uint64(7)
+    sc = np.array([1.0, 3.0, 3.0, 0.5])
+    assert lib.hesp_select_candidate(sc.ctypes.data, 4, 0, C.byref(st)) == 1
+    assert st.value == 7  # Hard draws nothing
+    sc = np.array([3.0, 1.0])
+    counts = np.zeros(2)
+    for _ in range(100_000):
+        counts[lib.hesp_select_candidate(sc.ctypes.data, 2, 1, C.byref(st))] += 1
+    assert abs(counts[0] / 1e5 - 0.75) < 0.01
+    assert lib.hesp_select_candidate(sc.ctypes.data, 0, 1, C.byref(st)) == -1
