@@ -277,7 +277,11 @@ int hesp_verify_trace(const hesp_engine* e, const hesp_trace* trace, char* buf, 
  * score, first in candidate order on ties; Soft: score-proportional draw
  * from hesp::Rng).  DESIGN.md §10 states the decisions the SPEC leaves open. */
 enum { HESP_SEL_ALL = 0, HESP_SEL_CP = 1, HESP_SEL_SHALLOW = 2 };
-enum { HESP_SAMPLE_HARD = 0, HESP_SAMPLE_SOFT = 1 };
+/* HESP_SAMPLE_EXACT (an extension, not in SPEC): the validity batch already
+ * simulated every candidate mutation, so pick the one with the smallest
+ * simulated makespan (first in candidate order on ties); `score` then
+ * records that makespan. */
+enum { HESP_SAMPLE_HARD = 0, HESP_SAMPLE_SOFT = 1, HESP_SAMPLE_EXACT = 2 };
 enum { HESP_ACT_NONE = -1, HESP_ACT_PARTITION = 0, HESP_ACT_MERGE = 1, HESP_ACT_REPARTITION = 2 };
 
 typedef struct {              /* SolverConfig, solver.hpp:20-28 */

@@ -141,7 +141,7 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
                           hesp_solver_result* out) {
   if (!e || !cfgp || !out || cfgp->iterations < 0 || cfgp->k_max < 2 || cfgp->overhead_factor < 1.0 ||
       cfgp->min_block < 1 || cfgp->task_selection < 0 || cfgp->task_selection > 2 || cfgp->sampling < 0 ||
-      cfgp->sampling > 1)
+      cfgp->sampling > 2)
     return HESP_E_INVALID;
   if (out->cap_history < cfgp->iterations || (!out->history && cfgp->iterations > 0)) return HESP_E_INVALID;
   const Problem& P = hesp_engine_problem(e);
@@ -342,14 +342,23 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
       if (r != 0) return r;
       out->n_simulated += (int64_t)cands.size();
       for (size_t i = 0; i < cands.size(); ++i)
-        if (outc[i].status == 0) valid.push_back(cands[i]);
+        if (outc[i].status == 0) {
+          valid.push_back(cands[i]);
+          if (cfg.sampling == HESP_SAMPLE_EXACT) valid.back().score = outc[i].makespan;
+        }
     }
     rec.n_valid = (int32_t)valid.size();
     if (!valid.empty()) {
       // ---- select_candidate ----
       std::vector<double> sc(valid.size());
       for (size_t i = 0; i < valid.size(); ++i) sc[i] = valid[i].score;
-      const size_t pick = select_index(sc.data(), sc.size(), cfg.sampling, rng);
+      size_t pick = 0;
+      if (cfg.sampling == HESP_SAMPLE_EXACT) {
+        for (size_t i = 1; i < sc.size(); ++i)
+          if (sc[i] < sc[pick]) pick = i;
+      } else {
+        pick = select_index(sc.data(), sc.size(), cfg.sampling, rng);
+      }
       const Cand& c = valid[pick];
       rec.action = c.action;
       rec.target = c.target;

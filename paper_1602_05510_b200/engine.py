@@ -138,7 +138,7 @@ class SolverResultC(C.Structure):
 
 
 TASK_SELECTION = {"All": 0, "CP": 1, "Shallow": 2}
-SAMPLING = {"Hard": 0, "Soft": 1}
+SAMPLING = {"Hard": 0, "Soft": 1, "Exact": 2}
 ACTIONS = {-1: None, 0: "Partition", 1: "Merge", 2: "Repartition"}
 
 

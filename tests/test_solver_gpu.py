@@ -45,3 +45,16 @@ def test_solver_best_state_reproduces(lib):
     hist, best, best_mk, best_it, _ = eng.solve(8, "CP", "Soft", 3)
     out, b = eng.eval_descs(np.array([best]))
     assert int(out[0]["status"]) == 0 and hbits(out[0]["makespan"]) == hbits(best_mk)
+
+
+def test_exact_lookahead_mode(lib):
+    """HESP_SAMPLE_EXACT: each applied mutation is the batch's best simulated
+    makespan, so the next state's traced makespan equals the recorded score
+    (trace kernel and batch kernels agree on the same descriptor)."""
+    p, _ = PARITY["c2"]
+    eng = make_engine(p)
+    hist, best, best_mk, best_it, _ = eng.solve(6, "All", "Exact", 0)
+    for i in range(len(hist) - 1):
+        if hist[i]["action"] >= 0:
+            assert hist[i + 1]["makespan"] == hist[i]["score"]
+    assert best_mk == min(hist["makespan"])
