@@ -225,3 +225,12 @@ def test_select_candidate_hard_and_soft_law():
         counts[lib.hesp_select_candidate(sc.ctypes.data, 2, 1, C.byref(st))] += 1
     assert abs(counts[0] / 1e5 - 0.75) < 0.01
     assert lib.hesp_select_candidate(sc.ctypes.data, 0, 1, C.byref(st)) == -1
+
+
+def test_reference_merge_round_trip_in_goldens():
+    """SPEC acceptance 3 on the reference itself: partition then merge is the
+    original graph -- the golden record of [(18, 2), merge 1] equals the base
+    tiling's, hashes included."""
+    a = read_golden("explicit_merge_c2")[0]
+    b = read_golden("explicit_c2")[0]
+    assert a.tobytes()[8:] == b.tobytes()[8:]

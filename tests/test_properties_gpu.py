@@ -108,3 +108,36 @@ def test_warp_and_scalar_engines_agree_at_scale(lib, name, count):
     b, bb = scalar.eval_generated(123_000, count)
     assert a.tobytes() == b.tobytes()
     assert (ba.makespan, ba.index, ba.n_ok) == (bb.makespan, bb.index, bb.n_ok)
+
+
+def test_merge_round_trip_and_flop_conservation(lib):
+    """SPEC acceptance 3: merge(partition(g)) reproduces g's schedule bit for
+    bit (same leaves, makespan, assignment and transfer hashes), for
+    partitions of every kind and tile count; acceptance 2: the leaves of
+    random partition/merge sequences keep sum(flops) = n^3/3 (1e-9 rel)."""
+    from paper_1602_05510_b200.engine import DESC_DTYPE, OP_MERGE
+    p, _ = PARITY["c2"]
+    eng = make_engine(p)
+    base = np.zeros(1, DESC_DTYPE)
+    out0, _ = eng.eval_descs(base)
+    cases = [(t, s) for t in (1, 2, 17, 18, 100, 500, 815) for s in (2, 4, 8)]
+    d = np.zeros(len(cases), DESC_DTYPE)
+    for i, (t, s) in enumerate(cases):
+        d[i]["n_ops"] = 2
+        d[i]["ops"][0] = (t, s)
+        d[i]["ops"][1] = (1, OP_MERGE)
+    out, _ = eng.eval_descs(d)
+    for i in range(len(cases)):
+        assert out[i].tobytes() == out0[0].tobytes(), cases[i]
+    n = float(p["n"])
+    pm = dict(p, merge_pct=35)
+    eng2 = make_engine(pm)
+    for desc in eng2.generate_host(0, 24):
+        tr = eng2.eval_trace(desc)
+        if tr.status:
+            continue
+        fl = 0.0
+        for e in tr.events:
+            if int(e["kind"]) == 0:
+                fl += task_flops(int(e["task_kind"]), int(e["b"]))
+        assert abs(fl - n ** 3 / 3.0) <= 1e-9 * n ** 3 / 3.0
