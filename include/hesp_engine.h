@@ -29,6 +29,7 @@ extern "C" {
 #endif
 
 /* ---- reference value types ------------------------------------------- */
+/* (hesp_fixture_load below fills these from the reference's own files.) */
 typedef struct {
   int32_t id;
   int64_t capacity_bytes;
@@ -132,6 +133,18 @@ enum {
 };
 
 typedef struct hesp_engine hesp_engine;
+
+/* The reference's fixture files read in C:
+ * Platform::from_json (platform.cpp:157-196) and PerfModel::from_analytic_json
+ * / from_table_csv (platform.cpp:238-320; a path ending in .csv is a table).
+ * Model entries of types the platform does not declare are dropped.  NULL on
+ * a parse error (message in hesp_last_error); the returned views stay valid
+ * until hesp_fixture_free. */
+typedef struct hesp_fixture hesp_fixture;
+hesp_fixture* hesp_fixture_load(const char* platform_path, const char* model_path);
+const hesp_platform* hesp_fixture_platform(const hesp_fixture* f);
+const hesp_perf_model* hesp_fixture_model(const hesp_fixture* f);
+void hesp_fixture_free(hesp_fixture* f);
 
 /* Validate inputs, precompute the model tables and the base tiling, upload
  * them and size the per-warp scratch.  Returns NULL on error. */

@@ -946,6 +946,7 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
 }  // extern "C"
 
 const hx::Problem& hesp_engine_problem(const hesp_engine* e) { return e->hp.p; }
+void hx::set_last_error(const std::string& msg) { g_last_error = msg; }
 const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e) { return e->last_graph; }
 
 extern "C" {

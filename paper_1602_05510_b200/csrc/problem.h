@@ -24,6 +24,9 @@ struct HostProblem {
 HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& model,
                           const hesp_sched_config& sched, const hesp_workload& wl);
 
+// Sets the message hesp_last_error() returns (engine_kernels.cu).
+void set_last_error(const std::string& msg);
+
 // PerfModel::task_time restated for one (kind, b, type); throws on miss.
 double host_task_time(const hesp_perf_model& m, int kind, long long b, int type, bool* known);
 

@@ -192,6 +192,7 @@ EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
     "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
+    "hesp_fixture_load", "hesp_fixture_platform", "hesp_fixture_model", "hesp_fixture_free",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
 
@@ -224,6 +225,13 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
     lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
+    lib.hesp_fixture_load.restype = C.c_void_p
+    lib.hesp_fixture_load.argtypes = [C.c_char_p, C.c_char_p]
+    lib.hesp_fixture_platform.restype = C.POINTER(PlatformC)
+    lib.hesp_fixture_platform.argtypes = [C.c_void_p]
+    lib.hesp_fixture_model.restype = C.POINTER(PerfModelC)
+    lib.hesp_fixture_model.argtypes = [C.c_void_p]
+    lib.hesp_fixture_free.argtypes = [C.c_void_p]
     lib.hesp_choose_p.restype = C.c_double
     lib.hesp_choose_p.argtypes = [C.c_double, C.c_int64, C.c_int64, C.c_int32]
     lib.hesp_select_candidate.restype = C.c_int32
@@ -360,10 +368,42 @@ class BatchEngine:
         self.h = C.c_void_p(h)
         self.workload, self.sched = workload, sched
 
+    @classmethod
+    def from_files(cls, platform_path: str, model_path: str, sched: SchedConfig, workload: Workload,
+                   device: int = 0) -> "BatchEngine":
+        """Engine from the reference's fixture files read by the library itself
+        (hesp_fixture_load: Platform::from_json / PerfModel::from_*)."""
+        lib = load_library()
+        fx = lib.hesp_fixture_load(platform_path.encode(), model_path.encode())
+        if not fx:
+            raise RuntimeError("hesp_fixture_load: " + lib.hesp_last_error().decode())
+        self = cls.__new__(cls)
+        self.lib = lib
+        self._fx = fx
+        self._pc = lib.hesp_fixture_platform(fx).contents
+        self._mc = lib.hesp_fixture_model(fx).contents
+        self._sc = SchedConfigC(ORDERING[sched.ordering], SELECTION[sched.selection], CACHING[sched.caching],
+                                0, sched.seed, sched.min_block)
+        sc = (C.c_int32 * 4)(*(list(workload.s_choices) + [0] * (4 - len(workload.s_choices))))
+        g = GenConfig(workload.seed, workload.k_max, workload.max_depth, workload.min_block,
+                      len(workload.s_choices), sc, workload.merge_pct)
+        self._wc = WorkloadC(workload.n, workload.elem_size, workload.s_base, g)
+        self._keep = []
+        h = lib.hesp_engine_create(device, C.byref(self._pc), C.byref(self._mc), C.byref(self._sc),
+                                   C.byref(self._wc))
+        if not h:
+            raise RuntimeError("hesp_engine_create: " + lib.hesp_last_error().decode())
+        self.h = C.c_void_p(h)
+        self.workload, self.sched = workload, sched
+        return self
+
     def close(self):
         if getattr(self, "h", None):
             self.lib.hesp_engine_destroy(self.h)
             self.h = None
+        if getattr(self, "_fx", None):
+            self.lib.hesp_fixture_free(self._fx)
+            self._fx = None
 
     def __del__(self):
         try:

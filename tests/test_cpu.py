@@ -234,3 +234,59 @@ def test_reference_merge_round_trip_in_goldens():
     a = read_golden("explicit_merge_c2")[0]
     b = read_golden("explicit_c2")[0]
     assert a.tobytes()[8:] == b.tobytes()[8:]
+
+
+# ---- C++ fixture loaders ----
+@pytest.mark.parametrize("plat,model", [("platform_cpugpu.json", "model_cpugpu.json"),
+                                        ("platform_cpugpu_evict.json", "model_cpugpu.json"),
+                                        ("platform_cpugpu.json", "model_cpugpu_table.csv"),
+                                        ("platform_biglittle.json", "model_biglittle.json"),
+                                        ("platform_serial.json", "model_biglittle.json")])
+def test_cpp_loaders_match_python_parse(plat, model):
+    """hesp_fixture_load reads every fixture to exactly the structs the Python
+    parser (the one every golden test runs on) builds."""
+    from paper_1602_05510_b200.engine import load_model, load_platform
+    lib = load_library()
+    fx = lib.hesp_fixture_load(os.path.join(FIXTURES, plat).encode(), os.path.join(FIXTURES, model).encode())
+    assert fx, lib.hesp_last_error()
+    try:
+        pc = lib.hesp_fixture_platform(fx).contents
+        mc = lib.hesp_fixture_model(fx).contents
+        pp = load_platform(plat)
+        keep = []
+        ref = pp._c(keep)
+        rm = load_model(model)._c(pp, keep)
+        assert (pc.n_spaces, pc.n_types, pc.n_procs, pc.n_links) == (ref.n_spaces, ref.n_types, ref.n_procs,
+                                                                     ref.n_links)
+        def fields(x):  # field values (struct padding is unspecified)
+            return tuple(getattr(x, f[0]) for f in x._fields_)
+        for i in range(pc.n_spaces):
+            assert fields(pc.spaces[i]) == fields(ref.spaces[i])
+        for i in range(pc.n_types):
+            assert pc.type_names[i] == ref.type_names[i]
+        for i in range(pc.n_procs):
+            assert fields(pc.procs[i]) == fields(ref.procs[i])
+        for i in range(pc.n_links):
+            assert fields(pc.links[i]) == fields(ref.links[i])
+        assert (mc.variant, mc.n_entries, mc.n_rows) == (rm.variant, rm.n_entries, rm.n_rows)
+        for i in range(mc.n_entries):
+            assert fields(mc.entries[i]) == fields(rm.entries[i])
+        for i in range(mc.n_rows):
+            assert fields(mc.rows[i]) == fields(rm.rows[i])
+    finally:
+        lib.hesp_fixture_free(fx)
+
+
+def test_cpp_loader_errors(tmp_path):
+    lib = load_library()
+    bad = tmp_path / "bad.json"
+    bad.write_text('{"spaces": [ {"id": 0, "capacity_bytes": 1} ], "types": [], "processors": [{"id":0,"type":"x","space":0}]}')
+    assert not lib.hesp_fixture_load(str(bad).encode(), os.path.join(FIXTURES, "model_cpugpu.json").encode())
+    assert b"unknown type" in lib.hesp_last_error()
+    bad.write_text('{"spaces": [')
+    assert not lib.hesp_fixture_load(str(bad).encode(), os.path.join(FIXTURES, "model_cpugpu.json").encode())
+    assert b"platform document" in lib.hesp_last_error()
+    csv = tmp_path / "m.csv"
+    csv.write_text("kind,proc_type,b,seconds\nGEMM,cpu,0,1.0\n")
+    assert not lib.hesp_fixture_load(os.path.join(FIXTURES, "platform_cpugpu.json").encode(), str(csv).encode())
+    assert b"b must be >= 1" in lib.hesp_last_error()

@@ -167,3 +167,18 @@ def test_min_reduce_over_torch_process_group(lib):
         assert (mk, idx) == (b.makespan, b.index)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["c2", "table", "c3", "evict_wt"])
+def test_engine_from_cpp_loaded_fixtures(lib, name):
+    """An engine created from hesp_fixture_load's structs reproduces the goldens."""
+    from paper_1602_05510_b200.engine import BatchEngine, FIXTURES, SchedConfig, Workload
+    import os
+    p, count = PARITY[name]
+    sched = SchedConfig(p["ordering"], p["selection"], p["caching"], p["sched_seed"], p["min_block"])
+    wl = Workload(p["n"], p["elem"], p["s_base"], p["seed"], p["k_max"], p["max_depth"], p["min_block"],
+                  p["s_choices"], p.get("merge_pct", 0))
+    eng = BatchEngine.from_files(os.path.join(FIXTURES, p["platform"]), os.path.join(FIXTURES, p["model"]),
+                                 sched, wl)
+    out, _ = eng.eval_generated(0, count)
+    assert not compare(out, read_golden(name))
