@@ -1,16 +1,19 @@
 // engine_kernels.cu — sm_100a kernels and the C ABI (include/hesp_engine.h).
 //
 // K1 per chunk of candidates, two persistent kernels (one warp per candidate,
-//    indices pulled from a global atomic counter -- candidates vary ~10x in
-//    cost: early CoherenceError vs a full 1.3k-task schedule):
+//    indices pulled from a global atomic counter over a longest-first order:
+//    candidates vary ~10x in cost, early CoherenceError vs a full 1.3k-task
+//    schedule; order_keys* + a CUB radix sort build the order):
 //    build_kernel: generate/load the descriptor, expand the DAG, dependences;
 //    sim_kernel:   the event loop, 32-byte outcome, per-warp best.
 //    Splitting the phases keeps every resident warp in the same code
 //    (instruction-fetch stalls 52% -> ~25%) and lets each phase have its own
-//    register budget.
+//    register budget.  sim_thread_kernel (HESP_SIM_THREAD=1) is the measured
+//    thread-per-candidate alternative (profiles/README.md).
 // K2 reduce_best: grid-level argmin of (makespan, index) over status == 0.
-// The multi-GPU min-reduce over NVLink (K3) lives in the host driver
-// (paper_1602_05510_b200/engine.py) on 16 bytes per rank.
+// K3 hesp_min_reduce: the cross-GPU winner, two int64 MIN all-reduces over
+//    the caller's NCCL communicator (NVLink / NVSwitch), NCCL dlopen'ed.
+// detail_kernel: one candidate with the full trace (Engine<DevWarp, true>).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
@@ -368,7 +371,7 @@ struct hesp_engine {
   size_t h_cap = 0;
   cudaStream_t stream = nullptr;
   long long launches = 0;
-  // phase-split mode (HESP_SPLIT=1): per-candidate slots for one chunk
+  // per-candidate slots of one chunk (build -> simulate hand-off)
   bool split = true;
   uint8_t* d_cslots = nullptr;
   unsigned long long chunk = 0;      // max candidates per chunk (memory budget)
@@ -692,7 +695,7 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     if (cap < 1024) cap = 1024;
     e->chunk = want < cap ? want : cap;
   }
-  // per-warp slots only for the fused kernel; one slot for hesp_eval_detail otherwise
+  // one slot for the single-candidate detail / trace kernel
   if ((c = cudaMalloc(&e->d_scratch, (size_t)(e->split ? 1 : e->n_slots) * e->L.total)) != cudaSuccess)
     return fail(c, "malloc scratch");
   if ((c = cudaMallocHost(&e->h_best, sizeof(hesp_best))) != cudaSuccess) return fail(c, "malloc host");
