@@ -348,6 +348,13 @@ int32_t hesp_select_candidate(const double* scores, int32_t n, int32_t sampling,
 int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfg,
                hesp_solver_result* out);
 
+/* n_chains independent solver chains (own config, seed, initial state and
+ * result each) advanced in lockstep: per iteration ONE launch traces every
+ * chain's state (one warp each) and ONE device batch validates every chain's
+ * candidate mutations.  Chain c's result equals hesp_solve with cfgs[c]. */
+int hesp_solve_batch(hesp_engine* e, int32_t n_chains, const hesp_cand_desc* initial /* n_chains or NULL */,
+                     const hesp_solver_config* cfgs, hesp_solver_result* outs);
+
 /* Cross-GPU winner: every rank passes its own batch
  * best; on return `best` holds the exact lexicographic (makespan, lowest
  * global index) argmin over all ranks of `nccl_comm` and the summed work

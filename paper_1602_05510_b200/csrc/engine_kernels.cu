@@ -344,6 +344,35 @@ __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* 
   }
 }
 
+// Many candidates' schedules at once (the batched solver): one warp per
+// candidate, the trace engine in schedule-only mode (E4 fast path, no logs),
+// per-candidate output regions.
+__global__ void schedule_kernel(const hesp_cand_desc* __restrict__ descs, uint8_t* slots, int32_t cap,
+                                int32_t* proc, double* start, double* end, hesp_outcome* out, TraceBufs* tbs) {
+  __shared__ Small smem;
+  __shared__ hesp_cand_desc sd;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) sd = descs[b];
+  __syncwarp();
+  uint8_t* slot = slots + (size_t)b * c_problem.lay.total;
+  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &smem);
+  eng.tr_proc = proc + (size_t)b * cap;
+  eng.tr_start = start + (size_t)b * cap;
+  eng.tr_end = end + (size_t)b * cap;
+  eng.tr_cap = cap;
+  eng.tb = tbs + b;
+  const Outcome o = eng.run(sd);
+  if (threadIdx.x == 0) {
+    hesp_outcome r;
+    r.status = o.status;
+    r.n_leaves = o.n_leaves;
+    r.makespan = o.makespan;
+    r.assign_hash = o.assign_hash;
+    r.xfer_hash = o.xfer_hash;
+    out[b] = r;
+  }
+}
+
 }  // namespace
 
 struct hesp_engine {
@@ -396,6 +425,18 @@ struct hesp_engine {
   int32_t* d_trace_proc = nullptr;
   double *d_trace_start = nullptr, *d_trace_end = nullptr;
   hesp_outcome* d_trace_out = nullptr;
+  // batched schedule-only traces (hx::schedule_batch), grown on demand
+  std::vector<void*> sched_bufs;
+  int sched_cap = 0;
+  uint8_t* d_sslots = nullptr;
+  int32_t *d_sproc = nullptr, *d_sleaves = nullptr, *d_slpoff = nullptr, *d_slpcnt = nullptr, *d_slpreds = nullptr;
+  double *d_sstart = nullptr, *d_send = nullptr;
+  TaskMeta *d_slmeta = nullptr, *d_stmeta = nullptr;
+  Region* d_sbregion = nullptr;
+  int32_t* d_sbisint = nullptr;
+  PartEntry* d_sparts = nullptr;
+  TraceBufs* d_stbs = nullptr;
+  hesp_outcome* d_sout = nullptr;
 };
 
 namespace {
@@ -406,8 +447,17 @@ bool ck(cudaError_t e, const char* what) {
   return false;
 }
 
+// Buffers grow geometrically (x1.5, at least 1024 entries): callers such as
+// the solver issue batches of slowly varying size, and every reallocation is
+// a synchronising cudaFree + cudaMalloc(Host).
+size_t grown(size_t need, size_t have) {
+  const size_t g = have + have / 2;
+  return need > g ? (need > 1024 ? need : 1024) : g;
+}
+
 bool grow_out(hesp_engine* e, size_t n) {
   if (n <= e->out_cap) return true;
+  n = grown(n, e->out_cap);
   if (e->d_out) cudaFree(e->d_out);
   e->d_out = nullptr;
   if (!ck(cudaMalloc(&e->d_out, n * sizeof(hesp_outcome)), "cudaMalloc outcomes")) return false;
@@ -417,6 +467,7 @@ bool grow_out(hesp_engine* e, size_t n) {
 
 bool grow_host(hesp_engine* e, size_t n) {
   if (n <= e->h_cap) return true;
+  n = grown(n, e->h_cap);
   if (e->h_descs) cudaFreeHost(e->h_descs);
   if (e->h_out) cudaFreeHost(e->h_out);
   e->h_descs = nullptr;
@@ -431,8 +482,11 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
                  hesp_outcome* d_out, cudaStream_t st) {
   // equal-size chunks under the memory cap: each chunk pays one load-balance tail
   const unsigned long long nchunks = count ? (count + e->chunk - 1) / e->chunk : 1;
-  const unsigned long long need = count ? (count + nchunks - 1) / nchunks : 1;
+  const unsigned long long per = count ? (count + nchunks - 1) / nchunks : 1;  // equal-size chunks
+  unsigned long long need = per;
   if (need > e->cslots_n) {
+    need = grown(need, e->cslots_n);
+    if (need > e->chunk) need = e->chunk > per ? e->chunk : per;
     if (e->d_cslots) cudaFree(e->d_cslots);
     e->d_cslots = nullptr;
     e->cslots_n = 0;
@@ -451,7 +505,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     if (!ck(cudaMalloc(&e->d_sort_tmp, e->sort_tmp_bytes ? e->sort_tmp_bytes : 1), "malloc sort tmp"))
       return HESP_E_CUDA;
   }
-  const unsigned long long chunk = e->cslots_n;
+  const unsigned long long chunk = per;
   if (!ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
           "problem -> constant"))
     return HESP_E_CUDA;
@@ -471,7 +525,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     const hesp_cand_desc* cd = d_descs ? d_descs + c0 : nullptr;
     if (e->lpt && !cd && n > 1) {  // generated candidates: materialise the descriptors to order them
       if (!e->d_gen) {
-        if (!ck(cudaMalloc(&e->d_gen, chunk * sizeof(hesp_cand_desc)), "malloc gen descs")) return HESP_E_CUDA;
+        if (!ck(cudaMalloc(&e->d_gen, e->cslots_n * sizeof(hesp_cand_desc)), "malloc gen descs")) return HESP_E_CUDA;
       }
       gen_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(first + c0, n, e->d_gen);
       e->launches += 1;
@@ -721,6 +775,7 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_sort_tmp);
   cudaFree(e->d_gen);
   for (void* q : e->trace_bufs) cudaFree(q);
+  for (void* q : e->sched_bufs) cudaFree(q);
   cudaFree(e->d_wbest);
   cudaFree(e->d_best);
   cudaFree(e->d_counter);
@@ -777,8 +832,9 @@ int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
   if (count > e->desc_cap) {
     if (e->d_descs) cudaFree(e->d_descs);
     e->d_descs = nullptr;
-    if (!ck(cudaMalloc(&e->d_descs, count * sizeof(hesp_cand_desc)), "malloc descs")) return HESP_E_CUDA;
-    e->desc_cap = count;
+    const size_t cap = grown(count, e->desc_cap);
+    if (!ck(cudaMalloc(&e->d_descs, cap * sizeof(hesp_cand_desc)), "malloc descs")) return HESP_E_CUDA;
+    e->desc_cap = cap;
   }
   if (!grow_out(e, count) || !grow_host(e, count)) return HESP_E_CUDA;
   std::memcpy(e->h_descs, descs, count * sizeof(hesp_cand_desc));
@@ -949,6 +1005,99 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
 }  // extern "C"
 
 const hx::Problem& hesp_engine_problem(const hesp_engine* e) { return e->hp.p; }
+
+int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::vector<TraceGraph>& graphs,
+                       std::vector<TraceLogs>& logs, std::vector<hesp_outcome>& outs) {
+  if (!e || !descs || B < 1) return HESP_E_INVALID;
+  cudaSetDevice(e->device);
+  const Problem& P = e->hp.p;
+  const size_t T = P.maxt, E = P.maxedges, NB = P.maxb;
+  if (B > e->sched_cap) {
+    for (void* q : e->sched_bufs) cudaFree(q);
+    e->sched_bufs.clear();
+    e->sched_cap = 0;
+    std::vector<void*>& o = e->sched_bufs;
+    const size_t b = (size_t)B;
+    const bool ok = dalloc(&e->d_sslots, b * e->L.total, o) && dalloc(&e->d_sproc, b * T, o) &&
+                    dalloc(&e->d_sstart, b * T, o) && dalloc(&e->d_send, b * T, o) &&
+                    dalloc(&e->d_sleaves, b * T, o) && dalloc(&e->d_slmeta, b * T, o) &&
+                    dalloc(&e->d_slpoff, b * T, o) && dalloc(&e->d_slpcnt, b * T, o) &&
+                    dalloc(&e->d_slpreds, b * E, o) && dalloc(&e->d_sbregion, b * NB, o) &&
+                    dalloc(&e->d_sbisint, b * NB, o) && dalloc(&e->d_sparts, b * MAXPART, o) &&
+                    dalloc(&e->d_stmeta, b * T, o) && dalloc(&e->d_stbs, b, o) && dalloc(&e->d_sout, b, o);
+    if (!ok) {
+      for (void* q : o) cudaFree(q);
+      o.clear();
+      return HESP_E_CUDA;
+    }
+    e->sched_cap = B;
+  }
+  std::vector<TraceBufs> tbs(B);
+  for (int b = 0; b < B; ++b) {
+    TraceBufs& t = tbs[b];
+    t = TraceBufs{};
+    t.lite = 1;
+    t.leaves = e->d_sleaves + b * T;
+    t.lmeta = e->d_slmeta + b * T;
+    t.lpoff = e->d_slpoff + b * T;
+    t.lpcnt = e->d_slpcnt + b * T;
+    t.lpreds = e->d_slpreds + b * E;
+    t.bregion = e->d_sbregion + b * NB;
+    t.bisint = e->d_sbisint + b * NB;
+    t.parts = e->d_sparts + (size_t)b * MAXPART;
+    t.tmeta = e->d_stmeta + b * T;
+    t.leaf_cap = (int)T;
+    t.pred_cap = (int)E;
+    t.block_cap = (int)NB;
+    t.task_cap = (int)T;
+  }
+  hesp_cand_desc* dd = nullptr;
+  if (!ck(cudaMalloc(&dd, (size_t)B * sizeof(hesp_cand_desc)), "malloc descs")) return HESP_E_CUDA;
+  cudaStream_t st = e->stream;
+  bool ok = ck(cudaMemcpyAsync(dd, descs, (size_t)B * sizeof(hesp_cand_desc), cudaMemcpyHostToDevice, st), "H2D") &&
+            ck(cudaMemcpyAsync(e->d_stbs, tbs.data(), (size_t)B * sizeof(TraceBufs), cudaMemcpyHostToDevice, st),
+               "H2D") &&
+            ck(cudaMemsetAsync(e->d_sproc, 0xff, (size_t)B * T * 4, st), "memset") &&
+            ck(cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, st), "problem");
+  if (ok) {
+    schedule_kernel<<<B, 32, 0, st>>>(dd, e->d_sslots, (int32_t)T, e->d_sproc, e->d_sstart, e->d_send, e->d_sout,
+                                      e->d_stbs);
+    e->launches += 1;
+    ok = ck(cudaStreamSynchronize(st), "schedule kernel");
+  }
+  std::vector<TraceBufs> hb(B);
+  outs.assign(B, hesp_outcome{});
+  ok = ok && d2h(hb, e->d_stbs, B) && ck(cudaMemcpy(outs.data(), e->d_sout, B * sizeof(hesp_outcome),
+                                                   cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(dd);
+  if (!ok) return HESP_E_CUDA;
+  std::vector<int32_t> proc;
+  std::vector<double> s0, s1;
+  ok = d2h(proc, e->d_sproc, (size_t)B * T) && d2h(s0, e->d_sstart, (size_t)B * T) && d2h(s1, e->d_send, (size_t)B * T);
+  if (!ok) return HESP_E_CUDA;
+  graphs.assign(B, TraceGraph{});
+  logs.assign(B, TraceLogs{});
+  for (int b = 0; b < B; ++b) {
+    if (hb[b].overflow) {
+      g_last_error = "schedule batch: trace buffers overflowed";
+      return HESP_E_CUDA;
+    }
+    if (outs[b].status != 0) continue;
+    TraceGraph& g = graphs[b];
+    TraceLogs& L = logs[b];
+    L.proc.assign(proc.begin() + b * T, proc.begin() + (b + 1) * T);
+    L.start.assign(s0.begin() + b * T, s0.begin() + (b + 1) * T);
+    L.end.assign(s1.begin() + b * T, s1.begin() + (b + 1) * T);
+    const TraceBufs& t = tbs[b];
+    ok = d2h(g.leaves, t.leaves, (size_t)hb[b].nleaves) && d2h(g.meta, t.lmeta, (size_t)hb[b].nleaves) &&
+         d2h(g.poff, t.lpoff, (size_t)hb[b].nleaves) && d2h(g.pcnt, t.lpcnt, (size_t)hb[b].nleaves) &&
+         d2h(g.preds, t.lpreds, (size_t)hb[b].npreds) && d2h(g.parts, t.parts, (size_t)hb[b].nparts) &&
+         d2h(g.tmeta, t.tmeta, (size_t)hb[b].ntasks);
+    if (!ok) return HESP_E_CUDA;
+    g.valid = true;
+  }
+  return HESP_OK;
+}
 void hx::set_last_error(const std::string& msg) { g_last_error = msg; }
 const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e) { return e->last_graph; }
 

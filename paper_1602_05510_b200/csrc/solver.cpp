@@ -137,61 +137,40 @@ extern "C" int32_t hesp_select_candidate(const double* scores, int32_t n, int32_
   return (int32_t)i;
 }
 
-extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfgp,
-                          hesp_solver_result* out) {
-  if (!e || !cfgp || !out || cfgp->iterations < 0 || cfgp->k_max < 2 || cfgp->overhead_factor < 1.0 ||
-      cfgp->min_block < 1 || cfgp->task_selection < 0 || cfgp->task_selection > 2 || cfgp->sampling < 0 ||
-      cfgp->sampling > 2)
-    return HESP_E_INVALID;
-  if (out->cap_history < cfgp->iterations || (!out->history && cfgp->iterations > 0)) return HESP_E_INVALID;
-  const Problem& P = hesp_engine_problem(e);
-  const hesp_solver_config cfg = *cfgp;
-  Ctx cx{P, cfg};
-  Rng rng{cfg.seed};
+namespace {
+
+// One solver chain (a state, its rng, its output record).
+struct Chain {
+  hesp_solver_config cfg;
+  Rng rng;
   hesp_cand_desc cur;
-  std::memset(&cur, 0, sizeof cur);
-  if (initial) cur = *initial;
-  out->n_history = 0;
-  out->best_makespan = 0;
-  out->best_iteration = -1;
-  out->n_simulated = 0;
-  std::memset(&out->best, 0, sizeof out->best);
-  // trace arrays, grown on HESP_E_LIMIT
-  std::vector<hesp_assignment> A(4096);
-  std::vector<hesp_transfer> X(8192);
-  std::vector<hesp_residency> R(16384);
-  std::vector<hesp_event> E(32768);
-  std::vector<hesp_load_step> S(8192);
-  std::vector<hesp_cand_desc> batch;
-  std::vector<hesp_outcome> outc;
-  for (int it = 0; it < cfg.iterations; ++it) {
-    hesp_trace tr{};
-    int rc;
-    for (;;) {
-      tr = hesp_trace{};
-      tr.cap_assign = (int32_t)A.size();
-      tr.cap_xfer = (int32_t)X.size();
-      tr.cap_res = (int32_t)R.size();
-      tr.cap_events = (int32_t)E.size();
-      tr.cap_steps = (int32_t)S.size();
-      tr.assignments = A.data();
-      tr.transfers = X.data();
-      tr.residency = R.data();
-      tr.events = E.data();
-      tr.steps = S.data();
-      tr.flags = HESP_TRACE_SCHEDULE_ONLY;
-      rc = hesp_eval_trace(e, &cur, &tr);
-      if (rc != HESP_E_LIMIT) break;
-      A.resize(std::max<size_t>(A.size(), tr.n_assign));
-      X.resize(std::max<size_t>(X.size(), tr.n_xfer));
-      R.resize(std::max<size_t>(R.size(), tr.n_res));
-      E.resize(std::max<size_t>(E.size(), tr.n_events));
-      S.resize(std::max<size_t>(S.size(), tr.n_steps));
-    }
-    ++out->n_simulated;
-    if (rc != 0) return rc;  // only the initial state can fail (mutations are filtered)
-    const TraceGraph& g = hesp_engine_last_graph(e);
-    const double makespan = tr.outcome.makespan;
+  hesp_solver_result* out;
+  std::vector<hesp_assignment> A;
+  std::vector<hesp_load_step> S;
+  hesp_solver_iteration rec;
+  std::vector<Cand> cands;
+  size_t first = 0;  // offset of this chain's mutations in the shared batch
+};
+
+bool valid_cfg(const hesp_solver_config* c) {
+  return c && c->iterations >= 0 && c->k_max >= 2 && c->overhead_factor >= 1.0 && c->min_block >= 1 &&
+         c->task_selection >= 0 && c->task_selection <= 2 && c->sampling >= 0 && c->sampling <= 2;
+}
+
+hesp_cand_desc mutate(const hesp_cand_desc& cur, const Cand& c) {
+  hesp_cand_desc d = cur;
+  if (c.action != HESP_ACT_PARTITION) d.ops[d.n_ops++] = hesp_op{c.target, HESP_OP_MERGE};
+  if (c.action != HESP_ACT_MERGE) d.ops[d.n_ops++] = hesp_op{c.parent, c.k};
+  return d;
+}
+
+// Metrics + candidate collection of one chain's traced state.
+void collect(Chain& ch, const Problem& P, const TraceGraph& g, const hesp_trace& tr, int it) {
+  const hesp_solver_config& cfg = ch.cfg;
+  Ctx cx{P, cfg};
+  hesp_solver_result* out = ch.out;
+  const hesp_assignment* A = tr.assignments;
+  const double makespan = tr.outcome.makespan;
     // ---- graph facts: clusters, membership, depth ----
     std::map<int, int> cluster_of;   // member task -> live cluster id
     std::map<int, int> parent_of;    // partitioned task -> live cluster id
@@ -228,17 +207,16 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
     rec.dag_depth = depth;
     rec.avg_block_side = den > 0 ? num / den : 0.0;
     rec.avg_load_pct = 100.0 * tr.avg_load;
+    ch.rec = rec;
     if (out->best_iteration < 0 || makespan < out->best_makespan) {
       out->best_makespan = makespan;
       out->best_iteration = it;
-      out->best = cur;
+      out->best = ch.cur;
     }
-    if (it + 1 == cfg.iterations) {  // the last round's mutation could never be simulated
-      out->history[out->n_history++] = rec;
-      break;
-    }
+    ch.cands.clear();
+    if (it + 1 == cfg.iterations) return;  // the last round's mutation could never be simulated
+    std::vector<Cand>& cands = ch.cands;
     // ---- collect_candidates ----
-    std::vector<Cand> cands;
     std::vector<int> tasks;  // selected leaves, id order
     if (cfg.task_selection == HESP_SEL_ALL) {
       for (const auto& [id, a] : asg) tasks.push_back(id);
@@ -318,56 +296,129 @@ extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const h
       const double rep = merge + std::max(0.0, span - est);
       if (rep > 0) cands.push_back({HESP_ACT_REPARTITION, c, pe.task, (int)k, rep, par.b});
     }
-    // op budget of the descriptor
+    const hesp_cand_desc& cur = ch.cur;
     cands.erase(std::remove_if(cands.begin(), cands.end(),
                                [&](const Cand& c) {
                                  return cur.n_ops + (c.action == HESP_ACT_REPARTITION ? 2 : 1) > HESP_MAX_OPS;
                                }),
                 cands.end());
-    rec.n_candidates = (int32_t)cands.size();
-    // ---- validity filter: every mutation in one device batch ----
-    auto mutate = [&](const Cand& c) {
-      hesp_cand_desc d = cur;
-      if (c.action != HESP_ACT_PARTITION) d.ops[d.n_ops++] = hesp_op{c.target, HESP_OP_MERGE};
-      if (c.action != HESP_ACT_MERGE) d.ops[d.n_ops++] = hesp_op{c.parent, c.k};
-      return d;
-    };
-    std::vector<Cand> valid;
-    if (!cands.empty()) {
-      batch.resize(cands.size());
-      outc.resize(cands.size());
-      for (size_t i = 0; i < cands.size(); ++i) batch[i] = mutate(cands[i]);
-      hesp_best b{};
-      const int r = hesp_eval_descs(e, batch.data(), batch.size(), 0, outc.data(), &b);
-      if (r != 0) return r;
-      out->n_simulated += (int64_t)cands.size();
-      for (size_t i = 0; i < cands.size(); ++i)
-        if (outc[i].status == 0) {
-          valid.push_back(cands[i]);
-          if (cfg.sampling == HESP_SAMPLE_EXACT) valid.back().score = outc[i].makespan;
-        }
-    }
-    rec.n_valid = (int32_t)valid.size();
-    if (!valid.empty()) {
-      // ---- select_candidate ----
-      std::vector<double> sc(valid.size());
-      for (size_t i = 0; i < valid.size(); ++i) sc[i] = valid[i].score;
-      size_t pick = 0;
-      if (cfg.sampling == HESP_SAMPLE_EXACT) {
-        for (size_t i = 1; i < sc.size(); ++i)
-          if (sc[i] < sc[pick]) pick = i;
-      } else {
-        pick = select_index(sc.data(), sc.size(), cfg.sampling, rng);
+    ch.rec.n_candidates = (int32_t)cands.size();
+}
+
+// Runs n chains in lockstep: one batched schedule trace of every state and
+// one device batch of every chain's candidate mutations per iteration.
+int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hesp_solver_config* cfgs,
+                 hesp_solver_result* outs) {
+  const Problem& P = hesp_engine_problem(e);
+  std::vector<Chain> chains(n);
+  int iters = 0;
+  for (int c = 0; c < n; ++c) {
+    Chain& ch = chains[c];
+    ch.cfg = cfgs[c];
+    ch.rng = Rng{cfgs[c].seed};
+    std::memset(&ch.cur, 0, sizeof ch.cur);
+    if (initial) ch.cur = initial[c];
+    ch.out = &outs[c];
+    ch.out->n_history = 0;
+    ch.out->best_makespan = 0;
+    ch.out->best_iteration = -1;
+    ch.out->n_simulated = 0;
+    std::memset(&ch.out->best, 0, sizeof ch.out->best);
+    ch.A.resize((size_t)P.maxt);
+    ch.S.resize(2 * (size_t)P.maxt + 2);
+    iters = std::max(iters, ch.cfg.iterations);
+  }
+  std::vector<hesp_cand_desc> states, batch;
+  std::vector<hesp_outcome> souts, outc;
+  std::vector<TraceGraph> graphs;
+  std::vector<hx::TraceLogs> logs;
+  std::vector<int> live;
+  for (int it = 0; it < iters; ++it) {
+    live.clear();
+    states.clear();
+    for (int c = 0; c < n; ++c)
+      if (it < chains[c].cfg.iterations) {
+        live.push_back(c);
+        states.push_back(chains[c].cur);
       }
-      const Cand& c = valid[pick];
-      rec.action = c.action;
-      rec.target = c.target;
-      rec.d = c.d;
-      rec.p = c.action == HESP_ACT_MERGE ? 1.0 : 1.0 / (double)c.k;
-      rec.score = c.score;
-      cur = mutate(c);
+    int r = hx::schedule_batch(e, states.data(), (int)states.size(), graphs, logs, souts);
+    if (r != HESP_OK) return r;
+    batch.clear();
+    for (size_t q = 0; q < live.size(); ++q) {
+      Chain& ch = chains[live[q]];
+      ++ch.out->n_simulated;
+      if (souts[q].status != 0) return souts[q].status;  // only an initial state can fail
+      hesp_trace tr{};
+      tr.cap_assign = (int32_t)ch.A.size();
+      tr.cap_steps = (int32_t)ch.S.size();
+      tr.assignments = ch.A.data();
+      tr.steps = ch.S.data();
+      tr.outcome = souts[q];
+      r = hx::finish_trace(P, graphs[q], logs[q], &tr, true);
+      if (r != HESP_OK) return r;
+      collect(ch, P, graphs[q], tr, it);
+      ch.first = batch.size();
+      for (const Cand& cd : ch.cands) batch.push_back(mutate(ch.cur, cd));
     }
-    out->history[out->n_history++] = rec;
+    // ---- validity filter: every chain's mutations in one device batch ----
+    if (!batch.empty()) {
+      outc.resize(batch.size());
+      hesp_best b{};
+      r = hesp_eval_descs(e, batch.data(), batch.size(), 0, outc.data(), &b);
+      if (r != 0) return r;
+    }
+    for (int c : live) {
+      Chain& ch = chains[c];
+      hesp_solver_iteration rec = ch.rec;
+      std::vector<Cand> valid;
+      ch.out->n_simulated += (int64_t)ch.cands.size();
+      for (size_t i = 0; i < ch.cands.size(); ++i)
+        if (outc[ch.first + i].status == 0) {
+          valid.push_back(ch.cands[i]);
+          if (ch.cfg.sampling == HESP_SAMPLE_EXACT) valid.back().score = outc[ch.first + i].makespan;
+        }
+      rec.n_valid = (int32_t)valid.size();
+      if (!valid.empty()) {
+        // ---- select_candidate ----
+        std::vector<double> sc(valid.size());
+        for (size_t i = 0; i < valid.size(); ++i) sc[i] = valid[i].score;
+        size_t pick = 0;
+        if (ch.cfg.sampling == HESP_SAMPLE_EXACT) {
+          for (size_t i = 1; i < sc.size(); ++i)
+            if (sc[i] < sc[pick]) pick = i;
+        } else {
+          pick = select_index(sc.data(), sc.size(), ch.cfg.sampling, ch.rng);
+        }
+        const Cand& cd = valid[pick];
+        rec.action = cd.action;
+        rec.target = cd.target;
+        rec.d = cd.d;
+        rec.p = cd.action == HESP_ACT_MERGE ? 1.0 : 1.0 / (double)cd.k;
+        rec.score = cd.score;
+        ch.cur = mutate(ch.cur, cd);
+      }
+      ch.out->history[ch.out->n_history++] = rec;
+    }
   }
   return 0;
+}
+
+}  // namespace
+
+extern "C" int hesp_solve(hesp_engine* e, const hesp_cand_desc* initial, const hesp_solver_config* cfgp,
+                          hesp_solver_result* out) {
+  if (!e || !valid_cfg(cfgp) || !out) return HESP_E_INVALID;
+  if (out->cap_history < cfgp->iterations || (!out->history && cfgp->iterations > 0)) return HESP_E_INVALID;
+  return solve_chains(e, 1, initial, cfgp, out);
+}
+
+extern "C" int hesp_solve_batch(hesp_engine* e, int32_t n_chains, const hesp_cand_desc* initial,
+                                const hesp_solver_config* cfgs, hesp_solver_result* outs) {
+  if (!e || n_chains < 1 || !cfgs || !outs) return HESP_E_INVALID;
+  for (int c = 0; c < n_chains; ++c) {
+    if (!valid_cfg(&cfgs[c])) return HESP_E_INVALID;
+    if (outs[c].cap_history < cfgs[c].iterations || (!outs[c].history && cfgs[c].iterations > 0))
+      return HESP_E_INVALID;
+  }
+  return solve_chains(e, n_chains, initial, cfgs, outs);
 }

@@ -40,6 +40,14 @@ std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, con
 
 }  // namespace hx
 
+namespace hx {
+// Schedule-only traces of B candidates in one launch (one warp each):
+// per-candidate graph and (proc, start, end) by task id; outs[b].status != 0
+// leaves graphs[b] / logs[b] empty.  HESP_OK or a negative HESP_E_* code.
+int schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::vector<TraceGraph>& graphs,
+                   std::vector<TraceLogs>& logs, std::vector<hesp_outcome>& outs);
+}  // namespace hx
+
 // engine internals the host-side solver reads (engine_kernels.cu)
 const hx::Problem& hesp_engine_problem(const hesp_engine* e);
 const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e);

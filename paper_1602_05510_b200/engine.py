@@ -191,7 +191,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_solve_batch", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
     "hesp_fixture_load", "hesp_fixture_platform", "hesp_fixture_model", "hesp_fixture_free",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
@@ -225,6 +225,7 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
     lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
+    lib.hesp_solve_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.hesp_fixture_load.restype = C.c_void_p
     lib.hesp_fixture_load.argtypes = [C.c_char_p, C.c_char_p]
     lib.hesp_fixture_platform.restype = C.POINTER(PlatformC)
@@ -526,6 +527,35 @@ class BatchEngine:
         C.memmove(C.byref(b), C.byref(best), C.sizeof(Best))
         self._check(self.lib.hesp_min_reduce(self.h, C.c_void_p(nccl_comm), C.byref(b)), "min_reduce")
         return b
+
+    def solve_batch(self, chains: list[dict]):
+        """hesp_solve_batch: independent chains in lockstep (one trace launch and
+        one candidate batch per iteration for all of them).  Each dict takes
+        solve()'s keyword arguments (iterations, task_selection, sampling, seed,
+        k_max, min_block, overhead_factor); returns one solve()-shaped tuple per chain."""
+        n = len(chains)
+        cfgs = (SolverConfigC * n)()
+        hists, res = [], (SolverResultC * n)()
+        for i, c in enumerate(chains):
+            it = c.get("iterations", 50)
+            cfgs[i] = SolverConfigC(it, TASK_SELECTION[c.get("task_selection", "All")],
+                                    SAMPLING[c.get("sampling", "Soft")], c.get("k_max", 8), c.get("seed", 0),
+                                    c.get("min_block", 64), c.get("overhead_factor", 1.1))
+            h = np.zeros(max(1, it), SOLVER_ITER_DTYPE)
+            hists.append(h)
+            res[i].cap_history = len(h)
+            res[i].history = h.ctypes.data
+        rc = self.lib.hesp_solve_batch(self.h, n, None, C.cast(cfgs, C.c_void_p), C.cast(res, C.c_void_p))
+        if rc < 0:
+            self._check(rc, "solve_batch")
+        if rc > 0:
+            raise RuntimeError(f"solve_batch: an initial state fails with status {rc} ({status_name(rc)})")
+        out = []
+        for i in range(n):
+            best = np.frombuffer(bytes(res[i].best), DESC_DTYPE)[0].copy()
+            out.append((hists[i][:res[i].n_history].copy(), best, float(res[i].best_makespan),
+                        int(res[i].best_iteration), int(res[i].n_simulated)))
+        return out
 
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)

@@ -58,3 +58,18 @@ def test_exact_lookahead_mode(lib):
         if hist[i]["action"] >= 0:
             assert hist[i + 1]["makespan"] == hist[i]["score"]
     assert best_mk == min(hist["makespan"])
+
+
+def test_batched_chains_equal_single_solves(lib):
+    """hesp_solve_batch: chains advanced in lockstep (shared trace launch and
+    shared candidate batch) give exactly the single-chain histories."""
+    p, _ = PARITY["policy_PL_EFT-P_WB"]
+    eng = make_engine(p)
+    chains = [dict(iterations=8, task_selection=sel, sampling=samp, seed=seed)
+              for sel, samp, seed in [("All", "Hard", 0), ("CP", "Soft", 3), ("Shallow", "Soft", 5),
+                                      ("All", "Exact", 0), ("All", "Soft", 11)]]
+    many = eng.solve_batch(chains)
+    for c, (h, best, mk, it, n) in zip(chains, many):
+        h1, best1, mk1, it1, n1 = eng.solve(c["iterations"], c["task_selection"], c["sampling"], c["seed"])
+        assert h.tobytes() == h1.tobytes()
+        assert (mk, it, n) == (mk1, it1, n1) and best.tobytes() == best1.tobytes()
