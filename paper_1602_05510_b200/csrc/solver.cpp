@@ -15,6 +15,8 @@
 // The host side only does the per-candidate arithmetic (one pass over the
 // leaves); every schedule is simulated by the sm_100a engine.
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -344,19 +346,44 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
     int r = hx::schedule_batch(e, states.data(), (int)states.size(), graphs, logs, souts);
     if (r != HESP_OK) return r;
     batch.clear();
+    for (size_t q = 0; q < live.size(); ++q)
+      if (souts[q].status != 0) return souts[q].status;  // only an initial state can fail
+    // per-chain host work (post-passes, scoring) is independent: spread the
+    // chains over the host threads
+    std::atomic<size_t> next{0};
+    std::atomic<int> err{0};
+    auto work = [&]() {
+      for (;;) {
+        const size_t q = next.fetch_add(1);
+        if (q >= live.size()) return;
+        Chain& ch = chains[live[q]];
+        ++ch.out->n_simulated;
+        hesp_trace tr{};
+        tr.cap_assign = (int32_t)ch.A.size();
+        tr.cap_steps = (int32_t)ch.S.size();
+        tr.assignments = ch.A.data();
+        tr.steps = ch.S.data();
+        tr.outcome = souts[q];
+        const int rr = hx::finish_trace(P, graphs[q], logs[q], &tr, true);
+        if (rr != HESP_OK) {
+          err = rr;
+          continue;
+        }
+        collect(ch, P, graphs[q], tr, it);
+      }
+    };
+    const unsigned hw = std::thread::hardware_concurrency();
+    const size_t nth = std::min<size_t>(live.size(), hw ? hw : 1);
+    if (nth <= 1) {
+      work();
+    } else {
+      std::vector<std::thread> pool;
+      for (size_t t = 0; t < nth; ++t) pool.emplace_back(work);
+      for (auto& t : pool) t.join();
+    }
+    if (err) return err;
     for (size_t q = 0; q < live.size(); ++q) {
       Chain& ch = chains[live[q]];
-      ++ch.out->n_simulated;
-      if (souts[q].status != 0) return souts[q].status;  // only an initial state can fail
-      hesp_trace tr{};
-      tr.cap_assign = (int32_t)ch.A.size();
-      tr.cap_steps = (int32_t)ch.S.size();
-      tr.assignments = ch.A.data();
-      tr.steps = ch.S.data();
-      tr.outcome = souts[q];
-      r = hx::finish_trace(P, graphs[q], logs[q], &tr, true);
-      if (r != HESP_OK) return r;
-      collect(ch, P, graphs[q], tr, it);
       ch.first = batch.size();
       for (const Cand& cd : ch.cands) batch.push_back(mutate(ch.cur, cd));
     }
