@@ -309,6 +309,8 @@ def main():
         out, b = eng.eval_descs(host_descs[i], first=firsts[s])
         global_best(b)
     e2e_s = time.perf_counter() - t0
+    # descriptors travel packed (offsets + used ops); count what was copied
+    h2d_bytes = int(eng.info().last_h2d_bytes)
     te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -336,7 +338,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_block(args.config, p, world, B),
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": B * DESC_DTYPE.itemsize,
+                    "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64},
             "gpu_launches": int(launches),
             "roofline": rf,

@@ -248,6 +248,19 @@ __global__ void __launch_bounds__(SIMT_THREADS, HESP_SIMT_MIN_BLOCKS)
   }
 }
 
+// Host descriptors travel packed (offsets + the used ops only: a C2
+// descriptor averages ~40 of its 520 bytes); this expands them in HBM.
+__global__ void unpack_descs(const uint32_t* __restrict__ off, const hesp_op* __restrict__ ops,
+                             unsigned long long count, hesp_cand_desc* __restrict__ out) {
+  const unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const uint32_t o = off[i], n = off[i + 1] - o;
+  hesp_cand_desc* d = out + i;
+  d->n_ops = (int32_t)n;
+  d->reserved = 0;
+  for (uint32_t k = 0; k < n; ++k) d->ops[k] = ops[o + k];
+}
+
 __global__ void init_best(WarpBest* __restrict__ wb, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) wb[i] = WarpBest{0.0, -1, 0, 0, 0, 0, 0};
@@ -406,6 +419,9 @@ struct hesp_engine {
   unsigned long long chunk = 0;      // max candidates per chunk (memory budget)
   unsigned long long cslots_n = 0;   // slots currently allocated
   uint32_t* d_order = nullptr;       // LPT order: keys/vals in, keys/vals out (4 x cslots_n)
+  uint8_t* d_pack = nullptr;         // packed host descriptors (hesp_eval_descs)
+  size_t pack_cap = 0;
+  size_t last_h2d_bytes = 0;
   hesp_cand_desc* d_gen = nullptr;   // generated descriptors of one chunk (LPT on generated batches)
   void* d_sort_tmp = nullptr;
   size_t sort_tmp_bytes = 0;
@@ -772,6 +788,7 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_scratch);
   cudaFree(e->d_cslots);
   cudaFree(e->d_order);
+  cudaFree(e->d_pack);
   cudaFree(e->d_sort_tmp);
   cudaFree(e->d_gen);
   for (void* q : e->trace_bufs) cudaFree(q);
@@ -804,6 +821,7 @@ int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info) {
   info->warps_per_block = WARPS_PER_BLOCK;
   info->blocks_per_sm = e->blocks_per_sm;
   info->chunk = e->split ? (int64_t)e->chunk : 0;
+  info->last_h2d_bytes = (int64_t)e->last_h2d_bytes;
   return HESP_OK;
 }
 
@@ -837,11 +855,37 @@ int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
     e->desc_cap = cap;
   }
   if (!grow_out(e, count) || !grow_host(e, count)) return HESP_E_CUDA;
-  std::memcpy(e->h_descs, descs, count * sizeof(hesp_cand_desc));
-  if (!ck(cudaMemcpyAsync(e->d_descs, e->h_descs, count * sizeof(hesp_cand_desc), cudaMemcpyHostToDevice,
-                          e->stream),
-          "descs H2D"))
+  // pack into the pinned staging buffer: offsets[count + 1], then the used ops
+  // (always fits: 4 (count + 1) + 8 * sum(n_ops) <= 520 * count)
+  uint32_t* hoff = reinterpret_cast<uint32_t*>(e->h_descs);
+  hesp_op* hops = reinterpret_cast<hesp_op*>(reinterpret_cast<uint8_t*>(e->h_descs) + ((4 * (count + 1) + 7) & ~7ULL));
+  uint32_t tot = 0;
+  for (uint64_t i = 0; i < count; ++i) {
+    hoff[i] = tot;
+    int n = descs[i].n_ops;
+    n = n < 0 ? 0 : (n > HESP_MAX_OPS ? HESP_MAX_OPS : n);
+    std::memcpy(hops + tot, descs[i].ops, (size_t)n * sizeof(hesp_op));
+    tot += (uint32_t)n;
+  }
+  hoff[count] = tot;
+  const size_t ops_at = (4 * (count + 1) + 7) & ~7ULL;
+  const size_t bytes = ops_at + (size_t)tot * sizeof(hesp_op);
+  if (bytes > e->pack_cap) {
+    if (e->d_pack) cudaFree(e->d_pack);
+    e->d_pack = nullptr;
+    const size_t cap = grown(bytes, e->pack_cap);
+    if (!ck(cudaMalloc(&e->d_pack, cap), "malloc pack")) return HESP_E_CUDA;
+    e->pack_cap = cap;
+  }
+  if (!ck(cudaMemcpyAsync(e->d_pack, e->h_descs, bytes, cudaMemcpyHostToDevice, e->stream), "descs H2D"))
     return HESP_E_CUDA;
+  e->last_h2d_bytes = bytes;
+  if (count) {
+    unpack_descs<<<(unsigned)((count + 255) / 256), 256, 0, e->stream>>>(
+        reinterpret_cast<const uint32_t*>(e->d_pack), reinterpret_cast<const hesp_op*>(e->d_pack + ops_at), count,
+        e->d_descs);
+    e->launches += 1;
+  }
   int r = launch_eval(e, e->d_descs, first_index, count, e->d_out, e->stream);
   if (r) return r;
   if (!ck(cudaMemcpyAsync(e->h_out, e->d_out, count * sizeof(hesp_outcome), cudaMemcpyDeviceToHost, e->stream),
