@@ -364,6 +364,20 @@ int hesp_solve_batch(hesp_engine* e, int32_t n_chains, const hesp_cand_desc* ini
  * PyTorch's).  NCCL is resolved at run time (libnccl.so.2), not linked. */
 int hesp_min_reduce(hesp_engine* e, void* nccl_comm, hesp_best* best);
 
+/* ---------------------------------------------------------------------------
+ * Neighbours of built states (local search, the solver's batches): candidate
+ * k is bases[nbrs[k].base] followed by its own 1-2 extra ops.  Each base is
+ * expanded once into a template slot; every neighbour copies it and applies
+ * only its extra ops.  Outcomes equal hesp_eval_descs on the concatenated
+ * descriptors (same ids, blocks and schedules), index k = first + k. */
+typedef struct {
+  int32_t base;    /* index into bases */
+  int32_t n_ops;   /* 0..2 extra ops */
+  hesp_op ops[2];
+} hesp_neighbor;
+int hesp_eval_neighbors(hesp_engine* e, const hesp_cand_desc* bases, int32_t n_bases, const hesp_neighbor* nbrs,
+                        uint64_t count, hesp_outcome* out, hesp_best* best);
+
 /* Engine facts: kernel launches issued so far, base tiling sizes, slots. */
 typedef struct {
   int64_t kernel_launches;

@@ -2568,6 +2568,58 @@ struct Engine {
       if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
       else apply_op(d.ops[k].task, d.ops[k].s);
     }
+    finish_build();
+  }
+
+  // Neighbour evaluation (hesp_eval_neighbors): a base state's op sequence is
+  // applied once into a template slot (build_template); each neighbour copies
+  // the template's graph arrays and applies only its own extra ops.  Same
+  // ids, blocks and hash-table contents as replaying every op.
+  HXN void build_template(const hesp_cand_desc& d) {
+    reset_to_base();
+    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
+      if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
+      else apply_op(d.ops[k].task, d.ops[k].s);
+    }
+    if (wp.lane() == 0) {
+      SlotHeader h{};
+      h.status = status;
+      h.ntasks = ntasks;
+      h.nblocks = nblocks;
+      h.pad = npart;
+      *hdr() = h;
+    }
+    wp.sync();
+  }
+  HXN void build_neighbor(const uint8_t* tslot, int n_extra, const hesp_op* extra) {
+    const SlotHeader th = *(const SlotHeader*)(tslot + PB.lay.hdr);
+    auto copy = [&](size_t off, size_t bytes) {  // 4-byte words, lane-strided
+      const uint32_t* src = (const uint32_t*)(tslot + off);
+      uint32_t* dst = (uint32_t*)(slot + off);
+      NOUNROLL for (size_t i = wp.lane(); i < bytes / 4; i += WP::W) dst[i] = src[i];
+    };
+    const int nt = th.ntasks - nbt, nb = th.nblocks - nbb;
+    copy(PB.lay.tm, sizeof(TaskMeta) * (size_t)(nt > 0 ? nt : 0));
+    copy(PB.lay.bm, sizeof(BlockMeta) * (size_t)(nb > 0 ? nb : 0));
+    copy(PB.lay.bref, 4 * (size_t)(nb > 0 ? nb : 0));
+    copy(PB.lay.rht, 2 * (size_t)RHT);
+    copy(PB.lay.part, sizeof(PartEntry) * (size_t)th.pad);
+    copy(PB.lay.tmis, ((size_t)nbb + 3) & ~(size_t)3);
+    wp.sync();
+    status = th.status;
+    ntasks = th.ntasks;
+    nblocks = th.nblocks;
+    npart = th.pad;
+    makespan = 0.0;
+    ahash = xhash = 0;
+    NOUNROLL for (int k = 0; k < n_extra && !status; ++k) {
+      if (extra[k].s == HESP_OP_MERGE) apply_merge(extra[k].task);
+      else apply_op(extra[k].task, extra[k].s);
+    }
+    finish_build();
+  }
+
+  HXN void finish_build() {
     sum_k = 0;
     nleaves = 0;
     nedges = 0;

@@ -130,6 +130,39 @@ __global__ void order_keys(const uint8_t* __restrict__ slots, unsigned long long
   vals[k] = (uint32_t)k;
 }
 
+__global__ void template_kernel(const hesp_cand_desc* __restrict__ bases, uint8_t* tslots) {
+  __shared__ Small smem;
+  __shared__ hesp_cand_desc sd;
+  const int b = blockIdx.x;
+  if (threadIdx.x == 0) sd = bases[b];
+  __syncwarp();
+  Engine<DevWarp> eng(DevWarp{}, c_problem, tslots + (size_t)b * c_problem.lay.total, &smem);
+  eng.build_template(sd);
+}
+
+__global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
+    neighbor_build_kernel(const hesp_neighbor* __restrict__ nbrs, const uint8_t* __restrict__ tslots,
+                          unsigned long long count, uint8_t* slots, unsigned long long* counter) {
+  __shared__ Small smem[WARPS_PER_BLOCK];
+  __shared__ hesp_neighbor snb[WARPS_PER_BLOCK];
+  const int wib = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const Problem& pb = c_problem;
+  for (;;) {
+    unsigned long long k = 0;
+    if (lane == 0) k = atomicAdd(counter, 1ULL);
+    k = __shfl_sync(0xffffffffu, k, 0);
+    if (k >= count) break;
+    if (lane < 6) ((int32_t*)&snb[wib])[lane] = ((const int32_t*)(nbrs + k))[lane];
+    __syncwarp();
+    const hesp_neighbor& nb = snb[wib];
+    const int n_ops = nb.n_ops < 0 ? 0 : (nb.n_ops > 2 ? 2 : nb.n_ops);
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    eng.build_neighbor(tslots + (size_t)nb.base * pb.lay.total, n_ops, nb.ops);
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
                WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter,
@@ -419,6 +452,10 @@ struct hesp_engine {
   unsigned long long chunk = 0;      // max candidates per chunk (memory budget)
   unsigned long long cslots_n = 0;   // slots currently allocated
   uint32_t* d_order = nullptr;       // LPT order: keys/vals in, keys/vals out (4 x cslots_n)
+  uint8_t* d_tslots = nullptr;       // template slots of hesp_eval_neighbors' bases
+  int tslots_n = 0;
+  hesp_neighbor* d_nbrs = nullptr;
+  size_t nbr_cap = 0;
   uint8_t* d_pack = nullptr;         // packed host descriptors (hesp_eval_descs)
   size_t pack_cap = 0;
   size_t last_h2d_bytes = 0;
@@ -495,7 +532,8 @@ bool grow_host(hesp_engine* e, size_t n) {
 }
 
 int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, uint64_t count,
-                 hesp_outcome* d_out, cudaStream_t st) {
+                 hesp_outcome* d_out, cudaStream_t st, const hesp_neighbor* d_nbrs = nullptr,
+                 const uint8_t* d_tslots = nullptr) {
   // equal-size chunks under the memory cap: each chunk pays one load-balance tail
   const unsigned long long nchunks = count ? (count + e->chunk - 1) / e->chunk : 1;
   const unsigned long long per = count ? (count + nchunks - 1) / nchunks : 1;  // equal-size chunks
@@ -539,7 +577,7 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     const bool timed = ci < hesp_engine::NEV;
     if (timed) cudaEventRecord(e->evc[ci][0], st);
     const hesp_cand_desc* cd = d_descs ? d_descs + c0 : nullptr;
-    if (e->lpt && !cd && n > 1) {  // generated candidates: materialise the descriptors to order them
+    if (e->lpt && !cd && !d_nbrs && n > 1) {  // generated candidates: materialise the descriptors to order them
       if (!e->d_gen) {
         if (!ck(cudaMalloc(&e->d_gen, e->cslots_n * sizeof(hesp_cand_desc)), "malloc gen descs")) return HESP_E_CUDA;
       }
@@ -559,8 +597,12 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
       border = vout;
       e->launches += 1;
     }
-    build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(cd, first + c0, n, e->d_cslots, e->d_counter,
-                                                                 border);
+    if (d_nbrs)
+      neighbor_build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(d_nbrs + c0, d_tslots, n,
+                                                                            e->d_cslots, e->d_counter);
+    else
+      build_kernel<<<e->n_build_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(cd, first + c0, n, e->d_cslots,
+                                                                   e->d_counter, border);
     const uint32_t* order = nullptr;
     if (e->lpt && n > 1) {
       uint32_t* kin = e->d_order;
@@ -789,6 +831,8 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_cslots);
   cudaFree(e->d_order);
   cudaFree(e->d_pack);
+  cudaFree(e->d_tslots);
+  cudaFree(e->d_nbrs);
   cudaFree(e->d_sort_tmp);
   cudaFree(e->d_gen);
   for (void* q : e->trace_bufs) cudaFree(q);
@@ -894,6 +938,59 @@ int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
   r = finish_best(e, best, e->stream);
   if (r) return r;
   if (!ck(cudaStreamSynchronize(e->stream), "sync")) return HESP_E_CUDA;
+  if (out) std::memcpy(out, e->h_out, count * sizeof(hesp_outcome));
+  return HESP_OK;
+}
+
+int hesp_eval_neighbors(hesp_engine* e, const hesp_cand_desc* bases, int32_t n_bases, const hesp_neighbor* nbrs,
+                        uint64_t count, hesp_outcome* out, hesp_best* best) {
+  if (!e || !bases || n_bases < 1 || (!nbrs && count)) return HESP_E_INVALID;
+  for (uint64_t k = 0; k < count; ++k)
+    if (nbrs[k].base < 0 || nbrs[k].base >= n_bases) {
+      g_last_error = "hesp_eval_neighbors: base index out of range";
+      return HESP_E_INVALID;
+    }
+  cudaSetDevice(e->device);
+  cudaStream_t st = e->stream;
+  if (n_bases > e->tslots_n) {
+    if (e->d_tslots) cudaFree(e->d_tslots);
+    e->d_tslots = nullptr;
+    e->tslots_n = 0;
+    if (!ck(cudaMalloc(&e->d_tslots, (size_t)n_bases * e->L.total), "malloc template slots")) return HESP_E_CUDA;
+    e->tslots_n = n_bases;
+  }
+  if (count > e->nbr_cap) {
+    if (e->d_nbrs) cudaFree(e->d_nbrs);
+    e->d_nbrs = nullptr;
+    const size_t cap = grown(count, e->nbr_cap);
+    if (!ck(cudaMalloc(&e->d_nbrs, cap * sizeof(hesp_neighbor)), "malloc neighbours")) return HESP_E_CUDA;
+    e->nbr_cap = cap;
+  }
+  if ((size_t)n_bases > e->desc_cap) {
+    if (e->d_descs) cudaFree(e->d_descs);
+    e->d_descs = nullptr;
+    const size_t cap = grown((size_t)n_bases, e->desc_cap);
+    if (!ck(cudaMalloc(&e->d_descs, cap * sizeof(hesp_cand_desc)), "malloc descs")) return HESP_E_CUDA;
+    e->desc_cap = cap;
+  }
+  if (!grow_out(e, count) || !grow_host(e, count)) return HESP_E_CUDA;
+  bool ok = ck(cudaMemcpyAsync(e->d_descs, bases, (size_t)n_bases * sizeof(hesp_cand_desc), cudaMemcpyHostToDevice,
+                               st), "bases H2D") &&
+            (!count || ck(cudaMemcpyAsync(e->d_nbrs, nbrs, count * sizeof(hesp_neighbor), cudaMemcpyHostToDevice, st),
+                          "neighbours H2D")) &&
+            ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st),
+               "problem -> constant");
+  if (!ok) return HESP_E_CUDA;
+  template_kernel<<<n_bases, 32, 0, st>>>(e->d_descs, e->d_tslots);
+  e->launches += 1;
+  int r = launch_split(e, nullptr, 0, count, e->d_out, st, e->d_nbrs, e->d_tslots);
+  if (r) return r;
+  if (!ck(cudaMemcpyAsync(e->h_out, e->d_out, count * sizeof(hesp_outcome), cudaMemcpyDeviceToHost, st),
+          "outcomes D2H"))
+    return HESP_E_CUDA;
+  r = finish_best(e, best, st);
+  if (r) return r;
+  if (!ck(cudaStreamSynchronize(st), "sync")) return HESP_E_CUDA;
   if (out) std::memcpy(out, e->h_out, count * sizeof(hesp_outcome));
   return HESP_OK;
 }

@@ -229,7 +229,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.part = take(sizeof(PartEntry) * MAXPART);
   L.dstack = take(3 * 4 * (size_t)MAXPART);
   L.small = take(SMALL_BYTES);  // per-candidate Small of the thread-per-candidate simulate kernel
-  L.tmis = take(NB);            // per base tile: holds a non-dyadic block (partial overlaps possible)
+  L.tmis = take((NB + 3) & ~(size_t)3);  // per base tile: holds a non-dyadic block (partial overlaps possible)
   L.wrt = take(B);              // per block: written since t=0 (gather's coherence check)
   L.pmk = take(4 * T);          // per task: last task whose predecessor list took it (dedup)
   L.valid = take(8 * B * S);

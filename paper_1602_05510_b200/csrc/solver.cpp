@@ -330,7 +330,8 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
     ch.S.resize(2 * (size_t)P.maxt + 2);
     iters = std::max(iters, ch.cfg.iterations);
   }
-  std::vector<hesp_cand_desc> states, batch;
+  std::vector<hesp_cand_desc> states;
+  std::vector<hesp_neighbor> nbrs;
   std::vector<hesp_outcome> souts, outc;
   std::vector<TraceGraph> graphs;
   std::vector<hx::TraceLogs> logs;
@@ -345,7 +346,6 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
       }
     int r = hx::schedule_batch(e, states.data(), (int)states.size(), graphs, logs, souts);
     if (r != HESP_OK) return r;
-    batch.clear();
     for (size_t q = 0; q < live.size(); ++q)
       if (souts[q].status != 0) return souts[q].status;  // only an initial state can fail
     // per-chain host work (post-passes, scoring) is independent: spread the
@@ -382,16 +382,24 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
       for (auto& t : pool) t.join();
     }
     if (err) return err;
+    // ---- validity filter: every chain's mutations in one device batch, as
+    // neighbours of the chain states (each state expanded once on the device)
+    nbrs.clear();
     for (size_t q = 0; q < live.size(); ++q) {
       Chain& ch = chains[live[q]];
-      ch.first = batch.size();
-      for (const Cand& cd : ch.cands) batch.push_back(mutate(ch.cur, cd));
+      ch.first = nbrs.size();
+      for (const Cand& cd : ch.cands) {
+        hesp_neighbor nb{};
+        nb.base = (int32_t)q;
+        if (cd.action != HESP_ACT_PARTITION) nb.ops[nb.n_ops++] = hesp_op{cd.target, HESP_OP_MERGE};
+        if (cd.action != HESP_ACT_MERGE) nb.ops[nb.n_ops++] = hesp_op{cd.parent, cd.k};
+        nbrs.push_back(nb);
+      }
     }
-    // ---- validity filter: every chain's mutations in one device batch ----
-    if (!batch.empty()) {
-      outc.resize(batch.size());
+    if (!nbrs.empty()) {
+      outc.resize(nbrs.size());
       hesp_best b{};
-      r = hesp_eval_descs(e, batch.data(), batch.size(), 0, outc.data(), &b);
+      r = hesp_eval_neighbors(e, states.data(), (int32_t)states.size(), nbrs.data(), nbrs.size(), outc.data(), &b);
       if (r != 0) return r;
     }
     for (int c : live) {

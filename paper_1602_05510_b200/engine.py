@@ -182,6 +182,8 @@ class Trace:
         return out
 
 
+NEIGHBOR_DTYPE = np.dtype([("base", "<i4"), ("n_ops", "<i4"), ("ops", "<i4", (2, 2))])
+
 OUTCOME_DTYPE = np.dtype([("status", "<i4"), ("n_leaves", "<i4"), ("makespan", "<f8"),
                           ("assign_hash", "<u8"), ("xfer_hash", "<u8")])
 assert OUTCOME_DTYPE.itemsize == C.sizeof(Outcome) == 32
@@ -191,7 +193,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_solve_batch", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_solve_batch", "hesp_eval_neighbors", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
     "hesp_fixture_load", "hesp_fixture_platform", "hesp_fixture_model", "hesp_fixture_free",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
@@ -226,6 +228,8 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
     lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
     lib.hesp_solve_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
+    lib.hesp_eval_neighbors.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p,
+                                        C.POINTER(Best)]
     lib.hesp_fixture_load.restype = C.c_void_p
     lib.hesp_fixture_load.argtypes = [C.c_char_p, C.c_char_p]
     lib.hesp_fixture_platform.restype = C.POINTER(PlatformC)
@@ -556,6 +560,16 @@ class BatchEngine:
             out.append((hists[i][:res[i].n_history].copy(), best, float(res[i].best_makespan),
                         int(res[i].best_iteration), int(res[i].n_simulated)))
         return out
+
+    def eval_neighbors(self, bases: np.ndarray, nbrs: np.ndarray):
+        """hesp_eval_neighbors: candidate k = bases[nbrs[k].base] + nbrs[k].ops[:n_ops]."""
+        bases = np.ascontiguousarray(bases, DESC_DTYPE)
+        nbrs = np.ascontiguousarray(nbrs, NEIGHBOR_DTYPE)
+        out = np.zeros(len(nbrs), OUTCOME_DTYPE)
+        best = Best()
+        self._check(self.lib.hesp_eval_neighbors(self.h, bases.ctypes.data, len(bases), nbrs.ctypes.data, len(nbrs),
+                                                 out.ctypes.data, C.byref(best)), "eval_neighbors")
+        return out, best
 
     def generate_host(self, first: int, count: int) -> np.ndarray:
         d = np.zeros(count, DESC_DTYPE)

@@ -182,3 +182,38 @@ def test_engine_from_cpp_loaded_fixtures(lib, name):
                                  sched, wl)
     out, _ = eng.eval_generated(0, count)
     assert not compare(out, read_golden(name))
+
+
+def test_neighbors_equal_replayed_descriptors(lib):
+    """hesp_eval_neighbors (template state + 1-2 extra ops, merges included)
+    gives exactly the outcome records of replaying the full descriptors."""
+    from paper_1602_05510_b200.engine import NEIGHBOR_DTYPE, OP_MERGE
+    p, _ = PARITY["merge_c2"]
+    eng = make_engine(p)
+    bases = eng.generate_host(0, 6)
+    rng = np.random.default_rng(7)
+    nb = np.zeros(3000, NEIGHBOR_DTYPE)
+    full = np.zeros(3000, bases.dtype)
+    for k in range(3000):
+        b = int(rng.integers(0, len(bases)))
+        base = bases[b]
+        n0 = int(base["n_ops"])
+        m = int(rng.integers(0, 3))
+        ops = []
+        for _ in range(m):
+            if rng.random() < 0.25:
+                ops.append((int(rng.integers(0, 6)), OP_MERGE))
+            else:
+                ops.append((int(rng.integers(1, 1400)), int(rng.choice([2, 3, 4]))))
+        nb[k]["base"], nb[k]["n_ops"] = b, m
+        for i, o in enumerate(ops):
+            nb[k]["ops"][i] = o
+        full[k] = base
+        full[k]["n_ops"] = n0 + m
+        for i, o in enumerate(ops):
+            full[k]["ops"][n0 + i] = o
+    a, ba = eng.eval_neighbors(bases, nb)
+    r, br = eng.eval_descs(full)
+    assert a.tobytes() == r.tobytes()
+    assert (ba.makespan, ba.index, ba.n_ok) == (br.makespan, br.index, br.n_ok)
+    assert len(np.unique(a["status"])) > 1  # the mix hits error statuses too
