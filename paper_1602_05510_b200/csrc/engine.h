@@ -469,8 +469,10 @@ struct Engine {
       }
       return found;
     }
-    if (rsame(reg(0), r)) return 0;
-    if (rsame(reg(t), r)) return t;
+    if (r.rows >= PB.base_b || r.cols >= PB.base_b) {  // only a tile- or root-sized region can be either
+      if (rsame(reg(0), r)) return 0;
+      if (rsame(reg(t), r)) return t;
+    }
     if (rht_usable()) {  // open addressing over the candidate's own blocks
       unsigned i = rhash(r) & (RHT - 1);
       NOUNROLL for (;;) {
