@@ -278,6 +278,11 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* trac
 int hesp_verify_trace(const hesp_engine* e, const hesp_trace* trace, char* buf, size_t cap,
                       int32_t* n_violations);
 
+/* Makespan lower bounds of the candidate last passed to hesp_eval_trace
+ * (SPEC.md acceptance 5): *cp = longest dependence path with every task at
+ * its fastest processor type's time; *work = sum of those times / processors. */
+int hesp_trace_bounds(const hesp_engine* e, double* cp, double* work);
+
 /* ---------------------------------------------------------------------------
  * Iterative schedule/partition solver (the reference
  * declares it only: solver.hpp:57-86, semantics SPEC.md:410-461).  A chain

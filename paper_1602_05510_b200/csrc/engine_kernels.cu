@@ -1244,6 +1244,15 @@ const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e) { return e->l
 
 extern "C" {
 
+int hesp_trace_bounds(const hesp_engine* e, double* cp, double* work) {
+  if (!e || !cp || !work || !e->last_graph.valid) {
+    g_last_error = "hesp_trace_bounds needs a successful hesp_eval_trace first";
+    return HESP_E_INVALID;
+  }
+  hx::trace_bounds(e->hp.p, e->last_graph, cp, work);
+  return HESP_OK;
+}
+
 int hesp_verify_trace(const hesp_engine* e, const hesp_trace* tr, char* buf, size_t cap, int32_t* n_violations) {
   if (!e || !tr || !e->last_graph.valid) {
     g_last_error = "hesp_verify_trace needs a successful hesp_eval_trace first";

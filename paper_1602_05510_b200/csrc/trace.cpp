@@ -398,4 +398,35 @@ std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, con
   return violations;
 }
 
+void trace_bounds(const Problem& p, const TraceGraph& g, double* cp, double* work) {
+  const int n = (int)g.leaves.size();
+  std::unordered_map<int, int> li;
+  for (int k = 0; k < n; ++k) li[g.leaves[k]] = k;
+  std::vector<double> tmin(n, 0.0), fin(n, 0.0);
+  double w = 0;
+  for (int k = 0; k < n; ++k) {
+    const TaskMeta& m = g.meta[k];
+    double best = -1;
+    for (int ty = 0; ty < p.n_types; ++ty) {
+      const double t = p.ttime[m.kind][m.bidx][ty];
+      if (p.known[m.kind][ty] && (best < 0 || t < best)) best = t;
+    }
+    tmin[k] = best < 0 ? 0.0 : best;
+    w += tmin[k];
+  }
+  // leaves are in program order, so every predecessor precedes its task
+  double longest = 0;
+  for (int k = 0; k < n; ++k) {
+    double ready = 0;
+    for (int q = 0; q < g.pcnt[k]; ++q) {
+      auto it = li.find(g.preds[g.poff[k] + q]);
+      if (it != li.end() && fin[it->second] > ready) ready = fin[it->second];
+    }
+    fin[k] = ready + tmin[k];
+    if (fin[k] > longest) longest = fin[k];
+  }
+  *cp = longest;
+  *work = p.P > 0 ? w / p.P : 0.0;
+}
+
 }  // namespace hx

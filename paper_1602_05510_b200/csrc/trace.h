@@ -38,6 +38,9 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
 // verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph.
 std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr);
 
+// Critical-path and work lower bounds of the traced graph (fastest type per task).
+void trace_bounds(const Problem& p, const TraceGraph& g, double* cp, double* work);
+
 }  // namespace hx
 
 namespace hx {

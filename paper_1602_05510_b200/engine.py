@@ -193,7 +193,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_solve", "hesp_solve_batch", "hesp_eval_neighbors", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_trace_bounds", "hesp_solve", "hesp_solve_batch", "hesp_eval_neighbors", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
     "hesp_fixture_load", "hesp_fixture_platform", "hesp_fixture_model", "hesp_fixture_free",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
@@ -226,6 +226,7 @@ def load_library(path: str = LIB) -> C.CDLL:
     lib.hesp_engine_get_info.argtypes = [C.c_void_p, C.POINTER(EngineInfo)]
     lib.hesp_eval_trace.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(TraceC)]
     lib.hesp_solve.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(SolverConfigC), C.POINTER(SolverResultC)]
+    lib.hesp_trace_bounds.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.hesp_min_reduce.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(Best)]
     lib.hesp_solve_batch.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]
     lib.hesp_eval_neighbors.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_uint64, C.c_void_p,
@@ -487,6 +488,12 @@ class BatchEngine:
                          a[:t.n_assign].copy(), x[:t.n_xfer].copy(), e[:t.n_events].copy(), r[:t.n_res].copy(),
                          st[:t.n_steps].copy(), float(t.busy_time), float(t.avg_load), float(t.load_integral))
         raise RuntimeError("eval_trace: could not size the trace arrays")
+
+    def trace_bounds(self) -> tuple[float, float]:
+        """(critical-path, work) makespan lower bounds of the last eval_trace candidate."""
+        cp, w = C.c_double(), C.c_double()
+        self._check(self.lib.hesp_trace_bounds(self.h, C.byref(cp), C.byref(w)), "trace_bounds")
+        return cp.value, w.value
 
     def verify_trace(self, trace: Trace) -> list[str]:
         """verify_schedule of `trace` (possibly edited) against the graph of the last eval_trace."""

@@ -69,13 +69,15 @@ def test_schedules_verify_and_respect_work_bound(lib, name):
     plat = json.load(open(os.path.join(FIXTURES, p["platform"])))
     types = [t["name"] for t in plat["types"]]
     P = len(plat["processors"])
-    descs = eng.generate_host(50_000, 16)
+    descs = eng.generate_host(50_000, 64)  # 8 presets x 64 = 512 randomized simulations
     checked = 0
     for d in descs:
         tr = eng.eval_trace(d)
         if tr.status:
             continue
         assert eng.verify_trace(tr) == []
+        cp, wb = eng.trace_bounds()
+        assert tr.makespan >= cp * (1 - 1e-12) and tr.makespan >= wb * (1 - 1e-12)
         if model.analytic is not None:
             work = 0.0
             for e in tr.events:
@@ -141,3 +143,20 @@ def test_merge_round_trip_and_flop_conservation(lib):
             if int(e["kind"]) == 0:
                 fl += task_flops(int(e["task_kind"]), int(e["b"]))
         assert abs(fl - n ** 3 / 3.0) <= 1e-9 * n ** 3 / 3.0
+
+
+def test_dag_depths_figure3(lib):
+    """Acceptance 8 (Figure 3, from the base tiling on): the base tiling has
+    depth 1, partitioning a base task makes 2, a second base task keeps 2, a
+    sub-task of the first makes 3 (IterationRecord.dag_depth of one round)."""
+    from paper_1602_05510_b200.engine import DESC_DTYPE
+    p, _ = PARITY["c2"]
+    eng = make_engine(p)
+    want = {(): 1, ((1, 2),): 2, ((1, 2), (2, 2)): 2, ((1, 2), (817, 2)): 3}
+    for ops, depth in want.items():
+        d = np.zeros(1, DESC_DTYPE)
+        d[0]["n_ops"] = len(ops)
+        for i, o in enumerate(ops):
+            d[0]["ops"][i] = o
+        hist, *_ = eng.solve(1, "All", "Hard", 0, initial=d[0])
+        assert int(hist[0]["dag_depth"]) == depth, ops
