@@ -73,3 +73,22 @@ def test_batched_chains_equal_single_solves(lib):
         h1, best1, mk1, it1, n1 = eng.solve(c["iterations"], c["task_selection"], c["sampling"], c["seed"])
         assert h.tobytes() == h1.tobytes()
         assert (mk, it, n) == (mk1, it1, n1) and best.tobytes() == best1.tobytes()
+
+
+def test_table1_desk_scale(lib):
+    """SPEC acceptance 9 at desk scale (1 fast + 4 slow processors, 8x speed
+    ratio, n = 4096): started from the best homogeneous uniform tiling over
+    s in {2, 4, 8, 16}, the solver (All/Soft, 200 iterations) improves on it
+    strictly for FCFS/R-P and never loses for PL/EFT-P."""
+    from paper_1602_05510_b200.configs import preset
+    fix = ("platform_fastslow.json", "model_fastslow.json")
+    for ordering, selection, strict in [("FCFS", "R-P", True), ("PL", "EFT-P", False)]:
+        homo = {}
+        for s in (2, 4, 8, 16):
+            eng = make_engine(preset(fix, 4096, 8, s, 0, ordering=ordering, selection=selection, sched_seed=1))
+            o, _ = eng.eval_generated(0, 1)
+            homo[s] = float(o[0]["makespan"])
+        best_s = min(homo, key=homo.get)
+        eng = make_engine(preset(fix, 4096, 8, best_s, 0, ordering=ordering, selection=selection, sched_seed=1))
+        hist, best, mk, it, _ = eng.solve(200, "All", "Soft", 0)
+        assert mk < homo[best_s] if strict else mk <= homo[best_s], (ordering, mk, homo)
