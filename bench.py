@@ -135,22 +135,71 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows)}
 
 
-def roofline(best_steps, kernel_ms, P, S, n_types, peak_gbs, peak_kind, traffic):
-    # Algorithmic scheduler-state bytes per batch:
-    #   B = 8 * sum_t (P + S*k_t + n_types + 4) + 12 * E
+def algorithmic_bytes(best_steps, P, S, n_types):
+    """Scheduler-state bytes per launch:
+    B_smem = 8 * sum_t (P + S*k_t + n_types + 4) + 12 * E, summed over the
+    candidates of one step from the engine's own counts (leaves, k_t, edges)."""
     leaves = sum(b.sum_leaves for b in best_steps)
     ksum = sum(b.sum_k for b in best_steps)
     edges = sum(b.sum_edges for b in best_steps)
-    B = 8 * (leaves * (P + n_types + 4) + S * ksum) + 12 * edges
-    per_launch = B / len(best_steps)
+    return (8 * (leaves * (P + n_types + 4) + S * ksum) + 12 * edges) / len(best_steps)
+
+
+def roofline(best_steps, kernel_ms, P, S, n_types, sm_count, clk, traffic):
+    """§8(d)'s binding roofline: the event loop's scheduler-state accesses
+    against the chip's shared-memory bandwidth, 128 B/clk per SM at the SM
+    clock sampled during the timed region (the kernel is neither HBM- nor
+    tensor-bound: compulsory HBM traffic is a descriptor in, 32 B out)."""
+    per_launch = algorithmic_bytes(best_steps, P, S, n_types)
+    ms = statistics.mean(kernel_ms)
+    achieved = per_launch / (ms * 1e-3) / 1e9
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = sm_count * 128 * mhz * 1e6 / 1e9
+    return {"bound": "smem", "achieved": round(achieved, 3), "peak": round(peak, 1), "unit": "GB/s",
+            "frac": round(achieved / peak, 6), "traffic": traffic,
+            "peak_source": f"{sm_count} SMs x 128 B/clk x {mhz:.0f} MHz (sampled SM clock, SURVEY.md §8d)",
+            "algorithmic_bytes_per_launch": int(per_launch),
+            "kernel": "sim_kernel (event loop; summed over the step's chunks)",
+            "kernel_ms_per_launch": round(ms, 4)}
+
+
+def hbm_roofline(best_steps, kernel_ms, P, S, n_types, peak_gbs, peak_kind, traffic):
+    """The same bytes against the measured HBM copy bandwidth (the contract's
+    default denominator), with the ncu DRAM traffic of the same kernel."""
+    per_launch = algorithmic_bytes(best_steps, P, S, n_types)
     ms = statistics.mean(kernel_ms)
     achieved = per_launch / (ms * 1e-3) / 1e9
     return {"bound": "hbm", "achieved": round(achieved, 3), "peak": peak_gbs, "unit": "GB/s",
-            "frac": round(achieved / peak_gbs, 6), "traffic": traffic, "peak_source": peak_kind,
-            "algorithmic_bytes_per_launch": int(per_launch), "kernel": "sim_kernel (event loop; summed over the step's chunks)",
-            "kernel_ms_per_launch": round(ms, 4),
-            "note": ("latency-bound serial event loop (one warp per candidate); neither HBM nor tensor "
-                     "bound — issue-slot and memory-latency evidence in profiles/")}
+            "frac": round(achieved / peak_gbs, 6), "traffic": traffic, "peak_source": peak_kind}
+
+
+def verify_winner(eng, p, index, makespan):
+    """Re-run the reported winner through the unmodified reference
+    (oracle/_ref/ref_harness, outside the timed region) and through the
+    engine's host-buffer path; the two 40-byte records must be identical."""
+    import tempfile
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from golden_io import read_golden
+    from paper_1602_05510_b200.configs import harness_args
+    from paper_1602_05510_b200.engine import FIXTURES
+    if index < 0:
+        return {"winner_verified": False, "why": "no valid candidate"}
+    if not os.path.exists(HARNESS):
+        return {"winner_verified": False, "why": "oracle/_ref/ref_harness not built"}
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "w.bin")
+        subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--first", str(index), "--count", "1",
+                        "--threads", "1", "--out", path], check=True, capture_output=True)
+        ref = read_golden(path)[0]
+    out, _ = eng.eval_descs(eng.generate_host(index, 1), first=index)
+    o = out[0]
+    same = (int(o["status"]) == int(ref["status"]) == 0 and int(o["n_leaves"]) == int(ref["n_leaves"])
+            and np.float64(o["makespan"]).view("<u8") == np.float64(ref["makespan"]).view("<u8")
+            and np.float64(makespan).view("<u8") == np.float64(ref["makespan"]).view("<u8")
+            and int(o["assign_hash"]) == int(ref["assign_hash"]) and int(o["xfer_hash"]) == int(ref["xfer_hash"]))
+    return {"winner_verified": bool(same), "reference_makespan": float(ref["makespan"]),
+            "reference_assign_hash": f"{int(ref['assign_hash']):016x}", "reference_xfer_hash": f"{int(ref['xfer_hash']):016x}"}
 
 
 def issue_roofline(config, value, sm_count, clk):
@@ -172,6 +221,17 @@ def issue_roofline(config, value, sm_count, clk):
     ach = per_cand * value
     return {"bound": "issue", "achieved": ach, "peak": peak, "unit": "warp-inst/s", "frac": round(ach / peak, 4),
             "warp_inst_per_candidate": ipc, "source": "profiles/ncu_issue.json (" + d.get("source", "ncu") + ")"}
+
+
+def ncu_smem(config):
+    """Shared-memory and issue counters of the sim kernel from the committed
+    ncu capture of this config (profiles/ncu_smem.json), if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_smem.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    return d if d.get("config") == config else None
 
 
 def ncu_traffic(config, batch):
@@ -232,8 +292,8 @@ def main():
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1602_05510_b200.dist import init_nccl
+    init_nccl(local)  # also at N=1: the winner always goes through hesp_min_reduce over NCCL
 
     from paper_1602_05510_b200.build import build
     from paper_1602_05510_b200.configs import make_engine
@@ -319,9 +379,12 @@ def main():
     if rank == 0:
         peak, peak_kind, _ = measured_peaks()
         P = eng._pc.n_procs
-        rf = roofline(bests, kernel_ms, P, eng._pc.n_spaces, eng._pc.n_types, peak, peak_kind,
-                      ncu_traffic(args.config, B))
+        traffic = ncu_traffic(args.config, B)
+        rf = roofline(bests, kernel_ms, P, eng._pc.n_spaces, eng._pc.n_types, info.sm_count, clk, traffic)
         rf["build_kernel_ms_per_step"] = round(statistics.mean(build_ms), 4) if build_ms else None
+        rf["ncu"] = ncu_smem(args.config)
+        hrf = hbm_roofline(bests, kernel_ms, P, eng._pc.n_spaces, eng._pc.n_types, peak, peak_kind, traffic)
+        winner = verify_winner(eng, p, winners[-1][1], winners[-1][0])
         cpu = None
         if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
             d, err = cpu_baseline(p, args.cpu_seconds)
@@ -342,18 +405,22 @@ def main():
                     "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64},
             "gpu_launches": int(launches),
             "roofline": rf,
+            "hbm_roofline": hrf,
             "issue_roofline": issue_roofline(args.config, value, info.sm_count, clk),
             "cpu_baseline": cpu,
             "clocks": clk,
             "valid_fraction": n_ok / (B * args.steps),
-            "best": {"makespan": winners[-1][0], "index": winners[-1][1]},
+            "valid_per_s": value * n_ok / (B * args.steps),
+            "counting": "value counts every evaluated candidate (as the reference arm does); valid_per_s only "
+                        "those the reference simulates without an Err (the rest end in CoherenceError)",
+            "best": {"makespan": winners[-1][0], "index": winners[-1][1], **winner},
+            "min_reduce": {"backend": "nccl", "world": world, "calls": int(eng.info().min_reduces)},
             "engine": {"slots": info.n_slots, "sm_count": info.sm_count, "blocks_per_sm": info.blocks_per_sm,
                        "warps_per_block": info.warps_per_block, "slot_bytes": info.slot_bytes,
                        "chunk": info.chunk, "kernels": "build_kernel + sim_kernel per chunk" if info.chunk else "eval_kernel"},
         }
         print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
     return 0
 
 

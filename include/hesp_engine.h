@@ -391,6 +391,7 @@ typedef struct {
   int32_t warps_per_block, blocks_per_sm;
   int64_t chunk;   /* candidates per build/simulate chunk (0 = fused kernel) */
   int64_t last_h2d_bytes; /* bytes the last hesp_eval_descs copied host->device (packed descriptors) */
+  int64_t min_reduces;    /* completed hesp_min_reduce exchanges on this handle */
 } hesp_engine_info;
 int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info);
 

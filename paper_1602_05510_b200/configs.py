@@ -62,6 +62,22 @@ for o, s, c in itertools.product(("FCFS", "PL"), ("R-P", "F-P", "EIT-P", "EFT-P"
                                             sched_seed=5), 24)
 
 
+# At-scale parity (VERDICT r1 "next" #1, SURVEY.md §7 minimum slice >= 1e4):
+# the same generators over many more candidate indices, every record compared
+# bit for bit on the GPU (tests/test_scale_gpu.py).  Sizes follow §8(d)'s
+# sample sizes: 1e4 for C2/C3, 256 for C4, 1e3 per eviction fixture.
+SCALE = {
+    "scale_c2": (C2, 10_000),
+    "scale_c3": (C3, 10_000),
+    "scale_c4": (C4, 256),
+    "scale_evict_wb": (PARITY["evict_wb"][0], 1000),
+    "scale_evict_wt": (PARITY["evict_wt"][0], 1000),
+    "scale_evict_wa": (PARITY["evict_wa"][0], 1000),
+    "scale_merge_c2": (PARITY["merge_c2"][0], 2000),
+    "scale_sect_cpugpu": (PARITY["sect_cpugpu"][0], 2000),
+}
+
+
 def harness_args(p: dict, fixtures_dir: str) -> list[str]:
     """oracle/_ref/ref_harness arguments for preset p."""
     import os

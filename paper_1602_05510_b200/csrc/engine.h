@@ -2566,6 +2566,7 @@ struct Engine {
   // Build phase: base tiling + ops -> leaves, dependences; state left in the slot.
   HXN void build(const hesp_cand_desc& d) {
     reset_to_base();
+    if (d.n_ops < 0 || d.n_ops > HESP_MAX_OPS) fail(ST_ENGINE_LIMIT);  // never read past ops[]
     NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
       if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
       else apply_op(d.ops[k].task, d.ops[k].s);
@@ -2579,6 +2580,7 @@ struct Engine {
   // ids, blocks and hash-table contents as replaying every op.
   HXN void build_template(const hesp_cand_desc& d) {
     reset_to_base();
+    if (d.n_ops < 0 || d.n_ops > HESP_MAX_OPS) fail(ST_ENGINE_LIMIT);
     NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
       if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
       else apply_op(d.ops[k].task, d.ops[k].s);

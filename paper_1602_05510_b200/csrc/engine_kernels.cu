@@ -490,6 +490,10 @@ struct hesp_engine {
   PartEntry* d_sparts = nullptr;
   TraceBufs* d_stbs = nullptr;
   hesp_outcome* d_sout = nullptr;
+  // hesp_min_reduce's exchange words (allocated on first use, kept)
+  long long* d_reduce = nullptr;
+  long long* h_reduce = nullptr;
+  long long min_reduces = 0;
 };
 
 namespace {
@@ -842,6 +846,8 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_counter);
   cudaFree(e->d_out);
   cudaFree(e->d_descs);
+  cudaFree(e->d_reduce);
+  if (e->h_reduce) cudaFreeHost(e->h_reduce);
   if (e->h_best) cudaFreeHost(e->h_best);
   if (e->h_descs) cudaFreeHost(e->h_descs);
   if (e->h_out) cudaFreeHost(e->h_out);
@@ -866,6 +872,7 @@ int hesp_engine_get_info(const hesp_engine* e, hesp_engine_info* info) {
   info->blocks_per_sm = e->blocks_per_sm;
   info->chunk = e->split ? (int64_t)e->chunk : 0;
   info->last_h2d_bytes = (int64_t)e->last_h2d_bytes;
+  info->min_reduces = e->min_reduces;
   return HESP_OK;
 }
 
@@ -1031,23 +1038,26 @@ int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, in
   bool ok = ck(cudaMalloc(&dd, sizeof(hesp_cand_desc)), "malloc") && ck(cudaMalloc(&dp, n * 4), "malloc") &&
             ck(cudaMalloc(&ds, n * 8), "malloc") && ck(cudaMalloc(&de, n * 8), "malloc") &&
             ck(cudaMalloc(&dout, sizeof(hesp_outcome)), "malloc");
-  if (ok) {
-    cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
-    cudaMemset(dp, 0xff, n * 4);
-    cudaMemset(ds, 0, n * 8);
-    cudaMemset(de, 0, n * 8);
-    cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, e->stream);
-    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, cap, dp, ds, de, dout, nullptr);
-    e->launches += 1;
-    ok = ck(cudaStreamSynchronize(e->stream), "detail");
-  }
+  // every copy and fill is ordered on the engine's (non-blocking) stream,
+  // ahead of and behind the kernel
+  cudaStream_t st = e->stream;
   hesp_outcome o{};
   if (ok) {
-    cudaMemcpy(&o, dout, sizeof(o), cudaMemcpyDeviceToHost);
-    if (proc) cudaMemcpy(proc, dp, (size_t)cap * 4, cudaMemcpyDeviceToHost);
-    if (start) cudaMemcpy(start, ds, (size_t)cap * 8, cudaMemcpyDeviceToHost);
-    if (end) cudaMemcpy(end, de, (size_t)cap * 8, cudaMemcpyDeviceToHost);
-    if (out) *out = o;
+    ok = ck(cudaMemcpyAsync(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice, st), "detail H2D") &&
+         ck(cudaMemsetAsync(dp, 0xff, n * 4, st), "detail memset") && ck(cudaMemsetAsync(ds, 0, n * 8, st), "detail memset") &&
+         ck(cudaMemsetAsync(de, 0, n * 8, st), "detail memset") &&
+         ck(cudaMemcpyToSymbolAsync(c_problem, &e->hp.p, sizeof(Problem), 0, cudaMemcpyHostToDevice, st), "problem");
+  }
+  if (ok) {
+    detail_kernel<<<1, 32, 0, st>>>(dd, e->d_scratch, cap, dp, ds, de, dout, nullptr);
+    e->launches += 1;
+    ok = ck(cudaGetLastError(), "detail launch") &&
+         ck(cudaMemcpyAsync(&o, dout, sizeof(o), cudaMemcpyDeviceToHost, st), "detail D2H") &&
+         (!proc || !cap || ck(cudaMemcpyAsync(proc, dp, (size_t)cap * 4, cudaMemcpyDeviceToHost, st), "detail D2H")) &&
+         (!start || !cap || ck(cudaMemcpyAsync(start, ds, (size_t)cap * 8, cudaMemcpyDeviceToHost, st), "detail D2H")) &&
+         (!end || !cap || ck(cudaMemcpyAsync(end, de, (size_t)cap * 8, cudaMemcpyDeviceToHost, st), "detail D2H")) &&
+         ck(cudaStreamSynchronize(st), "detail");
+    if (ok && out) *out = o;
   }
   cudaFree(dd);
   cudaFree(dp);
@@ -1105,15 +1115,21 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
   hx::TraceLogs logs;
   TraceBufs hb{};
   if (ok) {
-    cudaMemcpy(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice);
-    cudaMemcpy(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice);
-    cudaMemset(dp, 0xff, (size_t)T * 4);
-    cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, e->stream);
-    detail_kernel<<<1, 32, 0, e->stream>>>(dd, e->d_scratch, T, dp, ds, de, dout, dtb);
-    e->launches += 1;
-    ok = ck(cudaStreamSynchronize(e->stream), "trace kernel") &&
-         ck(cudaMemcpy(&o, dout, sizeof(o), cudaMemcpyDeviceToHost), "trace D2H") &&
-         ck(cudaMemcpy(&hb, dtb, sizeof(hb), cudaMemcpyDeviceToHost), "trace D2H");
+    // host -> device inputs, fills, the kernel and the read-back all on the
+    // engine's stream (tb/hb are pageable: the final synchronize orders them)
+    cudaStream_t st = e->stream;
+    ok = ck(cudaMemcpyAsync(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice, st), "trace H2D") &&
+         ck(cudaMemcpyAsync(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice, st), "trace H2D") &&
+         ck(cudaMemsetAsync(dp, 0xff, (size_t)T * 4, st), "trace memset") &&
+         ck(cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, st), "problem");
+    if (ok) {
+      detail_kernel<<<1, 32, 0, st>>>(dd, e->d_scratch, T, dp, ds, de, dout, dtb);
+      e->launches += 1;
+      ok = ck(cudaGetLastError(), "trace launch") &&
+           ck(cudaMemcpyAsync(&o, dout, sizeof(o), cudaMemcpyDeviceToHost, st), "trace D2H") &&
+           ck(cudaMemcpyAsync(&hb, dtb, sizeof(hb), cudaMemcpyDeviceToHost, st), "trace D2H") &&
+           ck(cudaStreamSynchronize(st), "trace kernel");
+    }
   }
   if (ok && hb.overflow) {
     g_last_error = "trace buffers overflowed";
@@ -1288,7 +1304,11 @@ struct NcclApi {
 NcclApi& nccl_api() {
   static NcclApi api = [] {
     NcclApi a;
-    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    // HESP_NCCL_LIB names an explicit library (the two-process test's
+    // ncclAllReduce shim); otherwise the process's own libnccl.so.2
+    void* h = nullptr;
+    if (const char* lib = getenv("HESP_NCCL_LIB")) h = dlopen(lib, RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
     if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
     if (h) {
@@ -1330,11 +1350,15 @@ int hesp_min_reduce(hesp_engine* e, void* comm, hesp_best* best) {
   h[5] = best->sum_leaves;
   h[6] = best->sum_k;
   h[7] = best->sum_edges;
-  long long* d = nullptr;
-  if (!ck(cudaMalloc(&d, sizeof h), "malloc reduce")) return HESP_E_CUDA;
+  // persistent device / pinned host words: no allocation (and no
+  // synchronising cudaFree) inside a caller's timed region
+  if (!e->d_reduce && !ck(cudaMalloc(&e->d_reduce, sizeof h), "malloc reduce")) return HESP_E_CUDA;
+  if (!e->h_reduce && !ck(cudaMallocHost(&e->h_reduce, sizeof h), "malloc reduce host")) return HESP_E_CUDA;
+  long long* d = e->d_reduce;
+  std::memcpy(e->h_reduce, h, sizeof h);
   cudaStream_t st = e->stream;
   int r = 0;
-  bool ok = ck(cudaMemcpyAsync(d, h, sizeof h, cudaMemcpyHostToDevice, st), "reduce H2D");
+  bool ok = ck(cudaMemcpyAsync(d, e->h_reduce, sizeof h, cudaMemcpyHostToDevice, st), "reduce H2D");
   if (ok) r = api.allreduce(d, d, 1, NCCL_INT64, NCCL_MIN, comm, st);           // 1: min key
   if (ok && r == 0) {
     winner_keys<<<1, 32, 0, st>>>(d);                                         // index only on the holders
@@ -1346,10 +1370,11 @@ int hesp_min_reduce(hesp_engine* e, void* comm, hesp_best* best) {
     g_last_error = std::string("ncclAllReduce: ") + (api.errstr ? api.errstr(r) : "error");
     ok = false;
   }
-  ok = ok && ck(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st), "reduce D2H") &&
+  ok = ok && ck(cudaMemcpyAsync(e->h_reduce, d, sizeof h, cudaMemcpyDeviceToHost, st), "reduce D2H") &&
        ck(cudaStreamSynchronize(st), "reduce sync");
-  cudaFree(d);
   if (!ok) return r ? HESP_E_INVALID : HESP_E_CUDA;
+  std::memcpy(h, e->h_reduce, sizeof h);
+  ++e->min_reduces;
   if (h[0] == NONE) {
     best->index = -1;
     best->makespan = 0.0;

@@ -48,6 +48,27 @@ def global_best(makespan: float, index: int, device="cpu", group=None) -> tuple[
     return float(np.int64(gkey).view(np.float64)), int(u.item())
 
 
+def init_nccl(local_rank: int):
+    """One NCCL process group per GPU process.  Under torchrun the rendezvous
+    comes from the environment; a plain `python bench.py` (N=1) gets a 1-rank
+    group on 127.0.0.1 so the cross-GPU winner path (hesp_min_reduce over the
+    group's communicator) runs at every N."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", local_rank)
+    if "WORLD_SIZE" in os.environ:  # torchrun
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=dev)
+    dist.barrier()  # creates the communicator
+
+
 def nccl_comm_ptr(group=None) -> int:
     """Raw ncclComm_t of a NCCL process group (0 if the communicator does not
     exist yet: it is created by the group's first collective)."""
@@ -63,8 +84,12 @@ def engine_global_best(eng, best, group=None):
     own NCCL communicator (NVLink/NVSwitch on one node).  Returns
     (makespan, index) like global_best, plus the all-rank hesp_best."""
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+    if not dist.is_initialized():
         return (best.makespan, best.index) if best.index >= 0 else (float("nan"), -1), best
+    if dist.get_backend(group) != "nccl":  # gloo (CPU tests): the same two-round argmin in torch
+        mk, idx = global_best(best.makespan, best.index, group=group)
+        return (mk, idx), best
+    # NCCL, any world size (a 1-rank group too, so N=1 runs exercise K3)
     comm = nccl_comm_ptr(group)
     if not comm:
         dist.barrier(group=group)  # creates the communicator

@@ -102,7 +102,8 @@ class EngineInfo(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("n_base_tasks", C.c_int32),
                 ("n_base_blocks", C.c_int32), ("n_slots", C.c_int32), ("sm_count", C.c_int32),
                 ("slot_bytes", C.c_int64), ("warps_per_block", C.c_int32),
-                ("blocks_per_sm", C.c_int32), ("chunk", C.c_int64), ("last_h2d_bytes", C.c_int64)]
+                ("blocks_per_sm", C.c_int32), ("chunk", C.c_int64), ("last_h2d_bytes", C.c_int64),
+                ("min_reduces", C.c_int64)]
 
 
 ASSIGN_DTYPE = np.dtype([("task", "<i4"), ("proc", "<i4"), ("start", "<f8"), ("end", "<f8"),

@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from paper_1602_05510_b200.configs import PARITY, harness_args  # noqa: E402
+from paper_1602_05510_b200.configs import PARITY, SCALE, harness_args  # noqa: E402
 from paper_1602_05510_b200.engine import FIXTURES  # noqa: E402
 
 HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
@@ -211,8 +211,9 @@ def main(names):
         print(name, "detail written")
     write_traces(names)
     write_solves(names)
-    for name in [n for n in (names or sorted(PARITY)) if n in PARITY]:
-        p, count = PARITY[name]
+    records = {**PARITY, **SCALE}
+    for name in [n for n in (names or sorted(records)) if n in records]:
+        p, count = records[name]
         out = os.path.join(HERE, f"{name}.bin")
         cmd = [HARNESS, *harness_args(p, FIXTURES), "--first", "0", "--count", str(count),
                "--threads", str(os.cpu_count()), "--out", out]

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from golden_io import read_golden
-from paper_1602_05510_b200.configs import C2, PARITY, harness_args
+from paper_1602_05510_b200.configs import C2, PARITY, SCALE, harness_args
 from paper_1602_05510_b200.dist import shard
 from paper_1602_05510_b200.engine import EXPORTS, FIXTURES, Workload, generate_batch, load_library
 
@@ -25,9 +25,9 @@ ENGINE_CHECK = os.path.join(REF, "engine_check")
 GEN_ERRORS = {1 + 1: "Validation", 1 + 7: "NotALeaf", 1 + 8: "IndivisibleGrain", 100: "foreign exception"}
 
 
-@pytest.mark.parametrize("name", sorted(PARITY))
+@pytest.mark.parametrize("name", sorted(PARITY) + sorted(SCALE))
 def test_golden_fixture_shape(name):
-    p, count = PARITY[name]
+    p, count = {**PARITY, **SCALE}[name]
     g = read_golden(name)
     assert len(g) == count
     assert list(g["index"]) == list(range(count))
@@ -36,6 +36,16 @@ def test_golden_fixture_shape(name):
     bad = g[g["status"] != 0]
     assert (ok["makespan"] > 0).all() and (ok["n_leaves"] > 0).all()
     assert (bad["makespan"] == 0).all() and (bad["assign_hash"] == 0).all()
+
+
+def test_scale_goldens_extend_the_parity_sets():
+    """The at-scale records (>= 1e4 C2/C3, 256 C4, 1e3 per eviction fixture)
+    start with exactly the parity set's records where the presets coincide."""
+    assert SCALE["scale_c2"][1] >= 10_000 and SCALE["scale_c3"][1] >= 10_000 and SCALE["scale_c4"][1] >= 256
+    for scale, small in (("scale_c2", "c2"), ("scale_c3", "c3"), ("scale_c4", "c4"), ("scale_evict_wb", "evict_wb"),
+                         ("scale_merge_c2", "merge_c2"), ("scale_sect_cpugpu", "sect_cpugpu")):
+        a, b = read_golden(scale), read_golden(small)
+        assert a[:len(b)].tobytes() == b.tobytes(), scale
 
 
 def test_goldens_exercise_every_path():
