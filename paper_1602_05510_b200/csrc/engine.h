@@ -219,6 +219,7 @@ struct DevWarp {
 #endif
 
 HX double dmax(double a, double b) { return a < b ? b : a; }  // == std::max
+HX double dmin(double a, double b) { return b < a ? b : a; }
 #if defined(__CUDACC__)
 HX int ctz32(unsigned m) { return __ffs((int)m) - 1; }
 HX int popc32(unsigned m) { return __popc(m); }
@@ -248,17 +249,37 @@ HX uint64_t dbits(double x) {
 }
 
 // Small per-warp state (shared memory on the device).
+// State of the lean event loop across its cold exits (sim_lean): the loop
+// returns to its driver for every call-requiring step, so no value is live
+// across a call inside the hot loop and nothing spills.
+struct LeanState {
+  double tnow, mk, pmin;
+  int32_t pool_n, committed, done, nr, first;
+  int32_t phase;                  // resume point of the task in progress: 0 none, 1 acquire, 2 coherence done, 3 write-back done
+  int32_t r_k, r_p, r_s;          // block being acquired, processor, space
+  double r_inputs, r_start, r_end;
+  int32_t op, op_b, op_s, pad_;   // cold request
+  double op_at, op_at2, op_result;
+};
+
 struct Small {
   double proc_free[MAXP];
   double link_free[MAXL];
   long long used[MAXS];
-  double est[MAXS];
-  int32_t tmp_i[64];
-  double tmp_d[8];
   uint64_t ah, xh;  // event-loop result hashes (one copy per warp)
   int32_t ptype[MAXP], pspace[MAXP];
+  LeanState L;
 };
 static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
+
+#if defined(__CUDACC__)
+// One Small per warp of a CTA (<= 4 warps), declared at namespace scope so
+// every access compiles to LDS/STS (a Small* parameter would be a generic
+// pointer: LD/ST through the generic path).  Each kernel that touches it gets
+// its own per-CTA allocation.
+constexpr int SMALL_WARPS = 4;
+__shared__ Small g_small[SMALL_WARPS];
+#endif
 
 // ---------------------------------------------------------------------------
 // Engine
@@ -281,7 +302,7 @@ struct Engine {
   HX int4* bcell() const { return (int4*)(slot + PB.lay.bcell); }      // cell range per block
   HX uint16_t* rht() const { return (uint16_t*)(slot + PB.lay.rht); }  // region hash of new blocks
   HX uint8_t* pmark() const { return (uint8_t*)(slot + PB.lay.pmark); }  // 1 + partition entry per task id
-  HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - nbb
+  HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - n_bb()
   HX PartEntry* part() const { return (PartEntry*)(slot + PB.lay.part); }  // clusters, by id
   HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
   HX uint8_t* tmis() const { return (uint8_t*)(slot + PB.lay.tmis); }
@@ -317,7 +338,13 @@ struct Engine {
   HX Region* gs_reg2() const { return (Region*)(slot + PB.lay.gs_reg2); }
   // scalars (uniform across lanes)
   int32_t status = 0;
-  int32_t nbt, nbb;        // base task / block counts (overlay boundary)
+  // base task / block counts (overlay boundary), space count, main space:
+  // read from the problem (constant memory), never from `this` (the engine
+  // object lives in local memory on the device)
+  HX int n_bt() const { return PB.n_base_tasks; }
+  HX int n_bb() const { return PB.n_base_blocks; }
+  HX int n_sp() const { return PB.S; }
+  HX int msp() const { return PB.main_space; }
   int32_t ntasks, nblocks;  // next ids
   int32_t npart = 0;
   int32_t nleaves = 0;
@@ -329,7 +356,6 @@ struct Engine {
   double makespan = 0.0;
   uint64_t ahash = 0, xhash = 0;
   uint64_t rng = 0;
-  int32_t S, mainsp;
   // No-eviction fast path (DESIGN.md §3 E4): when every block but the root
   // fits in every space (plus the root in main), ensure_capacity can never
   // evict, so LRU stamps, pins, mat/dirty flags and `used` -- read only by
@@ -400,26 +426,31 @@ struct Engine {
   }
 
   HX Engine(WP w, const Problem& p, uint8_t* slot_, Small* s) : wp(w), pbp(&p), sm(s), slot(slot_) {
-    nbt = p.n_base_tasks;
-    nbb = p.n_base_blocks;
-    S = p.S;
-    mainsp = p.main_space;
   }
 
   HX void fail(int32_t code) {
     if (status == 0) status = code;
   }
 
+  // The warp's Small: real shared memory on the device (warp-wide engine),
+  // the caller's buffer for the width-1 instantiations.
+  HX Small& SM() const {
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) return g_small[threadIdx.x >> 5];
+#endif
+    return *sm;
+  }
+
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
-  HX TaskMeta task(int id) const { return id < nbt ? PB.base_tasks[id] : tm()[id - nbt]; }
-  HX const BlockMeta& bmeta(int b) const { return b < nbb ? PB.base_blocks[b] : bm()[b - nbb]; }
+  HX TaskMeta task(int id) const { return id < n_bt() ? PB.base_tasks[id] : tm()[id - n_bt()]; }
+  HX const BlockMeta& bmeta(int b) const { return b < n_bb() ? PB.base_blocks[b] : bm()[b - n_bb()]; }
   HX Region reg(int b) const { return bmeta(b).r; }
   HX int tile_of(int b) const { return bmeta(b).tile; }
   HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * PB.elem; }
   HX long long bbytes(int b) const { return rbytes(reg(b)); }
-  HX double& V(int b, int s) { return valid()[(size_t)b * S + s]; }
-  HX double& LU(int b, int s) { return lastu()[(size_t)b * S + s]; }
-  HX double& PIN(int b, int s) { return pinu()[(size_t)b * S + s]; }
+  HX double& V(int b, int s) { return valid()[(size_t)b * n_sp() + s]; }
+  HX double& LU(int b, int s) { return lastu()[(size_t)b * n_sp() + s]; }
+  HX double& PIN(int b, int s) { return pinu()[(size_t)b * n_sp() + s]; }
   HX bool is_mat(int b, int s) const { return (bflags()[b] >> s) & 1u; }
   HX bool is_dirty(int b, int s) const { return (bflags()[b] >> (8 + s)) & 1u; }
   HX int part_index(int task) const {
@@ -453,7 +484,7 @@ struct Engine {
     h ^= h >> 15;
     return h * 0x27D4EB2Fu;
   }
-  HX bool rht_usable() const { return nblocks - nbb < RHT / 2; }
+  HX bool rht_usable() const { return nblocks - n_bb() < RHT / 2; }
 
   HXN int find_block(const Region& r, int t) {
     if (t < 0) {
@@ -478,13 +509,13 @@ struct Engine {
       NOUNROLL for (;;) {
         const int e = rht()[i];
         if (e == 0xffff) return -1;
-        if (rsame(bm()[e].r, r)) return nbb + e;
+        if (rsame(bm()[e].r, r)) return n_bb() + e;
         i = (i + 1) & (RHT - 1);
       }
     }
-    NOUNROLL for (int base = nbb; base < nblocks; base += WP::W) {
+    NOUNROLL for (int base = n_bb(); base < nblocks; base += WP::W) {
       const int b = base + wp.lane();
-      const bool hit = b < nblocks && bm()[b - nbb].tile == t && rsame(bm()[b - nbb].r, r);
+      const bool hit = b < nblocks && bm()[b - n_bb()].tile == t && rsame(bm()[b - n_bb()].r, r);
       const unsigned m = wp.ballot(hit);
       if (m) return base + ctz32(m);
     }
@@ -504,13 +535,13 @@ struct Engine {
     m.isint = isint ? 1 : 0;
     m.pad = 0;
     if (wp.lane() == 0) {
-      bm()[id - nbb] = m;
-      bref()[id - nbb] = 0;
+      bm()[id - n_bb()] = m;
+      bref()[id - n_bb()] = 0;
     }
-    if (t >= 0 && id - nbb < RHT / 2) {
+    if (t >= 0 && id - n_bb() < RHT / 2) {
       unsigned i = rhash(r) & (RHT - 1);
       while (rht()[i] != 0xffff) i = (i + 1) & (RHT - 1);
-      if (wp.lane() == 0) rht()[i] = (uint16_t)(id - nbb);
+      if (wp.lane() == 0) rht()[i] = (uint16_t)(id - n_bb());
     }
     wp.sync();
     return id;
@@ -541,7 +572,7 @@ struct Engine {
       wp.sync();
     }
     int nsect = 0;
-    const int lo = t < 0 ? 0 : nbb;
+    const int lo = t < 0 ? 0 : n_bb();
     NOUNROLL for (int base = lo; base < id; base += WP::W) {
       const int b = base + wp.lane();
       bool hit = false;
@@ -620,9 +651,9 @@ struct Engine {
     m.bidx = (int8_t)bi;
     const int id = ntasks++;
     if (wp.lane() == 0) {
-      tm()[id - nbt] = m;
+      tm()[id - n_bt()] = m;
       NOUNROLL for (int k = 0; k <= nr; ++k)
-        if (m.blk[k] >= nbb) ++bref()[m.blk[k] - nbb];
+        if (m.blk[k] >= n_bb()) ++bref()[m.blk[k] - n_bb()];
     }
     wp.sync();
   }
@@ -651,22 +682,22 @@ struct Engine {
     const PartEntry pe = part()[c];
     NOUNROLL for (int m = pe.child0; m < pe.child0 + pe.nchild; ++m)
       if (part_index(m) >= 0) return fail(ST_NESTED_CLUSTER);
-    if (c == 0 || pe.child0 < nbt) return fail(ST_ENGINE_LIMIT);
+    if (c == 0 || pe.child0 < n_bt()) return fail(ST_ENGINE_LIMIT);
     bool sect = false;
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
-      const BlockMeta& o = bm()[b - nbb];
+    NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W) {
+      const BlockMeta& o = bm()[b - n_bb()];
       if (o.isint && !dead_region(o.r)) sect = true;
     }
     if (wp.any(sect)) return fail(ST_ENGINE_LIMIT);
     NOUNROLL for (int m = pe.child0 + wp.lane(); m < pe.child0 + pe.nchild; m += WP::W) {
-      const TaskMeta t = tm()[m - nbt];
+      const TaskMeta t = tm()[m - n_bt()];
       NOUNROLL for (int k = 0; k <= t.nrd; ++k)
-        if (t.blk[k] >= nbb) wp.atomic_add(&bref()[t.blk[k] - nbb], -1);
+        if (t.blk[k] >= n_bb()) wp.atomic_add(&bref()[t.blk[k] - n_bb()], -1);
     }
     wp.sync();
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
-      BlockMeta& o = bm()[b - nbb];
-      if (!o.isint && bref()[b - nbb] == 0 && !dead_region(o.r)) {
+    NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W) {
+      BlockMeta& o = bm()[b - n_bb()];
+      if (!o.isint && bref()[b - n_bb()] == 0 && !dead_region(o.r)) {
         o.r.row = -1;
         o.r.col = -1;
         o.r.rows = 0;
@@ -681,7 +712,7 @@ struct Engine {
   // enumerate_partition loop nests (graph.cpp:301-392).
   HXN void apply_op(int task_id, int s_req) {
     if (task_id < 0 || task_id >= ntasks) return fail(ST_VALIDATION);
-    if (task_id >= nbt && dead_task(task_id)) return fail(ST_VALIDATION);  // merged away: unknown task
+    if (task_id >= n_bt() && dead_task(task_id)) return fail(ST_VALIDATION);  // merged away: unknown task
     if (part_index(task_id) >= 0) return fail(ST_NOT_A_LEAF);
     const double p = 1.0 / (double)s_req;
     if (!(p > 0.0 && p < 1.0)) return fail(ST_VALIDATION);
@@ -824,16 +855,16 @@ struct Engine {
   // Per-tile CSR of the candidate's own blocks (order inside a tile is
   // irrelevant: every consumer is order-independent or sorts).
   HXN void build_tiles() {
-    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_cnt()[i] = 0;
+    NOUNROLL for (int i = wp.lane(); i < n_bb(); i += WP::W) tl_cnt()[i] = 0;
     wp.sync();
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W)
-      if (!dead_region(bm()[b - nbb].r)) wp.atomic_add(&tl_cnt()[bm()[b - nbb].tile], 1);
+    NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W)
+      if (!dead_region(bm()[b - n_bb()].r)) wp.atomic_add(&tl_cnt()[bm()[b - n_bb()].tile], 1);
     wp.sync();
     // exclusive scan over base tiles
     int run = 0;
-    NOUNROLL for (int base = 0; base < nbb; base += WP::W) {
+    NOUNROLL for (int base = 0; base < n_bb(); base += WP::W) {
       const int i = base + wp.lane();
-      const int c = i < nbb ? tl_cnt()[i] : 0;
+      const int c = i < n_bb() ? tl_cnt()[i] : 0;
       int incl = c;
 #if defined(__CUDACC__)
       if constexpr (WP::W > 1) {
@@ -843,15 +874,15 @@ struct Engine {
         }
       }
 #endif
-      if (i < nbb) tl_head()[i] = run + incl - c;
+      if (i < n_bb()) tl_head()[i] = run + incl - c;
       run += wp.bcast(incl, WP::W - 1);
     }
     wp.sync();
-    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tl_ncb()[i] = 0;  // fill cursor
+    NOUNROLL for (int i = wp.lane(); i < n_bb(); i += WP::W) tl_ncb()[i] = 0;  // fill cursor
     wp.sync();
-    NOUNROLL for (int b = nbb + wp.lane(); b < nblocks; b += WP::W) {
-      if (dead_region(bm()[b - nbb].r)) continue;
-      const int t = bm()[b - nbb].tile;
+    NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W) {
+      if (dead_region(bm()[b - n_bb()].r)) continue;
+      const int t = bm()[b - n_bb()].tile;
       const int pos = wp.atomic_add(&tl_ncb()[t], 1);
       tl_ids()[tl_head()[t] + pos] = b;
     }
@@ -944,7 +975,7 @@ struct Engine {
   // Column/row boundaries of every tile's blocks -> cell grids.
   HXN void build_cells() {
     int nb_used = 0, nc_used = 0;
-    NOUNROLL for (int t = 1; t < nbb && !status; ++t) {
+    NOUNROLL for (int t = 1; t < n_bb() && !status; ++t) {
       const int cnt = tl_cnt()[t];
       if (cnt == 0) {
         if (wp.lane() == 0) {
@@ -1118,11 +1149,21 @@ struct Engine {
           NOUNROLL for (int k = 0; k < nw; ++k)
             if (simple_tile(w[k])) fl |= 1 << k;
           if (simple_tile(ws.out)) fl |= 8;
+          // bit 4: the working-set blocks are pairwise disjoint, so acquiring
+          // one never changes another's validity (the lean loop reads all of
+          // them in one round); bit 5: the output's coherence cone needs the
+          // general scan (the root, or a tile holding partial overlaps)
+          bool disj = true;
+          NOUNROLL for (int a = 0; a < nw; ++a)
+            NOUNROLL for (int c = a + 1; c < nw; ++c)
+              if (roverlap(reg(w[a]), reg(w[c]))) disj = false;
+          if (disj) fl |= 16;
+          if (ws.out == 0 || tmis()[tile_of(ws.out)]) fl |= 32;
           ws.pad = fl;
           wsb()[j] = ws;
         }
         int kt = 0;
-        bool fastj = j < nbt;
+        bool fastj = j < n_bt();
         NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
           bool dup = false;
           for (int q = 0; q < k; ++q) dup |= t.blk[q] == t.blk[k];
@@ -1161,7 +1202,7 @@ struct Engine {
         if (dup && k < t.nrd) continue;
         const bool writes = (k == t.nrd);
         const int myslot = slot++;
-        if (j < nbt && tl_cnt()[tile_of(b)] == 0) {
+        if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
           // unsubdivided tile of a base task: its base contribution (E5)
           const BasePreds& bp = PB.base_preds[j];
           const int off = bp.soff[myslot], cnt = bp.scnt[myslot];
@@ -1374,9 +1415,9 @@ struct Engine {
   }
 
   HX int source_space(int b, int exclude) {  // source_spaces().front() minus `exclude` (sim.cpp:341-350)
-    if (mainsp != exclude && V(b, mainsp) != ABSENT) return mainsp;
-    NOUNROLL for (int s = 0; s < S; ++s)
-      if (s != mainsp && s != exclude && V(b, s) != ABSENT) return s;
+    if (msp() != exclude && V(b, msp()) != ABSENT) return msp();
+    NOUNROLL for (int s = 0; s < n_sp(); ++s)
+      if (s != msp() && s != exclude && V(b, s) != ABSENT) return s;
     return -1;
   }
 
@@ -1393,9 +1434,9 @@ struct Engine {
     double hs[2] = {0.0, 0.0}, he[2] = {0.0, 0.0};
     NOUNROLL for (int h = 0; h < nh; ++h) {
       const int l = PB.route_l[src * MAXS + dst][h];
-      const double st = dmax(sm->link_free[l], rdy);
+      const double st = dmax(SM().link_free[l], rdy);
       const double en = st + PB.link_lat[l] + (double)bytes / PB.link_bw[l];
-      sm->link_free[l] = en;
+      SM().link_free[l] = en;
       rdy = en;
       if (h == 0) start0 = st;
       if (TRACE && h < 2) {
@@ -1423,7 +1464,7 @@ struct Engine {
   HX void setLU(int b, int s, double v) { LU(b, s) = v; }
   HX void setPIN(int b, int s, double v) { PIN(b, s) = v; }
   HX void add_used(int s, long long d) {
-    if (wp.lane() == 0) sm->used[s] += d;
+    if (wp.lane() == 0) SM().used[s] += d;
     wp.sync();
   }
 
@@ -1454,7 +1495,7 @@ struct Engine {
   HXN void ensure_capacity(int s, long long bytes, double at) {
     const long long cap = PB.cap[s];
     if (bytes > cap) return fail(ST_CAPACITY);
-    while (sm->used[s] + bytes > cap) {
+    while (SM().used[s] + bytes > cap) {
       // LRU victim: min (stamp, id) among unpinned materialised blocks
       double bst = ABSENT;
       double dummy = 0.0;
@@ -1463,11 +1504,11 @@ struct Engine {
         const int b = base + wp.lane();
         if (b < nblocks && is_mat(b, s) && !(PIN(b, s) > now)) {
           bool ok = true;
-          if (s == mainsp) {
+          if (s == msp()) {
             if (b == 0) ok = false;  // roots are never evicted from main
             else {
               bool elsewhere = false;
-              NOUNROLL for (int s2 = 0; s2 < S; ++s2)
+              NOUNROLL for (int s2 = 0; s2 < n_sp(); ++s2)
                 if (s2 != s && V(b, s2) != ABSENT) elsewhere = true;
               ok = elsewhere;
             }
@@ -1488,19 +1529,19 @@ struct Engine {
       if (is_dirty(victim, s)) {
         if (!FLUSH) return fail(ST_ENGINE_INVARIANT);
         const double rdy = V(victim, s);
-        const double arr = plan_transfer(victim, nullptr, vbytes, s, mainsp, rdy, at);  // sim.cpp:408-409 passes `at`
+        const double arr = plan_transfer(victim, nullptr, vbytes, s, msp(), rdy, at);  // sim.cpp:408-409 passes `at`
         if (status) return;
         set_flag(victim, 1u << (8 + s), false);
-        reserve_bytes<false>(victim, mainsp, arr);
+        reserve_bytes<false>(victim, msp(), arr);
         if (status) return;
-        validate_from(victim, mainsp, arr);
+        validate_from(victim, msp(), arr);
       }
       set_flag(victim, 1u << s, false);
       setV(victim, s, ABSENT);
       add_used(s, -vbytes);
       if (TRACE && wp.lane() == 0) log_res(at, s, -vbytes, victim);
       setLU(victim, s, 0.0);
-      if (s != mainsp) {
+      if (s != msp()) {
         // views lose their backing when no materialised block covers them
         const Region vr = reg(victim);
         NOUNROLL for (int base = 0; base < nblocks; base += WP::W) {
@@ -1675,7 +1716,7 @@ struct Engine {
           b = t < 0 ? k : (k == 0 ? 0 : (k == 1 ? t : tl_ids()[head + k - 2]));
           if (b != blk && rcontains(target, reg(b))) {
             bool any = false;
-            NOUNROLL for (int q = 0; q < S; ++q)
+            NOUNROLL for (int q = 0; q < n_sp(); ++q)
               if (V(b, q) != ABSENT) any = true;
             hit = any;
           }
@@ -1758,10 +1799,10 @@ struct Engine {
         fail(ST_COHERENCE);
         return 0.0;
       }
-      if (s != mainsp)
+      if (s != msp())
         NOUNROLL for (int f = 0; f < nfr; ++f) {
           const Region fr = gs_reg2()[f];
-          arrival = dmax(arrival, plan_transfer(blk, &fr, rbytes(fr), mainsp, s, 0.0, now));
+          arrival = dmax(arrival, plan_transfer(blk, &fr, rbytes(fr), msp(), s, 0.0, now));
           if (status) return 0.0;
         }
     }
@@ -1794,12 +1835,12 @@ struct Engine {
       }
       if (!in) continue;
       if (fast) {
-        NOUNROLL for (int q = 0; q < S; ++q)
+        NOUNROLL for (int q = 0; q < n_sp(); ++q)
           if (q != ws) V(x, q) = ABSENT;
         continue;
       }
       uint32_t f = bflags()[x];
-      NOUNROLL for (int q = 0; q < S; ++q) {
+      NOUNROLL for (int q = 0; q < n_sp(); ++q) {
         if (q == ws) continue;
         if ((f >> q) & 1u) {
           freed[q] += rbytes(rx);
@@ -1813,7 +1854,7 @@ struct Engine {
     }
     wp.sync();
     if (fast) return;
-    NOUNROLL for (int q = 0; q < S; ++q) {
+    NOUNROLL for (int q = 0; q < n_sp(); ++q) {
       if (q == ws) continue;
       const long long fr = wp.suml(freed[q]);
       if (fr) add_used(q, -fr);
@@ -1850,10 +1891,10 @@ struct Engine {
 
   // WT / WA write-back of a task's output to main (sim.cpp:631-656).
   HXN void write_back(int out, int s, double end) {
-    const double arr = plan_transfer(out, nullptr, bbytes(out), s, mainsp, end, now);
+    const double arr = plan_transfer(out, nullptr, bbytes(out), s, msp(), end, now);
     if (status) return;
     pin(s, out, arr);
-    materialize<false>(out, mainsp, arr);
+    materialize<false>(out, msp(), arr);
     if (status) return;
     if (PB.caching == CACHE_WA) {  // write-around: drop the local copy (sim.cpp:643-655)
       if (!fast) {
@@ -1896,9 +1937,17 @@ struct Engine {
       NOUNROLL for (int x = 1 + wp.lane(); x < nblocks; x += WP::W) nonroot += bbytes(x);
       nonroot = wp.suml(nonroot);
       bool ok = true;
-      NOUNROLL for (int q = 0; q < S; ++q)
-        if (nonroot + (q == mainsp ? bbytes(0) : 0) > PB.cap[q]) ok = false;
+      NOUNROLL for (int q = 0; q < n_sp(); ++q)
+        if (nonroot + (q == msp() ? bbytes(0) : 0) > PB.cap[q]) ok = false;
       fast = ok && (!TRACE || (tb && tb->lite));  // the full trace keeps residency bookkeeping
+    }
+    if (fast && !TRACE && PB.loop == 0) {  // the batch kernels' lean loop
+      switch (PB.selection) {
+        case SEL_EFTP: return sim_lean<SEL_EFTP>();
+        case SEL_EITP: return sim_lean<SEL_EITP>();
+        case SEL_FP: return sim_lean<SEL_FP>();
+        default: return sim_lean<SEL_RP>();
+      }
     }
     switch (PB.selection) {
       case SEL_EFTP: return fast ? sim_loop<SEL_EFTP, true>() : sim_loop<SEL_EFTP, false>();
@@ -1916,20 +1965,20 @@ struct Engine {
     // init_memory (sim.cpp:323-339): root materialised in main, every block
     // valid in main at t=0 (views into the root data)
     NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
-      NOUNROLL for (int q = 0; q < S; ++q) {
-        V(x, q) = q == mainsp ? 0.0 : ABSENT;
+      NOUNROLL for (int q = 0; q < n_sp(); ++q) {
+        V(x, q) = q == msp() ? 0.0 : ABSENT;
         if (!fast) {
           LU(x, q) = 0.0;
           PIN(x, q) = NOPIN;
         }
       }
-      if (!fast) bflags()[x] = x == 0 ? (1u << mainsp) : 0u;  // read only by eviction bookkeeping
+      if (!fast) bflags()[x] = x == 0 ? (1u << msp()) : 0u;  // read only by eviction bookkeeping
       wrt()[x] = 0;
     }
-    NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) sm->used[q] = q == mainsp ? bbytes(0) : 0;
-    if (TRACE && wp.lane() == 0) log_res(0.0, mainsp, bbytes(0), 0);  // init_memory (sim.cpp:333)
+    NOUNROLL for (int q = wp.lane(); q < MAXS; q += WP::W) SM().used[q] = q == msp() ? bbytes(0) : 0;
+    if (TRACE && wp.lane() == 0) log_res(0.0, msp(), bbytes(0), 0);  // init_memory (sim.cpp:333)
     wp.sync();
-    if (sm->used[mainsp] > PB.cap[mainsp]) return fail(ST_CAPACITY);
+    if (SM().used[msp()] > PB.cap[msp()]) return fail(ST_CAPACITY);
     if (PB.ordering == ORD_PL) build_ct();
     if (status) return;
 
@@ -2008,17 +2057,17 @@ struct Engine {
     // lane-owned clocks and processor attributes
     LaneD est, estp;
     // processor clocks and attributes in the warp's Small, like the link clocks
-#define PF_OWN(q) sm->proc_free[q]
-#define PF_GET(p) sm->proc_free[p]
-#define PF_SET(p, v) (sm->proc_free[p] = (v))
-#define PTYPE(q) sm->ptype[q]
-#define PSPACE_OWN sm->pspace[wp.lane()]
-    NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) sm->proc_free[q] = 0.0;
+#define PF_OWN(q) SM().proc_free[q]
+#define PF_GET(p) SM().proc_free[p]
+#define PF_SET(p, v) (SM().proc_free[p] = (v))
+#define PTYPE(q) SM().ptype[q]
+#define PSPACE_OWN SM().pspace[wp.lane()]
+    NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) SM().proc_free[q] = 0.0;
     est.fill(0.0);
     estp.fill(0.0);
     NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) {
       PTYPE(q) = q < P ? PB.proc_type[q] : 0;
-      sm->pspace[q] = q < P ? PB.proc_space[q] : 0;
+      SM().pspace[q] = q < P ? PB.proc_space[q] : 0;
     }
 #if defined(__CUDACC__)
     const int eft_k = wp.lane() / S_, eft_sp = wp.lane() - (wp.lane() / S_) * S_;  // lane = (block, space)
@@ -2030,12 +2079,12 @@ struct Engine {
     // link clocks and the result hashes live in the warp's shared Small
     // (uniform values: every lane stores the same value and reads its own
     // store), which keeps them out of the register file the loop spills from
-    Small* const smw = sm;
-    smw->ah = 0;
-    smw->xh = 0;
-#define HAH smw->ah
-#define HXH smw->xh
-    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) smw->link_free[i] = 0.0;
+    Small& smw = SM();
+    smw.ah = 0;
+    smw.xh = 0;
+#define HAH smw.ah
+#define HXH smw.xh
+    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) smw.link_free[i] = 0.0;
     wp.sync();
     int st = 0;  // status mirror for the hot loop
     now = 0.0;
@@ -2051,9 +2100,9 @@ struct Engine {
       double hs[2] = {0.0, 0.0}, he[2] = {0.0, 0.0};
       NOUNROLL for (int h = 0; h < nh; ++h) {
         const int l = PB.route_l[src * MAXS + dst][h];
-        const double s0 = dmax(smw->link_free[l], rdy);
+        const double s0 = dmax(smw.link_free[l], rdy);
         const double en = s0 + PB.link_lat[l] + PB.hopq[l][bi];  // (s0 + lat) + bytes/bw
-        smw->link_free[l] = en;  // uniform: every lane stores the same value and reads its own store
+        smw.link_free[l] = en;  // uniform: every lane stores the same value and reads its own store
         rdy = en;
         if (h == 0) start0 = s0;
         if (TRACE && h < 2) {
@@ -2361,7 +2410,7 @@ struct Engine {
             {  // one lane: the reference's loop, space by space
             NOUNROLL for (int sp = wp.lane(); sp < S_; sp += WP::W) est.own(sp) = eft_space_h(sp, w, nw, noroute);
             if (wp.any(noroute)) return fail(ST_NO_ROUTE);
-            NOUNROLL for (int q = 0; q < P; ++q) estp.own(q) = est.get(sm->pspace[q]);  // estimate of each processor's space
+            NOUNROLL for (int q = 0; q < P; ++q) estp.own(q) = est.get(SM().pspace[q]);  // estimate of each processor's space
             }
           }
           double a = ABSENT, b2 = 0.0;
@@ -2386,7 +2435,7 @@ struct Engine {
         }
         if (p < 0) return fail(ST_NO_PROCESSORS);
         // ---------------- commit (sim.cpp:592-668) ----------------
-        const int s = sm->pspace[p];
+        const int s = SM().pspace[p];
         const int type = PTYPE(p);
         if (!fst) {
           long long wset = 0;
@@ -2537,25 +2586,763 @@ struct Engine {
   }
 
   // =========================================================================
+  // Lean event loop: the batch kernels' instance of sim.cpp:704-834 on the
+  // E4 fast path (no eviction possible).  Same decisions as sim_loop; built
+  // so the hot loop contains no call and keeps no value in local memory:
+  //   * the loop (lean_run, inlined into its driver) returns to the driver
+  //     for every step that needs a member call -- gather (sim.cpp:521-572),
+  //     the WT/WA write-back, coherence over the root or over a tile holding
+  //     partial overlaps -- with its state in the warp's Small (LeanState),
+  //     and resumes the task in progress where it left it;
+  //   * coherence over a subdivided tile is one lane-parallel pass over the
+  //     tile's scope (root, tile, its blocks): the invalidation cone
+  //     (sim.cpp:204-212) of a block in a tile without partial overlaps is
+  //     exactly the blocks containing it or inside it (E1), and
+  //     validate_from (sim.cpp:452-461) the blocks inside it;
+  //   * acquire (sim.cpp:501-519) reads V(b_k, q) of the whole working set
+  //     in one round, lane (k, q); a task's working-set blocks are pairwise
+  //     disjoint (STask flag bit 4, checked at build time), so acquiring one
+  //     never changes another, and only the transfers run in id order (the
+  //     per-link FIFO of plan_transfer, sim.cpp:468-499);
+  //   * EFT-P/EIT-P commit every ready task of an epoch, so the ready set is
+  //     the pool entries at the pool's minimum release time, kept
+  //     incrementally (no separate next-epoch scan);
+  //   * clocks, attributes and hashes live in the warp's Small (LDS/STS).
+  // =========================================================================
+  enum : int32_t { LEAN_DONE = 0, LEAN_GATHER = 1, LEAN_VALIDATE = 2, LEAN_COHERENCE = 3, LEAN_WRITEBACK = 4 };
+
+  template <int SELT>
+  HXN void sim_lean() {
+    const int P = PB.P;
+    Small& W = SM();
+    const int nl = nleaves;
+    // init_memory (sim.cpp:323-339): every block valid in main at t=0
+    NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
+      NOUNROLL for (int q = 0; q < n_sp(); ++q) V(x, q) = q == msp() ? 0.0 : ABSENT;
+      wrt()[x] = 0;
+    }
+    wp.sync();
+    if (bbytes(0) > PB.cap[msp()]) return fail(ST_CAPACITY);  // the root materialised in main (sim.cpp:335-336)
+    if (PB.ordering == ORD_PL) build_ct();
+    if (status) return;
+    // initial pool: leaves without predecessors, release 0
+    int pool_n = 0;
+    NOUNROLL for (int base = 0; base < nl; base += WP::W) {
+      const int li = base + wp.lane();
+      bool z = false;
+      int j = -1;
+      double key = 0.0;
+      if (li < nl) {
+        j = leaf()[li];
+        TState& st_ = ts()[j];
+        st_.rel = 0.0;
+        z = st_.missing == 0;
+        key = PB.ordering == ORD_PL ? st_.ct : 0.0;
+      }
+      const unsigned m = wp.ballot(z);
+      if (z) {
+        const int at = pool_n + popc32(m & wp.lt());
+        pool()[at] = j;
+        pool_rel()[at] = 0.0;
+        pool_key()[at] = key;
+      }
+      pool_n += popc32(m);
+    }
+    NOUNROLL for (int q = wp.lane(); q < MAXP; q += WP::W) {
+      W.proc_free[q] = 0.0;
+      W.ptype[q] = q < P ? PB.proc_type[q] : 0;
+      W.pspace[q] = q < P ? PB.proc_space[q] : 0;
+    }
+    NOUNROLL for (int i = wp.lane(); i < MAXL; i += WP::W) W.link_free[i] = 0.0;
+    wp.sync();
+    W.ah = 0;
+    W.xh = 0;
+    W.L.tnow = 0.0;
+    W.L.mk = 0.0;
+    W.L.pmin = 0.0;
+    W.L.pool_n = pool_n;
+    W.L.committed = 0;
+    W.L.done = 0;
+    W.L.nr = 0;
+    W.L.first = 1;
+    W.L.phase = 0;
+    rng = PB.sched_seed;
+    wp.sync();
+    // driver: run the hot loop; serve its cold requests with the member paths
+    NOUNROLL for (;;) {
+      const int op = lean_run<SELT>();
+      if (op == LEAN_DONE) break;
+      wp.sync();
+      now = W.L.tnow;
+      const int b = W.L.op_b, s = W.L.op_s;
+      const double at = W.L.op_at, at2 = W.L.op_at2;
+      if (op == LEAN_GATHER) {
+        const double r = gather(b, s);
+        wp.sync();
+        W.L.op_result = r;
+      } else if (op == LEAN_VALIDATE) {
+        validate_from(b, s, at);
+      } else if (op == LEAN_COHERENCE) {
+        invalidate_elsewhere(b, s, at);
+        validate_from(b, s, at2);
+      } else {
+        write_back(b, s, at);
+      }
+      wp.sync();
+      if (status) return;
+    }
+    if (status) return;
+    makespan = W.L.mk;
+    ahash += W.ah;
+    xhash += W.xh;
+  }
+
+  // The hot loop.  Returns LEAN_DONE (finished or failed: `status`) or a cold
+  // request in W.L (op, op_b, op_s, op_at, op_at2) with the loop state saved.
+  template <int SELT>
+  HX int lean_run() {
+    const int P = PB.P;
+    uint8_t* const sl = slot;
+#define LA(type, field) ((type*)(sl + PB.lay.field))
+#define LV(b, q) (LA(double, valid)[(b) * PB.S + (q)])
+#define LS PB.S
+#define LMS PB.main_space
+#define LPL (PB.ordering == ORD_PL)
+    constexpr bool waits = (SELT == SEL_RP || SELT == SEL_FP);
+    Small& W = SM();
+    const int nl = nleaves;
+    double tnow = W.L.tnow, mk = W.L.mk, pmin = W.L.pmin;
+    int pool_n = W.L.pool_n, committed = W.L.committed, done = W.L.done, nr = W.L.nr;
+    bool first = W.L.first != 0;
+    int phase = W.L.phase;
+#if defined(__CUDACC__)
+    const int lk = wp.lane() / LS, lq = wp.lane() - (wp.lane() / LS) * LS;  // lane = (block k, space q)
+#else
+    const int lk = 0, lq = 0;
+#endif
+    (void)lk;
+    (void)lq;
+    int st = 0;
+    // block regions through the local slot base, never through `this`
+    auto lreg = [&](int b) -> Region {
+      return b < PB.n_base_blocks ? PB.base_blocks[b].r : LA(const BlockMeta, bm)[b - PB.n_base_blocks].r;
+    };
+    auto ltile = [&](int b) -> int {
+      return b < PB.n_base_blocks ? PB.base_blocks[b].tile : LA(const BlockMeta, bm)[b - PB.n_base_blocks].tile;
+    };
+    // leave the loop: state into W.L (uniform stores), then a cold request
+    auto save = [&]() {
+      W.L.tnow = tnow;
+      W.L.mk = mk;
+      W.L.pmin = pmin;
+      W.L.pool_n = pool_n;
+      W.L.committed = committed;
+      W.L.done = done;
+      W.L.nr = nr;
+      W.L.first = first ? 1 : 0;
+    };
+    auto request = [&](int op, int b, int s, double at, double at2) -> int {
+      save();
+      W.L.op = op;
+      W.L.op_b = b;
+      W.L.op_s = s;
+      W.L.op_at = at;
+      W.L.op_at2 = at2;
+      wp.sync();
+      return op;
+    };
+    auto failed = [&](int code) -> int {
+      fail(code);
+      return LEAN_DONE;
+    };
+    // plan_transfer (sim.cpp:468-499) on the warp's link clocks
+    auto xfer = [&](int blk, long long nbytes, int bi, int src, int dst, double data_ready) -> double {
+      const int nh = PB.route_n[src * MAXS + dst];
+      if (nh == 0) {
+        st = ST_NO_ROUTE;
+        return 0.0;
+      }
+      double rdy = dmax(data_ready, tnow), start0 = 0.0;
+      NOUNROLL for (int h = 0; h < nh; ++h) {
+        const int l = PB.route_l[src * MAXS + dst][h];
+        const double s0 = dmax(W.link_free[l], rdy);
+        const double en = s0 + PB.link_lat[l] + PB.hopq[l][bi];  // (s0 + lat) + bytes/bw
+        W.link_free[l] = en;
+        rdy = en;
+        if (h == 0) start0 = s0;
+      }
+      if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
+      W.xh += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      return rdy;
+    };
+    // validate_from (sim.cpp:452-461), b != 0: b and every block inside it
+    auto validate = [&](int b, int s, double at, bool simple) {
+      if (simple) {
+        double& v = LV(b, s);
+        if (v > at) v = at;
+        return;
+      }
+      const int t = ltile(b);
+      const Region rb = lreg(b);
+      const int cnt = 2 + LA(const int, tl_cnt)[t];
+      const int head = LA(const int, tl_head)[t];
+      NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
+        const int x = k == 0 ? 0 : (k == 1 ? t : LA(const int, tl_ids)[head + k - 2]);
+        if (x == b || (x != 0 && x != t && rcontains(rb, lreg(x)))) {
+          double& v = LV(x, s);
+          if (v > at) v = at;
+        }
+      }
+      wp.sync();
+    };
+
+    NOUNROLL for (;;) {
+      if (phase == 0 && done >= nr) {
+        if (committed >= nl) {
+          save();
+          return LEAN_DONE;
+        }
+        // ---------------- epoch (E3) and ready set (sim.cpp:742-752) ----------------
+        nr = 0;
+        done = 0;
+        if (!waits) {
+          // every ready task commits in its epoch: ready = pool entries at the
+          // pool minimum; the remaining entries' minimum is the next epoch
+          if (!first && pool_n == 0) return failed(ST_INTERNAL);  // scheduler stalled
+          tnow = first ? 0.0 : pmin;
+          double nmin = ABSENT;
+          int keep = 0;
+          NOUNROLL for (int base = 0; base < pool_n; base += WP::W) {
+            const int k = base + wp.lane();
+            bool r = false, kp = false;
+            int j = -1;
+            double rl = 0.0, key = 0.0;
+            if (k < pool_n) {
+              j = LA(const int, pool)[k];
+              rl = LA(const double, pool_rel)[k];
+              key = LA(const double, pool_key)[k];
+              r = rl <= tnow;
+              kp = !r;
+              if (kp && rl < nmin) nmin = rl;
+            }
+            const unsigned m = wp.ballot(r), mk2 = wp.ballot(kp);
+            if (r) {
+              const int at = nr + popc32(m & wp.lt());
+              LA(int, gs_a)[at] = j;
+              LA(double, ready_key)[at] = key;
+            }
+            if (kp) {
+              const int at = keep + popc32(mk2 & wp.lt());
+              LA(int, pool)[at] = j;
+              LA(double, pool_rel)[at] = rl;
+              LA(double, pool_key)[at] = key;
+            }
+            nr += popc32(m);
+            keep += popc32(mk2);
+            wp.sync();
+          }
+          pmin = wp.mind(nmin);  // ABSENT when nothing stays behind
+          pool_n = keep;
+        } else {
+          if (!first) {
+            double nx = ABSENT;
+            NOUNROLL for (int k = wp.lane(); k < pool_n; k += WP::W) {
+              const double r = LA(const double, pool_rel)[k];
+              if (r > tnow && r < nx) nx = r;
+            }
+            NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
+              const double f = W.proc_free[q];
+              if (f > tnow && f < nx) nx = f;
+            }
+            nx = wp.mind(nx);
+            if (nx == ABSENT) return failed(ST_INTERNAL);
+            tnow = nx;
+          }
+          int keep = 0;
+          NOUNROLL for (int base = 0; base < pool_n; base += WP::W) {
+            const int k = base + wp.lane();
+            bool r = false, kp = false;
+            int j = -1;
+            double rl = 0.0, key = 0.0;
+            if (k < pool_n) {
+              j = LA(const int, pool)[k];
+              rl = LA(const double, pool_rel)[k];
+              key = LA(const double, pool_key)[k];
+              r = rl <= tnow;
+              kp = !r;
+            }
+            const unsigned m = wp.ballot(r), mk2 = wp.ballot(kp);
+            if (r) {
+              const int at = nr + popc32(m & wp.lt());
+              LA(int, gs_a)[at] = j;
+              LA(double, ready_key)[at] = key;
+            }
+            if (kp) {
+              const int at = keep + popc32(mk2 & wp.lt());
+              LA(int, pool)[at] = j;
+              LA(double, pool_rel)[at] = rl;
+              LA(double, pool_key)[at] = key;
+            }
+            nr += popc32(m);
+            keep += popc32(mk2);
+            wp.sync();
+          }
+          pool_n = keep;
+        }
+        first = false;
+        if (nr == 0) continue;
+        // order_ready (sim.cpp:117-134): FCFS (release asc, id asc) / PL (ct desc, id asc)
+        if (nr == 1) {
+          LA(int, ready)[0] = LA(const int, gs_a)[0];
+        } else {
+          NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
+            const int a = LA(const int, gs_a)[k];
+            const double ka = LA(const double, ready_key)[k];
+            int rank = 0;
+            NOUNROLL for (int q = 0; q < nr; ++q) {
+              const int c = LA(const int, gs_a)[q];
+              const double kc = LA(const double, ready_key)[q];
+              rank += (kc != ka) ? (LPL ? kc > ka : kc < ka) : (c < a);
+            }
+            LA(int, ready)[rank] = a;
+          }
+        }
+        wp.sync();
+      }
+      // ---------------- one ready task ----------------
+      const int j = LA(const int, ready)[done];
+      const STask tk = LA(const STask, wsb)[j];
+      const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
+      const int nw = tk.nw;
+      const long long tbytes = (long long)tk.b * tk.b * PB.elem;  // every block of a task has its side
+      int p = -1, s = 0, k0 = 0;
+      double inputs = 0.0, start = 0.0, end = 0.0;
+      if (phase != 0) {  // resuming after a cold step
+        p = W.L.r_p;
+        s = W.L.r_s;
+        start = W.L.r_start;
+        end = W.L.r_end;
+        if (phase == 1) {
+          k0 = W.L.r_k + 1;
+          inputs = W.L.r_inputs;
+          if (W.L.op == LEAN_GATHER) inputs = dmax(inputs, W.L.op_result);
+        }
+      } else {
+        const double rel = LA(const TState, ts)[j].rel;
+        // ---------------- select_processor (sim.cpp:136-192) ----------------
+        if (waits) {
+          unsigned idle_mask = 0;
+          NOUNROLL for (int q = wp.lane(); q < P; q += WP::W)
+            if (W.proc_free[q] <= tnow) idle_mask |= 1u << q;
+#if defined(__CUDACC__)
+          if constexpr (WP::W > 1) idle_mask = __reduce_or_sync(0xffffffffu, idle_mask);
+#endif
+          if (idle_mask == 0) {  // R-P/F-P wait for a processor (sim.cpp:800-801): the rest return to the pool
+            NOUNROLL for (int k = done + wp.lane(); k < nr; k += WP::W) {
+              const int jj = LA(const int, ready)[k];
+              const int at = pool_n + (k - done);
+              const TState tt = LA(const TState, ts)[jj];
+              LA(int, pool)[at] = jj;
+              LA(double, pool_rel)[at] = tt.rel;
+              LA(double, pool_key)[at] = LPL ? tt.ct : tt.rel;
+            }
+            wp.sync();
+            pool_n += nr - done;
+            done = nr;
+            continue;
+          }
+          if (SELT == SEL_RP) {
+            const int n = popc32(idle_mask);
+            const double u = (double)(rng_next() >> 11) * 0x1.0p-53;
+            const int k = (int)((unsigned long long)(u * (double)n) % (unsigned long long)n);
+            unsigned mmm = idle_mask;
+            for (int q = 0; q < k; ++q) mmm &= mmm - 1;
+            p = ctz32(mmm);
+          } else {  // F-P: fastest idle processor, lowest id
+            double a = ABSENT, b2 = 0.0;
+            int id = -1;
+            NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
+              if (!((idle_mask >> q) & 1u)) continue;
+              const double tt = PB.ttime[tkind][tbidx][W.ptype[q]];
+              if (id < 0 || tt < a) {
+                a = tt;
+                id = q;
+              }
+            }
+            wp.argmin_lane(a, b2, id);
+            p = id;
+          }
+        } else if (SELT == SEL_EFTP && WP::W == 1) {
+          // width 1: the reference's loop, space by space, then processor by processor
+          bool noroute = false;
+          double est[MAXS];
+          const int w[3] = {tk.ws0, tk.ws1, tk.ws2};
+          NOUNROLL for (int sp = 0; sp < LS; ++sp) {
+            double est_ = 0.0;
+            int al[6] = {-1, -1, -1, -1, -1, -1};
+            double av[6] = {0, 0, 0, 0, 0, 0};
+            NOUNROLL for (int k = 0; k < nw; ++k) {
+              const int b = w[k];
+              const double v = LV(b, sp);
+              if (v != ABSENT) {
+                est_ = dmax(est_, v);
+                continue;
+              }
+              int src = -1;
+              if (LMS != sp && LV(b, LMS) != ABSENT) src = LMS;
+              else
+                NOUNROLL for (int q = 0; q < LS; ++q)
+                  if (q != LMS && q != sp && LV(b, q) != ABSENT) {
+                    src = q;
+                    break;
+                  }
+              if (src < 0) continue;
+              const int nh = PB.route_n[src * MAXS + sp];
+              if (nh == 0) {
+                noroute = true;
+                continue;
+              }
+              double tarr = dmax(tnow, LV(b, src));
+              NOUNROLL for (int h = 0; h < nh; ++h) {
+                const int l = PB.route_l[src * MAXS + sp][h];
+                const double hop = PB.link_lat[l] + (double)tbytes / PB.link_bw[l];
+                double acc = 0.0;
+                bool placed = false;
+                for (int z = 0; z < 6; ++z) {
+                  if (!placed && (al[z] == l || al[z] < 0)) {
+                    al[z] = l;
+                    av[z] += hop;
+                    acc = av[z];
+                    placed = true;
+                  }
+                }
+                tarr += acc;
+              }
+              est_ = dmax(est_, tarr);
+            }
+            est[sp] = est_;
+          }
+          if (noroute) return failed(ST_NO_ROUTE);
+          double a = ABSENT, b2 = 0.0;
+          NOUNROLL for (int q = 0; q < P; ++q) {
+            const double nf = W.proc_free[q];
+            const double qa = dmax(dmax(nf, rel), est[W.pspace[q]]) + PB.ttime[tkind][tbidx][W.ptype[q]];
+            if (p < 0 || qa < a || (qa == a && nf < b2)) {
+              a = qa;
+              b2 = nf;
+              p = q;
+            }
+          }
+        } else {
+          double est_own = 0.0;  // EFT estimate of the lane's processor's space
+#if defined(__CUDACC__)
+          if (SELT == SEL_EFTP && WP::W > 1) {
+            // est_transfer_ready (sim.cpp:762-793), lane (k, sp): one round
+            // loads every V(b_k, sp); ballots give each block's valid-space
+            // mask; the reference's ordered per-link accumulators are rebuilt
+            // from the (<= 2) earlier blocks of the same space by shuffles;
+            // a segmented max gives the estimate per space
+            const unsigned FULL = 0xffffffffu;
+            const int lane = wp.lane();
+            const int Sx = LS;
+            const int k = lk, sp = lq;
+            const bool act = k < nw;
+            const int b = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
+            const double v = act ? LV(b, sp) : ABSENT;
+            const unsigned vm = __ballot_sync(FULL, act && v != ABSENT);
+            const unsigned mymask = act ? (vm >> (k * Sx)) & ((1u << Sx) - 1u) : 0u;
+            int src = -1;
+            if (act && v == ABSENT) {
+              if (LMS != sp && ((mymask >> LMS) & 1u)) {
+                src = LMS;
+              } else {
+                const unsigned o = mymask & ~(1u << LMS) & ~(1u << sp);
+                if (o) src = ctz32(o);
+              }
+            }
+            const double vsrc = __shfl_sync(FULL, v, src >= 0 ? k * Sx + src : lane);
+            int l0 = -1, l1 = -1, nh = 0;
+            double c0 = 0.0, c1 = 0.0;
+            if (src >= 0) {
+              nh = PB.route_n[src * MAXS + sp];
+              if (nh >= 1) {
+                l0 = PB.route_l[src * MAXS + sp][0];
+                c0 = PB.hopc[l0][tbidx];
+              }
+              if (nh >= 2) {
+                l1 = PB.route_l[src * MAXS + sp][1];
+                c1 = PB.hopc[l1][tbidx];
+              }
+            }
+            if (__any_sync(FULL, src >= 0 && nh == 0)) return failed(ST_NO_ROUTE);
+            double acc0 = 0.0, acc1 = 0.0;
+            const int rounds = __any_sync(FULL, src >= 0) ? nw - 1 : 0;
+#pragma unroll
+            for (int kp = 0; kp < 2; ++kp) {
+              if (kp >= rounds) break;
+              const int from = kp * Sx + sp < 32 ? kp * Sx + sp : lane;
+              const int pl0 = __shfl_sync(FULL, l0, from), pl1 = __shfl_sync(FULL, l1, from);
+              const double pc0 = __shfl_sync(FULL, c0, from), pc1 = __shfl_sync(FULL, c1, from);
+              if (kp < k) {
+                if (l0 >= 0 && pl0 == l0) acc0 += pc0;
+                if (l0 >= 0 && pl1 == l0) acc0 += pc1;
+                if (l1 >= 0 && pl0 == l1) acc1 += pc0;
+                if (l1 >= 0 && pl1 == l1) acc1 += pc1;
+              }
+            }
+            double val = 0.0;
+            if (act) {
+              if (v != ABSENT) {
+                val = v;
+              } else if (src >= 0) {
+                double tarr = dmax(tnow, vsrc);
+                acc0 += c0;
+                tarr += acc0;
+                if (nh == 2) {
+                  acc1 += c1;
+                  tarr += acc1;
+                }
+                val = tarr;
+              }
+            }
+            double e = val;
+#pragma unroll
+            for (int kp = 1; kp < 3; ++kp) {
+              const int from = kp * Sx + lane < 32 ? kp * Sx + lane : lane;
+              const double o = __shfl_sync(FULL, val, from);
+              if (lane < Sx && kp < nw) e = dmax(e, o);
+            }
+            est_own = __shfl_sync(FULL, e, W.pspace[lane]);
+          }
+#endif
+          double a = ABSENT, b2 = 0.0;
+          int id = -1;
+          NOUNROLL for (int q = wp.lane(); q < P; q += WP::W) {
+            const double nf = W.proc_free[q];
+            double qa, qb = 0.0;
+            if (SELT == SEL_EFTP) {
+              qa = dmax(dmax(nf, rel), est_own) + PB.ttime[tkind][tbidx][W.ptype[q]];
+              qb = nf;
+            } else {
+              qa = nf;  // EIT-P
+            }
+            if (id < 0 || qa < a || (qa == a && qb < b2)) {
+              a = qa;
+              b2 = qb;
+              id = q;
+            }
+          }
+          wp.argmin_lane(a, b2, id);
+          p = id;
+        }
+        if (p < 0) return failed(ST_NO_PROCESSORS);
+        s = W.pspace[p];
+      }
+      // ---------------- commit (sim.cpp:592-668) ----------------
+      if (phase <= 1) {
+        // acquire the working set in id order (std::set iteration, sim.cpp:597-611)
+#if defined(__CUDACC__)
+        if (WP::W > 1 && (tk.pad & 16)) {
+          const unsigned FULL = 0xffffffffu;
+          const bool act = lk >= k0 && lk < nw;
+          const int b = lk == 0 ? tk.ws0 : (lk == 1 ? tk.ws1 : tk.ws2);
+          const double v = act ? LV(b, lq) : ABSENT;
+          const unsigned vm = __ballot_sync(FULL, act && v != ABSENT);
+          NOUNROLL for (int k = k0; k < nw; ++k) {
+            const unsigned msk = (vm >> (k * LS)) & ((1u << LS) - 1u);
+            const double vk = __shfl_sync(FULL, v, k * LS + s);
+            if ((msk >> s) & 1u) {
+              inputs = dmax(inputs, vk);
+              continue;
+            }
+            const int bk = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
+            int src = -1;
+            if (LMS != s && ((msk >> LMS) & 1u)) {
+              src = LMS;
+            } else {
+              const unsigned o = msk & ~(1u << LMS) & ~(1u << s);
+              if (o) src = ctz32(o);
+            }
+            W.L.r_k = k;
+            W.L.r_p = p;
+            W.L.r_s = s;
+            W.L.phase = 1;
+            if (src < 0) {
+              W.L.r_inputs = inputs;
+              return request(LEAN_GATHER, bk, s, 0.0, 0.0);  // assemble from pieces (sim.cpp:521-572)
+            }
+            const double vs = __shfl_sync(FULL, v, k * LS + src);
+            const double arr = xfer(bk, tbytes, tbidx, src, s, vs);
+            if (st) return failed(st);
+            inputs = dmax(inputs, arr);
+            if (bk == 0) {
+              W.L.r_inputs = inputs;
+              return request(LEAN_VALIDATE, bk, s, arr, 0.0);
+            }
+            validate(bk, s, arr, (tk.pad >> k) & 1);
+          }
+        } else
+#endif
+        {
+          NOUNROLL for (int k = k0; k < nw; ++k) {
+            const int bk = k == 0 ? tk.ws0 : (k == 1 ? tk.ws1 : tk.ws2);
+            const double v = LV(bk, s);
+            if (v != ABSENT) {
+              inputs = dmax(inputs, v);
+              continue;
+            }
+            int src = -1;
+            if (LMS != s && LV(bk, LMS) != ABSENT) src = LMS;
+            else
+              NOUNROLL for (int q = 0; q < LS; ++q)
+                if (q != LMS && q != s && LV(bk, q) != ABSENT) {
+                  src = q;
+                  break;
+                }
+            W.L.r_k = k;
+            W.L.r_p = p;
+            W.L.r_s = s;
+            W.L.phase = 1;
+            if (src < 0) {
+              W.L.r_inputs = inputs;
+              return request(LEAN_GATHER, bk, s, 0.0, 0.0);
+            }
+            const double arr = xfer(bk, tbytes, tbidx, src, s, LV(bk, src));
+            if (st) return failed(st);
+            inputs = dmax(inputs, arr);
+            if (bk == 0) {
+              W.L.r_inputs = inputs;
+              return request(LEAN_VALIDATE, bk, s, arr, 0.0);
+            }
+            validate(bk, s, arr, (tk.pad >> k) & 1);
+          }
+        }
+        const double rel = LA(const TState, ts)[j].rel;
+        start = dmax(dmax(W.proc_free[p], rel), inputs);
+        end = start + PB.ttime[tkind][tbidx][W.ptype[p]];
+        if (!(end > tnow) || start < tnow) return failed(ST_ENGINE_INVARIANT);
+        W.proc_free[p] = end;
+        W.ah += hesp_assign_term(j, p, dbits(start), dbits(end));
+        mk = dmax(mk, end);
+        // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
+        // validate out and the blocks inside it here, valid[out] = end
+        const int out = tk.out;
+        if (tk.pad & 8) {  // unsubdivided tile: cone = {root, tile}, nothing inside
+          NOUNROLL for (int q = wp.lane(); q < LS; q += WP::W)
+            if (q != s) {
+              LV(0, q) = ABSENT;
+              LV(out, q) = ABSENT;
+            }
+          wp.sync();
+        } else if (tk.pad & 32) {  // the root, or partial overlaps in the tile: the general scans
+          W.L.r_p = p;
+          W.L.r_s = s;
+          W.L.r_start = start;
+          W.L.r_end = end;
+          W.L.phase = 2;
+          return request(LEAN_COHERENCE, out, s, start, end);
+        } else {
+          const int t = ltile(out);
+          const Region rb = lreg(out);
+          const int cnt = 2 + LA(const int, tl_cnt)[t];
+          const int head = LA(const int, tl_head)[t];
+          NOUNROLL for (int k = wp.lane(); k < cnt; k += WP::W) {
+            const int x = k == 0 ? 0 : (k == 1 ? t : LA(const int, tl_ids)[head + k - 2]);
+            const Region rx = lreg(x);
+            const bool inside_ = rcontains(rb, rx);
+            if (inside_ || rcontains(rx, rb)) {
+              NOUNROLL for (int q = 0; q < LS; ++q)
+                if (q != s) LV(x, q) = ABSENT;
+            }
+            if (inside_ && x != 0 && x != t) {
+              double& v = LV(x, s);
+              if (v > end) v = end;
+            }
+          }
+          wp.sync();
+        }
+      }
+      if (phase <= 2) {
+        const int out = tk.out;
+        LV(out, s) = end;
+        LA(uint8_t, wrt)[out] = 1;  // written since t=0 (gather's coherence check)
+        if (s != LMS && PB.caching != CACHE_WB) {  // WT / WA (sim.cpp:631-656); the headline policy is WB
+          W.L.r_p = p;
+          W.L.r_s = s;
+          W.L.r_start = start;
+          W.L.r_end = end;
+          W.L.phase = 3;
+          return request(LEAN_WRITEBACK, out, s, end, 0.0);
+        }
+      }
+      phase = 0;
+      W.L.phase = 0;
+      // release successors (sim.cpp:660-667): running max of predecessor
+      // ends; released tasks enter the pool with release time and key
+      {
+        const TState tj = LA(const TState, ts)[j];
+        int added = 0;
+        double amin = ABSENT;
+        NOUNROLL for (int base = 0; base < tj.scnt; base += WP::W) {
+          const int q = base + wp.lane();
+          bool rl = false;
+          int sj = -1;
+          double r = 0.0, key = 0.0;
+          if (q < tj.scnt) {
+            sj = LA(const int, succs)[tj.soff + q];
+            TState& ts_ = LA(TState, ts)[sj];
+            const int left = --ts_.missing;
+            r = dmax(ts_.rel, end);
+            ts_.rel = r;
+            rl = left == 0;
+            if (rl) {
+              key = LPL ? ts_.ct : r;
+              if (r < amin) amin = r;
+            }
+          }
+          const unsigned m = wp.ballot(rl);
+          if (rl) {
+            const int at = pool_n + added + popc32(m & wp.lt());
+            LA(int, pool)[at] = sj;
+            LA(double, pool_rel)[at] = r;
+            LA(double, pool_key)[at] = key;
+          }
+          added += popc32(m);
+        }
+        if (!waits && added) pmin = dmin(pmin, wp.mind(amin));
+        wp.sync();
+        pool_n += added;
+      }
+      ++committed;
+      ++done;
+    }
+#undef LA
+#undef LV
+#undef LS
+#undef LMS
+#undef LPL
+  }
+
+  // =========================================================================
   // One candidate, end to end
   // =========================================================================
 
   // Starts from the base tiling (root + base cluster, shared tables).
   HXN void reset_to_base() {
-    NOUNROLL for (int i = wp.lane(); i < nbb; i += WP::W) tmis()[i] = 0;
+    NOUNROLL for (int i = wp.lane(); i < n_bb(); i += WP::W) tmis()[i] = 0;
     NOUNROLL for (int i = wp.lane(); i < RHT / 2; i += WP::W) ((uint32_t*)rht())[i] = 0xffffffffu;
     wp.sync();
     status = 0;
-    ntasks = nbt;
-    nblocks = nbb;
+    ntasks = n_bt();
+    nblocks = n_bb();
     npart = 0;
     makespan = 0.0;
     ahash = xhash = 0;
-    if (nbt > 1) {  // the base op partitioned the root into tasks 1..nbt-1
+    if (n_bt() > 1) {  // the base op partitioned the root into tasks 1..n_bt()-1
       if (wp.lane() == 0) {
         part()[0].task = 0;
         part()[0].child0 = 1;
-        part()[0].nchild = nbt - 1;
+        part()[0].nchild = n_bt() - 1;
         part()[0].leaves = 0;
       }
       wp.sync();
@@ -2602,13 +3389,13 @@ struct Engine {
       uint32_t* dst = (uint32_t*)(slot + off);
       NOUNROLL for (size_t i = wp.lane(); i < bytes / 4; i += WP::W) dst[i] = src[i];
     };
-    const int nt = th.ntasks - nbt, nb = th.nblocks - nbb;
+    const int nt = th.ntasks - n_bt(), nb = th.nblocks - n_bb();
     copy(PB.lay.tm, sizeof(TaskMeta) * (size_t)(nt > 0 ? nt : 0));
     copy(PB.lay.bm, sizeof(BlockMeta) * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.bref, 4 * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.rht, 2 * (size_t)RHT);
     copy(PB.lay.part, sizeof(PartEntry) * (size_t)th.pad);
-    copy(PB.lay.tmis, ((size_t)nbb + 3) & ~(size_t)3);
+    copy(PB.lay.tmis, ((size_t)n_bb() + 3) & ~(size_t)3);
     wp.sync();
     status = th.status;
     ntasks = th.ntasks;

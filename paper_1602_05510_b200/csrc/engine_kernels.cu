@@ -46,6 +46,7 @@ struct WarpBest {
 };
 
 constexpr int WARPS_PER_BLOCK = 4;
+static_assert(WARPS_PER_BLOCK <= hx::SMALL_WARPS, "one Small per warp");
 // Register budgets (min resident CTAs of 4 warps per SM): the build phase
 // is latency-bound with a small live set (16 CTAs = 64 warps, 32 regs); the
 // event loop keeps ~60 values live and spills below 64 registers.
@@ -53,7 +54,7 @@ constexpr int WARPS_PER_BLOCK = 4;
 #define HESP_BUILD_MIN_BLOCKS 16
 #endif
 #ifndef HESP_SIM_MIN_BLOCKS
-#define HESP_SIM_MIN_BLOCKS 12
+#define HESP_SIM_MIN_BLOCKS 8
 #endif
 
 // The problem tables live in constant memory (hx::c_problem, engine.h):
@@ -71,7 +72,6 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     build_kernel(const hesp_cand_desc* __restrict__ descs, unsigned long long first_index,
                  unsigned long long count, uint8_t* slots, unsigned long long* counter,
                  const uint32_t* __restrict__ order) {
-  __shared__ Small smem[WARPS_PER_BLOCK];
   __shared__ hesp_cand_desc sdesc[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
       generate_desc(first_index + k, &d);
     }
     __syncwarp();
-    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &g_small[wib]);
     eng.build(d);
     __syncwarp();
   }
@@ -131,19 +131,17 @@ __global__ void order_keys(const uint8_t* __restrict__ slots, unsigned long long
 }
 
 __global__ void template_kernel(const hesp_cand_desc* __restrict__ bases, uint8_t* tslots) {
-  __shared__ Small smem;
   __shared__ hesp_cand_desc sd;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) sd = bases[b];
   __syncwarp();
-  Engine<DevWarp> eng(DevWarp{}, c_problem, tslots + (size_t)b * c_problem.lay.total, &smem);
+  Engine<DevWarp> eng(DevWarp{}, c_problem, tslots + (size_t)b * c_problem.lay.total, &g_small[0]);
   eng.build_template(sd);
 }
 
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     neighbor_build_kernel(const hesp_neighbor* __restrict__ nbrs, const uint8_t* __restrict__ tslots,
                           unsigned long long count, uint8_t* slots, unsigned long long* counter) {
-  __shared__ Small smem[WARPS_PER_BLOCK];
   __shared__ hesp_neighbor snb[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -157,7 +155,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
     __syncwarp();
     const hesp_neighbor& nb = snb[wib];
     const int n_ops = nb.n_ops < 0 ? 0 : (nb.n_ops > 2 ? 2 : nb.n_ops);
-    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &g_small[wib]);
     eng.build_neighbor(tslots + (size_t)nb.base * pb.lay.total, n_ops, nb.ops);
     __syncwarp();
   }
@@ -167,7 +165,6 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
                WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter,
                const uint32_t* __restrict__ order) {
-  __shared__ Small smem[WARPS_PER_BLOCK];
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
@@ -180,7 +177,7 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     k = __shfl_sync(0xffffffffu, k, 0);
     if (k >= count) break;
     if (order) k = order[k];
-    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &smem[wib]);
+    Engine<DevWarp> eng(DevWarp{}, pb, slots + (size_t)k * pb.lay.total, &g_small[wib]);
     const Outcome o = eng.sim_slot();
     if (lane == 0 && out) {
       hesp_outcome r;
@@ -370,11 +367,10 @@ __global__ void gen_kernel(unsigned long long first, unsigned long long count, h
 
 __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* slot, int32_t cap, int32_t* proc,
                               double* start, double* end, hesp_outcome* out, TraceBufs* tb) {
-  __shared__ Small smem;
   __shared__ hesp_cand_desc sd;
   if (threadIdx.x == 0) sd = *desc;
   __syncwarp();
-  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &smem);
+  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &g_small[0]);
   eng.tr_proc = proc;
   eng.tr_start = start;
   eng.tr_end = end;
@@ -395,13 +391,12 @@ __global__ void detail_kernel(const hesp_cand_desc* __restrict__ desc, uint8_t* 
 // per-candidate output regions.
 __global__ void schedule_kernel(const hesp_cand_desc* __restrict__ descs, uint8_t* slots, int32_t cap,
                                 int32_t* proc, double* start, double* end, hesp_outcome* out, TraceBufs* tbs) {
-  __shared__ Small smem;
   __shared__ hesp_cand_desc sd;
   const int b = blockIdx.x;
   if (threadIdx.x == 0) sd = descs[b];
   __syncwarp();
   uint8_t* slot = slots + (size_t)b * c_problem.lay.total;
-  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &smem);
+  Engine<DevWarp, true> eng(DevWarp{}, c_problem, slot, &g_small[0]);
   eng.tr_proc = proc + (size_t)b * cap;
   eng.tr_start = start + (size_t)b * cap;
   eng.tr_end = end + (size_t)b * cap;

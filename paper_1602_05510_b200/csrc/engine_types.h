@@ -132,6 +132,7 @@ struct Problem {
   hesp_gen_config gen;
   // ---- scheduling policy (SchedConfig, sim.hpp:26-32) ----
   int32_t ordering, selection, caching;
+  int32_t loop;  // event-loop variant of the batch kernels: 0 lean (default), 1 general (A/B: HESP_LOOP=1)
   uint64_t sched_seed;
   // ---- capacities of the per-candidate slot ----
   int32_t maxt, maxb, maxbnd, maxcells, maxrn, maxedges, maxpb, maxgs, maxgr;

@@ -9,6 +9,8 @@
 //     once with the width-1 instantiation of the engine itself.
 #include "problem.h"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <map>
@@ -194,6 +196,8 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   p.selection = sched.selection;
   p.caching = sched.caching;
   p.sched_seed = sched.seed;
+  p.loop = 0;
+  if (const char* lv = std::getenv("HESP_LOOP")) p.loop = std::atoi(lv);
   if (p.ordering < 0 || p.ordering > 1 || p.selection < 0 || p.selection > 3 || p.caching < 0 ||
       p.caching > 2)
     bad("unknown scheduling policy");

@@ -1,0 +1,7 @@
+# full ncu capture of build+sim kernels for one engine build (dev)
+LIB=$1; TAG=$2
+HESP_LIB=$LIB HESP_CHUNK=32768 timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sim_kernel" -s 1 -c 1 \
+    -o gpurun_out/prof_$TAG -f python scripts/probe_throughput.py C2 32768 > gpurun_out/prof_$TAG.log 2>&1
+ncu -i gpurun_out/prof_$TAG.ncu-rep --page source --csv --print-source cuda,sass -k sim_kernel > gpurun_out/src_$TAG.csv 2>/dev/null
+ncu -i gpurun_out/prof_$TAG.ncu-rep --page raw --csv > gpurun_out/raw_$TAG.csv 2>/dev/null
+ls -la gpurun_out/*$TAG*
