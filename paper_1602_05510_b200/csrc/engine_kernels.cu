@@ -1269,7 +1269,10 @@ int hesp_verify_trace(const hesp_engine* e, const hesp_trace* tr, char* buf, siz
     g_last_error = "hesp_verify_trace needs a successful hesp_eval_trace first";
     return HESP_E_INVALID;
   }
-  const auto v = hx::verify_trace(e->hp.p, e->last_graph, *tr);
+  cudaSetDevice(e->device);
+  std::vector<std::string> v;
+  const int rc = hx::verify_trace_device(e->hp.p, e->last_graph, *tr, e->stream, v);
+  if (rc != HESP_OK) return rc;
   if (n_violations) *n_violations = (int32_t)v.size();
   if (buf && cap) {
     std::string all;

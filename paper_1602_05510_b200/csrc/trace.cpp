@@ -7,7 +7,7 @@
 //   compute_idle_avgs                                sim.cpp:670-702
 //   busy_time, avg_load, LoadTrace::integral         sim.cpp:71-87
 //   compute_load_trace                               sim.cpp:975-991
-//   verify_schedule                                  sim.cpp:857-973
+// verify_schedule (sim.cpp:857-973) runs on the device: verify.cu.
 #include "trace.h"
 
 #include <algorithm>
@@ -28,17 +28,6 @@ const char* kind_name(int k) {  // to_string(TaskKind), platform.cpp:39-47
     case 3: return "GEMM";
   }
   return "?";
-}
-
-struct R64 {
-  int64_t row, col, rows, cols;
-};
-R64 r64(const Region& r) { return {r.row, r.col, r.rows, r.cols}; }
-bool contains(const R64& o, const R64& i) {  // graph.cpp:34-38
-  return i.row >= o.row && i.col >= o.col && i.row + i.rows <= o.row + o.rows && i.col + i.cols <= o.col + o.cols;
-}
-bool overlap(const R64& a, const R64& b) {  // graph.cpp:40-43
-  return a.row < b.row + b.rows && b.row < a.row + a.rows && a.col < b.col + b.cols && b.col < a.col + a.cols;
 }
 
 struct Ev {
@@ -238,164 +227,6 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
   for (size_t i = 0; i + 1 < times.size(); ++i) integral += active[i] * (times[i + 1] - times[i]);
   tr->load_integral = integral;
   return HESP_OK;
-}
-
-std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr) {
-  std::vector<std::string> violations;
-  const double eps = 1e-9 * std::max(1.0, tr.outcome.makespan);
-  const int main_space = p.main_space;
-  std::map<int, hesp_assignment> asg;  // SimResult::assignments
-  for (int i = 0; i < tr.n_assign; ++i) asg[tr.assignments[i].task] = tr.assignments[i];
-  std::unordered_map<int, int> li;
-  for (size_t k = 0; k < g.leaves.size(); ++k) li[g.leaves[k]] = (int)k;
-
-  // (a) per-processor intervals disjoint
-  std::map<int, std::vector<hesp_assignment>> per_proc;
-  for (const auto& [id, a] : asg) per_proc[a.proc].push_back(a);
-  for (auto& [proc, list] : per_proc) {
-    std::sort(list.begin(), list.end(),
-              [](const hesp_assignment& x, const hesp_assignment& y) { return x.start < y.start; });
-    for (size_t i = 1; i < list.size(); ++i)
-      if (list[i].start < list[i - 1].end - eps)
-        violations.push_back("processor " + std::to_string(proc) + ": tasks " + std::to_string(list[i - 1].task) +
-                             " and " + std::to_string(list[i].task) + " overlap");
-  }
-
-  // (b) dependence ordering over TaskGraph::edges(): the transitive reduction
-  // of the dependence relation in (src rank, dst rank) program order
-  // (graph.cpp:684-726).  The device's predecessor lists carry the same
-  // closure (E2), so the reduction is the reference's edge list.
-  {
-    const int n = (int)g.leaves.size();
-    std::vector<std::vector<int>> direct(n);
-    for (int v = 0; v < n; ++v)
-      for (int q = 0; q < g.pcnt[v]; ++q) {
-        const auto it = li.find(g.preds[g.poff[v] + q]);
-        if (it != li.end()) direct[it->second].push_back(v);
-      }
-    for (auto& d : direct) {
-      std::sort(d.begin(), d.end());
-      d.erase(std::unique(d.begin(), d.end()), d.end());
-    }
-    const size_t words = ((size_t)n + 63) / 64;
-    std::vector<uint64_t> reach((size_t)n * words, 0);
-    for (int u = n - 1; u >= 0; --u) {
-      uint64_t* row = &reach[(size_t)u * words];
-      for (int v : direct[u]) {
-        row[v / 64] |= 1ull << (v % 64);
-        const uint64_t* vrow = &reach[(size_t)v * words];
-        for (size_t w = 0; w < words; ++w) row[w] |= vrow[w];
-      }
-    }
-    auto bit = [&](int node, int target) { return (reach[(size_t)node * words + target / 64] >> (target % 64)) & 1u; };
-    for (int u = 0; u < n; ++u)
-      for (int v : direct[u]) {
-        bool redundant = false;
-        for (int w : direct[u]) {
-          if (w == v) continue;
-          if (bit(w, v)) {
-            redundant = true;
-            break;
-          }
-        }
-        if (redundant) continue;
-        const int src = g.leaves[u], dst = g.leaves[v];
-        auto si = asg.find(src), di = asg.find(dst);
-        if (si == asg.end() || di == asg.end()) {
-          violations.push_back("edge endpoint not scheduled");
-          continue;
-        }
-        if (di->second.start < si->second.end - eps)
-          violations.push_back("edge " + std::to_string(src) + "->" + std::to_string(dst) +
-                               " violated: dst starts before src ends");
-      }
-  }
-
-  // (c) read coherence (sim.cpp:897-959)
-  struct WriteEvt {
-    double end;
-    int space;
-    R64 region;
-  };
-  std::vector<WriteEvt> writes;
-  for (const auto& [id, a] : asg) {
-    const auto it = li.find(id);
-    if (it == li.end()) continue;
-    const TaskMeta& m = g.meta[it->second];
-    writes.push_back({a.end, p.proc_space[a.proc], r64(g.bregion[m.blk[m.nrd]])});
-  }
-  for (const auto& [id, a] : asg) {
-    const auto it = li.find(id);
-    if (it == li.end()) continue;
-    const TaskMeta& m = g.meta[it->second];
-    const int space = p.proc_space[a.proc];
-    for (int k = 0; k < m.nrd; ++k) {
-      const int rblk = m.blk[k];
-      const R64 rreg = r64(g.bregion[rblk]);
-      std::vector<int64_t> xv{rreg.col, rreg.col + rreg.cols};
-      std::vector<int64_t> yv{rreg.row, rreg.row + rreg.rows};
-      for (const auto& w : writes) {
-        if (!overlap(w.region, rreg)) continue;
-        xv.push_back(std::clamp(w.region.col, rreg.col, rreg.col + rreg.cols));
-        xv.push_back(std::clamp(w.region.col + w.region.cols, rreg.col, rreg.col + rreg.cols));
-        yv.push_back(std::clamp(w.region.row, rreg.row, rreg.row + rreg.rows));
-        yv.push_back(std::clamp(w.region.row + w.region.rows, rreg.row, rreg.row + rreg.rows));
-      }
-      std::sort(xv.begin(), xv.end());
-      xv.erase(std::unique(xv.begin(), xv.end()), xv.end());
-      std::sort(yv.begin(), yv.end());
-      yv.erase(std::unique(yv.begin(), yv.end()), yv.end());
-      bool fail_read = false;
-      for (size_t yi = 0; yi + 1 < yv.size() && !fail_read; ++yi)
-        for (size_t xi = 0; xi + 1 < xv.size() && !fail_read; ++xi) {
-          const R64 cell{yv[yi], xv[xi], yv[yi + 1] - yv[yi], xv[xi + 1] - xv[xi]};
-          double w_end = -1;
-          int w_space = main_space;
-          for (const auto& w : writes) {
-            if (w.end > a.start + eps) continue;
-            if (!contains(w.region, cell)) continue;
-            if (w.end > w_end) {
-              w_end = w.end;
-              w_space = w.space;
-            }
-          }
-          bool ok = false;
-          if (w_end >= 0 && w_space == space) ok = true;
-          if (!ok && w_end < 0 && space == main_space) ok = true;
-          if (!ok) {
-            const double lower = std::max(w_end, 0.0);
-            for (int xi2 = 0; xi2 < tr.n_xfer; ++xi2) {
-              const hesp_transfer& x = tr.transfers[xi2];
-              if (x.dst_space != space) continue;
-              const R64 xr = x.has_fragment ? R64{x.frag_row, x.frag_col, x.frag_rows, x.frag_cols}
-                                            : r64(g.bregion[x.block]);
-              if (!contains(xr, cell)) continue;
-              if (x.end <= a.start + eps && x.end >= lower - eps) {
-                ok = true;
-                break;
-              }
-            }
-          }
-          if (!ok) {
-            violations.push_back("task " + std::to_string(id) + " reads block " + std::to_string(rblk) +
-                                 " in space " + std::to_string(space) + " without a fresh local copy");
-            fail_read = true;
-          }
-        }
-    }
-  }
-
-  // (d) capacity respected at every residency change
-  std::map<int, int64_t> used;
-  for (int i = 0; i < tr.n_res; ++i) {
-    const hesp_residency& rc = tr.residency[i];
-    used[rc.space] += rc.delta_bytes;
-    if (used[rc.space] > p.cap[rc.space])
-      violations.push_back("space " + std::to_string(rc.space) + " exceeds capacity at t=" + std::to_string(rc.time));
-    if (used[rc.space] < 0)
-      violations.push_back("space " + std::to_string(rc.space) + " under-run at t=" + std::to_string(rc.time));
-  }
-  return violations;
 }
 
 void trace_bounds(const Problem& p, const TraceGraph& g, double* cp, double* work) {

@@ -6,6 +6,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "engine_types.h"
 #include "hesp_engine.h"
 
@@ -35,8 +37,11 @@ struct TraceLogs {
 int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr,
                  bool schedule_only = false);
 
-// verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph.
-std::vector<std::string> verify_trace(const Problem& p, const TraceGraph& g, const hesp_trace& tr);
+// verify_schedule (sim.cpp:857-973) over a hesp_trace and the candidate graph,
+// as data-parallel passes on the device (verify.cu); messages in `out`.
+// HESP_OK, HESP_E_CUDA or HESP_E_LIMIT.
+int verify_trace_device(const Problem& p, const TraceGraph& g, const hesp_trace& tr, cudaStream_t st,
+                        std::vector<std::string>& out);
 
 // Critical-path and work lower bounds of the traced graph (fastest type per task).
 void trace_bounds(const Problem& p, const TraceGraph& g, double* cp, double* work);

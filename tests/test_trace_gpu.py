@@ -88,3 +88,25 @@ def test_trace_agrees_with_batch_outcome(lib):
             assert hbits(tr.makespan) == hbits(out[i]["makespan"])
             assert len(tr.assignments) == int(out[i]["n_leaves"])
             assert eng.verify_trace(tr) == []
+
+
+def test_verify_c4_winner_fast_and_clean(lib):
+    """The device validator on a 32x32 (C4) schedule: clean on the engine's own
+    schedule, catches a moved task, and takes well under a second."""
+    import time
+    p, _ = PARITY["c4"]
+    eng = make_engine(p)
+    descs = eng.generate_host(0, 4)
+    out, _ = eng.eval_descs(descs)
+    k = int(np.nonzero(out["status"] == 0)[0][0])
+    tr = eng.eval_trace(descs[k])
+    assert tr.status == 0 and len(tr.assignments) > 5000
+    eng.verify_trace(tr)  # warm-up (module load)
+    t0 = time.perf_counter()
+    v = eng.verify_trace(tr)
+    dt = time.perf_counter() - t0
+    assert v == [] and dt < 1.0, (v[:3], dt)
+    a = tr.assignments
+    a["start"][100] -= 0.01
+    a["end"][100] -= 0.01
+    assert eng.verify_trace(tr)
