@@ -121,25 +121,29 @@ __global__ void vfy_edges(const int32_t* __restrict__ leaves, const int32_t* __r
   }
 }
 
-// (c) one warp per (leaf, read slot); per-warp smem scratch for the grid lines
-constexpr int VW = 4;         // warps per CTA
-constexpr int VLINES = 256;   // grid lines per axis per read (overflow is reported)
+// (c) one warp per (leaf, read slot).  The fragment grid's lines are kept as
+// bitmaps over the read's extent (offsets 0..cols / 0..rows) in shared
+// memory -- duplicates cost nothing -- and expanded to sorted line lists.
+constexpr int VW = 4;          // warps per CTA
+constexpr int VDIST = 512;     // distinct grid lines per axis (overflow is reported)
 __global__ void __launch_bounds__(VW * 32) vfy_reads(
     const int32_t* __restrict__ rd_task, const int32_t* __restrict__ rd_k, const int32_t* __restrict__ rd_blk,
     const int32_t* __restrict__ rd_space, const double* __restrict__ rd_start, const int32_t* __restrict__ rd_tile,
     int nreads, const VRegion* __restrict__ breg,
-    // writes by tile (CSR; task-id order inside a tile); bucket T = regions spanning tiles
+    // writes by tile (CSR; task-id order inside a tile); the last bucket holds regions spanning tiles
     const int32_t* __restrict__ w_off, const VRegion* __restrict__ w_reg, const double* __restrict__ w_end,
     const int32_t* __restrict__ w_space, int ntile_buckets,
     // transfers by (dst space, tile) (CSR), same spanning bucket per space
     const int32_t* __restrict__ x_off, const VRegion* __restrict__ x_reg, const double* __restrict__ x_end,
-    int main_space, double eps, Viol* out, int* nout, int cap) {
-  __shared__ int xs_[VW][VLINES], ys_[VW][VLINES], xsu[VW][VLINES], ysu[VW][VLINES];
+    int main_space, double eps, int bm_words, Viol* out, int* nout, int cap) {
+  extern __shared__ uint32_t vsm[];  // per warp: x bitmap, y bitmap (bm_words each), x list, y list (VDIST each)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * VW + w;
   if (r >= nreads) return;
-  int* xs = xs_[w];
-  int* ys = ys_[w];
+  uint32_t* bx = vsm + (size_t)w * (2 * bm_words + 2 * VDIST);
+  uint32_t* by = bx + bm_words;
+  int* xu = (int*)(by + bm_words);
+  int* yu = xu + VDIST;
   const VRegion rr = breg[rd_blk[r]];
   const int space = rd_space[r];
   const double a = rd_start[r];
@@ -152,77 +156,57 @@ __global__ void __launch_bounds__(VW * 32) vfy_reads(
     for (int bk = b0; bk <= b1; ++bk) f(bk);
     if (T >= 0) f(span);
   };
-  // ---- grid lines: the read's edges + every overlapping write's clamped edges
-  int nx = 0, ny = 0;
+  const int wx = (rr.cols >> 5) + 1, wy = (rr.rows >> 5) + 1;  // bitmap words in use
+  for (int k = lane; k < wx; k += 32) bx[k] = 0;
+  for (int k = lane; k < wy; k += 32) by[k] = 0;
+  __syncwarp();
   if (lane == 0) {
-    xs[0] = rr.col;
-    xs[1] = rr.col + rr.cols;
-    ys[0] = rr.row;
-    ys[1] = rr.row + rr.rows;
+    atomicOr(&bx[0], 1u);
+    atomicOr(&bx[rr.cols >> 5], 1u << (rr.cols & 31));
+    atomicOr(&by[0], 1u);
+    atomicOr(&by[rr.rows >> 5], 1u << (rr.rows & 31));
   }
-  nx = ny = 2;
-  bool over = false;
+  // every overlapping write's edges, clamped to the read (sim.cpp:908-916)
   for_buckets([&](int bk) {
-    for (int base = w_off[bk]; base < w_off[bk + 1]; base += 32) {
-      const int i = base + lane;
-      bool hit = false;
-      VRegion wr{0, 0, 0, 0};
-      if (i < w_off[bk + 1]) {
-        wr = w_reg[i];
-        hit = voverlap(wr, rr);
-      }
-      const unsigned m = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
-        const int at = 2 * __popc(m & ((1u << lane) - 1u));
-        if (nx + at + 1 < VLINES) {
-          xs[nx + at] = vclamp(wr.col, rr.col, rr.col + rr.cols);
-          xs[nx + at + 1] = vclamp(wr.col + wr.cols, rr.col, rr.col + rr.cols);
-          ys[ny + at] = vclamp(wr.row, rr.row, rr.row + rr.rows);
-          ys[ny + at + 1] = vclamp(wr.row + wr.rows, rr.row, rr.row + rr.rows);
-        }
-      }
-      nx += 2 * __popc(m);
-      ny += 2 * __popc(m);
+    for (int i = w_off[bk] + lane; i < w_off[bk + 1]; i += 32) {
+      const VRegion wr = w_reg[i];
+      if (!voverlap(wr, rr)) continue;
+      const int x0 = vclamp(wr.col, rr.col, rr.col + rr.cols) - rr.col;
+      const int x1 = vclamp(wr.col + wr.cols, rr.col, rr.col + rr.cols) - rr.col;
+      const int y0 = vclamp(wr.row, rr.row, rr.row + rr.rows) - rr.row;
+      const int y1 = vclamp(wr.row + wr.rows, rr.row, rr.row + rr.rows) - rr.row;
+      atomicOr(&bx[x0 >> 5], 1u << (x0 & 31));
+      atomicOr(&bx[x1 >> 5], 1u << (x1 & 31));
+      atomicOr(&by[y0 >> 5], 1u << (y0 & 31));
+      atomicOr(&by[y1 >> 5], 1u << (y1 & 31));
     }
   });
-  if (nx > VLINES) over = true;
   __syncwarp();
-  if (over) {
+  // sorted distinct lines: word-wise popcount prefix sums
+  auto expand = [&](const uint32_t* bm, int words, int origin, int* list) -> int {
+    int n = 0;
+    for (int base = 0; base < words; base += 32) {
+      const int k = base + lane;
+      const uint32_t m = k < words ? bm[k] : 0u;
+      const int c = __popc(m);
+      int incl = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int at = n + incl - c;
+      for (uint32_t mm = m; mm; mm &= mm - 1, ++at)
+        if (at < VDIST) list[at] = origin + 32 * k + (__ffs((int)mm) - 1);
+      n += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return n;
+  };
+  const int nxu = expand(bx, wx, rr.col, xu);
+  const int nyu = expand(by, wy, rr.row, yu);
+  __syncwarp();
+  if (nxu > VDIST || nyu > VDIST) {
     if (lane == 0) emit(out, nout, cap, Viol{-1, 0, 0, rd_task[r], 0, 0, 0.0});
     return;
-  }
-  // ---- sort (rank with the index as tie-break: a permutation), then unique
-  int* xu = xsu[w];
-  int* yu = ysu[w];
-  for (int i = lane; i < nx; i += 32) {
-    const int vx = xs[i], vy = ys[i];
-    int rx = 0, ry = 0;
-    for (int j = 0; j < nx; ++j) {
-      rx += xs[j] < vx || (xs[j] == vx && j < i);
-      ry += ys[j] < vy || (ys[j] == vy && j < i);
-    }
-    xu[rx] = vx;
-    yu[ry] = vy;
-  }
-  __syncwarp();
-  int nxu = 0, nyu = 0;
-  for (int base = 0; base < nx; base += 32) {  // in-place compaction: writes never pass the reads
-    const int i = base + lane;
-    int vx = 0, vy = 0;
-    bool kx = false, ky = false;
-    if (i < nx) {
-      vx = xu[i];
-      vy = yu[i];
-      kx = i == 0 || xu[i - 1] != vx;
-      ky = i == 0 || yu[i - 1] != vy;
-    }
-    const unsigned mx = __ballot_sync(0xffffffffu, kx), my = __ballot_sync(0xffffffffu, ky);
-    __syncwarp();
-    if (kx) xu[nxu + __popc(mx & ((1u << lane) - 1u))] = vx;
-    if (ky) yu[nyu + __popc(my & ((1u << lane) - 1u))] = vy;
-    nxu += __popc(mx);
-    nyu += __popc(my);
-    __syncwarp();
   }
   // ---- cells: freshest write before the read, then a copy that is fresh here
   const int ncell = (nxu - 1) * (nyu - 1);
@@ -452,10 +436,22 @@ int verify_trace_device(const Problem& P, const TraceGraph& g, const hesp_trace&
       vfy_edges<<<(n + 7) / 8, 256, 0, st>>>(d_leaves.p, d_poff.p, d_pcnt.p, d_preds.p, d_rank.p, d_aprocid.p, d_ast.p,
                                              d_aen.p, n, eps, d_out, d_n, cap);
     const int nreads = (int)rd_task.size();
-    if (nreads > 0)
-      vfy_reads<<<(nreads + VW - 1) / VW, VW * 32, 0, st>>>(d_rdt.p, d_rdk.p, d_rdb.p, d_rds.p, d_rdst.p, d_rdtile.p, nreads,
-                                                           d_breg.p, d_woff.p, d_wreg.p, d_wend.p, d_wsp.p, NT, d_xoff.p,
-                                                           d_xreg.p, d_xend.p, P.main_space, eps, d_out, d_n, cap);
+    if (nreads > 0) {
+      // bitmap words for the largest read extent
+      int ext = 0;
+      for (int b : rd_blk) ext = std::max(ext, std::max(g.bregion[b].rows, g.bregion[b].cols));
+      const int bm_words = (ext >> 5) + 1;
+      const size_t rsmem = (size_t)VW * (2 * bm_words + 2 * VDIST) * 4;
+      if (rsmem > 200 * 1024) {
+        set_last_error("verify: read extent too large for the device bitmaps");
+        return HESP_E_LIMIT;
+      }
+      cudaFuncSetAttribute(vfy_reads, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsmem);
+      vfy_reads<<<(nreads + VW - 1) / VW, VW * 32, rsmem, st>>>(d_rdt.p, d_rdk.p, d_rdb.p, d_rds.p, d_rdst.p, d_rdtile.p,
+                                                               nreads, d_breg.p, d_woff.p, d_wreg.p, d_wend.p, d_wsp.p, NT,
+                                                               d_xoff.p, d_xreg.p, d_xend.p, P.main_space, eps, bm_words,
+                                                               d_out, d_n, cap);
+    }
     if (tr.n_res > 0) vfy_capacity<<<1, 32, 0, st>>>(d_rsp.p, d_rd.p, d_rt.p, tr.n_res, d_cap.p, S, d_out, d_n, cap);
     int nv = 0;
     ok = cudaGetLastError() == cudaSuccess && cudaMemcpyAsync(&nv, d_n, sizeof(int), cudaMemcpyDeviceToHost, st) == cudaSuccess &&
@@ -477,7 +473,7 @@ int verify_trace_device(const Problem& P, const TraceGraph& g, const hesp_trace&
   }
   for (const Viol& v : viols)
     if (v.kind < 0) {
-      set_last_error("verify: a read's fragment grid exceeds the device scratch");
+      set_last_error("verify: a read's fragment grid exceeds the device scratch (VDIST lines per axis)");
       return HESP_E_LIMIT;
     }
   // (b) keep only covering pairs: (u, v) with no path of length >= 2 in the
