@@ -131,6 +131,12 @@ enum {
   HESP_E_NODEV = -3,   /* no usable sm_100 device */
   HESP_E_LIMIT = -4    /* a caller-provided trace array is too small (counts report the need) */
 };
+/* Per-candidate engine statuses (>= 200; below 200 a status is 1 + hesp::Err). */
+enum {
+  HESP_ST_ENGINE_LIMIT = 201,      /* a per-candidate buffer of the engine would overflow */
+  HESP_ST_ENGINE_INVARIANT = 202,  /* an equivalence the engine relies on was violated (never seen) */
+  HESP_ST_UNREPRODUCIBLE = 203     /* bridge: a TaskGraph whose history its replay cannot reproduce */
+};
 
 typedef struct hesp_engine hesp_engine;
 
@@ -283,6 +289,19 @@ int hesp_verify_trace(const hesp_engine* e, const hesp_trace* trace, char* buf, 
  * its fastest processor type's time; *work = sum of those times / processors. */
 int hesp_trace_bounds(const hesp_engine* e, double* cp, double* work);
 
+/* The data blocks of the candidate last passed to hesp_eval_trace, indexed by
+ * reference block id (DataDag::blocks(), graph.hpp:48-79): block k's region
+ * and is_intersection flag; ids consumed by blocks the candidate's merges
+ * erased have rows = cols = 0.  *n = the id count; writes min(n, cap)
+ * entries.  Returns HESP_OK or HESP_E_INVALID (no successful trace yet).
+ * (The reference-side bridge maps a caller's TaskGraph onto the engine's
+ * ids with it: include/hesp_b200_bridge.hpp.) */
+typedef struct {
+  int64_t row, col, rows, cols;
+  int32_t is_intersection, pad;
+} hesp_block_info;
+int hesp_trace_blocks(const hesp_engine* e, hesp_block_info* out, int32_t cap, int32_t* n);
+
 /* ---------------------------------------------------------------------------
  * Iterative schedule/partition solver (the reference
  * declares it only: solver.hpp:57-86, semantics SPEC.md:410-461).  A chain
@@ -292,8 +311,11 @@ int hesp_trace_bounds(const hesp_engine* e, double* cp, double* work);
  * SPEC's collect_candidates / score_candidate / choose_p define them, then
  * evaluates EVERY candidate mutation in one device batch and keeps only the
  * ones whose graph simulates (status 0) before select_candidate (Hard: max
- * score, first in candidate order on ties; Soft: score-proportional draw
- * from hesp::Rng).  DESIGN.md §10 states the decisions the SPEC leaves open. */
+ * score, lowest target id on ties, then candidate order; Soft:
+ * score-proportional draw from hesp::Rng).  A chain state holds at most
+ * HESP_MAX_OPS ops (merges append, they do not cancel): once candidates would
+ * exceed it they are dropped and budget_iteration records where that began.
+ * DESIGN.md §10 states the decisions the SPEC leaves open. */
 enum { HESP_SEL_ALL = 0, HESP_SEL_CP = 1, HESP_SEL_SHALLOW = 2 };
 /* HESP_SAMPLE_EXACT (an extension, not in SPEC): the validity batch already
  * simulated every candidate mutation, so pick the one with the smallest
@@ -334,7 +356,11 @@ typedef struct {
   hesp_cand_desc best;        /* best state found (min makespan, earliest iteration) */
   double best_makespan;
   int32_t best_iteration;
-  int32_t pad;
+  int32_t budget_iteration;   /* first iteration whose candidates were cut because the state
+                                 descriptor would exceed HESP_MAX_OPS ops, or overflowed the
+                                 engine's per-candidate slot (ids consumed by merged clusters
+                                 count): from there on the chain may differ from an uncapped
+                                 solve (-1: never) */
   int64_t n_simulated;        /* device simulations issued (states + candidate batches) */
 } hesp_solver_result;
 
@@ -343,9 +369,11 @@ typedef struct {
  * d < 2*min_block or no grid exists (GrainTooSmall). */
 double hesp_choose_p(double idle_avg, int64_t d, int64_t min_block, int32_t k_max);
 
-/* select_candidate (solver.hpp:78-80): Hard = index of the maximum score
- * (first on ties); Soft = score-proportional draw with hesp::Rng, whose
- * splitmix64 state *rng_state advances.  -1 for an empty list. */
+/* select_candidate (solver.hpp:78-80) over bare scores: Hard = index of the
+ * maximum score (first on ties: without target ids; hesp_solve breaks Hard
+ * ties by the lowest target id); Soft = score-proportional draw
+ * with hesp::Rng, whose splitmix64 state *rng_state advances.  -1 for an
+ * empty list. */
 int32_t hesp_select_candidate(const double* scores, int32_t n, int32_t sampling, uint64_t* rng_state);
 
 /* Runs solve() from `initial` (NULL = the base tiling).  Returns 0, the

@@ -6,6 +6,7 @@
 // GPU box: links oracle/_ref/libhesp_ref.so and the engine library).
 #include <cstdio>
 #include <cstring>
+#include <random>
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -14,7 +15,8 @@
 #include "hesp/platform.hpp"
 #include "hesp/sim.hpp"
 #include "hesp_b200_bridge.hpp"
-#include "json.hpp"  // nlohmann 3.11.3 (the reference's own parser dependency), for the fixture entries
+#include "json.hpp"
+#include "random_graphs.hpp"  // nlohmann 3.11.3 (the reference's own parser dependency), for the fixture entries
 
 namespace {
 std::string slurp(const std::string& p) {
@@ -70,6 +72,7 @@ int main(int argc, char** argv) {
   uint64_t first = 0, sseed = 0;
   hesp_gen_config gen{1, 8, 3, 64, 2, {2, 4, 0, 0}, 0};
   std::string ordering = "PL", selection = "EFT-P", caching = "WB";
+  int graphs = 0;  // --graphs N: N graphs built by random reference partition/merge/repartition calls
   for (int i = 1; i < argc; ++i) {
     std::string k = argv[i];
     auto v = [&]() { return std::string(argv[++i]); };
@@ -96,6 +99,7 @@ int main(int argc, char** argv) {
     else if (k == "--first") first = std::stoull(v());
     else if (k == "--count") count = std::stoi(v());
     else if (k == "--threads") v();
+    else if (k == "--graphs") graphs = std::stoi(v());
   }
   const auto plat = hesp::Platform::from_json(slurp(plat_p));
   const auto text = slurp(model_p);
@@ -135,6 +139,85 @@ int main(int argc, char** argv) {
                       e["peak_flops"].get<double>(), e["b_half"].get<double>());
   }
   hesp::b200::BatchSimulator gpu(plat, an, tab, cfg, n, elem, s_base, gen);
+  if (graphs > 0) {
+    // The TaskGraph drop-in: graphs built by arbitrary sequences of the
+    // reference's own mutators (partition_task / merge_cluster incl. the base
+    // cluster / repartition_cluster; failing calls leave the graph as is),
+    // simulated by hesp::simulate and by BatchSimulator::simulate(graph), and
+    // batch-evaluated by BatchSimulator::evaluate(graphs).
+    oracle::GraphStats gst_;
+    std::vector<hesp::TaskGraph> gs =
+        oracle::random_graphs(graphs, n, elem, s_base, gen.min_block, gen.seed * 7919 + first, &gst_);
+    const int calls = gst_.calls, base_merges = gst_.top_merges;
+    int ok = 0, failed = 0, bad = 0, unrepro = 0;
+    std::vector<int> ref_status(gs.size(), 0);
+    std::vector<double> ref_mk(gs.size(), 0.0);
+    for (std::size_t i = 0; i < gs.size(); ++i) {
+      hesp::SimResult ref, mine;
+      int gst = 0;
+      try {
+        ref = hesp::simulate(gs[i], plat, model, cfg);
+        ref_mk[i] = ref.makespan;
+      } catch (const hesp::Error& e) {
+        ref_status[i] = 1 + static_cast<int>(e.code());
+      }
+      try {
+        mine = gpu.simulate(gs[i]);
+      } catch (const hesp::Error& e) {
+        gst = 1 + static_cast<int>(e.code());
+      }
+      if (gst == 1 + static_cast<int>(hesp::Err::Internal) && ref_status[i] != gst) {
+        ++unrepro;  // the bridge refused: history not reproducible by the replay (explicit, never a wrong result)
+        continue;
+      }
+      if (ref_status[i] || gst) {
+        ++failed;
+        if (ref_status[i] != gst) {
+          ++bad;
+          const hesp_cand_desc d = gpu.describe(gs[i]);
+          std::printf("graph %zu: status ref %d gpu %d; ops", i, ref_status[i], gst);
+          for (int k = 0; k < d.n_ops; ++k) std::printf(" (%d,%d)", d.ops[k].task, d.ops[k].s);
+          std::printf("\n");
+        }
+        continue;
+      }
+      std::string why;
+      if (!same(ref, mine, &why)) {
+        ++bad;
+        std::printf("graph %zu: %s differs\n", i, why.c_str());
+        continue;
+      }
+      if (hesp::verify_schedule(mine, gs[i], plat) != hesp::verify_schedule(ref, gs[i], plat)) {
+        ++bad;
+        std::printf("graph %zu: verify_schedule differs\n", i);
+        continue;
+      }
+      ++ok;
+    }
+    hesp_best best{};
+    const auto out = gpu.evaluate(gs, &best);
+    int unrepro_batch = 0;
+    for (std::size_t i = 0; i < gs.size(); ++i) {
+      if (out[i].status == HESP_ST_UNREPRODUCIBLE) {
+        ++unrepro_batch;
+        continue;
+      }
+      if (out[i].status != ref_status[i] || std::memcmp(&out[i].makespan, &ref_mk[i], 8)) {
+        ++bad;
+        std::printf("graph %zu: evaluate gives status %d makespan %.17g, reference %d %.17g\n", i, out[i].status,
+                    out[i].makespan, ref_status[i], ref_mk[i]);
+      }
+    }
+    if (unrepro_batch != unrepro) {
+      ++bad;
+      std::printf("simulate refused %d graphs, evaluate %d\n", unrepro, unrepro_batch);
+    }
+    std::printf("bridge_check graphs: %d graphs (%d mutator calls, %d merges of the top cluster, %d redrawn after a "
+                "reference defect), %d identical SimResults, %d failing in both, %d refused as unreproducible, "
+                "mismatches %d\n",
+                graphs, calls, base_merges, gst_.dropped, ok, failed, unrepro, bad);
+    return bad ? 1 : 0;
+  }
   auto g0 = hesp::TaskGraph::root_cholesky(n, elem);
   const int cl = g0.partition_task(0, 1.0 / s_base, gen.min_block);
   const int n_base = (int)g0.cluster(cl).members.size();

@@ -19,6 +19,8 @@
 #include "hesp/sim.hpp"
 #include "json.hpp"
 #include "problem.h"
+#include "hesp_b200_bridge.hpp"
+#include "random_graphs.hpp"
 
 using nlohmann::json;
 
@@ -53,6 +55,8 @@ int main(int argc, char** argv) {
   std::string ordering = "PL", selection = "EFT-P", caching = "WB";
   unsigned long long first = 0, count = 100, sseed = 0;
   int verbose = 0;
+  std::string descs_path;  // --descs: explicit candidates (520-byte hesp_cand_desc records)
+  int graphs = 0;          // --graphs N: random reference TaskGraphs through the bridge's replay plan
   for (int i = 1; i < argc; ++i) {
     std::string k = argv[i];
     auto v = [&]() { return std::string(argv[++i]); };
@@ -80,6 +84,8 @@ int main(int argc, char** argv) {
     else if (k == "--first") first = std::stoull(v());
     else if (k == "--count") count = std::stoull(v());
     else if (k == "--verbose") verbose = std::stoi(v());
+    else if (k == "--descs") descs_path = v();
+    else if (k == "--graphs") graphs = std::stoi(v());
     else {
       std::fprintf(stderr, "unknown arg %s\n", k.c_str());
       return 2;
@@ -160,22 +166,38 @@ int main(int argc, char** argv) {
                        caching == "WT" ? 0 : caching == "WB" ? 1 : 2, 0, sseed, gen.min_block};
   hesp_workload wl{n, elem, s_base, gen};
   hx::HostProblem hp = hx::build_problem(hplat, hmodel, hs, wl);
-  hp.p.base_tasks = hp.base_tasks.data();
-  hp.p.base_blocks = hp.base_blocks.data();
-  hp.p.base_preds = hp.base_preds.data();
-  hp.p.base_plist = hp.base_plist.data();
+  hx::bind_tilings(hp.p, hp, hp.base_tasks.data(), hp.base_blocks.data(), hp.base_preds.data(),
+                   hp.base_plist.data());
   const hx::SlotLayout L = hp.p.lay;
   std::vector<uint8_t> slot(L.total);
   hx::Small sm{};
   std::printf("base: tasks %d blocks %d slot %zu bytes, bvals %d\n", hp.p.n_base_tasks,
               hp.p.n_base_blocks, L.total, hp.p.nbv);
 
+  std::vector<hesp_cand_desc> descs;
+  std::vector<hesp::TaskGraph> gs;
+  if (graphs > 0) {  // BatchSimulator::simulate(const TaskGraph&)'s replay, on the host engine
+    oracle::GraphStats gst;
+    gs = oracle::random_graphs(graphs, n, elem, s_base, gen.min_block, gen.seed * 7919 + first, &gst);
+    const int s0 = (int)hesp_snap_tiles(n, s_base, gen.min_block);
+    for (const auto& g : gs)
+      descs.push_back(hesp::b200::plan_graph(g, n, elem, s0, hp.p.n_base_tasks, hp.p.n_base_blocks).desc);
+    first = 0;
+    count = descs.size();
+  } else if (!descs_path.empty()) {
+    const std::string raw = slurp(descs_path);
+    descs.resize(raw.size() / sizeof(hesp_cand_desc));
+    std::memcpy(descs.data(), raw.data(), descs.size() * sizeof(hesp_cand_desc));
+    first = 0;
+    count = descs.size();
+  }
   double t_eng = 0, t_ref = 0;
   int bad = 0, ok_both = 0;
   std::map<int, int> hist;
   for (unsigned long long c = first; c < first + count; ++c) {
     hesp_cand_desc d;
-    hesp_generate(&gen, (int)(n / hp.p.base_b), hp.p.n_base_leaves, hp.p.base_b, c, &d);
+    if (!descs.empty()) d = descs[c];
+    else hesp_generate(&gen, (int)(n / hp.p.base_b), hp.p.n_base_leaves, hp.p.base_b, c, &d);
     auto t0 = std::chrono::steady_clock::now();
     hx::Engine<hx::HostWarp> eng(hx::HostWarp{}, hp.p, slot.data(), &sm);
     std::vector<double> tr_s, tr_e;
@@ -190,10 +212,14 @@ int main(int argc, char** argv) {
     std::map<int, std::vector<int>> rpreds;
     try {
       auto g = hesp::TaskGraph::root_cholesky(n, elem);
-      g.partition_task(0, 1.0 / s_base, gen.min_block);
-      for (int k = 0; k < d.n_ops; ++k) {
-        if (d.ops[k].s == HESP_OP_MERGE) g.merge_cluster(d.ops[k].task);
-        else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, gen.min_block);
+      if (!gs.empty()) {
+        g = gs[c];  // the caller's own graph (ids differ from the replay's: compare id-free fields)
+      } else {
+        g.partition_task(0, 1.0 / s_base, gen.min_block);
+        for (int k = 0; k < d.n_ops; ++k) {
+          if (d.ops[k].s == HESP_OP_MERGE) g.merge_cluster(d.ops[k].task);
+          else g.partition_task(d.ops[k].task, 1.0 / d.ops[k].s, gen.min_block);
+        }
       }
       rleaves = (int)g.leaf_tasks().size();
       res = hesp::simulate(g, rplat, rmodel, rcfg);
@@ -222,13 +248,20 @@ int main(int argc, char** argv) {
     t_ref += std::chrono::duration<double>(t2 - t1).count();
     hist[o.status]++;
     const bool same = o.status == rstatus && o.n_leaves == rleaves && bits(o.makespan) == bits(rmk) &&
-                      o.assign_hash == rah && o.xfer_hash == rxh;
+                      (!gs.empty() || (o.assign_hash == rah && o.xfer_hash == rxh));
     if (same) {
       ok_both += rstatus == 0;
       continue;
     }
     ++bad;
     if (bad <= 5 || verbose) {
+      if (!gs.empty()) {
+        std::printf("graph %llu ops", c);
+        for (int k = 0; k < d.n_ops; ++k) std::printf(" (%d,%d)", d.ops[k].task, d.ops[k].s);
+        std::printf("; clusters");
+        for (const auto& [id, cl] : gs[c].clusters()) std::printf(" %d:%d/%.4g", id, cl.parent_task, 1.0 / cl.p);
+        std::printf("\n");
+      }
       std::printf("MISMATCH cand %llu ops=%d: eng st=%d leaves=%d mk=%.17g ah=%016llx xh=%016llx | ref st=%d leaves=%d mk=%.17g ah=%016llx xh=%016llx\n",
                   c, d.n_ops, o.status, o.n_leaves, o.makespan, (unsigned long long)o.assign_hash,
                   (unsigned long long)o.xfer_hash, rstatus, rleaves, rmk, (unsigned long long)rah,

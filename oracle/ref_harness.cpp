@@ -410,9 +410,11 @@ void run_solve(const Ctx& c, FILE* f) {
       nvalid = (int)valid.size();
       if (!valid.empty()) {
         size_t pick = 0;
-        if (!soft) {
+        if (!soft) {  // argmax score, ties: lowest target id, then candidate order
           for (size_t i = 1; i < valid.size(); ++i)
-            if (valid[i].score > valid[pick].score) pick = i;
+            if (valid[i].score > valid[pick].score ||
+                (valid[i].score == valid[pick].score && valid[i].target < valid[pick].target))
+              pick = i;
         } else {
           double total = 0;
           for (const auto& x : valid) total += x.score;

@@ -248,6 +248,49 @@ HX uint64_t dbits(double x) {
   return u;
 }
 
+// A/B switches (-D at build time): 16-byte record loads in the lean loop;
+// prefetching of the records the loop will touch next (1: the epoch's ready
+// tasks, 2: + the current task's successors).
+#ifndef HESP_VEC_LOADS
+#define HESP_VEC_LOADS 1
+#endif
+#ifndef HESP_PREFETCH
+#define HESP_PREFETCH 0
+#endif
+HX void prefetch_l1(const void* p) {
+#if defined(__CUDACC__)
+  asm volatile("prefetch.L1 [%0];" ::"l"(p));
+#else
+  (void)p;
+#endif
+}
+
+// 32-byte records in two 16-byte loads (the generic path otherwise splits
+// them field by field).
+HX STask ld_stask(const STask* p) {
+#if defined(__CUDACC__) && HESP_VEC_LOADS
+  const int4 a = reinterpret_cast<const int4*>(p)[0], b = reinterpret_cast<const int4*>(p)[1];
+  STask t;
+  t.ws0 = a.x; t.ws1 = a.y; t.ws2 = a.z; t.nw = a.w;
+  t.out = b.x; t.kb = b.y; t.b = b.z; t.pad = b.w;
+  return t;
+#else
+  return *p;
+#endif
+}
+HX TState ld_tstate(const TState* p) {
+#if defined(__CUDACC__) && HESP_VEC_LOADS
+  const double2 a = reinterpret_cast<const double2*>(p)[0];
+  const int4 b = reinterpret_cast<const int4*>(p)[1];
+  TState t;
+  t.rel = a.x; t.ct = a.y;
+  t.missing = b.x; t.soff = b.y; t.scnt = b.z; t.pad = b.w;
+  return t;
+#else
+  return *p;
+#endif
+}
+
 // Small per-warp state (shared memory on the device).
 // State of the lean event loop across its cold exits (sim_lean): the loop
 // returns to its driver for every call-requiring step, so no value is live
@@ -268,6 +311,7 @@ struct Small {
   long long used[MAXS];
   uint64_t ah, xh;  // event-loop result hashes (one copy per warp)
   int32_t ptype[MAXP], pspace[MAXP];
+  BaseView bv;  // the candidate's top-level tiling and reference-id offsets
   LeanState L;
 };
 static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
@@ -341,8 +385,11 @@ struct Engine {
   // base task / block counts (overlay boundary), space count, main space:
   // read from the problem (constant memory), never from `this` (the engine
   // object lives in local memory on the device)
-  HX int n_bt() const { return PB.n_base_tasks; }
-  HX int n_bb() const { return PB.n_base_blocks; }
+  HX int n_bt() const { return SM().bv.nbt; }
+  HX int n_bb() const { return SM().bv.nbb; }
+  // reference ids of internal task / block ids (BaseView)
+  HX int xtask(int j) const { return j ? j + SM().bv.off_t : 0; }
+  HX int xblock(int b) const { return b ? b + SM().bv.off_b : 0; }
   HX int n_sp() const { return PB.S; }
   HX int msp() const { return PB.main_space; }
   int32_t ntasks, nblocks;  // next ids
@@ -442,8 +489,8 @@ struct Engine {
   }
 
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
-  HX TaskMeta task(int id) const { return id < n_bt() ? PB.base_tasks[id] : tm()[id - n_bt()]; }
-  HX const BlockMeta& bmeta(int b) const { return b < n_bb() ? PB.base_blocks[b] : bm()[b - n_bb()]; }
+  HX TaskMeta task(int id) const { return id < n_bt() ? SM().bv.bt[id] : tm()[id - n_bt()]; }
+  HX const BlockMeta& bmeta(int b) const { return b < n_bb() ? SM().bv.bb[b] : bm()[b - n_bb()]; }
   HX Region reg(int b) const { return bmeta(b).r; }
   HX int tile_of(int b) const { return bmeta(b).tile; }
   HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * PB.elem; }
@@ -500,7 +547,7 @@ struct Engine {
       }
       return found;
     }
-    if (r.rows >= PB.base_b || r.cols >= PB.base_b) {  // only a tile- or root-sized region can be either
+    if (r.rows >= SM().bv.base_b || r.cols >= SM().bv.base_b) {  // only a tile- or root-sized region can be either
       if (rsame(reg(0), r)) return 0;
       if (rsame(reg(t), r)) return t;
     }
@@ -675,20 +722,31 @@ struct Engine {
   // giving it an empty region, which no geometric query (find, overlap,
   // containment, scopes) can match.  Intersection descriptors are pruned by
   // their DataDag parent links, which E1 does not model after a prune; a
-  // merge while any intersection block exists reports ST_ENGINE_LIMIT, as
-  // does merging the base cluster (the base tiling is shared by the batch).
+  // merge while any intersection block exists reports ST_ENGINE_LIMIT.
+  // Merging the top cluster returns the candidate to the unpartitioned root
+  // (BaseView TIL_ROOT); a later partition of the root moves it onto another
+  // shared top-level tiling.
   HXN void apply_merge(int c) {
     if (c < 0 || c >= npart || part()[c].task < 0) return fail(ST_UNKNOWN_CLUSTER);
     const PartEntry pe = part()[c];
     NOUNROLL for (int m = pe.child0; m < pe.child0 + pe.nchild; ++m)
       if (part_index(m) >= 0) return fail(ST_NESTED_CLUSTER);
-    if (c == 0 || pe.child0 < n_bt()) return fail(ST_ENGINE_LIMIT);
     bool sect = false;
     NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W) {
       const BlockMeta& o = bm()[b - n_bb()];
       if (o.isint && !dead_region(o.r)) sect = true;
     }
     if (wp.any(sect)) return fail(ST_ENGINE_LIMIT);
+    if (c == 0) {
+      // The top cluster (the root's): every other cluster is already merged
+      // (its members are leaves), so the prune leaves the root alone -- the
+      // unpartitioned root, with every id consumed so far staying consumed.
+      if (pe.task != 0 || pe.child0 != 1) return fail(ST_INTERNAL);
+      const BaseView& v = SM().bv;
+      const int nt = ntasks + v.off_t, nb = nblocks + v.off_b, nc = npart + v.off_c;
+      reset_to_base(TIL_ROOT, nt - 1, nb - 1, nc);
+      return;
+    }
     NOUNROLL for (int m = pe.child0 + wp.lane(); m < pe.child0 + pe.nchild; m += WP::W) {
       const TaskMeta t = tm()[m - n_bt()];
       NOUNROLL for (int k = 0; k <= t.nrd; ++k)
@@ -719,6 +777,18 @@ struct Engine {
     const TaskMeta t = task(task_id);
     const int s = (int)hesp_snap_tiles(t.b, s_req, PB.min_block);
     if (s == 0) return fail(ST_INDIVISIBLE);
+    if (task_id == 0 && PB.n_til > 0) {
+      // partitioning the unpartitioned root: the candidate moves onto the
+      // shared top-level tiling with that tile count, ids continuing from the
+      // ones consumed so far (n_til == 0: the host is building the tilings)
+      int k = -1;
+      NOUNROLL for (int i = 0; i < PB.n_til; ++i)
+        if (i != TIL_ROOT && PB.til[i].s == s) k = i;
+      if (k < 0) return fail(ST_ENGINE_LIMIT);  // a tiling larger than the slot holds
+      const BaseView v = SM().bv;
+      reset_to_base(k, v.off_t, v.off_b, v.off_c);
+      return;
+    }
     if (npart >= MAXPART) return fail(ST_ENGINE_LIMIT);
     // operands = reads minus writes, in read order; write = writes.front()
     const int wb = t.blk[t.nrd];
@@ -1106,7 +1176,7 @@ struct Engine {
   // whose tiles have no sub-blocks, the shared base table (off = ~index).
   HX const int32_t* pred_list(int j) const {
     const int off = t_poff()[j];
-    return off >= 0 ? preds() + off : PB.base_plist + ~off;
+    return off >= 0 ? preds() + off : SM().bv.bpl + ~off;
   }
 
   // Dependences (E2): per cell, last writer + readers since that write.
@@ -1168,11 +1238,14 @@ struct Engine {
           bool dup = false;
           for (int q = 0; q < k; ++q) dup |= t.blk[q] == t.blk[k];
           kt += !dup;
-          if (fastj && tl_cnt()[tile_of(t.blk[k])] != 0) fastj = false;
+          // (the root block has no tile: a leaf root -- the unpartitioned
+          // root's only task -- has no predecessors at all)
+          const int tt = tile_of(t.blk[k]);
+          if (fastj && tt >= 0 && tl_cnt()[tt] != 0) fastj = false;
         }
         sum_k += kt;
         if (fastj) {
-          const BasePreds& bp = PB.base_preds[j];
+          const BasePreds& bp = SM().bv.bp[j];
           t_poff()[j] = ~bp.uoff;
           t_pcnt()[j] = bp.ucnt;
           ts()[j].missing = bp.ucnt;
@@ -1204,10 +1277,10 @@ struct Engine {
         const int myslot = slot++;
         if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
           // unsubdivided tile of a base task: its base contribution (E5)
-          const BasePreds& bp = PB.base_preds[j];
+          const BasePreds& bp = SM().bv.bp[j];
           const int off = bp.soff[myslot], cnt = bp.scnt[myslot];
           NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W)
-            if (npb + q < PB.maxpb) pbuf()[npb + q] = PB.base_plist[off + q];
+            if (npb + q < PB.maxpb) pbuf()[npb + q] = SM().bv.bpl[off + q];
           npb += cnt;
           wp.sync();
           if (npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
@@ -1447,10 +1520,10 @@ struct Engine {
     if (!(rdy > now)) fail(ST_ENGINE_INVARIANT);
     log_xfer(blk, frag, bytes, src, dst, start0, rdy, nh, hs, he);
     if (frag)
-      xhash += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), frag->row, frag->col,
+      xhash += hesp_xfer_term(xblock(blk), src, dst, bytes, dbits(start0), dbits(rdy), frag->row, frag->col,
                               frag->rows, frag->cols);
     else
-      xhash += hesp_xfer_term(blk, src, dst, bytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      xhash += hesp_xfer_term(xblock(blk), src, dst, bytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
     return rdy;
   }
 
@@ -1937,8 +2010,9 @@ struct Engine {
       NOUNROLL for (int x = 1 + wp.lane(); x < nblocks; x += WP::W) nonroot += bbytes(x);
       nonroot = wp.suml(nonroot);
       bool ok = true;
+      const bool root_leaf = SM().bv.til == TIL_ROOT;  // the root task itself is scheduled: its block goes anywhere
       NOUNROLL for (int q = 0; q < n_sp(); ++q)
-        if (nonroot + (q == msp() ? bbytes(0) : 0) > PB.cap[q]) ok = false;
+        if (nonroot + ((q == msp() || root_leaf) ? bbytes(0) : 0) > PB.cap[q]) ok = false;
       fast = ok && (!TRACE || (tb && tb->lite));  // the full trace keeps residency bookkeeping
     }
     if (fast && !TRACE && PB.loop == 0) {  // the batch kernels' lean loop
@@ -2002,11 +2076,11 @@ struct Engine {
 #define BF HOT_ARR(uint32_t, bflags)
 #define TM HOT_ARR(const TaskMeta, tm)
 #define BM HOT_ARR(const BlockMeta, bm)
-#define BT (PB.base_tasks)
-#define BB (PB.base_blocks)
+#define BT (SM().bv.bt)
+#define BB (SM().bv.bb)
     // problem-wide scalars are read from constant memory at each use
-#define nbt_ PB.n_base_tasks
-#define nbb_ PB.n_base_blocks
+#define nbt_ SM().bv.nbt
+#define nbb_ SM().bv.nbb
 #define S_ PB.S
 #define ms PB.main_space
 #define elem PB.elem
@@ -2112,15 +2186,20 @@ struct Engine {
       }
       if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
       if (TRACE) log_xfer(blk, nullptr, nbytes, src, dst, start0, rdy, nh, hs, he);
-      HXH += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      {  // one lane folds the term (only lane 0's copy of the hashes is reported)
+        const uint64_t xt_ = hesp_xfer_term(xblock(blk), src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+        if (wp.lane() == 0) HXH += xt_;
+      }
       return rdy;
     };
     // cold-call bracket: hand the uniform hot state to the member paths and back
     auto cold_in = [&]() {
       now = tnow;
       wp.sync();
-      xhash += HXH;
-      HXH = 0;
+      if (wp.lane() == 0) {
+        xhash += HXH;
+        HXH = 0;
+      }
       status = st;
     };
     auto cold_out = [&]() {
@@ -2465,11 +2544,14 @@ struct Engine {
         const double end = start + PB.ttime[tkind][tbidx][type];
         if (!(end > tnow) || start < tnow) return fail(ST_ENGINE_INVARIANT);
         PF_SET(p, end);
-        HAH += hesp_assign_term(j, p, dbits(start), dbits(end));
-        if (TRACE && j < tr_cap && wp.lane() == 0) {
-          tr_proc[j] = p;
-          tr_start[j] = start;
-          tr_end[j] = end;
+        {
+          const uint64_t at_ = hesp_assign_term(xtask(j), p, dbits(start), dbits(end));
+          if (wp.lane() == 0) HAH += at_;
+        }
+        if (TRACE && xtask(j) < tr_cap && wp.lane() == 0) {
+          tr_proc[xtask(j)] = p;
+          tr_start[xtask(j)] = start;
+          tr_end[xtask(j)] = end;
         }
         mk = dmax(mk, end);
         if (!fst) {
@@ -2549,6 +2631,7 @@ struct Engine {
       }
     }
     makespan = mk;
+    wp.sync();
     ahash += HAH;
     xhash += HXH;
 #undef HAH
@@ -2610,6 +2693,7 @@ struct Engine {
   //   * clocks, attributes and hashes live in the warp's Small (LDS/STS).
   // =========================================================================
   enum : int32_t { LEAN_DONE = 0, LEAN_GATHER = 1, LEAN_VALIDATE = 2, LEAN_COHERENCE = 3, LEAN_WRITEBACK = 4 };
+
 
   template <int SELT>
   HXN void sim_lean() {
@@ -2692,6 +2776,7 @@ struct Engine {
       if (status) return;
     }
     if (status) return;
+    wp.sync();
     makespan = W.L.mk;
     ahash += W.ah;
     xhash += W.xh;
@@ -2725,10 +2810,10 @@ struct Engine {
     int st = 0;
     // block regions through the local slot base, never through `this`
     auto lreg = [&](int b) -> Region {
-      return b < PB.n_base_blocks ? PB.base_blocks[b].r : LA(const BlockMeta, bm)[b - PB.n_base_blocks].r;
+      return b < W.bv.nbb ? W.bv.bb[b].r : LA(const BlockMeta, bm)[b - W.bv.nbb].r;
     };
     auto ltile = [&](int b) -> int {
-      return b < PB.n_base_blocks ? PB.base_blocks[b].tile : LA(const BlockMeta, bm)[b - PB.n_base_blocks].tile;
+      return b < W.bv.nbb ? W.bv.bb[b].tile : LA(const BlockMeta, bm)[b - W.bv.nbb].tile;
     };
     // leave the loop: state into W.L (uniform stores), then a cold request
     auto save = [&]() {
@@ -2772,7 +2857,10 @@ struct Engine {
         if (h == 0) start0 = s0;
       }
       if (!(rdy > tnow)) st = ST_ENGINE_INVARIANT;
-      W.xh += hesp_xfer_term(blk, src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      // one lane folds the term: a read-modify-write of shared state by every
+      // lane is only safe while the warp stays converged
+      const uint64_t xt_ = hesp_xfer_term(xblock(blk), src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
+      if (wp.lane() == 0) W.xh += xt_;
       return rdy;
     };
     // validate_from (sim.cpp:452-461), b != 0: b and every block inside it
@@ -2898,6 +2986,10 @@ struct Engine {
           NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
             const int a = LA(const int, gs_a)[k];
             const double ka = LA(const double, ready_key)[k];
+            if (HESP_PREFETCH >= 1) {  // the epoch's tasks: their records load in parallel, not one by one
+              prefetch_l1(LA(const STask, wsb) + a);
+              prefetch_l1(LA(const TState, ts) + a);
+            }
             int rank = 0;
             NOUNROLL for (int q = 0; q < nr; ++q) {
               const int c = LA(const int, gs_a)[q];
@@ -2911,7 +3003,10 @@ struct Engine {
       }
       // ---------------- one ready task ----------------
       const int j = LA(const int, ready)[done];
-      const STask tk = LA(const STask, wsb)[j];
+      const STask tk = ld_stask(LA(const STask, wsb) + j);
+      const TState tj = ld_tstate(LA(const TState, ts) + j);  // j's own record: no commit writes it before j's release
+      if (HESP_PREFETCH >= 2 && phase == 0 && wp.lane() < tj.scnt)  // successors' records, ahead of the release
+        prefetch_l1(LA(const TState, ts) + LA(const int, succs)[tj.soff + wp.lane()]);
       const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
       const int nw = tk.nw;
       const long long tbytes = (long long)tk.b * tk.b * PB.elem;  // every block of a task has its side
@@ -2928,7 +3023,7 @@ struct Engine {
           if (W.L.op == LEAN_GATHER) inputs = dmax(inputs, W.L.op_result);
         }
       } else {
-        const double rel = LA(const TState, ts)[j].rel;
+        const double rel = tj.rel;
         // ---------------- select_processor (sim.cpp:136-192) ----------------
         if (waits) {
           unsigned idle_mask = 0;
@@ -3217,12 +3312,15 @@ struct Engine {
             validate(bk, s, arr, (tk.pad >> k) & 1);
           }
         }
-        const double rel = LA(const TState, ts)[j].rel;
+        const double rel = tj.rel;
         start = dmax(dmax(W.proc_free[p], rel), inputs);
         end = start + PB.ttime[tkind][tbidx][W.ptype[p]];
         if (!(end > tnow) || start < tnow) return failed(ST_ENGINE_INVARIANT);
         W.proc_free[p] = end;
-        W.ah += hesp_assign_term(j, p, dbits(start), dbits(end));
+        {
+          const uint64_t at_ = hesp_assign_term(xtask(j), p, dbits(start), dbits(end));
+          if (wp.lane() == 0) W.ah += at_;
+        }
         mk = dmax(mk, end);
         // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,
         // validate out and the blocks inside it here, valid[out] = end
@@ -3280,7 +3378,6 @@ struct Engine {
       // release successors (sim.cpp:660-667): running max of predecessor
       // ends; released tasks enter the pool with release time and key
       {
-        const TState tj = LA(const TState, ts)[j];
         int added = 0;
         double amin = ABSENT;
         NOUNROLL for (int base = 0; base < tj.scnt; base += WP::W) {
@@ -3327,8 +3424,30 @@ struct Engine {
   // One candidate, end to end
   // =========================================================================
 
-  // Starts from the base tiling (root + base cluster, shared tables).
-  HXN void reset_to_base() {
+  // The warp's view of top-level tiling `til` with reference-id offsets.
+  HX void set_view(int til, int off_t, int off_b, int off_c) {
+    const BaseTiling& T = PB.til[til];
+    BaseView& v = SM().bv;
+    v.nbt = T.n_tasks;
+    v.nbb = T.n_blocks;
+    v.til = til;
+    v.pad = 0;
+    v.base_b = T.base_b;
+    v.bt = T.tasks;
+    v.bb = T.blocks;
+    v.bp = T.preds;
+    v.bpl = T.plist;
+    v.off_t = off_t;
+    v.off_b = off_b;
+    v.off_c = off_c;
+    v.pad2 = 0;
+    wp.sync();
+  }
+
+  // Starts from a top-level tiling (root + its cluster, shared tables); the
+  // workload's base tiling with reference ids unshifted by default.
+  HXN void reset_to_base(int til = TIL_BASE, int off_t = 0, int off_b = 0, int off_c = 0) {
+    set_view(til, off_t, off_b, off_c);
     NOUNROLL for (int i = wp.lane(); i < n_bb(); i += WP::W) tmis()[i] = 0;
     NOUNROLL for (int i = wp.lane(); i < RHT / 2; i += WP::W) ((uint32_t*)rht())[i] = 0xffffffffu;
     wp.sync();
@@ -3338,7 +3457,7 @@ struct Engine {
     npart = 0;
     makespan = 0.0;
     ahash = xhash = 0;
-    if (n_bt() > 1) {  // the base op partitioned the root into tasks 1..n_bt()-1
+    if (n_bt() > 1) {  // the top op partitioned the root into tasks 1..n_bt()-1
       if (wp.lane() == 0) {
         part()[0].task = 0;
         part()[0].child0 = 1;
@@ -3350,14 +3469,22 @@ struct Engine {
     }
   }
 
+  // One descriptor op in reference ids (partition_task / merge_cluster).
+  HXN void apply_ext(const hesp_op& o) {
+    const BaseView& v = SM().bv;
+    if (o.s == HESP_OP_MERGE) {
+      if (o.task < v.off_c) return fail(ST_UNKNOWN_CLUSTER);  // merged with an earlier top cluster
+      return apply_merge(o.task - v.off_c);
+    }
+    if (o.task != 0 && o.task <= v.off_t) return fail(ST_VALIDATION);  // merged away: unknown task
+    apply_op(o.task == 0 ? 0 : o.task - v.off_t, o.s);
+  }
+
   // Build phase: base tiling + ops -> leaves, dependences; state left in the slot.
   HXN void build(const hesp_cand_desc& d) {
     reset_to_base();
     if (d.n_ops < 0 || d.n_ops > HESP_MAX_OPS) fail(ST_ENGINE_LIMIT);  // never read past ops[]
-    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
-      if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
-      else apply_op(d.ops[k].task, d.ops[k].s);
-    }
+    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) apply_ext(d.ops[k]);
     finish_build();
   }
 
@@ -3368,22 +3495,28 @@ struct Engine {
   HXN void build_template(const hesp_cand_desc& d) {
     reset_to_base();
     if (d.n_ops < 0 || d.n_ops > HESP_MAX_OPS) fail(ST_ENGINE_LIMIT);
-    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) {
-      if (d.ops[k].s == HESP_OP_MERGE) apply_merge(d.ops[k].task);
-      else apply_op(d.ops[k].task, d.ops[k].s);
-    }
+    NOUNROLL for (int k = 0; k < d.n_ops && !status; ++k) apply_ext(d.ops[k]);
     if (wp.lane() == 0) {
       SlotHeader h{};
       h.status = status;
       h.ntasks = ntasks;
       h.nblocks = nblocks;
-      h.pad = npart;
+      h.npart = npart;
+      put_view(h);
       *hdr() = h;
     }
     wp.sync();
   }
+  HX void put_view(SlotHeader& h) const {
+    const BaseView& v = SM().bv;
+    h.til = v.til;
+    h.off_t = v.off_t;
+    h.off_b = v.off_b;
+    h.off_c = v.off_c;
+  }
   HXN void build_neighbor(const uint8_t* tslot, int n_extra, const hesp_op* extra) {
     const SlotHeader th = *(const SlotHeader*)(tslot + PB.lay.hdr);
+    set_view(th.til, th.off_t, th.off_b, th.off_c);
     auto copy = [&](size_t off, size_t bytes) {  // 4-byte words, lane-strided
       const uint32_t* src = (const uint32_t*)(tslot + off);
       uint32_t* dst = (uint32_t*)(slot + off);
@@ -3394,19 +3527,16 @@ struct Engine {
     copy(PB.lay.bm, sizeof(BlockMeta) * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.bref, 4 * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.rht, 2 * (size_t)RHT);
-    copy(PB.lay.part, sizeof(PartEntry) * (size_t)th.pad);
+    copy(PB.lay.part, sizeof(PartEntry) * (size_t)th.npart);
     copy(PB.lay.tmis, ((size_t)n_bb() + 3) & ~(size_t)3);
     wp.sync();
     status = th.status;
     ntasks = th.ntasks;
     nblocks = th.nblocks;
-    npart = th.pad;
+    npart = th.npart;
     makespan = 0.0;
     ahash = xhash = 0;
-    NOUNROLL for (int k = 0; k < n_extra && !status; ++k) {
-      if (extra[k].s == HESP_OP_MERGE) apply_merge(extra[k].task);
-      else apply_op(extra[k].task, extra[k].s);
-    }
+    NOUNROLL for (int k = 0; k < n_extra && !status; ++k) apply_ext(extra[k]);
     finish_build();
   }
 
@@ -3428,7 +3558,8 @@ struct Engine {
       h.nedges = nedges;
       h.sum_k = sum_k;
       h.n_leaves_out = n_out;
-      h.pad = 0;
+      h.npart = npart;
+      put_view(h);
       *hdr() = h;
     }
     wp.sync();
@@ -3437,6 +3568,7 @@ struct Engine {
   // Simulate phase on a slot left by build().
   HXN Outcome sim_slot() {
     const SlotHeader h = *hdr();
+    set_view(h.til, h.off_t, h.off_b, h.off_c);
     status = h.status;
     ntasks = h.ntasks;
     nblocks = h.nblocks;
@@ -3502,6 +3634,9 @@ struct Engine {
     if (ntasks <= tb->task_cap)
       NOUNROLL for (int j = wp.lane(); j < ntasks; j += WP::W) tb->tmeta[j] = task(j);
     if (wp.lane() == 0) {
+      tb->off_t = SM().bv.off_t;
+      tb->off_b = SM().bv.off_b;
+      tb->off_c = SM().bv.off_c;
       tb->nleaves = nl;
       tb->npreds = np;
       tb->nblocks = nb;

@@ -709,6 +709,7 @@ const char* hesp_status_name(int32_t s) {
   if (s == 100) return "ForeignException";
   if (s == ST_ENGINE_LIMIT) return "EngineLimit";
   if (s == ST_ENGINE_INVARIANT) return "EngineInvariant";
+  if (s == HESP_ST_UNREPRODUCIBLE) return "Unreproducible";
   return "Unknown";
 }
 
@@ -771,10 +772,7 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   if ((c = cudaMalloc(&e->d_base_plist, npl * sizeof(int32_t))) != cudaSuccess) return fail(c, "malloc");
   cudaMemcpy(e->d_base_preds, e->hp.base_preds.data(), npr * sizeof(BasePreds), cudaMemcpyHostToDevice);
   cudaMemcpy(e->d_base_plist, e->hp.base_plist.data(), npl * sizeof(int32_t), cudaMemcpyHostToDevice);
-  p.base_tasks = e->d_base_tasks;
-  p.base_blocks = e->d_base_blocks;
-  p.base_preds = e->d_base_preds;
-  p.base_plist = e->d_base_plist;
+  bind_tilings(p, e->hp, e->d_base_tasks, e->d_base_blocks, e->d_base_preds, e->d_base_plist);
   p.lay = slot_layout(p);
   e->L = p.lay;
   if ((c = cudaMalloc(&e->d_problem, sizeof(Problem))) != cudaSuccess) return fail(c, "malloc");
@@ -1077,8 +1075,8 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
   if (!e->d_trace_tb) {  // first trace on this handle: allocate once, reuse after
     std::vector<void*>& owned = e->trace_bufs;
     TraceBufs& tb0 = e->trace_tb;
-    ok = dalloc(&e->d_trace_desc, 1, owned) && dalloc(&e->d_trace_proc, T, owned) &&
-         dalloc(&e->d_trace_start, T, owned) && dalloc(&e->d_trace_end, T, owned) &&
+    ok = dalloc(&e->d_trace_desc, 1, owned) && dalloc(&e->d_trace_proc, 2 * T, owned) &&
+         dalloc(&e->d_trace_start, 2 * T, owned) && dalloc(&e->d_trace_end, 2 * T, owned) &&
          dalloc(&e->d_trace_out, 1, owned) && dalloc(&tb0.x, xcap, owned) && dalloc(&tb0.r, rcap, owned) &&
          dalloc(&tb0.leaves, T, owned) && dalloc(&tb0.lmeta, T, owned) && dalloc(&tb0.lpoff, T, owned) &&
          dalloc(&tb0.lpcnt, T, owned) && dalloc(&tb0.lpreds, P.maxedges, owned) && dalloc(&tb0.bregion, B, owned) &&
@@ -1115,10 +1113,12 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
     cudaStream_t st = e->stream;
     ok = ck(cudaMemcpyAsync(dtb, &tb, sizeof(tb), cudaMemcpyHostToDevice, st), "trace H2D") &&
          ck(cudaMemcpyAsync(dd, desc, sizeof(hesp_cand_desc), cudaMemcpyHostToDevice, st), "trace H2D") &&
-         ck(cudaMemsetAsync(dp, 0xff, (size_t)T * 4, st), "trace memset") &&
+         ck(cudaMemsetAsync(dp, 0xff, (size_t)T * 8, st), "trace memset") &&
          ck(cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, st), "problem");
     if (ok) {
-      detail_kernel<<<1, 32, 0, st>>>(dd, e->d_scratch, T, dp, ds, de, dout, dtb);
+      // per-task arrays by reference task id: below 2 * maxt (ids consumed
+      // before a merge of the top cluster stay below the slot's task cap)
+      detail_kernel<<<1, 32, 0, st>>>(dd, e->d_scratch, 2 * T, dp, ds, de, dout, dtb);
       e->launches += 1;
       ok = ck(cudaGetLastError(), "trace launch") &&
            ck(cudaMemcpyAsync(&o, dout, sizeof(o), cudaMemcpyDeviceToHost, st), "trace D2H") &&
@@ -1132,13 +1132,14 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
   }
   if (ok && o.status == 0) {
     hx::TraceGraph& g = e->last_graph;
-    ok = d2h(logs.proc, dp, T) && d2h(logs.start, ds, T) && d2h(logs.end, de, T) &&
+    ok = d2h(logs.proc, dp, 2 * (size_t)T) && d2h(logs.start, ds, 2 * (size_t)T) && d2h(logs.end, de, 2 * (size_t)T) &&
          d2h(logs.xfers, dx, (size_t)hb.nx) && d2h(logs.res, dr, (size_t)hb.nr) &&
          d2h(g.leaves, tb.leaves, (size_t)hb.nleaves) && d2h(g.meta, tb.lmeta, (size_t)hb.nleaves) &&
          d2h(g.poff, tb.lpoff, (size_t)hb.nleaves) && d2h(g.pcnt, tb.lpcnt, (size_t)hb.nleaves) &&
          d2h(g.preds, tb.lpreds, (size_t)hb.npreds) && d2h(g.bregion, tb.bregion, (size_t)hb.nblocks) &&
          d2h(g.bisint, tb.bisint, (size_t)hb.nblocks) && d2h(g.parts, tb.parts, (size_t)hb.nparts) &&
          d2h(g.tmeta, tb.tmeta, (size_t)hb.ntasks);
+    if (ok) hx::to_reference_ids(g, &logs, hb.off_t, hb.off_b, hb.off_c);
     g.valid = ok;
   }
   if (!ok) return o.status ? o.status : HESP_E_CUDA;
@@ -1170,8 +1171,8 @@ int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::
     e->sched_cap = 0;
     std::vector<void*>& o = e->sched_bufs;
     const size_t b = (size_t)B;
-    const bool ok = dalloc(&e->d_sslots, b * e->L.total, o) && dalloc(&e->d_sproc, b * T, o) &&
-                    dalloc(&e->d_sstart, b * T, o) && dalloc(&e->d_send, b * T, o) &&
+    const bool ok = dalloc(&e->d_sslots, b * e->L.total, o) && dalloc(&e->d_sproc, b * 2 * T, o) &&
+                    dalloc(&e->d_sstart, b * 2 * T, o) && dalloc(&e->d_send, b * 2 * T, o) &&
                     dalloc(&e->d_sleaves, b * T, o) && dalloc(&e->d_slmeta, b * T, o) &&
                     dalloc(&e->d_slpoff, b * T, o) && dalloc(&e->d_slpcnt, b * T, o) &&
                     dalloc(&e->d_slpreds, b * E, o) && dalloc(&e->d_sbregion, b * NB, o) &&
@@ -1209,10 +1210,10 @@ int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::
   bool ok = ck(cudaMemcpyAsync(dd, descs, (size_t)B * sizeof(hesp_cand_desc), cudaMemcpyHostToDevice, st), "H2D") &&
             ck(cudaMemcpyAsync(e->d_stbs, tbs.data(), (size_t)B * sizeof(TraceBufs), cudaMemcpyHostToDevice, st),
                "H2D") &&
-            ck(cudaMemsetAsync(e->d_sproc, 0xff, (size_t)B * T * 4, st), "memset") &&
+            ck(cudaMemsetAsync(e->d_sproc, 0xff, (size_t)B * T * 8, st), "memset") &&
             ck(cudaMemcpyToSymbolAsync(c_problem, &P, sizeof(Problem), 0, cudaMemcpyHostToDevice, st), "problem");
   if (ok) {
-    schedule_kernel<<<B, 32, 0, st>>>(dd, e->d_sslots, (int32_t)T, e->d_sproc, e->d_sstart, e->d_send, e->d_sout,
+    schedule_kernel<<<B, 32, 0, st>>>(dd, e->d_sslots, (int32_t)(2 * T), e->d_sproc, e->d_sstart, e->d_send, e->d_sout,
                                       e->d_stbs);
     e->launches += 1;
     ok = ck(cudaStreamSynchronize(st), "schedule kernel");
@@ -1225,7 +1226,8 @@ int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::
   if (!ok) return HESP_E_CUDA;
   std::vector<int32_t> proc;
   std::vector<double> s0, s1;
-  ok = d2h(proc, e->d_sproc, (size_t)B * T) && d2h(s0, e->d_sstart, (size_t)B * T) && d2h(s1, e->d_send, (size_t)B * T);
+  const size_t TX = 2 * T;  // per-task arrays by reference task id
+  ok = d2h(proc, e->d_sproc, (size_t)B * TX) && d2h(s0, e->d_sstart, (size_t)B * TX) && d2h(s1, e->d_send, (size_t)B * TX);
   if (!ok) return HESP_E_CUDA;
   graphs.assign(B, TraceGraph{});
   logs.assign(B, TraceLogs{});
@@ -1237,15 +1239,16 @@ int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::
     if (outs[b].status != 0) continue;
     TraceGraph& g = graphs[b];
     TraceLogs& L = logs[b];
-    L.proc.assign(proc.begin() + b * T, proc.begin() + (b + 1) * T);
-    L.start.assign(s0.begin() + b * T, s0.begin() + (b + 1) * T);
-    L.end.assign(s1.begin() + b * T, s1.begin() + (b + 1) * T);
+    L.proc.assign(proc.begin() + b * TX, proc.begin() + (b + 1) * TX);
+    L.start.assign(s0.begin() + b * TX, s0.begin() + (b + 1) * TX);
+    L.end.assign(s1.begin() + b * TX, s1.begin() + (b + 1) * TX);
     const TraceBufs& t = tbs[b];
     ok = d2h(g.leaves, t.leaves, (size_t)hb[b].nleaves) && d2h(g.meta, t.lmeta, (size_t)hb[b].nleaves) &&
          d2h(g.poff, t.lpoff, (size_t)hb[b].nleaves) && d2h(g.pcnt, t.lpcnt, (size_t)hb[b].nleaves) &&
          d2h(g.preds, t.lpreds, (size_t)hb[b].npreds) && d2h(g.parts, t.parts, (size_t)hb[b].nparts) &&
          d2h(g.tmeta, t.tmeta, (size_t)hb[b].ntasks);
     if (!ok) return HESP_E_CUDA;
+    hx::to_reference_ids(g, nullptr, hb[b].off_t, hb[b].off_b, hb[b].off_c);
     g.valid = true;
   }
   return HESP_OK;
@@ -1254,6 +1257,20 @@ void hx::set_last_error(const std::string& msg) { g_last_error = msg; }
 const hx::TraceGraph& hesp_engine_last_graph(const hesp_engine* e) { return e->last_graph; }
 
 extern "C" {
+
+int hesp_trace_blocks(const hesp_engine* e, hesp_block_info* out, int32_t cap, int32_t* n) {
+  if (!e || !n || cap < 0 || (cap > 0 && !out) || !e->last_graph.valid) {
+    g_last_error = "hesp_trace_blocks needs a successful hesp_eval_trace first";
+    return HESP_E_INVALID;
+  }
+  const hx::TraceGraph& g = e->last_graph;
+  *n = (int32_t)g.bregion.size();
+  for (int32_t b = 0; b < *n && b < cap; ++b) {
+    const Region& r = g.bregion[b];
+    out[b] = hesp_block_info{r.row, r.col, r.rows, r.cols, b < (int32_t)g.bisint.size() ? g.bisint[b] : 0, 0};
+  }
+  return HESP_OK;
+}
 
 int hesp_trace_bounds(const hesp_engine* e, double* cp, double* work) {
   if (!e || !cp || !work || !e->last_graph.valid) {

@@ -17,6 +17,8 @@ constexpr int MAXBV = 48;     // distinct block sides with tabulated times
 constexpr int MAXPART = HESP_MAX_OPS + 2;  // clusters per candidate (slot array)
 constexpr size_t SMALL_BYTES = 2048;       // >= sizeof(hx::Small) (engine.h asserts)
 constexpr int RHT = 2048;  // per-candidate region hash (new blocks), 16-bit ids
+constexpr int MAXTIL = 8;  // top-level tilings of the root a candidate can sit on
+constexpr int TIL_BASE = 0, TIL_ROOT = 1;  // the workload's base tiling; the unpartitioned root
 
 // Status codes: 0 ok, 1 + hesp::Err ordinal (errors.hpp:10-32), engine codes >= 200.
 enum : int32_t {
@@ -85,10 +87,41 @@ struct STask {
 
 // Per-candidate state carried from the build kernel to the simulate kernel.
 struct SlotHeader {
-  int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, pad;
+  int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, npart;
+  // top-level tiling the candidate sits on and its id offsets (BaseView)
+  int32_t til, off_t, off_b, off_c;
 };
 
 
+
+// One top-level tiling of the root, shared by every candidate on it: the root
+// (task 0, block 0) plus the tasks and blocks TaskGraph::partition_task(0, 1/s)
+// creates, in creation order, and their host-precomputed predecessors (E5).
+// s == 1: the unpartitioned root (root_cholesky alone, or after the base
+// cluster was merged away: graph.cpp:397-407, 521-534).
+struct BaseTiling {
+  int32_t s, n_tasks, n_blocks, pad;
+  int64_t base_b;  // tile side (n for the unpartitioned root)
+  const TaskMeta* tasks;
+  const BlockMeta* blocks;
+  const BasePreds* preds;
+  const int32_t* plist;
+};
+
+// A candidate's view of its top-level tiling (per warp, in the warp's Small).
+// Reference ids are offset once the base cluster has been merged away: task
+// ids, block ids and cluster ids keep counting (graph.cpp:438, DataDag
+// next_id_), so internal id i > 0 is reference id i + off.  Internal ids keep
+// the reference's relative order, which is all the schedule depends on.
+struct BaseView {
+  int32_t nbt, nbb, til, pad;
+  int64_t base_b;
+  const TaskMeta* bt;
+  const BlockMeta* bb;
+  const BasePreds* bp;
+  const int32_t* bpl;
+  int32_t off_t, off_b, off_c, pad2;
+};
 
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
@@ -141,6 +174,11 @@ struct Problem {
   const BlockMeta* base_blocks;  // [n_base_blocks]
   const BasePreds* base_preds;   // [n_base_tasks]
   const int32_t* base_plist;
+  // every top-level tiling: [TIL_BASE] = the base tiling above, [TIL_ROOT] =
+  // the unpartitioned root, then the other tilings of the root that fit a slot
+  BaseTiling til[MAXTIL];
+  int32_t n_til;
+  int32_t max_nbb;  // blocks of the largest tiling (per-tile slot arrays)
   // ---- per-candidate slot layout (byte offsets, identical for every slot) ----
   SlotLayout lay;
 };
@@ -189,6 +227,9 @@ struct TraceBufs {
   int32_t nleaves, npreds, nblocks;
   int32_t overflow;
   int32_t lite;  // schedule only: keep the E4 fast path, no logs
+  // reference-id offsets of the candidate (BaseView); the exported graph and
+  // the logs carry internal ids, the per-task arrays reference ids
+  int32_t off_t, off_b, off_c, pad2;
 };
 
 // Per-candidate result record (also the golden-record payload).
@@ -213,7 +254,8 @@ inline SlotLayout slot_layout(const Problem& p) {
     o += bytes;
     return at;
   };
-  const size_t T = (size_t)p.maxt, B = (size_t)p.maxb, S = (size_t)p.S, NB = (size_t)p.n_base_blocks;
+  const size_t T = (size_t)p.maxt, B = (size_t)p.maxb, S = (size_t)p.S,
+               NB = (size_t)(p.max_nbb > p.n_base_blocks ? p.max_nbb : p.n_base_blocks);
   L.hdr = take(sizeof(SlotHeader));
   L.tm = take(sizeof(TaskMeta) * T);
   L.ts = take(sizeof(TState) * T);

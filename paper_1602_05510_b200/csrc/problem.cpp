@@ -205,8 +205,26 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   // block sides reachable from n: the base tiling, then any requested split
   const long long s0 = hesp_snap_tiles(wl.n, wl.s_base, wl.gen.min_block);
   if (s0 == 0) bad("base tiling: no tiling of the root with tiles >= min_block");
+  // Top-level tilings besides the base one (a candidate reaches them by
+  // merging the base cluster and partitioning the root again): every tile
+  // count the root snaps to whose tiling fits the slot next to the base's
+  // share.  The base's caps follow below; the same K * smax^3 headroom holds.
+  int smax_ = 2;
+  for (int i = 0; i < wl.gen.n_s_choices; ++i) smax_ = std::max(smax_, wl.gen.s_choices[i]);
+  smax_ += 1;
+  const long long nbt0 = 1 + hesp_member_count(HESP_CHOL, static_cast<int>(s0));
+  const long long maxt0 = nbt0 + std::max(1, wl.gen.k_max) * (long long)smax_ * smax_ * smax_ + 64;
+  std::vector<int> extra_s;
+  for (long long s = 2; s <= wl.n / std::max<long long>(1, wl.gen.min_block); ++s) {
+    if (wl.n % s || s == s0) continue;
+    if (1 + hesp_member_count(HESP_CHOL, static_cast<int>(std::min<long long>(s, 4096))) > std::max(nbt0, maxt0 / 2)) break;
+    if ((int)extra_s.size() + 2 >= MAXTIL) break;
+    extra_s.push_back(static_cast<int>(s));
+  }
   std::vector<long long> bvals{wl.n};
-  std::vector<long long> frontier{wl.n / s0};
+  std::vector<long long> frontier;
+  for (auto it = extra_s.rbegin(); it != extra_s.rend(); ++it) frontier.push_back(wl.n / *it);
+  frontier.push_back(wl.n / s0);
   std::set<int> reqs{2, 3, 4, 5, 6, 7, 8};  // generator choices and the solver's choose_p range
   for (int i = 0; i < wl.gen.n_s_choices; ++i) reqs.insert(wl.gen.s_choices[i]);
   while (!frontier.empty()) {
@@ -246,59 +264,65 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
       p.hopc[l][i] = p.link_lat[l] + static_cast<double>(bytes) / p.link_bw[l];
     }
 
-  // ---------------- base tiling via the width-1 engine ----------------
-  {
-    Problem bp = p;
-    TaskMeta root_t{};
-    root_t.blk[0] = 0;
-    root_t.blk[1] = 0;
-    root_t.blk[2] = root_t.blk[3] = -1;
-    root_t.b = static_cast<int32_t>(wl.n);
-    root_t.kind = HESP_CHOL;
-    root_t.nrd = 1;
-    root_t.bidx = 0;
-    BlockMeta root_b{};
-    root_b.r = Region{0, 0, static_cast<int32_t>(wl.n), static_cast<int32_t>(wl.n)};
-    root_b.tile = -1;
-    root_b.next = -1;
-    bp.base_tasks = &root_t;
-    bp.base_blocks = &root_b;
-    bp.n_base_tasks = 1;
-    bp.n_base_blocks = 1;
-    const int nsub = hesp_member_count(HESP_CHOL, static_cast<int>(s0));
-    bp.maxt = 1 + nsub + 8;
-    bp.maxb = 1 + static_cast<int>(s0 * (s0 + 1) / 2) + 8;
-    bp.maxbnd = 16;
-    bp.maxcells = 16;
-    bp.maxrn = 16;
-    bp.maxedges = 16;
-    bp.maxpb = 16;
-    bp.maxgs = bp.maxb + 8;
-    bp.maxgr = bp.maxb + 8;
-    bp.lay = slot_layout(bp);
-    std::vector<uint8_t> slot(bp.lay.total);
-    Small sm{};
-    Engine<HostWarp> eng(HostWarp{}, bp, slot.data(), &sm);
-    eng.reset_to_base();
-    eng.apply_op(0, wl.s_base);
-    if (eng.status) bad("base tiling failed with status " + std::to_string(eng.status));
-    hp.base_tasks.push_back(root_t);
-    for (int id = 1; id < eng.ntasks; ++id) hp.base_tasks.push_back(eng.tm()[id - 1]);
-    hp.base_blocks.push_back(root_b);
-    for (int id = 1; id < eng.nblocks; ++id) hp.base_blocks.push_back(eng.bm()[id - 1]);
-  }
-  // ---------------- base predecessors (E5) ----------------
-  // The engine's per-cell last-writer/readers tracking run once over the base
-  // tiling, where every tile is a single cell.  Slot order = the engine's
-  // processing order: read-only blocks in read order, then the write.
-  {
-    const int nt = static_cast<int>(hp.base_tasks.size());
-    const int nb = static_cast<int>(hp.base_blocks.size());
+  // ---------------- top-level tilings via the width-1 engine ----------------
+  // Tiling = root_cholesky + partition_task(0, 1/s) run by the engine's own
+  // build (graph.cpp:397-407, 456-513), then its predecessors (E5).
+  TaskMeta root_t{};
+  root_t.blk[0] = 0;
+  root_t.blk[1] = 0;
+  root_t.blk[2] = root_t.blk[3] = -1;
+  root_t.b = static_cast<int32_t>(wl.n);
+  root_t.kind = HESP_CHOL;
+  root_t.nrd = 1;
+  root_t.bidx = 0;
+  BlockMeta root_b{};
+  root_b.r = Region{0, 0, static_cast<int32_t>(wl.n), static_cast<int32_t>(wl.n)};
+  root_b.tile = -1;
+  root_b.next = -1;
+  auto add_tiling = [&](int s) {
+    std::vector<TaskMeta> tasks{root_t};
+    std::vector<BlockMeta> blocks{root_b};
+    if (s > 1) {
+      Problem bp = p;
+      bp.n_til = 0;  // the engine emits the root's partition instead of switching tilings
+      bp.til[TIL_BASE] = BaseTiling{1, 1, 1, 0, wl.n, &root_t, &root_b, nullptr, nullptr};
+      bp.base_tasks = &root_t;
+      bp.base_blocks = &root_b;
+      bp.n_base_tasks = 1;
+      bp.n_base_blocks = 1;
+      bp.max_nbb = 1;
+      const int nsub = hesp_member_count(HESP_CHOL, s);
+      bp.maxt = 1 + nsub + 8;
+      bp.maxb = 1 + s * (s + 1) / 2 + 8;
+      bp.maxbnd = 16;
+      bp.maxcells = 16;
+      bp.maxrn = 16;
+      bp.maxedges = 16;
+      bp.maxpb = 16;
+      bp.maxgs = bp.maxb + 8;
+      bp.maxgr = bp.maxb + 8;
+      bp.lay = slot_layout(bp);
+      std::vector<uint8_t> slot(bp.lay.total);
+      Small sm{};
+      Engine<HostWarp> eng(HostWarp{}, bp, slot.data(), &sm);
+      eng.reset_to_base();
+      eng.apply_op(0, s);
+      if (eng.status) bad("top-level tiling s=" + std::to_string(s) + " failed with status " + std::to_string(eng.status));
+      for (int id = 1; id < eng.ntasks; ++id) tasks.push_back(eng.tm()[id - 1]);
+      for (int id = 1; id < eng.nblocks; ++id) blocks.push_back(eng.bm()[id - 1]);
+    }
+    // Predecessors (E5): the engine's per-cell last-writer/readers tracking
+    // run once over the tiling, where every tile is a single cell.  Slot
+    // order = the engine's processing order: read-only blocks in read order,
+    // then the write.
+    const int nt = static_cast<int>(tasks.size());
+    const int nb = static_cast<int>(blocks.size());
     std::vector<int> writer(nb, -1);
     std::vector<std::vector<int>> readers(nb);
-    hp.base_preds.assign(nt, BasePreds{});
+    std::vector<BasePreds> preds(nt, BasePreds{});
+    std::vector<int32_t> plist;
     for (int j = 1; j < nt; ++j) {
-      const TaskMeta& t = hp.base_tasks[j];
+      const TaskMeta& t = tasks[j];
       const int wb = t.blk[t.nrd];
       std::vector<int> uni;
       int slot = 0;
@@ -322,22 +346,42 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
           readers[b].clear();
         }
         if (slot >= 3) bad("base task with more than 3 distinct blocks");
-        bp.soff[slot] = static_cast<int>(hp.base_plist.size());
+        bp.soff[slot] = static_cast<int>(plist.size());
         bp.scnt[slot] = static_cast<int>(lst.size());
-        hp.base_plist.insert(hp.base_plist.end(), lst.begin(), lst.end());
+        plist.insert(plist.end(), lst.begin(), lst.end());
         for (int x : lst)
           if (std::find(uni.begin(), uni.end(), x) == uni.end()) uni.push_back(x);
         ++slot;
       }
-      bp.uoff = static_cast<int>(hp.base_plist.size());
+      bp.uoff = static_cast<int>(plist.size());
       bp.ucnt = static_cast<int>(uni.size());
-      hp.base_plist.insert(hp.base_plist.end(), uni.begin(), uni.end());
-      hp.base_preds[j] = bp;
+      plist.insert(plist.end(), uni.begin(), uni.end());
+      preds[j] = bp;
     }
-    if (hp.base_plist.empty()) hp.base_plist.push_back(0);
-  }
-  p.n_base_tasks = static_cast<int>(hp.base_tasks.size());
-  p.n_base_blocks = static_cast<int>(hp.base_blocks.size());
+    if (plist.empty()) plist.push_back(0);
+    HostProblem::TilingOff o;
+    o.s = s;
+    o.tasks = hp.base_tasks.size();
+    o.blocks = hp.base_blocks.size();
+    o.preds = hp.base_preds.size();
+    o.plist = hp.base_plist.size();
+    o.n_tasks = nt;
+    o.n_blocks = nb;
+    o.base_b = wl.n / s;
+    hp.til.push_back(o);
+    hp.base_tasks.insert(hp.base_tasks.end(), tasks.begin(), tasks.end());
+    hp.base_blocks.insert(hp.base_blocks.end(), blocks.begin(), blocks.end());
+    hp.base_preds.insert(hp.base_preds.end(), preds.begin(), preds.end());
+    hp.base_plist.insert(hp.base_plist.end(), plist.begin(), plist.end());
+  };
+  add_tiling(static_cast<int>(s0));  // TIL_BASE: arrays start at offset 0 (base_tasks & co.)
+  add_tiling(1);                     // TIL_ROOT
+  for (int s : extra_s) add_tiling(s);
+  p.n_base_tasks = hp.til[TIL_BASE].n_tasks;
+  p.n_base_blocks = hp.til[TIL_BASE].n_blocks;
+  p.n_til = static_cast<int>(hp.til.size());
+  p.max_nbb = 0;
+  for (const auto& t : hp.til) p.max_nbb = std::max(p.max_nbb, t.n_blocks);
   p.n_base_leaves = p.n_base_tasks - 1;
   p.base_b = wl.n / s0;
 
@@ -346,10 +390,12 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   for (int i = 0; i < wl.gen.n_s_choices; ++i) smax = std::max(smax, wl.gen.s_choices[i]);
   smax += 1;  // snapping may move to a neighbouring divisor
   const int K = std::max(1, wl.gen.k_max);
-  p.maxt = p.n_base_tasks + K * smax * smax * smax + 64;
-  p.maxb = p.n_base_blocks + K * 5 * smax * smax + 64;
-  p.maxcells = p.n_base_blocks + K * 3 * 256 + 256;
-  p.maxbnd = 4 * p.maxb + 4 * p.n_base_blocks + 64;
+  int max_nbt = 0;
+  for (const auto& t : hp.til) max_nbt = std::max(max_nbt, t.n_tasks);
+  p.maxt = max_nbt + K * smax * smax * smax + 64;
+  p.maxb = p.max_nbb + K * 5 * smax * smax + 64;
+  p.maxcells = p.max_nbb + K * 3 * 256 + 256;
+  p.maxbnd = 4 * p.maxb + 4 * p.max_nbb + 64;
   // reader nodes and arena edges only arise for tasks touching subdivided
   // tiles (E5); overflow of any cap is reported as ST_ENGINE_LIMIT, never
   // silently truncated
@@ -359,7 +405,22 @@ HostProblem build_problem(const hesp_platform& plat, const hesp_perf_model& mode
   p.maxgs = std::max(p.maxt, 4 * p.maxb + 8);
   p.maxgr = p.maxb + 64;
   p.lay = slot_layout(p);
+  bind_tilings(p, hp, hp.base_tasks.data(), hp.base_blocks.data(), hp.base_preds.data(), hp.base_plist.data());
   return hp;
+}
+
+void bind_tilings(Problem& p, const HostProblem& hp, const TaskMeta* tasks, const BlockMeta* blocks,
+                  const BasePreds* preds, const int32_t* plist) {
+  p.base_tasks = tasks;
+  p.base_blocks = blocks;
+  p.base_preds = preds;
+  p.base_plist = plist;
+  p.n_til = static_cast<int>(hp.til.size());
+  for (int i = 0; i < p.n_til; ++i) {
+    const auto& o = hp.til[i];
+    p.til[i] = BaseTiling{o.s, o.n_tasks, o.n_blocks, 0, o.base_b, tasks + o.tasks, blocks + o.blocks,
+                          preds + o.preds, plist + o.plist};
+  }
 }
 
 }  // namespace hx

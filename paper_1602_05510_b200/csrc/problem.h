@@ -13,11 +13,23 @@ namespace hx {
 // arrays the device copies point at after upload.
 struct HostProblem {
   Problem p{};
+  // every top-level tiling's arrays, concatenated (TIL_BASE first)
   std::vector<TaskMeta> base_tasks;
   std::vector<BlockMeta> base_blocks;
   std::vector<BasePreds> base_preds;
   std::vector<int32_t> base_plist;
+  struct TilingOff {
+    int s, n_tasks, n_blocks;
+    long long base_b;
+    size_t tasks, blocks, preds, plist;  // offsets into the arrays above
+  };
+  std::vector<TilingOff> til;
 };
+
+// Points p's base arrays and tilings at copies of hp's arrays (host vectors
+// or their device uploads).
+void bind_tilings(Problem& p, const HostProblem& hp, const TaskMeta* tasks, const BlockMeta* blocks,
+                  const BasePreds* preds, const int32_t* plist);
 
 // Validates (Platform::validate, platform.cpp:91-138; PerfModel::analytic,
 // platform.cpp:312-325) and precomputes everything; throws std::runtime_error.

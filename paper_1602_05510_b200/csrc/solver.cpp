@@ -103,12 +103,14 @@ struct Ctx {
   }
 };
 
-// select_candidate over scores in candidate order (shared by hesp_solve)
-size_t select_index(const double* sc, size_t n, int sampling, Rng& rng) {
+// select_candidate over scores in candidate order (shared by hesp_solve).
+// Hard: argmax score, ties to the lowest target id (a task id
+// for partitions, a cluster id for merges/repartitions), then candidate order.
+size_t select_index(const double* sc, const int32_t* tg, size_t n, int sampling, Rng& rng) {
   size_t pick = 0;
   if (sampling == HESP_SAMPLE_HARD) {
     for (size_t i = 1; i < n; ++i)
-      if (sc[i] > sc[pick]) pick = i;
+      if (sc[i] > sc[pick] || (sc[i] == sc[pick] && tg && tg[i] < tg[pick])) pick = i;
     return pick;
   }
   double total = 0;
@@ -134,7 +136,7 @@ extern "C" double hesp_choose_p(double idle_avg, int64_t d, int64_t min_block, i
 extern "C" int32_t hesp_select_candidate(const double* scores, int32_t n, int32_t sampling, uint64_t* rng_state) {
   if (n <= 0 || !scores || !rng_state) return -1;
   Rng rng{*rng_state};
-  const size_t i = select_index(scores, (size_t)n, sampling, rng);
+  const size_t i = select_index(scores, nullptr, (size_t)n, sampling, rng);
   *rng_state = rng.s;
   return (int32_t)i;
 }
@@ -257,9 +259,9 @@ void collect(Chain& ch, const Problem& P, const TraceGraph& g, const hesp_trace&
       const double score = std::max(0.0, (a.end - a.start) - est);
       if (score > 0) cands.push_back({HESP_ACT_PARTITION, id, id, (int)k, score, m.b});
     }
-    for (int c = 1; c < (int)g.parts.size(); ++c) {  // innermost clusters (not the base one)
+    for (int c = 0; c < (int)g.parts.size(); ++c) {  // innermost clusters (not the base one: the root's)
       const PartEntry& pe = g.parts[c];
-      if (pe.task < 0) continue;
+      if (pe.task <= 0) continue;
       bool flat = true;
       double lo = 0, hi = 0, isum = 0;
       for (int mm = pe.child0; mm < pe.child0 + pe.nchild && flat; ++mm) {
@@ -299,11 +301,13 @@ void collect(Chain& ch, const Problem& P, const TraceGraph& g, const hesp_trace&
       if (rep > 0) cands.push_back({HESP_ACT_REPARTITION, c, pe.task, (int)k, rep, par.b});
     }
     const hesp_cand_desc& cur = ch.cur;
+    const size_t before = cands.size();
     cands.erase(std::remove_if(cands.begin(), cands.end(),
                                [&](const Cand& c) {
                                  return cur.n_ops + (c.action == HESP_ACT_REPARTITION ? 2 : 1) > HESP_MAX_OPS;
                                }),
                 cands.end());
+    if (cands.size() < before && out->budget_iteration < 0) out->budget_iteration = it;  // op budget reached
     ch.rec.n_candidates = (int32_t)cands.size();
 }
 
@@ -324,6 +328,7 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
     ch.out->n_history = 0;
     ch.out->best_makespan = 0;
     ch.out->best_iteration = -1;
+    ch.out->budget_iteration = -1;
     ch.out->n_simulated = 0;
     std::memset(&ch.out->best, 0, sizeof ch.out->best);
     ch.A.resize((size_t)P.maxt);
@@ -407,22 +412,31 @@ int solve_chains(hesp_engine* e, int n, const hesp_cand_desc* initial, const hes
       hesp_solver_iteration rec = ch.rec;
       std::vector<Cand> valid;
       ch.out->n_simulated += (int64_t)ch.cands.size();
-      for (size_t i = 0; i < ch.cands.size(); ++i)
+      for (size_t i = 0; i < ch.cands.size(); ++i) {
         if (outc[ch.first + i].status == 0) {
           valid.push_back(ch.cands[i]);
           if (ch.cfg.sampling == HESP_SAMPLE_EXACT) valid.back().score = outc[ch.first + i].makespan;
         }
+        // a mutation beyond the slot's capacity (ids consumed by merged
+        // clusters count too): the chain has outgrown the engine's sizing
+        if (outc[ch.first + i].status == HESP_ST_ENGINE_LIMIT && ch.out->budget_iteration < 0)
+          ch.out->budget_iteration = rec.iteration;
+      }
       rec.n_valid = (int32_t)valid.size();
       if (!valid.empty()) {
         // ---- select_candidate ----
         std::vector<double> sc(valid.size());
-        for (size_t i = 0; i < valid.size(); ++i) sc[i] = valid[i].score;
+        std::vector<int32_t> tg(valid.size());
+        for (size_t i = 0; i < valid.size(); ++i) {
+          sc[i] = valid[i].score;
+          tg[i] = valid[i].target;
+        }
         size_t pick = 0;
         if (ch.cfg.sampling == HESP_SAMPLE_EXACT) {
           for (size_t i = 1; i < sc.size(); ++i)
             if (sc[i] < sc[pick]) pick = i;
         } else {
-          pick = select_index(sc.data(), sc.size(), ch.cfg.sampling, ch.rng);
+          pick = select_index(sc.data(), tg.data(), sc.size(), ch.cfg.sampling, ch.rng);
         }
         const Cand& cd = valid[pick];
         rec.action = cd.action;

@@ -55,6 +55,50 @@ std::vector<std::pair<double, int>> deltas_of(const hesp_trace& tr) {
 
 }  // namespace
 
+void to_reference_ids(TraceGraph& g, TraceLogs* logs, int off_t, int off_b, int off_c) {
+  if (off_t == 0 && off_b == 0 && off_c == 0) return;
+  auto xt = [&](int j) { return j > 0 ? j + off_t : j; };
+  auto xb = [&](int b) { return b > 0 ? b + off_b : b; };
+  auto meta = [&](TaskMeta m) {
+    for (int k = 0; k < 4; ++k) m.blk[k] = xb(m.blk[k]);
+    return m;
+  };
+  for (auto& j : g.leaves) j = xt(j);
+  for (auto& j : g.preds) j = xt(j);
+  for (auto& m : g.meta) m = meta(m);
+  if (!g.bregion.empty()) {  // ids consumed before the top merge: erased blocks
+    std::vector<Region> r(g.bregion.size() + off_b, Region{0, 0, 0, 0});
+    std::vector<int32_t> in(g.bisint.size() + off_b, 0);
+    for (size_t b = 0; b < g.bregion.size(); ++b) r[xb((int)b)] = g.bregion[b];
+    for (size_t b = 0; b < g.bisint.size(); ++b) in[xb((int)b)] = g.bisint[b];
+    g.bregion.swap(r);
+    g.bisint.swap(in);
+  }
+  {
+    TaskMeta gone{};
+    gone.blk[0] = gone.blk[1] = gone.blk[2] = gone.blk[3] = -1;
+    gone.nrd = -1;
+    std::vector<TaskMeta> t(g.tmeta.size() + (g.tmeta.empty() ? 0 : off_t), gone);
+    for (size_t j = 0; j < g.tmeta.size(); ++j) t[xt((int)j)] = meta(g.tmeta[j]);
+    g.tmeta.swap(t);
+  }
+  {
+    std::vector<PartEntry> c(g.parts.size() + off_c, PartEntry{-1, 0, 0, 0});  // merged before the top merge
+    for (size_t i = 0; i < g.parts.size(); ++i) {
+      PartEntry e = g.parts[i];
+      if (e.task >= 0) e.task = xt(e.task);
+      else e.task = -2 - xt(-2 - e.task);
+      e.child0 = xt(e.child0);
+      c[i + off_c] = e;
+    }
+    g.parts.swap(c);
+  }
+  if (logs) {
+    for (auto& x : logs->xfers) x.block = xb(x.block);
+    for (auto& r : logs->res) r.block = xb(r.block);
+  }
+}
+
 int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr, bool schedule_only) {
   // assignments in task-id order (std::map order of SimResult::assignments)
   int na = 0;

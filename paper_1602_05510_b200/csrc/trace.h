@@ -33,6 +33,10 @@ struct TraceLogs {
   std::vector<ResLog> res;     // emission order (ties are identical records)
 };
 
+// Rewrites an exported graph (and the logs' block ids) from the engine's
+// internal ids to reference ids (BaseView offsets; identity when all are 0).
+void to_reference_ids(TraceGraph& g, TraceLogs* logs, int off_t, int off_b, int off_c);
+
 // Fills the caller's hesp_trace arrays; HESP_OK or HESP_E_LIMIT.
 int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, hesp_trace* tr,
                  bool schedule_only = false);

@@ -135,7 +135,7 @@ SOLVER_ITER_DTYPE = np.dtype([("iteration", "<i4"), ("action", "<i4"), ("target"
 class SolverResultC(C.Structure):
     _fields_ = [("cap_history", C.c_int32), ("n_history", C.c_int32), ("history", C.c_void_p),
                 ("best", CandDesc), ("best_makespan", C.c_double), ("best_iteration", C.c_int32),
-                ("pad", C.c_int32), ("n_simulated", C.c_int64)]
+                ("budget_iteration", C.c_int32), ("n_simulated", C.c_int64)]
 
 
 TASK_SELECTION = {"All": 0, "CP": 1, "Shallow": 2}
@@ -194,7 +194,7 @@ assert DESC_DTYPE.itemsize == C.sizeof(CandDesc) == 520
 EXPORTS = [
     "hesp_engine_create", "hesp_eval_generated", "hesp_eval_descs", "hesp_eval_descs_device",
     "hesp_generate_device", "hesp_generate_host", "hesp_generate_batch", "hesp_eval_detail",
-    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_trace_bounds", "hesp_solve", "hesp_solve_batch", "hesp_eval_neighbors", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
+    "hesp_engine_get_info", "hesp_eval_trace", "hesp_verify_trace", "hesp_trace_bounds", "hesp_trace_blocks", "hesp_solve", "hesp_solve_batch", "hesp_eval_neighbors", "hesp_min_reduce", "hesp_choose_p", "hesp_select_candidate",
     "hesp_fixture_load", "hesp_fixture_platform", "hesp_fixture_model", "hesp_fixture_free",
     "hesp_engine_destroy", "hesp_last_error", "hesp_status_name",
 ]
@@ -530,6 +530,8 @@ class BatchEngine:
         if rc > 0:
             raise RuntimeError(f"solve: initial state fails with status {rc} ({status_name(rc)})")
         best = np.frombuffer(bytes(res.best), DESC_DTYPE)[0].copy()
+        # first iteration whose candidates hit the descriptor's op budget (-1: never)
+        self.last_budget_iteration = int(res.budget_iteration)
         return hist[:res.n_history].copy(), best, float(res.best_makespan), int(res.best_iteration), \
             int(res.n_simulated)
 
@@ -563,6 +565,7 @@ class BatchEngine:
         if rc > 0:
             raise RuntimeError(f"solve_batch: an initial state fails with status {rc} ({status_name(rc)})")
         out = []
+        self.last_budget_iterations = [int(res[i].budget_iteration) for i in range(n)]
         for i in range(n):
             best = np.frombuffer(bytes(res[i].best), DESC_DTYPE)[0].copy()
             out.append((hists[i][:res[i].n_history].copy(), best, float(res[i].best_makespan),

@@ -74,7 +74,31 @@ MERGE_OPS = [
     [(1, 2), (2, 2), (17, 4), ("m", 2), (18, 2), ("m", 1)],  # interleaved, shared blocks survive
     [(2, 4), (17, 2), ("m", 1), (3, 2), ("m", 3), (2, 2)],
 ]
+# Merging the base cluster (cluster 0, graph.cpp:521-534) returns the graph to
+# the unpartitioned root; ids stay consumed, so a later partition of the root
+# (ids from 817 on C2) puts the candidate on another top-level tiling.  Ext.
+# cluster ids keep counting as well (the first cluster after the merge is 1).
+BASEMERGE_OPS = [
+    [("m", 0)],                                     # the unpartitioned root: one CHOL(16384)
+    [("m", 0), (0, 8)],                             # 8x8 tiling, tasks 817..936
+    [("m", 0), (0, 16)],                            # the base tiling again, ids shifted by 816
+    [("m", 0), (0, 4), (817, 2)],                   # 4x4 tiling, its first CHOL split
+    [("m", 0), (0, 8), ("m", 1)],                   # back to the root
+    [("m", 0), (0, 8), ("m", 1), (0, 4)],           # and onto a third tiling
+    [(18, 2), ("m", 0)],                            # base member partitioned -> NestedCluster
+    [(18, 2), ("m", 1), ("m", 0), (0, 8)],          # ids consumed by a merged cluster first
+    [("m", 0), ("m", 0)],                           # merged twice -> UnknownCluster
+    [("m", 0), (5, 2)],                             # partition an erased task -> Validation
+    [("m", 0), (0, 2), (817, 2), (818, 2)],         # 2x2 tiling, CHOL and TRSM split
+    [("m", 0), (0, 3)],                             # snaps to 2
+    [("m", 0), (0, 16), (834, 4), (820, 2)],        # base tiling shifted, GEMM(2,1,0) and TRSM split
+    [("m", 0), (0, 8), (820, 2), ("m", 1)],         # top cluster with a partitioned member -> NestedCluster
+    [("m", 0), (0, 8), (820, 2), ("m", 2), ("m", 1), (0, 16), (1000, 2)],  # inner, top, re-tile, split
+    [(1, 2), (17, 4), ("m", 2), ("m", 1), ("m", 0), (0, 4), (0, 2)],  # root partitioned again -> NotALeaf
+]
 EXPLICIT = {
+    "explicit_basemerge_c2": ("c2", BASEMERGE_OPS),
+    "explicit_basemerge_evict": ("evict_wb", BASEMERGE_OPS),
     "explicit_merge_c2": ("c2", MERGE_OPS),
     "explicit_c2": ("c2", EXPLICIT_OPS),
     "explicit_c3": ("c3", EXPLICIT_OPS),
@@ -97,6 +121,9 @@ TRACES = {
     "evict_wb_0": ("evict_wb", 0), "evict_wt_1": ("evict_wt", 1), "evict_wa_0": ("evict_wa", 0),
     "sect_cpugpu_0": ("sect_cpugpu", 0), "deep_biglittle_1": ("deep_biglittle", 1),
     "policy_PL_EFT-P_WA_10": ("policy_PL_EFT-P_WA", 10), "policy_FCFS_R-P_WT_5": ("policy_FCFS_R-P_WT", 5),
+    # explicit descriptors (preset, index, descs): candidates after a merge of the base cluster
+    "basemerge_c2_12": ("c2", 12, "explicit_basemerge_c2"),
+    "basemerge_evict_12": ("evict_wb", 12, "explicit_basemerge_evict"),
 }
 # verify_schedule on edited schedules: (trace, task to move, seconds earlier)
 SHIFTS = {
@@ -113,6 +140,9 @@ SOLVES = {
     "small_shallow_soft": ("policy_PL_EFT-P_WB", 12, "Shallow", "Soft", 5),
     "small_rp_all_soft": ("policy_FCFS_R-P_WB", 10, "All", "Soft", 9),
     "c2_all_soft": ("c2", 5, "All", "Soft", 1),
+    # long horizon: parity up to the op budget of the chain state
+    "small_all_soft_long": ("policy_PL_EFT-P_WB", 120, "All", "Soft", 2),
+    "small_all_hard_long": ("policy_PL_EFT-P_WB", 90, "All", "Hard", 4),
 }
 
 
@@ -136,21 +166,24 @@ def write_solves(names):
 def write_traces(names):
     import gzip
     import json
-    for name, (preset_name, idx) in TRACES.items():
+    for name, (preset_name, idx, *descs) in TRACES.items():
         if names and f"trace_{name}" not in names:
             continue
         p, _ = PARITY[preset_name]
-        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx)], check=True,
+        extra = ["--descs", os.path.join(HERE, f"{descs[0]}.descs")] if descs else []
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), *extra, "--trace", str(idx)], check=True,
                            capture_output=True, text=True)
         d = json.loads(r.stdout)
         d["preset"] = preset_name
+        if descs:
+            d["descs"] = descs[0]
         with gzip.open(os.path.join(HERE, f"trace_{name}.json.gz"), "wt") as f:
             json.dump(d, f, separators=(",", ":"))
         print("trace", name, len(d["assignments"]), "tasks", len(d["transfers"]), "transfers")
     for name, (tname, task_rank, by) in SHIFTS.items():
         if names and f"shift_{name}" not in names:
             continue
-        preset_name, idx = TRACES[tname]
+        preset_name, idx = TRACES[tname][:2]
         p, _ = PARITY[preset_name]
         base = json.loads(subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx)], check=True,
                                          capture_output=True, text=True).stdout)

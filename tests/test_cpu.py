@@ -154,6 +154,35 @@ def test_host_engine_matches_reference(name):
     assert r.returncode == 0
 
 
+@pytest.mark.skipif(not os.path.exists(ENGINE_CHECK), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("name,preset", [("explicit_basemerge_c2", "c2"), ("explicit_basemerge_evict", "evict_wb"),
+                                         ("explicit_merge_c2", "c2"), ("explicit_c2", "c2"),
+                                         ("explicit_sect", "sect_cpugpu")])
+def test_host_engine_matches_reference_explicit(name, preset):
+    """Engine<HostWarp> on the hand-built descriptors (merges of the base
+    cluster, top-level re-tilings, error statuses) vs the reference library."""
+    from golden_io import GOLDEN_DIR
+    p, _ = PARITY[preset]
+    r = subprocess.run([ENGINE_CHECK, *harness_args(p, FIXTURES), "--descs", os.path.join(GOLDEN_DIR, f"{name}.descs")],
+                       capture_output=True, text=True, timeout=600)
+    assert "mismatches 0" in r.stdout, r.stdout[-2000:]
+    assert r.returncode == 0
+
+
+@pytest.mark.skipif(not os.path.exists(ENGINE_CHECK), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("preset", ["c2", "evict_wb", "c3", "sect_cpugpu", "policy_FCFS_R-P_WT"])
+def test_host_engine_matches_reference_on_taskgraphs(preset):
+    """The TaskGraph drop-in's replay (include/hesp_b200_bridge.hpp plan_graph):
+    reference graphs built by random partition_task / merge_cluster (top cluster
+    included) / repartition_cluster sequences, replayed as descriptors on the
+    width-1 engine, give the reference's status, leaf count and makespan bits."""
+    p, _ = PARITY[preset]
+    r = subprocess.run([ENGINE_CHECK, *harness_args(p, FIXTURES), "--graphs", "40"], capture_output=True, text=True,
+                       timeout=600)
+    assert "mismatches 0" in r.stdout, r.stdout[-2000:]
+    assert r.returncode == 0
+
+
 @pytest.mark.skipif(not os.path.isdir("/root/reference/proj/include"), reason="reference headers absent")
 def test_reference_side_bridge_compiles(tmp_path):
     """include/hesp_b200_bridge.hpp compiles against the reference's own hesp:: types."""

@@ -52,7 +52,8 @@ def test_descs_path_matches_generated(lib):
     assert (b1.makespan, b1.index) == (b2.makespan, b2.index)
 
 
-EXPLICIT = {"explicit_c2": "c2", "explicit_c3": "c3", "explicit_sect": "sect_cpugpu", "explicit_merge_c2": "c2"}
+EXPLICIT = {"explicit_c2": "c2", "explicit_c3": "c3", "explicit_sect": "sect_cpugpu", "explicit_merge_c2": "c2",
+            "explicit_basemerge_c2": "c2", "explicit_basemerge_evict": "evict_wb"}
 
 
 @pytest.mark.parametrize("name", sorted(EXPLICIT))

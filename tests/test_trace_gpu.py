@@ -24,7 +24,13 @@ def engine(preset):
 def traced(name):
     g = read_trace(name)
     eng = engine(g["preset"])
-    desc = eng.generate_host(g["index"], 1)
+    if g.get("descs"):  # an explicit descriptor (e.g. after a merge of the base cluster)
+        import os
+        from golden_io import GOLDEN_DIR
+        from paper_1602_05510_b200.engine import DESC_DTYPE
+        desc = np.fromfile(os.path.join(GOLDEN_DIR, f"{g['descs']}.descs"), DESC_DTYPE)[g["index"]:g["index"] + 1]
+    else:
+        desc = eng.generate_host(g["index"], 1)
     return g, eng, eng.eval_trace(desc[0])
 
 
