@@ -257,6 +257,26 @@ HX uint64_t dbits(double x) {
 #ifndef HESP_PREFETCH
 #define HESP_PREFETCH 0
 #endif
+// Folding a hash term into the warp's shared copy: a read-modify-write by
+// every lane is only correct while the warp is converged, so (1) one lane
+// folds, or (2) the warp reconverges first; (0) the unguarded form (A/B only).
+#ifndef HESP_HASH_FOLD
+#define HESP_HASH_FOLD 1
+#endif
+#if HESP_HASH_FOLD == 1
+#define HASH_FOLD(acc, t)                   \
+  do {                                      \
+    if (wp.lane() == 0) (acc) += (t);       \
+  } while (0)
+#elif HESP_HASH_FOLD == 2
+#define HASH_FOLD(acc, t) \
+  do {                    \
+    wp.sync();            \
+    (acc) += (t);         \
+  } while (0)
+#else
+#define HASH_FOLD(acc, t) ((acc) += (t))
+#endif
 HX void prefetch_l1(const void* p) {
 #if defined(__CUDACC__)
   asm volatile("prefetch.L1 [%0];" ::"l"(p));
@@ -2860,7 +2880,7 @@ struct Engine {
       // one lane folds the term: a read-modify-write of shared state by every
       // lane is only safe while the warp stays converged
       const uint64_t xt_ = hesp_xfer_term(xblock(blk), src, dst, nbytes, dbits(start0), dbits(rdy), 0, 0, 0, 0);
-      if (wp.lane() == 0) W.xh += xt_;
+      HASH_FOLD(W.xh, xt_);
       return rdy;
     };
     // validate_from (sim.cpp:452-461), b != 0: b and every block inside it
@@ -3319,7 +3339,7 @@ struct Engine {
         W.proc_free[p] = end;
         {
           const uint64_t at_ = hesp_assign_term(xtask(j), p, dbits(start), dbits(end));
-          if (wp.lane() == 0) W.ah += at_;
+          HASH_FOLD(W.ah, at_);
         }
         mk = dmax(mk, end);
         // write coherence (sim.cpp:625-628): invalidate the cone elsewhere,

@@ -19,6 +19,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -756,6 +757,10 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   int bbps = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bbps, build_kernel, WARPS_PER_BLOCK * 32, 0);
   if (bbps < 1) bbps = 1;
+  // A/B knobs: resident CTAs per SM below the occupancy limit (fewer warps
+  // in flight, a smaller concurrent working set)
+  if (const char* v = getenv("HESP_BUILD_CTAS")) bbps = std::max(1, std::min(bbps, atoi(v)));
+  if (const char* v = getenv("HESP_SIM_CTAS")) bps = std::max(1, std::min(bps, atoi(v)));
   e->n_build_blocks = prop.multiProcessorCount * bbps;
   if (bps < 1) bps = 1;
   e->blocks_per_sm = bps;

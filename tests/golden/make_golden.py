@@ -123,6 +123,8 @@ TRACES = {
     "policy_PL_EFT-P_WA_10": ("policy_PL_EFT-P_WA", 10), "policy_FCFS_R-P_WT_5": ("policy_FCFS_R-P_WT", 5),
     # explicit descriptors (preset, index, descs): candidates after a merge of the base cluster
     "basemerge_c2_12": ("c2", 12, "explicit_basemerge_c2"),
+    "basemerge_c2_3": ("c2", 3, "explicit_basemerge_c2"),   # 4x4 top tiling: tiles span base tiles
+    "basemerge_c2_0": ("c2", 0, "explicit_basemerge_c2"),   # the bare root as the only task
     "basemerge_evict_12": ("evict_wb", 12, "explicit_basemerge_evict"),
 }
 # verify_schedule on edited schedules: (trace, task to move, seconds earlier)
@@ -131,6 +133,7 @@ SHIFTS = {
     "c2_1_late": ("c2_1", 400, -0.02),
     "evict_wb_0_early": ("evict_wb_0", 30, 0.005),
     "sect_cpugpu_0_late": ("sect_cpugpu_0", 20, -0.01),
+    "basemerge_c2_3_early": ("basemerge_c2_3", 10, 0.05),
 }
 
 # SPEC solver runs (hesp_solve parity): name -> (preset, iterations, selection, sampling, seed)
@@ -183,12 +186,13 @@ def write_traces(names):
     for name, (tname, task_rank, by) in SHIFTS.items():
         if names and f"shift_{name}" not in names:
             continue
-        preset_name, idx = TRACES[tname][:2]
+        preset_name, idx, *descs = TRACES[tname]
         p, _ = PARITY[preset_name]
-        base = json.loads(subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx)], check=True,
+        extra = ["--descs", os.path.join(HERE, f"{descs[0]}.descs")] if descs else []
+        base = json.loads(subprocess.run([HARNESS, *harness_args(p, FIXTURES), *extra, "--trace", str(idx)], check=True,
                                          capture_output=True, text=True).stdout)
         task = base["assignments"][task_rank][0]
-        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), "--trace", str(idx), "--shift-task", str(task),
+        r = subprocess.run([HARNESS, *harness_args(p, FIXTURES), *extra, "--trace", str(idx), "--shift-task", str(task),
                             "--shift-by", repr(by)], check=True, capture_output=True, text=True)
         d = json.loads(r.stdout)
         out = {"trace": tname, "task": task, "shift_by": by, "violations": d["violations"]}
