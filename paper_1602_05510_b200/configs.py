@@ -57,6 +57,10 @@ PARITY["merge_c2"] = (preset(CPUGPU, 16384, 4, 16, 12, seed=21, merge_pct=35), 6
 PARITY["merge_evict"] = (preset(CPUGPU_EVICT, 16384, 4, 16, 10, seed=22, merge_pct=30), 24)
 PARITY["merge_c3"] = (preset(BIGLITTLE, 8192, 8, 16, 10, seed=23, merge_pct=40, ordering="FCFS",
                              selection="F-P"), 32)
+# merges on non-nested tilings: merge_cluster while intersection descriptors live (graph.cpp:214-266)
+PARITY["merge_sect"] = (preset(CPUGPU, 6144, 4, 8, 10, s_choices=(2, 3, 4), seed=41, merge_pct=35), 96)
+PARITY["merge_sect_bl"] = (preset(BIGLITTLE, 6144, 8, 8, 10, s_choices=(2, 3, 4), seed=42, merge_pct=40,
+                                  ordering="FCFS", selection="EIT-P"), 64)
 for o, s, c in itertools.product(("FCFS", "PL"), ("R-P", "F-P", "EIT-P", "EFT-P"), ("WT", "WB", "WA")):
     PARITY[f"policy_{o}_{s}_{c}"] = (preset(CPUGPU, 4096, 4, 8, 8, seed=7, ordering=o, selection=s, caching=c,
                                             sched_seed=5), 24)
@@ -75,6 +79,7 @@ SCALE = {
     "scale_evict_wa": (PARITY["evict_wa"][0], 1000),
     "scale_merge_c2": (PARITY["merge_c2"][0], 2000),
     "scale_sect_cpugpu": (PARITY["sect_cpugpu"][0], 2000),
+    "scale_merge_sect": (PARITY["merge_sect"][0], 2000),
 }
 
 

@@ -367,6 +367,7 @@ struct Engine {
   HX uint16_t* rht() const { return (uint16_t*)(slot + PB.lay.rht); }  // region hash of new blocks
   HX uint8_t* pmark() const { return (uint8_t*)(slot + PB.lay.pmark); }  // 1 + partition entry per task id
   HX int32_t* bref() const { return (int32_t*)(slot + PB.lay.bref); }     // by candidate block id - n_bb()
+  HX int32_t* xpar() const { return (int32_t*)(slot + PB.lay.xpar); }     // [candidate block - n_bb()][XPAR]
   HX PartEntry* part() const { return (PartEntry*)(slot + PB.lay.part); }  // clusters, by id
   HX int32_t* dstack() const { return (int32_t*)(slot + PB.lay.dstack); }
   HX uint8_t* tmis() const { return (uint8_t*)(slot + PB.lay.tmis); }
@@ -414,6 +415,7 @@ struct Engine {
   HX int msp() const { return PB.main_space; }
   int32_t ntasks, nblocks;  // next ids
   int32_t npart = 0;
+  int32_t nxp = 0;  // candidate intersection descriptors holding extra (non-Hasse) parent links
   int32_t nleaves = 0;
   int32_t n_tl_ids = 0;
   int32_t nedges = 0;
@@ -604,6 +606,7 @@ struct Engine {
     if (wp.lane() == 0) {
       bm()[id - n_bb()] = m;
       bref()[id - n_bb()] = 0;
+      NOUNROLL for (int k = 0; k < XPAR; ++k) xpar()[(id - n_bb()) * XPAR + k] = -1;
     }
     if (t >= 0 && id - n_bb() < RHT / 2) {
       unsigned i = rhash(r) & (RHT - 1);
@@ -611,7 +614,206 @@ struct Engine {
       if (wp.lane() == 0) rht()[i] = (uint16_t)(id - n_bb());
     }
     wp.sync();
+    if (nxp > 0 && t >= 0) xpar_on_create(id, t);
     return id;
+  }
+
+  // ---- DataDag parent links of intersection descriptors (graph.cpp:142-266) ----
+  // A prune erases an intersection descriptor when any of its *parents* dies
+  // (graph.cpp:221-228).  Its parents are its minimal strict containers (E1:
+  // create() links a block to them and unlinks the pairs it bridges,
+  // graph.cpp:142-189) plus the links get_or_create adds when a partial
+  // overlap's intersection already exists (graph.cpp:203-206), which need
+  // not be minimal.  Those extra links are kept per intersection (xpar) and
+  // dropped exactly when create() would unlink them.
+
+  // Minimal strict containers of region r among the live blocks of tile t
+  // (root and tile included), excluding block `self`; into out[], count
+  // returned (-1: more than cap).
+  HXN int min_containers(const Region& r, int t, int self, int* out, int cap) {
+    int n = 0;
+    auto consider = [&](int x) {
+      if (x == self) return;
+      const Region rx = reg(x);
+      if (dead_region(rx) || rsame(rx, r) || !rcontains(rx, r)) return;
+      // minimal: no other live container strictly inside x
+      bool minimal = true;
+      NOUNROLL for (int y = n_bb(); y < nblocks && minimal; ++y) {
+        if (y == self || y == x || tile_of(y) != t) continue;
+        const Region ry = reg(y);
+        if (!dead_region(ry) && !rsame(ry, r) && rcontains(ry, r) && !rsame(ry, rx) && rcontains(rx, ry))
+          minimal = false;
+      }
+      if (x == 0 && minimal && !rsame(reg(t), r) && rcontains(reg(t), r)) minimal = false;  // the tile is inside the root
+      if (minimal) {
+        if (n < cap) out[n] = x;
+        ++n;
+      }
+    };
+    consider(0);
+    consider(t);
+    NOUNROLL for (int x = n_bb(); x < nblocks; ++x)
+      if (tile_of(x) == t) consider(x);
+    return n <= cap ? n : -1;
+  }
+  HX int32_t& XP(int b, int k) const { return xpar()[(b - n_bb()) * XPAR + k]; }
+  HX void xpar_remove(int b, int v) {
+    int w = 0;
+    for (int k = 0; k < XPAR; ++k) {
+      const int e = XP(b, k);
+      if (e >= 0 && e != v) XP(b, w++) = e;
+    }
+    for (; w < XPAR; ++w) XP(b, w) = -1;
+  }
+  HX bool xpar_add(int b, int v) {  // false: no room
+    for (int k = 0; k < XPAR; ++k) {
+      const int e = XP(b, k);
+      if (e == v) return true;
+      if (e < 0) {
+        if (k == 0) ++nxp;
+        XP(b, k) = v;
+        return true;
+      }
+    }
+    return false;
+  }
+  // create(N) unlinks (p, c) for p in parents(N), c in children(N) (the
+  // maximal blocks strictly inside N): an intersection's extra parent p goes
+  // when N now sits between them.  Lane 0 works, the warp waits (rare path:
+  // only candidates with extra links).
+  HXN void xpar_on_create(int nid, int t) {
+    if (wp.lane() == 0) {
+      const Region rn = reg(nid);
+      int par[8];
+      const int np = min_containers(rn, t, nid, par, 8);
+      if (np < 0) {
+        fail(ST_ENGINE_LIMIT);
+      } else {
+        NOUNROLL for (int i = n_bb(); i < nblocks; ++i) {
+          if (i == nid || !bmeta(i).isint || XP(i, 0) < 0 || tile_of(i) != t) continue;
+          const Region ri = reg(i);
+          if (dead_region(ri) || rsame(ri, rn) || !rcontains(rn, ri)) continue;
+          bool maximal = true;  // no live block strictly between i and N
+          NOUNROLL for (int y = n_bb(); y < nblocks && maximal; ++y) {
+            if (y == i || y == nid || tile_of(y) != t) continue;
+            const Region ry = reg(y);
+            if (!dead_region(ry) && !rsame(ry, ri) && !rsame(ry, rn) && rcontains(ry, ri) && rcontains(rn, ry))
+              maximal = false;
+          }
+          if (!maximal) continue;
+          NOUNROLL for (int k = 0; k < np; ++k) xpar_remove(i, par[k]);
+          if (XP(i, 0) < 0) --nxp;
+        }
+      }
+    }
+    nxp = wp.bcast(nxp, 0);
+    status = wp.bcast(status, 0);
+    wp.sync();
+  }
+  // prune_unreferenced's treatment of intersection descriptors (graph.cpp:
+  // 216-228, 256-262) before the non-intersection blocks of a merge die:
+  // in id order, an intersection dies when any parent is dead.  `top`: the
+  // merge of the top cluster (every block but the root dies).  A survivor
+  // left with a dead parent would be relinked (graph.cpp:229-255): 201.  A
+  // dying intersection a live task still references makes the reference's
+  // own infer_dependences throw std::out_of_range from map::at: status 100.
+  HXN void prune_intersections(bool top) {
+    if (wp.lane() == 0) {
+      int32_t* dead = gs_b();  // scratch: candidate block -> 1 if dead
+      NOUNROLL for (int b = n_bb(); b < nblocks; ++b) {
+        const BlockMeta& o = bm()[b - n_bb()];
+        dead[b - n_bb()] = !dead_region(o.r) && !o.isint && (top || bref()[b - n_bb()] == 0);
+      }
+      auto is_dead = [&](int p) -> bool { return p >= n_bb() ? dead[p - n_bb()] != 0 : (top && p != 0); };
+      bool limit = false;
+      for (int pass = 0; pass < 2 && !limit; ++pass) {
+        NOUNROLL for (int i = n_bb(); i < nblocks && !limit; ++i) {
+          const BlockMeta& o = bm()[i - n_bb()];
+          if (!o.isint || dead_region(o.r) || (pass == 0 && dead[i - n_bb()])) continue;
+          if (pass == 1 && dead[i - n_bb()]) continue;
+          int par[8];
+          const int np = min_containers(o.r, o.tile, i, par, 8);
+          if (np < 0) {
+            limit = true;
+            break;
+          }
+          bool d = false;
+          NOUNROLL for (int k = 0; k < np; ++k) d |= is_dead(par[k]);
+          NOUNROLL for (int k = 0; k < XPAR; ++k) d |= XP(i, k) >= 0 && is_dead(XP(i, k));
+          if (pass == 0) {
+            dead[i - n_bb()] = d ? 1 : 0;
+          } else if (d) {
+            // survived with a dead parent (a higher-id intersection died
+            // after it was checked): it inherits links to its nearest alive
+            // ancestors through dead blocks (alive_ancestors, graph.cpp:229-255)
+            if (top) {
+              limit = true;
+              break;
+            }
+            int work[16], nw = 0;
+            auto push_dead_parents = [&](int b) {
+              int pp[8];
+              const Region rb = reg(b);
+              const int n2 = min_containers(rb, tile_of(b), b, pp, 8);
+              if (n2 < 0) {
+                limit = true;
+                return;
+              }
+              auto visit = [&](int q) {
+                if (is_dead(q)) {
+                  bool seen = false;
+                  for (int z = 0; z < nw; ++z) seen |= work[z] == q;
+                  if (!seen) {
+                    if (nw < 16) work[nw++] = q;
+                    else limit = true;
+                  }
+                } else if (!xpar_add(i, q)) {
+                  limit = true;
+                }
+              };
+              NOUNROLL for (int k = 0; k < n2; ++k) visit(pp[k]);
+              if (b >= n_bb() && bmeta(b).isint)
+                NOUNROLL for (int k = 0; k < XPAR; ++k)
+                  if (XP(b, k) >= 0) visit(XP(b, k));
+            };
+            push_dead_parents(i);
+            NOUNROLL for (int z = 0; z < nw && !limit; ++z) push_dead_parents(work[z]);
+            NOUNROLL for (int z = 0; z < nw; ++z) xpar_remove(i, work[z]);  // the dead ones go with the erase
+          }
+        }
+      }
+      if (limit) {
+        fail(ST_ENGINE_LIMIT);
+      } else {
+        NOUNROLL for (int i = n_bb(); i < nblocks; ++i) {
+          BlockMeta& o = bm()[i - n_bb()];
+          if (!o.isint || !dead[i - n_bb()]) continue;
+          if (!top && bref()[i - n_bb()] > 0) {
+            // erased while a task still references it: the reference's
+            // infer_dependences throws at once if that task is a leaf; a
+            // dangling reference from a partitioned task is not modelled
+            bool leaf_ref = false;
+            NOUNROLL for (int m = n_bt(); m < ntasks; ++m) {
+              if (dead_task(m)) continue;
+              const TaskMeta tmm = tm()[m - n_bt()];
+              bool refs = false;
+              NOUNROLL for (int k = 0; k <= tmm.nrd; ++k) refs |= tmm.blk[k] == i;
+              if (refs && part_index(m) < 0) leaf_ref = true;
+            }
+            fail(leaf_ref ? ST_FOREIGN : ST_ENGINE_LIMIT);
+          }
+          if (XP(i, 0) >= 0) --nxp;
+          NOUNROLL for (int k = 0; k < XPAR; ++k) XP(i, k) = -1;
+          o.r.row = -1;
+          o.r.col = -1;
+          o.r.rows = 0;
+          o.r.cols = 0;
+        }
+      }
+    }
+    nxp = wp.bcast(nxp, 0);
+    status = wp.bcast(status, 0);
+    wp.sync();
   }
 
   // r is a dyadic square of base tile t: side = tile side / 2^k at an offset
@@ -673,8 +875,19 @@ struct Engine {
       const int c1 = (o.col + o.cols < r.col + r.cols) ? o.col + o.cols : r.col + r.cols;
       sct.rows = r1 - sct.row;
       sct.cols = c1 - sct.col;
-      if (find_block(sct, t) < 0) {
+      const int ex = find_block(sct, t);
+      if (ex < 0) {
         if (create_block(sct, true, t) < 0) return -1;
+      } else if (bmeta(ex).isint) {
+        // link(id, ex), link(other, ex) (graph.cpp:203-206): not necessarily Hasse
+        bool ok = true;
+        if (wp.lane() == 0) ok = xpar_add(ex, id) && xpar_add(ex, gs_a()[k]);
+        nxp = wp.bcast(nxp, 0);
+        wp.sync();
+        if (wp.any(!ok)) {
+          fail(ST_ENGINE_LIMIT);
+          return -1;
+        }
       }
     }
     return id;
@@ -756,8 +969,12 @@ struct Engine {
       const BlockMeta& o = bm()[b - n_bb()];
       if (o.isint && !dead_region(o.r)) sect = true;
     }
-    if (wp.any(sect)) return fail(ST_ENGINE_LIMIT);
+    const bool with_sect = wp.any(sect);
     if (c == 0) {
+      if (with_sect) {
+        prune_intersections(true);
+        if (status) return;
+      }
       // The top cluster (the root's): every other cluster is already merged
       // (its members are leaves), so the prune leaves the root alone -- the
       // unpartitioned root, with every id consumed so far staying consumed.
@@ -773,6 +990,10 @@ struct Engine {
         if (t.blk[k] >= n_bb()) wp.atomic_add(&bref()[t.blk[k] - n_bb()], -1);
     }
     wp.sync();
+    if (with_sect) {
+      prune_intersections(false);
+      if (status) return;
+    }
     NOUNROLL for (int b = n_bb() + wp.lane(); b < nblocks; b += WP::W) {
       BlockMeta& o = bm()[b - n_bb()];
       if (!o.isint && bref()[b - n_bb()] == 0 && !dead_region(o.r)) {
@@ -3475,6 +3696,7 @@ struct Engine {
     ntasks = n_bt();
     nblocks = n_bb();
     npart = 0;
+    nxp = 0;
     makespan = 0.0;
     ahash = xhash = 0;
     if (n_bt() > 1) {  // the top op partitioned the root into tasks 1..n_bt()-1
@@ -3522,6 +3744,7 @@ struct Engine {
       h.ntasks = ntasks;
       h.nblocks = nblocks;
       h.npart = npart;
+      h.nxp = nxp;
       put_view(h);
       *hdr() = h;
     }
@@ -3546,6 +3769,7 @@ struct Engine {
     copy(PB.lay.tm, sizeof(TaskMeta) * (size_t)(nt > 0 ? nt : 0));
     copy(PB.lay.bm, sizeof(BlockMeta) * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.bref, 4 * (size_t)(nb > 0 ? nb : 0));
+    copy(PB.lay.xpar, 4 * (size_t)XPAR * (size_t)(nb > 0 ? nb : 0));
     copy(PB.lay.rht, 2 * (size_t)RHT);
     copy(PB.lay.part, sizeof(PartEntry) * (size_t)th.npart);
     copy(PB.lay.tmis, ((size_t)n_bb() + 3) & ~(size_t)3);
@@ -3554,6 +3778,7 @@ struct Engine {
     ntasks = th.ntasks;
     nblocks = th.nblocks;
     npart = th.npart;
+    nxp = th.nxp;
     makespan = 0.0;
     ahash = xhash = 0;
     NOUNROLL for (int k = 0; k < n_extra && !status; ++k) apply_ext(extra[k]);
@@ -3570,7 +3795,7 @@ struct Engine {
     if (!status) build_cells();
     if (!status) build_deps();
     if (wp.lane() == 0) {
-      SlotHeader h;
+      SlotHeader h{};
       h.status = status;
       h.ntasks = ntasks;
       h.nblocks = nblocks;
@@ -3579,6 +3804,7 @@ struct Engine {
       h.sum_k = sum_k;
       h.n_leaves_out = n_out;
       h.npart = npart;
+      h.nxp = nxp;
       put_view(h);
       *hdr() = h;
     }

@@ -18,6 +18,7 @@ constexpr int MAXPART = HESP_MAX_OPS + 2;  // clusters per candidate (slot array
 constexpr size_t SMALL_BYTES = 2048;       // >= sizeof(hx::Small) (engine.h asserts)
 constexpr int RHT = 2048;  // per-candidate region hash (new blocks), 16-bit ids
 constexpr int MAXTIL = 8;  // top-level tilings of the root a candidate can sit on
+constexpr int XPAR = 4;    // extra DataDag parent links kept per intersection descriptor
 constexpr int TIL_BASE = 0, TIL_ROOT = 1;  // the workload's base tiling; the unpartitioned root
 
 // Status codes: 0 ok, 1 + hesp::Err ordinal (errors.hpp:10-32), engine codes >= 200.
@@ -34,6 +35,7 @@ enum : int32_t {
   ST_NO_PROCESSORS = 1 + 14,
   ST_COHERENCE = 1 + 19,
   ST_INTERNAL = 1 + 20,
+  ST_FOREIGN = 100,           // the reference throws a non-hesp exception (std::out_of_range) here
   ST_ENGINE_LIMIT = 201,      // a per-candidate buffer of the engine overflowed
   ST_ENGINE_INVARIANT = 202,  // an equivalence assumption of the engine was violated
 };
@@ -90,6 +92,8 @@ struct SlotHeader {
   int32_t status, ntasks, nblocks, nleaves, nedges, sum_k, n_leaves_out, npart;
   // top-level tiling the candidate sits on and its id offsets (BaseView)
   int32_t til, off_t, off_b, off_c;
+  int32_t nxp;  // intersection descriptors holding extra parent links (Engine::nxp)
+  int32_t pad1, pad2, pad3;
 };
 
 
@@ -126,7 +130,7 @@ struct BaseView {
 // Byte layout of one per-warp slot (all arrays in global memory).
 struct SlotLayout {
   size_t hdr, tm, ts, t_poff, t_pcnt, leaf, wsb;
-  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, part, dstack, small, tmis, wrt, pmk;
+  size_t bm, bflags, valid, lastu, pinu, bcell, rht, pmark, bref, xpar, part, dstack, small, tmis, wrt, pmk;
   size_t tl_head, tl_cnt, tl_boff, tl_nrb, tl_ncb, tl_coff, tl_ids;
   size_t bnd, c_writer, c_rhead, rnode, preds, succs, pool, pool_rel, pool_key, ready, ready_key, pbuf;
   size_t gs_a, gs_b, gs_reg, gs_reg2;  // gs_reg* sized maxgr
@@ -269,6 +273,7 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.rht = take(2 * (size_t)RHT);
   L.pmark = take(T);
   L.bref = take(4 * B);  // task references per candidate block (merge pruning)
+  L.xpar = take(4 * (size_t)XPAR * B);  // per candidate intersection: non-Hasse DataDag parents
   L.part = take(sizeof(PartEntry) * MAXPART);
   L.dstack = take(3 * 4 * (size_t)MAXPART);
   L.small = take(SMALL_BYTES);  // per-candidate Small of the thread-per-candidate simulate kernel
