@@ -257,6 +257,10 @@ HX uint64_t dbits(double x) {
 #ifndef HESP_PREFETCH
 #define HESP_PREFETCH 0
 #endif
+#ifndef HESP_XPAR  // A/B only: 0 drops the intersection-link emulation (E7)
+#define HESP_XPAR 1
+#endif
+
 // Folding a hash term into the warp's shared copy: a read-modify-write by
 // every lane is only correct while the warp is converged, so (1) one lane
 // folds, or (2) the warp reconverges first; (0) the unguarded form (A/B only).
@@ -332,6 +336,8 @@ struct Small {
   uint64_t ah, xh;  // event-loop result hashes (one copy per warp)
   int32_t ptype[MAXP], pspace[MAXP];
   BaseView bv;  // the candidate's top-level tiling and reference-id offsets
+  int32_t nxp;  // candidate intersection descriptors holding extra (non-Hasse) DataDag parent links
+  int32_t nxp_pad;
   LeanState L;
 };
 static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
@@ -406,16 +412,38 @@ struct Engine {
   // base task / block counts (overlay boundary), space count, main space:
   // read from the problem (constant memory), never from `this` (the engine
   // object lives in local memory on the device)
-  HX int n_bt() const { return SM().bv.nbt; }
-  HX int n_bb() const { return SM().bv.nbb; }
+  HX int n_bt() const {
+    return SM().bv.nbt;
+  }
+  HX int n_bb() const {
+    return SM().bv.nbb;
+  }
+  HX const TaskMeta* bt_() const {
+    return SM().bv.bt;
+  }
+  HX const BlockMeta* bb_() const {
+    return SM().bv.bb;
+  }
+  HX const BasePreds* bp_() const {
+    return SM().bv.bp;
+  }
+  HX const int32_t* bpl_() const {
+    return SM().bv.bpl;
+  }
+  HX long long base_b_() const {
+    return SM().bv.base_b;
+  }
   // reference ids of internal task / block ids (BaseView)
-  HX int xtask(int j) const { return j ? j + SM().bv.off_t : 0; }
-  HX int xblock(int b) const { return b ? b + SM().bv.off_b : 0; }
+  HX int xtask(int j) const {
+    return j ? j + SM().bv.off_t : 0;
+  }
+  HX int xblock(int b) const {
+    return b ? b + SM().bv.off_b : 0;
+  }
   HX int n_sp() const { return PB.S; }
   HX int msp() const { return PB.main_space; }
   int32_t ntasks, nblocks;  // next ids
   int32_t npart = 0;
-  int32_t nxp = 0;  // candidate intersection descriptors holding extra (non-Hasse) parent links
   int32_t nleaves = 0;
   int32_t n_tl_ids = 0;
   int32_t nedges = 0;
@@ -511,8 +539,8 @@ struct Engine {
   }
 
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
-  HX TaskMeta task(int id) const { return id < n_bt() ? SM().bv.bt[id] : tm()[id - n_bt()]; }
-  HX const BlockMeta& bmeta(int b) const { return b < n_bb() ? SM().bv.bb[b] : bm()[b - n_bb()]; }
+  HX TaskMeta task(int id) const { return id < n_bt() ? bt_()[id] : tm()[id - n_bt()]; }
+  HX const BlockMeta& bmeta(int b) const { return b < n_bb() ? bb_()[b] : bm()[b - n_bb()]; }
   HX Region reg(int b) const { return bmeta(b).r; }
   HX int tile_of(int b) const { return bmeta(b).tile; }
   HX long long rbytes(const Region& r) const { return (long long)r.rows * r.cols * PB.elem; }
@@ -569,7 +597,7 @@ struct Engine {
       }
       return found;
     }
-    if (r.rows >= SM().bv.base_b || r.cols >= SM().bv.base_b) {  // only a tile- or root-sized region can be either
+    if (r.rows >= base_b_() || r.cols >= base_b_()) {  // only a tile- or root-sized region can be either
       if (rsame(reg(0), r)) return 0;
       if (rsame(reg(t), r)) return t;
     }
@@ -606,7 +634,8 @@ struct Engine {
     if (wp.lane() == 0) {
       bm()[id - n_bb()] = m;
       bref()[id - n_bb()] = 0;
-      NOUNROLL for (int k = 0; k < XPAR; ++k) xpar()[(id - n_bb()) * XPAR + k] = -1;
+      if (isint)  // extra parent links are only ever read for intersection descriptors
+        NOUNROLL for (int k = 0; k < XPAR; ++k) xpar()[(id - n_bb()) * XPAR + k] = -1;
     }
     if (t >= 0 && id - n_bb() < RHT / 2) {
       unsigned i = rhash(r) & (RHT - 1);
@@ -614,7 +643,9 @@ struct Engine {
       if (wp.lane() == 0) rht()[i] = (uint16_t)(id - n_bb());
     }
     wp.sync();
-    if (nxp > 0 && t >= 0) xpar_on_create(id, t);
+#if HESP_XPAR
+    if (t >= 0 && SM().nxp > 0) xpar_on_create(id, t);  // (shared memory: no local-memory load per block)
+#endif
     return id;
   }
 
@@ -670,7 +701,7 @@ struct Engine {
       const int e = XP(b, k);
       if (e == v) return true;
       if (e < 0) {
-        if (k == 0) ++nxp;
+        if (k == 0) ++SM().nxp;
         XP(b, k) = v;
         return true;
       }
@@ -681,10 +712,13 @@ struct Engine {
   // maximal blocks strictly inside N): an intersection's extra parent p goes
   // when N now sits between them.  Lane 0 works, the warp waits (rare path:
   // only candidates with extra links).
+  // scratch for the rare link paths below (lane 0): the gather region
+  // buffer, unused while a candidate is being built
+  HX int32_t* lscratch() const { return (int32_t*)gs_reg(); }
   HXN void xpar_on_create(int nid, int t) {
     if (wp.lane() == 0) {
       const Region rn = reg(nid);
-      int par[8];
+      int* par = lscratch();
       const int np = min_containers(rn, t, nid, par, 8);
       if (np < 0) {
         fail(ST_ENGINE_LIMIT);
@@ -702,11 +736,10 @@ struct Engine {
           }
           if (!maximal) continue;
           NOUNROLL for (int k = 0; k < np; ++k) xpar_remove(i, par[k]);
-          if (XP(i, 0) < 0) --nxp;
+          if (XP(i, 0) < 0) --SM().nxp;
         }
       }
     }
-    nxp = wp.bcast(nxp, 0);
     status = wp.bcast(status, 0);
     wp.sync();
   }
@@ -731,7 +764,7 @@ struct Engine {
           const BlockMeta& o = bm()[i - n_bb()];
           if (!o.isint || dead_region(o.r) || (pass == 0 && dead[i - n_bb()])) continue;
           if (pass == 1 && dead[i - n_bb()]) continue;
-          int par[8];
+          int* par = lscratch();
           const int np = min_containers(o.r, o.tile, i, par, 8);
           if (np < 0) {
             limit = true;
@@ -750,9 +783,10 @@ struct Engine {
               limit = true;
               break;
             }
-            int work[16], nw = 0;
+            int* work = lscratch() + 16;
+            int nw = 0;
             auto push_dead_parents = [&](int b) {
-              int pp[8];
+              int* pp = lscratch() + 8;
               const Region rb = reg(b);
               const int n2 = min_containers(rb, tile_of(b), b, pp, 8);
               if (n2 < 0) {
@@ -802,7 +836,7 @@ struct Engine {
             }
             fail(leaf_ref ? ST_FOREIGN : ST_ENGINE_LIMIT);
           }
-          if (XP(i, 0) >= 0) --nxp;
+          if (XP(i, 0) >= 0) --SM().nxp;
           NOUNROLL for (int k = 0; k < XPAR; ++k) XP(i, k) = -1;
           o.r.row = -1;
           o.r.col = -1;
@@ -811,7 +845,6 @@ struct Engine {
         }
       }
     }
-    nxp = wp.bcast(nxp, 0);
     status = wp.bcast(status, 0);
     wp.sync();
   }
@@ -878,11 +911,10 @@ struct Engine {
       const int ex = find_block(sct, t);
       if (ex < 0) {
         if (create_block(sct, true, t) < 0) return -1;
-      } else if (bmeta(ex).isint) {
+      } else if (HESP_XPAR && bmeta(ex).isint) {
         // link(id, ex), link(other, ex) (graph.cpp:203-206): not necessarily Hasse
         bool ok = true;
         if (wp.lane() == 0) ok = xpar_add(ex, id) && xpar_add(ex, gs_a()[k]);
-        nxp = wp.bcast(nxp, 0);
         wp.sync();
         if (wp.any(!ok)) {
           fail(ST_ENGINE_LIMIT);
@@ -1417,7 +1449,7 @@ struct Engine {
   // whose tiles have no sub-blocks, the shared base table (off = ~index).
   HX const int32_t* pred_list(int j) const {
     const int off = t_poff()[j];
-    return off >= 0 ? preds() + off : SM().bv.bpl + ~off;
+    return off >= 0 ? preds() + off : bpl_() + ~off;
   }
 
   // Dependences (E2): per cell, last writer + readers since that write.
@@ -1486,7 +1518,7 @@ struct Engine {
         }
         sum_k += kt;
         if (fastj) {
-          const BasePreds& bp = SM().bv.bp[j];
+          const BasePreds& bp = bp_()[j];
           t_poff()[j] = ~bp.uoff;
           t_pcnt()[j] = bp.ucnt;
           ts()[j].missing = bp.ucnt;
@@ -1518,10 +1550,10 @@ struct Engine {
         const int myslot = slot++;
         if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
           // unsubdivided tile of a base task: its base contribution (E5)
-          const BasePreds& bp = SM().bv.bp[j];
+          const BasePreds& bp = bp_()[j];
           const int off = bp.soff[myslot], cnt = bp.scnt[myslot];
           NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W)
-            if (npb + q < PB.maxpb) pbuf()[npb + q] = SM().bv.bpl[off + q];
+            if (npb + q < PB.maxpb) pbuf()[npb + q] = bpl_()[off + q];
           npb += cnt;
           wp.sync();
           if (npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
@@ -2317,11 +2349,11 @@ struct Engine {
 #define BF HOT_ARR(uint32_t, bflags)
 #define TM HOT_ARR(const TaskMeta, tm)
 #define BM HOT_ARR(const BlockMeta, bm)
-#define BT (SM().bv.bt)
-#define BB (SM().bv.bb)
+#define BT (bt_())
+#define BB (bb_())
     // problem-wide scalars are read from constant memory at each use
-#define nbt_ SM().bv.nbt
-#define nbb_ SM().bv.nbb
+#define nbt_ n_bt()
+#define nbb_ n_bb()
 #define S_ PB.S
 #define ms PB.main_space
 #define elem PB.elem
@@ -3051,10 +3083,10 @@ struct Engine {
     int st = 0;
     // block regions through the local slot base, never through `this`
     auto lreg = [&](int b) -> Region {
-      return b < W.bv.nbb ? W.bv.bb[b].r : LA(const BlockMeta, bm)[b - W.bv.nbb].r;
+      return b < n_bb() ? bb_()[b].r : LA(const BlockMeta, bm)[b - n_bb()].r;
     };
     auto ltile = [&](int b) -> int {
-      return b < W.bv.nbb ? W.bv.bb[b].tile : LA(const BlockMeta, bm)[b - W.bv.nbb].tile;
+      return b < n_bb() ? bb_()[b].tile : LA(const BlockMeta, bm)[b - n_bb()].tile;
     };
     // leave the loop: state into W.L (uniform stores), then a cold request
     auto save = [&]() {
@@ -3696,7 +3728,7 @@ struct Engine {
     ntasks = n_bt();
     nblocks = n_bb();
     npart = 0;
-    nxp = 0;
+    SM().nxp = 0;
     makespan = 0.0;
     ahash = xhash = 0;
     if (n_bt() > 1) {  // the top op partitioned the root into tasks 1..n_bt()-1
@@ -3712,7 +3744,7 @@ struct Engine {
   }
 
   // One descriptor op in reference ids (partition_task / merge_cluster).
-  HXN void apply_ext(const hesp_op& o) {
+  HX void apply_ext(const hesp_op& o) {
     const BaseView& v = SM().bv;
     if (o.s == HESP_OP_MERGE) {
       if (o.task < v.off_c) return fail(ST_UNKNOWN_CLUSTER);  // merged with an earlier top cluster
@@ -3744,7 +3776,7 @@ struct Engine {
       h.ntasks = ntasks;
       h.nblocks = nblocks;
       h.npart = npart;
-      h.nxp = nxp;
+      h.nxp = SM().nxp;
       put_view(h);
       *hdr() = h;
     }
@@ -3778,7 +3810,7 @@ struct Engine {
     ntasks = th.ntasks;
     nblocks = th.nblocks;
     npart = th.npart;
-    nxp = th.nxp;
+    SM().nxp = th.nxp;
     makespan = 0.0;
     ahash = xhash = 0;
     NOUNROLL for (int k = 0; k < n_extra && !status; ++k) apply_ext(extra[k]);
@@ -3804,7 +3836,7 @@ struct Engine {
       h.sum_k = sum_k;
       h.n_leaves_out = n_out;
       h.npart = npart;
-      h.nxp = nxp;
+      h.nxp = SM().nxp;
       put_view(h);
       *hdr() = h;
     }
