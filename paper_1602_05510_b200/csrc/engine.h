@@ -338,6 +338,9 @@ struct Small {
   BaseView bv;  // the candidate's top-level tiling and reference-id offsets
   int32_t nxp;  // candidate intersection descriptors holding extra (non-Hasse) DataDag parent links
   int32_t nxp_pad;
+  double* vstage;  // the lean loop's valid-time table in shared memory (HESP_VSTAGE experiment), else null
+  double* vst_base;  // this warp's staging area and its capacity in doubles (set by sim_kernel)
+  int32_t vst_cap, vst_pad;
   LeanState L;
 };
 static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
@@ -381,7 +384,15 @@ struct Engine {
   HX int32_t* pmk() const { return (int32_t*)(slot + PB.lay.pmk); }
   HX BlockMeta* bm() const { return (BlockMeta*)(slot + PB.lay.bm); }
   HX uint32_t* bflags() const { return (uint32_t*)(slot + PB.lay.bflags); }
-  HX double* valid() const { return (double*)(slot + PB.lay.valid); }
+  HX double* valid() const {
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) {
+      double* vs = SM().vstage;  // SMEM-staging experiment (sim_kernel, HESP_VSTAGE > 0)
+      if (vs) return vs;
+    }
+#endif
+    return (double*)(slot + PB.lay.valid);
+  }
   HX double* lastu() const { return (double*)(slot + PB.lay.lastu); }
   HX double* pinu() const { return (double*)(slot + PB.lay.pinu); }
   HX int32_t* tl_head() const { return (int32_t*)(slot + PB.lay.tl_head); }
@@ -2267,6 +2278,12 @@ struct Engine {
   // (gather, eviction bookkeeping, coherence over subdivided tiles).
   HXN void simulate() {
     const int P = PB.P;
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) {
+      SM().vstage = nullptr;  // only sim_lean stages
+      wp.sync();
+    }
+#endif
     if (nleaves == 0) return fail(ST_VALIDATION);
     if (P < 1) return fail(ST_NO_PROCESSORS);
     // check_models (sim.cpp:312-321)
@@ -2973,6 +2990,12 @@ struct Engine {
     const int P = PB.P;
     Small& W = SM();
     const int nl = nleaves;
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) {  // SMEM-staging experiment: the valid-time table in shared memory when it fits
+      W.vstage = (W.vst_cap > 0 && nblocks * PB.S <= W.vst_cap) ? W.vst_base : nullptr;
+      wp.sync();
+    }
+#endif
     // init_memory (sim.cpp:323-339): every block valid in main at t=0
     NOUNROLL for (int x = wp.lane(); x < nblocks; x += WP::W) {
       NOUNROLL for (int q = 0; q < n_sp(); ++q) V(x, q) = q == msp() ? 0.0 : ABSENT;
@@ -3062,12 +3085,13 @@ struct Engine {
     const int P = PB.P;
     uint8_t* const sl = slot;
 #define LA(type, field) ((type*)(sl + PB.lay.field))
-#define LV(b, q) (LA(double, valid)[(b) * PB.S + (q)])
+#define LV(b, q) (vbase_[(b) * PB.S + (q)])
 #define LS PB.S
 #define LMS PB.main_space
 #define LPL (PB.ordering == ORD_PL)
     constexpr bool waits = (SELT == SEL_RP || SELT == SEL_FP);
     Small& W = SM();
+    double* const vbase_ = (WP::W > 1 && W.vstage) ? W.vstage : LA(double, valid);
     const int nl = nleaves;
     double tnow = W.L.tnow, mk = W.L.mk, pmin = W.L.pmin;
     int pool_n = W.L.pool_n, committed = W.L.committed, done = W.L.done, nr = W.L.nr;

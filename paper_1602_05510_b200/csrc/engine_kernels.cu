@@ -165,11 +165,15 @@ __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_BUILD_MIN_BLOCKS)
 __global__ void __launch_bounds__(WARPS_PER_BLOCK * 32, HESP_SIM_MIN_BLOCKS)
     sim_kernel(unsigned long long first_index, unsigned long long count, hesp_outcome* __restrict__ out,
                WarpBest* __restrict__ wbest, int accumulate, uint8_t* slots, unsigned long long* counter,
-               const uint32_t* __restrict__ order) {
+               const uint32_t* __restrict__ order, int vst_cap) {
+  extern __shared__ double g_vst[];  // SMEM-staging experiment (HESP_VSTAGE): vst_cap doubles per warp
   const int wib = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const long long gw = (long long)blockIdx.x * WARPS_PER_BLOCK + wib;
   const Problem& pb = c_problem;
+  g_small[wib].vst_base = g_vst + (size_t)wib * vst_cap;
+  g_small[wib].vst_cap = vst_cap;
+  __syncwarp();
   WarpBest b{0.0, -1, 0, 0, 0, 0, 0};
   if (accumulate) b = wbest[gw];
   for (;;) {
@@ -460,6 +464,7 @@ struct hesp_engine {
   size_t sort_tmp_bytes = 0;
   bool lpt = true;
   bool sim_thread = false;           // HESP_SIM_THREAD=1: thread-per-candidate simulate kernel
+  int vst_cap = 0;                   // HESP_VSTAGE=<bytes per warp>: valid times staged in shared memory (experiment)
   int n_simt_blocks = 0;
   int n_wbest = 0;                   // entries of d_wbest (max of both simulate grids, in warps)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -620,8 +625,9 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
       sim_thread_kernel<<<e->n_simt_blocks, SIMT_THREADS, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
                                                                    e->d_wbest, e->d_cslots, order);
     else
-      sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, 0, st>>>(first + c0, n, d_out ? d_out + c0 : nullptr,
-                                                                 e->d_wbest, acc, e->d_cslots, e->d_counter + 1, order);
+      sim_kernel<<<e->n_blocks, WARPS_PER_BLOCK * 32, (size_t)WARPS_PER_BLOCK * e->vst_cap * 8, st>>>(
+          first + c0, n, d_out ? d_out + c0 : nullptr, e->d_wbest, acc, e->d_cslots, e->d_counter + 1, order,
+          e->vst_cap);
     if (timed) cudaEventRecord(e->evc[ci][2], st);
     e->nev_used = ci + 1 < hesp_engine::NEV ? ci + 1 : hesp_engine::NEV;
     e->launches += 2;
@@ -753,7 +759,13 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     return fail(c, "stream");
   e->sm_count = prop.multiProcessorCount;
   int bps = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sim_kernel, WARPS_PER_BLOCK * 32, 0);
+  if (const char* v = getenv("HESP_VSTAGE")) {
+    e->vst_cap = std::max(0, atoi(v)) / 8;
+    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         WARPS_PER_BLOCK * e->vst_cap * 8);
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, sim_kernel, WARPS_PER_BLOCK * 32,
+                                                (size_t)WARPS_PER_BLOCK * e->vst_cap * 8);
   int bbps = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bbps, build_kernel, WARPS_PER_BLOCK * 32, 0);
   if (bbps < 1) bbps = 1;
