@@ -635,7 +635,9 @@ int launch_split(hesp_engine* e, const hesp_cand_desc* d_descs, uint64_t first, 
     if (count == 0) break;
   }
   cudaEventRecord(e->ev1, st);
-  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->n_wbest, e->d_best);
+  // only the entries this call's simulate grid wrote (the array is sized for
+  // the larger of the two grids)
+  reduce_best<<<1, 1024, 0, st>>>(e->d_wbest, e->sim_thread ? e->n_wbest : e->n_slots, e->d_best);
   e->launches += 1;
   if (!ck(cudaGetLastError(), "split launch")) return HESP_E_CUDA;
   return HESP_OK;
@@ -808,8 +810,8 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
   if ((c = cudaMalloc(&e->d_counter, 2 * sizeof(unsigned long long))) != cudaSuccess) return fail(c, "malloc");
   {
     e->split = true;
-    // Chunk = candidates whose slots are resident at once: up to 65536,
-    // bounded by ~35% of free device memory.
+    // Chunk = candidates whose slots are resident at once: up to 131072
+    // (HESP_CHUNK), bounded by 60% of free device memory (HESP_MEM_FRAC).
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const char* mf = getenv("HESP_MEM_FRAC");
