@@ -761,6 +761,23 @@ hesp_engine* hesp_engine_create(int device, const hesp_platform* platform, const
     return fail(c, "stream");
   e->sm_count = prop.multiProcessorCount;
   int bps = 0;
+  // A/B knob: the unified L1/SMEM split (percent of the maximum carveout)
+  {
+    // The simulate kernel needs ~50 KB of shared memory at 8 CTAs/SM; the
+    // driver's default split gives it a 100 KB carve-out.  The smallest split
+    // that holds it (64 KB) leaves 192 KB of L1 for the per-candidate state:
+    // L1 hit 71 % -> 79 %, +1-2 % (profiles/README.md).  Kept only when the
+    // occupancy stays the same.
+    int before = 0, after = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&before, sim_kernel, WARPS_PER_BLOCK * 32, 0);
+    const char* v = getenv("HESP_CARVEOUT_SIM");
+    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, v ? atoi(v) : 22);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&after, sim_kernel, WARPS_PER_BLOCK * 32, 0);
+    if (!v && after < before)
+      cudaFuncSetAttribute(sim_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, -1);  // driver default
+  }
+  if (const char* v = getenv("HESP_CARVEOUT_BUILD"))
+    cudaFuncSetAttribute(build_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
   if (const char* v = getenv("HESP_VSTAGE")) {
     e->vst_cap = std::max(0, atoi(v)) / 8;
     cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
