@@ -360,14 +360,18 @@ def main():
 
     # ---- e2e through the C ABI with host buffers (H2D descs, D2H outcomes) ----
     host_descs = [eng.generate_host(firsts[s], B) for s in range(args.warmup, nsteps)]
-    eng.eval_descs(host_descs[0], first=firsts[args.warmup])  # warm the pinned staging
+    for w in range(max(1, args.warmup)):  # warm the host path (pinned staging, page tables) like the device path
+        eng.eval_descs(host_descs[w % len(host_descs)], first=firsts[args.warmup + w % len(host_descs)])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    e2e_steps = []
     t0 = time.perf_counter()
     for i, s in enumerate(range(args.warmup, nsteps)):
+        ts = time.perf_counter()
         out, b = eng.eval_descs(host_descs[i], first=firsts[s])
         global_best(b)
+        e2e_steps.append(round(1e3 * (time.perf_counter() - ts), 2))
     e2e_s = time.perf_counter() - t0
     # descriptors travel packed (offsets + used ops); count what was copied
     h2d_bytes = int(eng.info().last_h2d_bytes)
@@ -402,7 +406,7 @@ def main():
             "config": config_block(args.config, p, world, B),
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": h2d_bytes,
-                    "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64},
+                    "d2h_bytes_per_step": B * OUTCOME_DTYPE.itemsize + 64, "step_ms": e2e_steps},
             "gpu_launches": int(launches),
             "roofline": rf,
             "hbm_roofline": hrf,

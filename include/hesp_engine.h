@@ -193,8 +193,10 @@ int hesp_generate_host(const hesp_engine* e, uint64_t first_index, uint64_t coun
 int hesp_generate_batch(const hesp_gen_config* gen, int32_t s_base_snapped, int32_t n_base, int64_t base_b,
                         uint64_t first_index, uint64_t count, hesp_cand_desc* descs);
 
-/* Per-task schedule of one candidate: for every task id < cap, proc/start/end
- * (proc = -1 for non-leaf or unscheduled ids).  Returns the outcome status. */
+/* Per-task schedule of one candidate: for every (reference) task id < cap,
+ * proc/start/end (proc = -1 for non-leaf, merged-away or unscheduled ids; ids
+ * keep counting across merges of the base cluster, so size cap by the ids the
+ * descriptor's ops consume).  Returns the outcome status. */
 int hesp_eval_detail(hesp_engine* e, const hesp_cand_desc* desc, int32_t cap, int32_t* proc,
                      double* start, double* end, hesp_outcome* out);
 
