@@ -352,6 +352,11 @@ static_assert(sizeof(Small) <= SMALL_BYTES, "slot reserve for Small");
 // its own per-CTA allocation.
 constexpr int SMALL_WARPS = 4;
 __shared__ Small g_small[SMALL_WARPS];
+// The candidate's top-level tiling view and link counter, apart from Small so
+// the build kernels (which need only these) do not carve Small's ~1 KB per
+// warp of event-loop state out of their L1.
+__shared__ BaseView g_bview[SMALL_WARPS];
+__shared__ int32_t g_nxp[SMALL_WARPS];
 #endif
 
 // ---------------------------------------------------------------------------
@@ -424,32 +429,32 @@ struct Engine {
   // read from the problem (constant memory), never from `this` (the engine
   // object lives in local memory on the device)
   HX int n_bt() const {
-    return SM().bv.nbt;
+    return BV().nbt;
   }
   HX int n_bb() const {
-    return SM().bv.nbb;
+    return BV().nbb;
   }
   HX const TaskMeta* bt_() const {
-    return SM().bv.bt;
+    return BV().bt;
   }
   HX const BlockMeta* bb_() const {
-    return SM().bv.bb;
+    return BV().bb;
   }
   HX const BasePreds* bp_() const {
-    return SM().bv.bp;
+    return BV().bp;
   }
   HX const int32_t* bpl_() const {
-    return SM().bv.bpl;
+    return BV().bpl;
   }
   HX long long base_b_() const {
-    return SM().bv.base_b;
+    return BV().base_b;
   }
   // reference ids of internal task / block ids (BaseView)
   HX int xtask(int j) const {
-    return j ? j + SM().bv.off_t : 0;
+    return j ? j + BV().off_t : 0;
   }
   HX int xblock(int b) const {
-    return b ? b + SM().bv.off_b : 0;
+    return b ? b + BV().off_b : 0;
   }
   HX int n_sp() const { return PB.S; }
   HX int msp() const { return PB.main_space; }
@@ -547,6 +552,18 @@ struct Engine {
     if constexpr (WP::W > 1) return g_small[threadIdx.x >> 5];
 #endif
     return *sm;
+  }
+  HX BaseView& BV() const {
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) return g_bview[threadIdx.x >> 5];
+#endif
+    return sm->bv;
+  }
+  HX int32_t& NXP() const {
+#if defined(__CUDACC__)
+    if constexpr (WP::W > 1) return g_nxp[threadIdx.x >> 5];
+#endif
+    return sm->nxp;
   }
 
   // ---- overlay accessors (base graph shared, candidate deltas private) ----
@@ -655,7 +672,7 @@ struct Engine {
     }
     wp.sync();
 #if HESP_XPAR
-    if (t >= 0 && SM().nxp > 0) xpar_on_create(id, t);  // (shared memory: no local-memory load per block)
+    if (t >= 0 && NXP() > 0) xpar_on_create(id, t);  // (shared memory: no local-memory load per block)
 #endif
     return id;
   }
@@ -712,7 +729,7 @@ struct Engine {
       const int e = XP(b, k);
       if (e == v) return true;
       if (e < 0) {
-        if (k == 0) ++SM().nxp;
+        if (k == 0) ++NXP();
         XP(b, k) = v;
         return true;
       }
@@ -747,7 +764,7 @@ struct Engine {
           }
           if (!maximal) continue;
           NOUNROLL for (int k = 0; k < np; ++k) xpar_remove(i, par[k]);
-          if (XP(i, 0) < 0) --SM().nxp;
+          if (XP(i, 0) < 0) --NXP();
         }
       }
     }
@@ -847,7 +864,7 @@ struct Engine {
             }
             fail(leaf_ref ? ST_FOREIGN : ST_ENGINE_LIMIT);
           }
-          if (XP(i, 0) >= 0) --SM().nxp;
+          if (XP(i, 0) >= 0) --NXP();
           NOUNROLL for (int k = 0; k < XPAR; ++k) XP(i, k) = -1;
           o.r.row = -1;
           o.r.col = -1;
@@ -1022,7 +1039,7 @@ struct Engine {
       // (its members are leaves), so the prune leaves the root alone -- the
       // unpartitioned root, with every id consumed so far staying consumed.
       if (pe.task != 0 || pe.child0 != 1) return fail(ST_INTERNAL);
-      const BaseView& v = SM().bv;
+      const BaseView& v = BV();
       const int nt = ntasks + v.off_t, nb = nblocks + v.off_b, nc = npart + v.off_c;
       reset_to_base(TIL_ROOT, nt - 1, nb - 1, nc);
       return;
@@ -1069,7 +1086,7 @@ struct Engine {
       NOUNROLL for (int i = 0; i < PB.n_til; ++i)
         if (i != TIL_ROOT && PB.til[i].s == s) k = i;
       if (k < 0) return fail(ST_ENGINE_LIMIT);  // a tiling larger than the slot holds
-      const BaseView v = SM().bv;
+      const BaseView v = BV();
       reset_to_base(k, v.off_t, v.off_b, v.off_c);
       return;
     }
@@ -2300,7 +2317,7 @@ struct Engine {
       NOUNROLL for (int x = 1 + wp.lane(); x < nblocks; x += WP::W) nonroot += bbytes(x);
       nonroot = wp.suml(nonroot);
       bool ok = true;
-      const bool root_leaf = SM().bv.til == TIL_ROOT;  // the root task itself is scheduled: its block goes anywhere
+      const bool root_leaf = BV().til == TIL_ROOT;  // the root task itself is scheduled: its block goes anywhere
       NOUNROLL for (int q = 0; q < n_sp(); ++q)
         if (nonroot + ((q == msp() || root_leaf) ? bbytes(0) : 0) > PB.cap[q]) ok = false;
       fast = ok && (!TRACE || (tb && tb->lite));  // the full trace keeps residency bookkeeping
@@ -3724,7 +3741,7 @@ struct Engine {
   // The warp's view of top-level tiling `til` with reference-id offsets.
   HX void set_view(int til, int off_t, int off_b, int off_c) {
     const BaseTiling& T = PB.til[til];
-    BaseView& v = SM().bv;
+    BaseView& v = BV();
     v.nbt = T.n_tasks;
     v.nbb = T.n_blocks;
     v.til = til;
@@ -3752,7 +3769,7 @@ struct Engine {
     ntasks = n_bt();
     nblocks = n_bb();
     npart = 0;
-    SM().nxp = 0;
+    NXP() = 0;
     makespan = 0.0;
     ahash = xhash = 0;
     if (n_bt() > 1) {  // the top op partitioned the root into tasks 1..n_bt()-1
@@ -3769,7 +3786,7 @@ struct Engine {
 
   // One descriptor op in reference ids (partition_task / merge_cluster).
   HX void apply_ext(const hesp_op& o) {
-    const BaseView& v = SM().bv;
+    const BaseView& v = BV();
     if (o.s == HESP_OP_MERGE) {
       if (o.task < v.off_c) return fail(ST_UNKNOWN_CLUSTER);  // merged with an earlier top cluster
       return apply_merge(o.task - v.off_c);
@@ -3800,14 +3817,14 @@ struct Engine {
       h.ntasks = ntasks;
       h.nblocks = nblocks;
       h.npart = npart;
-      h.nxp = SM().nxp;
+      h.nxp = NXP();
       put_view(h);
       *hdr() = h;
     }
     wp.sync();
   }
   HX void put_view(SlotHeader& h) const {
-    const BaseView& v = SM().bv;
+    const BaseView& v = BV();
     h.til = v.til;
     h.off_t = v.off_t;
     h.off_b = v.off_b;
@@ -3834,7 +3851,7 @@ struct Engine {
     ntasks = th.ntasks;
     nblocks = th.nblocks;
     npart = th.npart;
-    SM().nxp = th.nxp;
+    NXP() = th.nxp;
     makespan = 0.0;
     ahash = xhash = 0;
     NOUNROLL for (int k = 0; k < n_extra && !status; ++k) apply_ext(extra[k]);
@@ -3860,7 +3877,7 @@ struct Engine {
       h.sum_k = sum_k;
       h.n_leaves_out = n_out;
       h.npart = npart;
-      h.nxp = SM().nxp;
+      h.nxp = NXP();
       put_view(h);
       *hdr() = h;
     }
@@ -3936,9 +3953,9 @@ struct Engine {
     if (ntasks <= tb->task_cap)
       NOUNROLL for (int j = wp.lane(); j < ntasks; j += WP::W) tb->tmeta[j] = task(j);
     if (wp.lane() == 0) {
-      tb->off_t = SM().bv.off_t;
-      tb->off_b = SM().bv.off_b;
-      tb->off_c = SM().bv.off_c;
+      tb->off_t = BV().off_t;
+      tb->off_b = BV().off_b;
+      tb->off_c = BV().off_c;
       tb->nleaves = nl;
       tb->npreds = np;
       tb->nblocks = nb;
