@@ -257,6 +257,9 @@ HX uint64_t dbits(double x) {
 #ifndef HESP_PREFETCH
 #define HESP_PREFETCH 0
 #endif
+#ifndef HESP_MATCH_DEDUP
+#define HESP_MATCH_DEDUP 1
+#endif
 #ifndef HESP_XPAR  // A/B only: 0 drops the intersection-link emulation (E7)
 #define HESP_XPAR 1
 #endif
@@ -1652,6 +1655,22 @@ struct Engine {
       }
       // dedup -> preds arena
       int m = 0;
+#if defined(__CUDACC__)
+      if (WP::W > 1 && HESP_MATCH_DEDUP && npb <= WP::W) {
+        // one round, no memory atomics: a candidate is kept by the lowest
+        // lane holding its value (first occurrence, the same order as below)
+        const int q = wp.lane();
+        const int v = q < npb ? pbuf()[q] : -1 - q;  // distinct fillers
+        const unsigned same = __match_any_sync(0xffffffffu, v);
+        const bool keep = q < npb && (same & ((1u << q) - 1u)) == 0u;
+        const unsigned mk = wp.ballot(keep);
+        if (keep) {
+          const int at = nedges + popc32(mk & wp.lt());
+          if (at < PB.maxedges) preds()[at] = v;
+        }
+        m = popc32(mk);
+      } else
+#endif
       NOUNROLL for (int base = 0; base < npb; base += WP::W) {
         const int q = base + wp.lane();
         bool keep = false;
