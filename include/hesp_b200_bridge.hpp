@@ -328,14 +328,18 @@ class BatchSimulator {
         recheck = true;
       }
     }
-    if (recheck && best) {  // the winner among the graphs that stand
-      *best = hesp_best{};
+    if (recheck && best) {  // the winner (and the valid count) among the graphs that stand
+      best->makespan = 0.0;
       best->index = -1;
-      for (std::size_t k = 0; k < out.size(); ++k)
-        if (out[k].status == 0 && (best->index < 0 || out[k].makespan < best->makespan)) {
+      best->n_ok = 0;
+      for (std::size_t k = 0; k < out.size(); ++k) {
+        if (out[k].status != 0) continue;
+        ++best->n_ok;
+        if (best->index < 0 || out[k].makespan < best->makespan) {
           best->makespan = out[k].makespan;
           best->index = (std::int64_t)k;
         }
+      }
     }
     return out;
   }
