@@ -12,6 +12,6 @@ print(' '.join(harness_args(p, FIXTURES)))")
   oracle/_ref/ref_harness $args --first $2 --count $3 --threads $(nproc) --out build/validation/$1_$2_$3.bin
 }
 run C2 1000000 100000
-run C4 1000 5000
+run C4 1000 600
 run merge_sect 10000 20000
 run C3 1000000 50000
