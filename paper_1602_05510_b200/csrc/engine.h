@@ -248,14 +248,9 @@ HX uint64_t dbits(double x) {
   return u;
 }
 
-// A/B switches (-D at build time): 16-byte record loads in the lean loop;
-// prefetching of the records the loop will touch next (1: the epoch's ready
-// tasks, 2: + the current task's successors).
+// A/B switches (-D at build time): 16-byte record loads in the lean loop.
 #ifndef HESP_VEC_LOADS
 #define HESP_VEC_LOADS 1
-#endif
-#ifndef HESP_PREFETCH
-#define HESP_PREFETCH 0
 #endif
 #ifndef HESP_MATCH_DEDUP
 #define HESP_MATCH_DEDUP 1
@@ -284,13 +279,6 @@ HX uint64_t dbits(double x) {
 #else
 #define HASH_FOLD(acc, t) ((acc) += (t))
 #endif
-HX void prefetch_l1(const void* p) {
-#if defined(__CUDACC__)
-  asm volatile("prefetch.L1 [%0];" ::"l"(p));
-#else
-  (void)p;
-#endif
-}
 
 // 32-byte records in two 16-byte loads (the generic path otherwise splits
 // them field by field).
@@ -3319,10 +3307,6 @@ struct Engine {
           NOUNROLL for (int k = wp.lane(); k < nr; k += WP::W) {
             const int a = LA(const int, gs_a)[k];
             const double ka = LA(const double, ready_key)[k];
-            if (HESP_PREFETCH >= 1) {  // the epoch's tasks: their records load in parallel, not one by one
-              prefetch_l1(LA(const STask, wsb) + a);
-              prefetch_l1(LA(const TState, ts) + a);
-            }
             int rank = 0;
             NOUNROLL for (int q = 0; q < nr; ++q) {
               const int c = LA(const int, gs_a)[q];
@@ -3338,8 +3322,6 @@ struct Engine {
       const int j = LA(const int, ready)[done];
       const STask tk = ld_stask(LA(const STask, wsb) + j);
       const TState tj = ld_tstate(LA(const TState, ts) + j);  // j's own record: no commit writes it before j's release
-      if (HESP_PREFETCH >= 2 && phase == 0 && wp.lane() < tj.scnt)  // successors' records, ahead of the release
-        prefetch_l1(LA(const TState, ts) + LA(const int, succs)[tj.soff + wp.lane()]);
       const int tkind = tk.kb & 0xff, tbidx = tk.kb >> 8;
       const int nw = tk.nw;
       const long long tbytes = (long long)tk.b * tk.b * PB.elem;  // every block of a task has its side
