@@ -25,6 +25,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.h"
@@ -37,6 +38,34 @@ using namespace hx;
 namespace {
 
 thread_local std::string g_last_error;
+
+// Host threads for the per-candidate host loops of the end-to-end path
+// (descriptor packing, outcome copy-out): one below 16k candidates, else up
+// to 8 (HESP_HOST_THREADS overrides).
+int host_threads(uint64_t count) {
+  int n = 1;
+  if (count >= 16384) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    n = (int)std::min<unsigned>(8u, hc > 1 ? hc : 1u);
+  }
+  if (const char* v = getenv("HESP_HOST_THREADS")) n = std::max(1, atoi(v));
+  return n;
+}
+
+// fn(t, a, b) over nthr contiguous ranges [a, b) of [0, count); range 0 on the caller.
+template <class F>
+void host_ranges(uint64_t count, int nthr, F&& fn) {
+  auto lo = [&](int t) { return count * (uint64_t)t / (uint64_t)nthr; };
+  if (nthr <= 1) {
+    fn(0, 0, count);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nthr - 1);
+  for (int t = 1; t < nthr; ++t) th.emplace_back([&, t] { fn(t, lo(t), lo(t + 1)); });
+  fn(0, lo(0), lo(1));
+  for (auto& x : th) x.join();
+}
 
 struct WarpBest {
   double makespan;
@@ -939,16 +968,33 @@ int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
   if (!grow_out(e, count) || !grow_host(e, count)) return HESP_E_CUDA;
   // pack into the pinned staging buffer: offsets[count + 1], then the used ops
   // (always fits: 4 (count + 1) + 8 * sum(n_ops) <= 520 * count)
+  // (host threads over index ranges: a count pass, a scan of the per-range
+  // totals, then each range writes its offsets and ops -- the same bytes as
+  // one serial pass; it is host time inside every end-to-end call)
   uint32_t* hoff = reinterpret_cast<uint32_t*>(e->h_descs);
   hesp_op* hops = reinterpret_cast<hesp_op*>(reinterpret_cast<uint8_t*>(e->h_descs) + ((4 * (count + 1) + 7) & ~7ULL));
-  uint32_t tot = 0;
-  for (uint64_t i = 0; i < count; ++i) {
-    hoff[i] = tot;
-    int n = descs[i].n_ops;
-    n = n < 0 ? 0 : (n > HESP_MAX_OPS ? HESP_MAX_OPS : n);
-    std::memcpy(hops + tot, descs[i].ops, (size_t)n * sizeof(hesp_op));
-    tot += (uint32_t)n;
-  }
+  auto nops = [&](uint64_t i) {
+    const int n = descs[i].n_ops;
+    return (uint32_t)(n < 0 ? 0 : (n > HESP_MAX_OPS ? HESP_MAX_OPS : n));
+  };
+  const int nthr = host_threads(count);
+  std::vector<uint32_t> part(nthr + 1, 0);
+  host_ranges(count, nthr, [&](int t, uint64_t a, uint64_t b) {
+    uint32_t s = 0;
+    for (uint64_t i = a; i < b; ++i) s += nops(i);
+    part[t + 1] = s;
+  });
+  for (int t = 0; t < nthr; ++t) part[t + 1] += part[t];
+  host_ranges(count, nthr, [&](int t, uint64_t a, uint64_t b) {
+    uint32_t tot = part[t];
+    for (uint64_t i = a; i < b; ++i) {
+      hoff[i] = tot;
+      const uint32_t n = nops(i);
+      std::memcpy(hops + tot, descs[i].ops, (size_t)n * sizeof(hesp_op));
+      tot += n;
+    }
+  });
+  const uint32_t tot = part[nthr];
   hoff[count] = tot;
   const size_t ops_at = (4 * (count + 1) + 7) & ~7ULL;
   const size_t bytes = ops_at + (size_t)tot * sizeof(hesp_op);
@@ -976,7 +1022,10 @@ int hesp_eval_descs(hesp_engine* e, const hesp_cand_desc* descs, uint64_t count,
   r = finish_best(e, best, e->stream);
   if (r) return r;
   if (!ck(cudaStreamSynchronize(e->stream), "sync")) return HESP_E_CUDA;
-  if (out) std::memcpy(out, e->h_out, count * sizeof(hesp_outcome));
+  if (out)
+    host_ranges(count, nthr, [&](int, uint64_t a, uint64_t b) {
+      std::memcpy(out + a, e->h_out + a, (b - a) * sizeof(hesp_outcome));
+    });
   return HESP_OK;
 }
 
