@@ -47,6 +47,9 @@ namespace hx {
 struct int4 {
   int x, y, z, w;
 };
+struct int2 {
+  int x, y;
+};
 #endif
 
 #if defined(__CUDACC__)
@@ -410,6 +413,10 @@ struct Engine {
   HX double* ready_key() const { return (double*)(slot + PB.lay.ready_key); }
   HX int32_t* ready() const { return (int32_t*)(slot + PB.lay.ready); }
   HX int32_t* pbuf() const { return (int32_t*)(slot + PB.lay.pbuf); }
+  // build_deps' per-task access records (4 x int2 per task id), over the
+  // simulate-only pool/ready arrays (written only once the event loop starts;
+  // slot_layout checks the span)
+  HX int2* dacc() const { return (int2*)(slot + PB.lay.pool); }
   HX int32_t* gs_a() const { return (int32_t*)(slot + PB.lay.gs_a); }
   HX int32_t* gs_b() const { return (int32_t*)(slot + PB.lay.gs_b); }
   HX Region* gs_reg() const { return (Region*)(slot + PB.lay.gs_reg); }
@@ -1541,6 +1548,41 @@ struct Engine {
           t_poff()[j] = ~bp.uoff;
           t_pcnt()[j] = bp.ucnt;
           ts()[j].missing = bp.ucnt;
+        } else {
+          // the serial pass's per-access facts, resolved here in parallel:
+          // distinct blocks (read-only ones in read order, then the write),
+          // each either a base contribution (x = -1 - slot, E5) or its cell
+          // rectangle (x = first cell, y = w | rows << 11 | row stride << 22);
+          // nacc = 0 leaves the task to the serial pass's own derivation
+          const int wb = t.blk[t.nrd];
+          int2* rec = dacc() + 4 * j;
+          int na = 0;
+          bool packed = true;
+          NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
+            const int b = t.blk[k];
+            if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
+            bool dup = false;
+            NOUNROLL for (int q = 0; q < k; ++q)
+              if (t.blk[q] == b && q < t.nrd) dup = true;
+            if (dup && k < t.nrd) continue;
+            int2 r;
+            if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
+              r.x = -1 - na;
+              r.y = 0;
+            } else {
+              int tt, r0, r1, c0, c1;
+              cell_range(b, tt, r0, r1, c0, c1);
+              const int nc = tl_ncb()[tt] - 1;
+              const int w = c1 - c0, rows = r1 - r0;
+              if (w >= 2048 || rows >= 2048 || nc >= 1024) packed = false;
+              r.x = tl_coff()[tt] + r0 * nc + c0;
+              r.y = w | (rows << 11) | (nc << 22);
+            }
+            if (na < 4) rec[na] = r;
+            ++na;
+          }
+          if (na > 4) packed = false;
+          j |= (packed ? na : 0) << 28;
         }
         isslow = !fastj;
       }
@@ -1552,24 +1594,57 @@ struct Engine {
     sum_k = wp.sumi(sum_k);
     // ---- pass A (serial in program order): cell tracking for the slow leaves
     NOUNROLL for (int si = 0; si < nslow && !status; ++si) {
-      const int j = slow[si];
-      const TaskMeta t = task(j);
-      const int wb = t.blk[t.nrd];
+      const int j = slow[si] & 0x0fffffff;
+      const int nacc = (int)((unsigned)slow[si] >> 28);
+      const int2* rec = dacc() + 4 * j;
+      TaskMeta t;
+      int nsteps;
+      if (nacc) {
+        nsteps = nacc;
+      } else {
+        t = task(j);
+        nsteps = t.nrd + 1;
+      }
       int npb = 0;
       int slot = 0;
       // distinct blocks, read-only ones first in read order, then the write
-      NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
-        const int b = t.blk[k];
-        if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
-        bool dup = false;
-        NOUNROLL for (int q = 0; q < k; ++q)
-          if (t.blk[q] == b && q < t.nrd) dup = true;
-        if (dup && k < t.nrd) continue;
-        const bool writes = (k == t.nrd);
-        const int myslot = slot++;
-        if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
+      NOUNROLL for (int k = 0; k < nsteps; ++k) {
+        bool writes;
+        int2 r;
+        int w, nc, rows;
+        if (nacc) {
+          r = rec[k];
+          writes = k == nacc - 1;
+          w = r.y & 2047;
+          rows = (r.y >> 11) & 2047;
+          nc = (int)((unsigned)r.y >> 22);
+        } else {
+          const int wb = t.blk[t.nrd];
+          const int b = t.blk[k];
+          if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
+          bool dup = false;
+          NOUNROLL for (int q = 0; q < k; ++q)
+            if (t.blk[q] == b && q < t.nrd) dup = true;
+          if (dup && k < t.nrd) continue;
+          writes = (k == t.nrd);
+          if (j < n_bt() && tl_cnt()[tile_of(b)] == 0) {
+            r.x = -1 - slot;
+            r.y = 0;
+          } else {
+            int tt, r0, r1, c0, c1;
+            cell_range(b, tt, r0, r1, c0, c1);
+            nc = tl_ncb()[tt] - 1;
+            r.x = tl_coff()[tt] + r0 * nc + c0;
+            r.y = 0;
+            rows = r1 - r0;
+            w = c1 - c0;
+          }
+        }
+        ++slot;
+        if (r.x < 0) {
           // unsubdivided tile of a base task: its base contribution (E5)
           const BasePreds& bp = bp_()[j];
+          const int myslot = -1 - r.x;
           const int off = bp.soff[myslot], cnt = bp.scnt[myslot];
           NOUNROLL for (int q = wp.lane(); q < cnt; q += WP::W)
             if (npb + q < PB.maxpb) pbuf()[npb + q] = bpl_()[off + q];
@@ -1578,12 +1653,8 @@ struct Engine {
           if (npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
           continue;
         }
-        int tt, r0, r1, c0, c1;
-        cell_range(b, tt, r0, r1, c0, c1);
-        const int nc = tl_ncb()[tt] - 1;
-        const int w = c1 - c0;
-        const int ncells = (r1 - r0) * w;
-        const int cbase = tl_coff()[tt];
+        const int ncells = rows * w;
+        const int cfirst = r.x;
         const float rw = 1.0f / (float)w;  // q / w via a corrected float reciprocal (q < 2^20)
         NOUNROLL for (int base = 0; base < ncells; base += WP::W) {
           const int q = base + wp.lane();
@@ -1592,7 +1663,7 @@ struct Engine {
             int rq = (int)((float)q * rw);
             if (rq * w > q) --rq;
             else if ((rq + 1) * w <= q) ++rq;
-            cell = cbase + (r0 + rq) * nc + (c0 + (q - rq * w));
+            cell = cfirst + rq * nc + (q - rq * w);
           }
           // last writer
           int wr = cell >= 0 ? c_writer()[cell] : -1;

@@ -296,6 +296,8 @@ inline SlotLayout slot_layout(const Problem& p) {
   L.rnode = take(8 * (size_t)p.maxrn);
   L.preds = take(4 * (size_t)p.maxedges);
   L.succs = take(4 * (size_t)p.maxedges);
+  // pool .. ready_key stay back to back: build_deps keeps 4 int2 access
+  // records per task over their 4+8+8+4+8 = 32 bytes per task (Engine::dacc)
   L.pool = take(4 * T);
   L.pool_rel = take(8 * T);
   L.pool_key = take(8 * T);
