@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhesp_b200.so")
 
-SOURCES = ["engine_kernels.cu", "verify.cu", "problem.cpp", "trace.cpp", "solver.cpp", "loaders.cpp"]
+SOURCES = ["engine_kernels.cu", "verify.cu", "loadtrace.cu", "problem.cpp", "trace.cpp", "solver.cpp", "loaders.cpp"]
 HEADERS = ["engine.h", "engine_types.h", "problem.h", "trace.h"]
 
 

@@ -484,6 +484,8 @@ struct hesp_engine {
   hesp_neighbor* d_nbrs = nullptr;
   size_t nbr_cap = 0;
   uint8_t* d_pack = nullptr;         // packed host descriptors (hesp_eval_descs)
+  void* d_lt = nullptr;              // load post-pass scratch (loadtrace.cu)
+  size_t lt_cap = 0;
   size_t pack_cap = 0;
   size_t last_h2d_bytes = 0;
   hesp_cand_desc* d_gen = nullptr;   // generated descriptors of one chunk (LPT on generated batches)
@@ -707,6 +709,23 @@ bool dalloc(T** p, size_t n, std::vector<void*>& owned) {
   owned.push_back(*p);
   return true;
 }
+
+// Load post-passes of B traces (by-task-id arrays of nid entries each) on the
+// engine's stream, into logs[b] (null entries skipped).
+int load_traces(hesp_engine* e, const int32_t* proc, const double* start, const double* end, int nid, int B,
+                std::vector<hx::TraceLogs*>& logs) {
+  const size_t need = hx::load_trace_scratch_bytes(nid, B);
+  if (need > e->lt_cap) {
+    if (e->d_lt) cudaFree(e->d_lt);
+    e->d_lt = nullptr;
+    e->lt_cap = 0;
+    if (!ck(cudaMalloc(&e->d_lt, need), "malloc load-trace scratch")) return HESP_E_CUDA;
+    e->lt_cap = need;
+  }
+  const int r = hx::load_trace_device(proc, start, end, nid, B, e->hp.p.P, e->d_lt, e->stream, logs);
+  if (r != HESP_OK) g_last_error = "load-trace post-pass failed";
+  return r;
+}
 template <class T>
 bool d2h(std::vector<T>& v, const T* d, size_t n) {
   v.resize(n);
@@ -895,6 +914,7 @@ void hesp_engine_destroy(hesp_engine* e) {
   cudaFree(e->d_cslots);
   cudaFree(e->d_order);
   cudaFree(e->d_pack);
+  cudaFree(e->d_lt);
   cudaFree(e->d_tslots);
   cudaFree(e->d_nbrs);
   cudaFree(e->d_sort_tmp);
@@ -1228,6 +1248,11 @@ int hesp_eval_trace(hesp_engine* e, const hesp_cand_desc* desc, hesp_trace* tr) 
          d2h(g.tmeta, tb.tmeta, (size_t)hb.ntasks);
     if (ok) hx::to_reference_ids(g, &logs, hb.off_t, hb.off_b, hb.off_c);
     g.valid = ok;
+    if (ok) {
+      std::vector<hx::TraceLogs*> one{&logs};
+      const int r = load_traces(e, dp, ds, de, 2 * T, 1, one);
+      if (r != HESP_OK) return r;
+    }
   }
   if (!ok) return o.status ? o.status : HESP_E_CUDA;
   tr->outcome = o;
@@ -1337,6 +1362,13 @@ int hx::schedule_batch(hesp_engine* e, const hesp_cand_desc* descs, int B, std::
     if (!ok) return HESP_E_CUDA;
     hx::to_reference_ids(g, nullptr, hb[b].off_t, hb[b].off_b, hb[b].off_c);
     g.valid = true;
+  }
+  {
+    std::vector<hx::TraceLogs*> lp(B, nullptr);
+    for (int b = 0; b < B; ++b)
+      if (outs[b].status == 0) lp[b] = &logs[b];
+    const int r = load_traces(e, e->d_sproc, e->d_sstart, e->d_send, (int)TX, B, lp);
+    if (r != HESP_OK) return r;
   }
   return HESP_OK;
 }

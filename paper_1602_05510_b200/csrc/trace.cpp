@@ -1,13 +1,13 @@
 // trace.cpp — host post-passes of the full-trace path (see trace.h).
 //
 // The schedule itself comes from the device (Engine<DevWarp, true>); this
-// file only reproduces what the reference does with its SimResult after the
-// event loop, in the same IEEE operation order:
+// file only orders the device logs the way the reference orders its
+// SimResult after the event loop:
 //   ordering of events / residency log / transfers   sim.cpp:813-831
-//   compute_idle_avgs                                sim.cpp:670-702
-//   busy_time, avg_load, LoadTrace::integral         sim.cpp:71-87
-//   compute_load_trace                               sim.cpp:975-991
-// verify_schedule (sim.cpp:857-973) runs on the device: verify.cu.
+// The load post-passes (compute_idle_avgs sim.cpp:670-702, busy_time /
+// LoadTrace::integral sim.cpp:71-87, compute_load_trace sim.cpp:975-991) run
+// on the device (loadtrace.cu); verify_schedule (sim.cpp:857-973) too
+// (verify.cu).
 #include "trace.h"
 
 #include <algorithm>
@@ -39,18 +39,6 @@ void hop_link(const Problem& p, int src, int dst, int h, int32_t* hs, int32_t* h
   const int l = p.route_l[src * MAXS + dst][h];
   *hs = p.link_src[l];
   *hd = p.link_dst[l];
-}
-
-// (start, +1) / (end, -1) deltas of the assignments, sorted (sim.cpp:672-677, 977-982)
-std::vector<std::pair<double, int>> deltas_of(const hesp_trace& tr) {
-  std::vector<std::pair<double, int>> d;
-  d.reserve(2 * (size_t)tr.n_assign);
-  for (int i = 0; i < tr.n_assign; ++i) {
-    d.push_back({tr.assignments[i].start, +1});
-    d.push_back({tr.assignments[i].end, -1});
-  }
-  std::sort(d.begin(), d.end());
-  return d;
 }
 
 }  // namespace
@@ -227,49 +215,20 @@ int finish_trace(const Problem& p, const TraceGraph& g, const TraceLogs& logs, h
     });
     for (size_t i = 0; i < ev.size(); ++i) tr->events[i] = ev[i].e;
   }
-  // compute_idle_avgs (sim.cpp:670-702)
-  const int P = p.P;
-  const auto d = deltas_of(*tr);
-  std::vector<double> times;
-  std::vector<int> active;
-  {
-    int cur = 0;
-    for (size_t i = 0; i < d.size();) {
-      const double t = d[i].first;
-      while (i < d.size() && d[i].first == t) cur += d[i++].second;
-      times.push_back(t);
-      active.push_back(cur);
-    }
-  }
-  std::vector<double> cum(times.size(), 0.0);
-  for (size_t i = 1; i < times.size(); ++i) cum[i] = cum[i - 1] + (P - active[i - 1]) * (times[i] - times[i - 1]);
-  auto idle_up_to = [&](double t) {
-    auto it = std::upper_bound(times.begin(), times.end(), t);
-    if (it == times.begin()) return 0.0;
-    const size_t k = (size_t)(it - times.begin()) - 1;
-    return cum[k] + (P - active[k]) * (t - times[k]);
-  };
-  for (int i = 0; i < na; ++i) {
-    hesp_assignment& a = tr->assignments[i];
-    const double dur = a.end - a.start;
-    a.idle_avg = dur > 0 ? (idle_up_to(a.end) - idle_up_to(a.start)) / dur : 0.0;
-  }
-  // compute_load_trace (sim.cpp:975-991): same grouping as above
-  tr->n_steps = (int32_t)times.size();
-  for (size_t i = 0; i < times.size(); ++i) {
-    tr->steps[i].time = times[i];
-    tr->steps[i].active = active[i];
+  // load post-passes: computed on the device (loadtrace.cu)
+  if (!logs.has_load || logs.idle.size() < logs.proc.size()) return HESP_E_INVALID;
+  for (int i = 0; i < na; ++i) tr->assignments[i].idle_avg = logs.idle[tr->assignments[i].task];
+  tr->n_steps = (int32_t)logs.steps_time.size();
+  for (size_t i = 0; i < logs.steps_time.size(); ++i) {
+    tr->steps[i].time = logs.steps_time[i];
+    tr->steps[i].active = logs.steps_active[i];
     tr->steps[i].pad = 0;
   }
-  // SimResult::busy_time / avg_load, LoadTrace::integral (sim.cpp:71-87)
-  double busy = 0;
-  for (int i = 0; i < na; ++i) busy += tr->assignments[i].end - tr->assignments[i].start;
-  tr->busy_time = busy;
+  tr->busy_time = logs.busy;
   const double mk = tr->outcome.makespan;
-  tr->avg_load = (mk <= 0 || P < 1) ? 0.0 : busy / (P * mk);
-  double integral = 0;
-  for (size_t i = 0; i + 1 < times.size(); ++i) integral += active[i] * (times[i + 1] - times[i]);
-  tr->load_integral = integral;
+  const int P = p.P;
+  tr->avg_load = (mk <= 0 || P < 1) ? 0.0 : logs.busy / (P * mk);  // SimResult::avg_load (sim.cpp:78-87)
+  tr->load_integral = logs.integral;
   return HESP_OK;
 }
 

@@ -31,7 +31,23 @@ struct TraceLogs {
   std::vector<double> start, end;
   std::vector<XferLog> xfers;  // emission order
   std::vector<ResLog> res;     // emission order (ties are identical records)
+  // load post-passes computed on the device (load_trace_device)
+  bool has_load = false;
+  std::vector<double> idle;  // idle_avg by task id
+  std::vector<double> steps_time;
+  std::vector<int32_t> steps_active;
+  double busy = 0.0, integral = 0.0;
 };
+
+// Load post-passes (compute_idle_avgs, compute_load_trace, busy_time,
+// LoadTrace::integral) of B traces on the device (loadtrace.cu): one CTA per
+// trace over (proc, start, end) by task id (nid ids per trace, trace b at
+// offset b * nid), scratch of load_trace_scratch_bytes(nid, B) device bytes;
+// fills out[b] (skipped when null).  HESP_OK, HESP_E_CUDA or HESP_E_LIMIT.
+constexpr size_t LOAD_TRACE_SMEM = 160 * 1024;  // sort keys in shared memory up to this size
+size_t load_trace_scratch_bytes(int nid, int B);
+int load_trace_device(const int32_t* proc, const double* start, const double* end, int nid, int B, int P,
+                      void* scratch, cudaStream_t st, std::vector<TraceLogs*>& out);
 
 // Rewrites an exported graph (and the logs' block ids) from the engine's
 // internal ids to reference ids (BaseView offsets; identity when all are 0).
