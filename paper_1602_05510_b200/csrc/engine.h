@@ -40,6 +40,11 @@
 #define HXN inline
 #define NOUNROLL
 #endif
+// successor-CSR loops of build_deps: independent atomics per predecessor
+#ifndef HESP_SUCC_UNROLL
+#define HESP_SUCC_UNROLL 4
+#endif
+constexpr int kSuccUnroll = HESP_SUCC_UNROLL;
 
 namespace hx {
 
@@ -1766,7 +1771,7 @@ struct Engine {
       const int32_t* pl_ = pred_list(j);
       const int cnt = t_pcnt()[j];
       total += cnt;
-      NOUNROLL for (int q = 0; q < cnt; ++q) wp.atomic_add(&ts()[pl_[q]].scnt, 1);
+      _Pragma("unroll kSuccUnroll") for (int q = 0; q < cnt; ++q) wp.atomic_add(&ts()[pl_[q]].scnt, 1);
     }
     wp.sync();
     total = wp.sumi(total);
@@ -1796,7 +1801,7 @@ struct Engine {
       const int j = leaf()[li];
       const int32_t* pl_ = pred_list(j);
       const int cnt = t_pcnt()[j];
-      NOUNROLL for (int q = 0; q < cnt; ++q) {
+      _Pragma("unroll kSuccUnroll") for (int q = 0; q < cnt; ++q) {
         const int p = pl_[q];
         const int pos = wp.atomic_add(&ts()[p].scnt, 1);
         succs()[ts()[p].soff + pos] = j;
