@@ -62,7 +62,12 @@ void host_ranges(uint64_t count, int nthr, F&& fn) {
   }
   std::vector<std::thread> th;
   th.reserve(nthr - 1);
-  for (int t = 1; t < nthr; ++t) th.emplace_back([&, t] { fn(t, lo(t), lo(t + 1)); });
+  int t = 1;
+  try {
+    for (; t < nthr; ++t) th.emplace_back([&fn, &lo, t] { fn(t, lo(t), lo(t + 1)); });
+  } catch (...) {  // no thread for range t: the caller runs the remaining ranges itself
+  }
+  for (int r = t; r < nthr; ++r) fn(r, lo(r), lo(r + 1));
   fn(0, lo(0), lo(1));
   for (auto& x : th) x.join();
 }
