@@ -1496,6 +1496,7 @@ struct Engine {
     wp.sync();
     // ---- pass 0 (parallel): classify leaves, take base preds for the fast ones
     int nslow = 0;
+    int sk = 0;  // this lane's share of sum_k (a register, not the engine object in local memory)
     int* const slow = gs_b();
     NOUNROLL for (int base = 0; base < nleaves; base += WP::W) {
       const int li = base + wp.lane();
@@ -1547,7 +1548,7 @@ struct Engine {
           const int tt = tile_of(t.blk[k]);
           if (fastj && tt >= 0 && tl_cnt()[tt] != 0) fastj = false;
         }
-        sum_k += kt;
+        sk += kt;
         if (fastj) {
           const BasePreds& bp = bp_()[j];
           t_poff()[j] = ~bp.uoff;
@@ -1596,9 +1597,17 @@ struct Engine {
       nslow += popc32(m);
     }
     wp.sync();
-    sum_k = wp.sumi(sum_k);
+    sum_k = wp.sumi(sum_k + sk);
     // ---- pass A (serial in program order): cell tracking for the slow leaves
-    NOUNROLL for (int si = 0; si < nslow && !status; ++si) {
+    // (the edge count lives in a register for the pass; only a fail() ends
+    // the pass early, so status is checked once)
+    if (status) return;
+    int ne = nedges;
+    auto bail = [&](int code) {
+      nedges = ne;
+      fail(code);
+    };
+    NOUNROLL for (int si = 0; si < nslow; ++si) {
       const int j = slow[si] & 0x0fffffff;
       const int nacc = (int)((unsigned)slow[si] >> 28);
       const int2* rec = dacc() + 4 * j;
@@ -1655,7 +1664,7 @@ struct Engine {
             if (npb + q < PB.maxpb) pbuf()[npb + q] = bpl_()[off + q];
           npb += cnt;
           wp.sync();
-          if (npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
+          if (npb > PB.maxpb) return bail(ST_ENGINE_LIMIT);
           continue;
         }
         const int ncells = rows * w;
@@ -1715,7 +1724,7 @@ struct Engine {
           }
           wp.sync();
         }
-        if (rn_used > PB.maxrn || npb > PB.maxpb) return fail(ST_ENGINE_LIMIT);
+        if (rn_used > PB.maxrn || npb > PB.maxpb) return bail(ST_ENGINE_LIMIT);
       }
       // dedup -> preds arena
       int m = 0;
@@ -1729,7 +1738,7 @@ struct Engine {
         const bool keep = q < npb && (same & ((1u << q) - 1u)) == 0u;
         const unsigned mk = wp.ballot(keep);
         if (keep) {
-          const int at = nedges + popc32(mk & wp.lt());
+          const int at = ne + popc32(mk & wp.lt());
           if (at < PB.maxedges) preds()[at] = v;
         }
         m = popc32(mk);
@@ -1747,21 +1756,21 @@ struct Engine {
         }
         const unsigned mk = wp.ballot(keep);
         if (keep) {
-          const int at = nedges + m + popc32(mk & wp.lt());
+          const int at = ne + m + popc32(mk & wp.lt());
           if (at < PB.maxedges) preds()[at] = v;
         }
         m += popc32(mk);
       }
-      if (nedges + m > PB.maxedges) return fail(ST_ENGINE_LIMIT);
+      if (ne + m > PB.maxedges) return bail(ST_ENGINE_LIMIT);
       if (wp.lane() == 0) {
-        t_poff()[j] = nedges;
+        t_poff()[j] = ne;
         t_pcnt()[j] = m;
         ts()[j].missing = m;
       }
       wp.sync();
-      nedges += m;
+      ne += m;
     }
-    if (status) return;
+    nedges = ne;
     // ---- pass B (parallel): successors CSR from all predecessor lists
     NOUNROLL for (int li = wp.lane(); li < nleaves; li += WP::W) ts()[leaf()[li]].scnt = 0;
     wp.sync();
