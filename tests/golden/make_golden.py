@@ -126,6 +126,8 @@ TRACES = {
     "basemerge_c2_3": ("c2", 3, "explicit_basemerge_c2"),   # 4x4 top tiling: tiles span base tiles
     "basemerge_c2_0": ("c2", 0, "explicit_basemerge_c2"),   # the bare root as the only task
     "basemerge_evict_12": ("evict_wb", 12, "explicit_basemerge_evict"),
+    # 32x32 tiles (~6.2k tasks): the load post-pass sorts ~12k events (128 KB of keys in shared memory)
+    "c4_0": ("c4", 0),
 }
 # verify_schedule on edited schedules: (trace, task to move, seconds earlier)
 SHIFTS = {

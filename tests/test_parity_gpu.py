@@ -52,6 +52,33 @@ def test_descs_path_matches_generated(lib):
     assert (b1.makespan, b1.index) == (b2.makespan, b2.index)
 
 
+@pytest.mark.parametrize("threads", ["1", "5", None])
+def test_host_packing_threads(lib, monkeypatch, threads):
+    """hesp_eval_descs packs host descriptors (and copies outcomes out) on
+    host threads from 16k candidates on (HESP_HOST_THREADS forces a count):
+    every split gives the device-generator path's outcomes, and the first
+    records are the reference's."""
+    p, count = PARITY["c2"]
+    eng = make_engine(p)
+    n = 20000
+    descs = eng.generate_host(0, n)
+    descs["n_ops"][7] = 0  # ragged: an empty descriptor (the base tiling itself) mid-range
+    if threads is None:
+        monkeypatch.delenv("HESP_HOST_THREADS", raising=False)
+    else:
+        monkeypatch.setenv("HESP_HOST_THREADS", threads)
+    out1, b1 = eng.eval_descs(descs, first=0)
+    monkeypatch.delenv("HESP_HOST_THREADS", raising=False)
+    ref, rb = eng.eval_generated(0, n)
+    keep = np.ones(n, bool)
+    keep[7] = False
+    assert np.array_equal(out1[keep], ref[keep])
+    bad = compare(out1[:count][keep[:count]], read_golden("c2")[keep[:count]])
+    assert not bad, "\n".join(bad[:5])
+    base, _ = eng.eval_descs(descs[7:8], first=7)
+    assert np.array_equal(out1[7:8], base)
+
+
 EXPLICIT = {"explicit_c2": "c2", "explicit_c3": "c3", "explicit_sect": "sect_cpugpu", "explicit_merge_c2": "c2",
             "explicit_basemerge_c2": "c2", "explicit_basemerge_evict": "evict_wb"}
 
