@@ -73,7 +73,8 @@ def test_host_packing_threads(lib, monkeypatch, threads):
     keep = np.ones(n, bool)
     keep[7] = False
     assert np.array_equal(out1[keep], ref[keep])
-    bad = compare(out1[:count][keep[:count]], read_golden("c2")[keep[:count]])
+    g = read_golden("c2")
+    bad = compare(out1, g[g["index"] != 7])
     assert not bad, "\n".join(bad[:5])
     base, _ = eng.eval_descs(descs[7:8], first=7)
     assert np.array_equal(out1[7:8], base)
