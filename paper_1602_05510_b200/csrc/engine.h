@@ -1539,8 +1539,13 @@ struct Engine {
         }
         int kt = 0;
         bool fastj = j < n_bt();
-        NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
+        // (loops over the <= 4 block slots unrolled: constant indices keep
+        // the task record in registers instead of a local-memory copy)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k > t.nrd) break;
           bool dup = false;
+#pragma unroll
           for (int q = 0; q < k; ++q) dup |= t.blk[q] == t.blk[k];
           kt += !dup;
           // (the root block has no tile: a leaf root -- the unpartitioned
@@ -1560,15 +1565,18 @@ struct Engine {
           // each either a base contribution (x = -1 - slot, E5) or its cell
           // rectangle (x = first cell, y = w | rows << 11 | row stride << 22);
           // nacc = 0 leaves the task to the serial pass's own derivation
-          const int wb = t.blk[t.nrd];
+          const int wb = t.nrd == 0 ? t.blk[0] : (t.nrd == 1 ? t.blk[1] : (t.nrd == 2 ? t.blk[2] : t.blk[3]));
           int2* rec = dacc() + 4 * j;
           int na = 0;
           bool packed = true;
-          NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k > t.nrd) break;
             const int b = t.blk[k];
             if (k < t.nrd && b == wb) continue;  // in-place read: covered by the write
             bool dup = false;
-            NOUNROLL for (int q = 0; q < k; ++q)
+#pragma unroll
+            for (int q = 0; q < k; ++q)
               if (t.blk[q] == b && q < t.nrd) dup = true;
             if (dup && k < t.nrd) continue;
             int2 r;
