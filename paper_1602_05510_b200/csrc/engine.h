@@ -1513,7 +1513,7 @@ struct Engine {
           ws.ws1 = nw > 1 ? w[1] : -1;
           ws.ws2 = nw > 2 ? w[2] : -1;
           ws.nw = nw;
-          ws.out = t.blk[t.nrd];
+          ws.out = t.nrd == 0 ? t.blk[0] : (t.nrd == 1 ? t.blk[1] : (t.nrd == 2 ? t.blk[2] : t.blk[3]));
           ws.kb = (int)t.kind | ((int)t.bidx << 8);
           ws.b = t.b;
           // static per-block facts the event loop would otherwise look up per
@@ -1521,17 +1521,20 @@ struct Engine {
           // sub-blocks (no descendants, no intersections), bit 3 = the same
           // for the output block (tile membership is fixed after the build)
           int fl = 0;
-          NOUNROLL for (int k = 0; k < nw; ++k)
-            if (simple_tile(w[k])) fl |= 1 << k;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (k < nw && simple_tile(w[k])) fl |= 1 << k;
           if (simple_tile(ws.out)) fl |= 8;
           // bit 4: the working-set blocks are pairwise disjoint, so acquiring
           // one never changes another's validity (the lean loop reads all of
           // them in one round); bit 5: the output's coherence cone needs the
           // general scan (the root, or a tile holding partial overlaps)
           bool disj = true;
-          NOUNROLL for (int a = 0; a < nw; ++a)
-            NOUNROLL for (int c = a + 1; c < nw; ++c)
-              if (roverlap(reg(w[a]), reg(w[c]))) disj = false;
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = a + 1; c < 4; ++c)
+              if (c < nw && roverlap(reg(w[a]), reg(w[c]))) disj = false;
           if (disj) fl |= 16;
           if (ws.out == 0 || tmis()[tile_of(ws.out)]) fl |= 32;
           ws.pad = fl;
@@ -2342,18 +2345,29 @@ struct Engine {
   // Working set of a task: distinct blocks of reads u writes in id order
   // (the std::set iteration of sim.cpp:597-598 and sim.cpp:768-769).
   static HX int working_set(const TaskMeta& t, int* w) {
+    // the task's distinct blocks, ascending; the <= 4 block slots unrolled
+    // with constant indices so the caller's w[] can stay in registers
     int nw = 0;
-    NOUNROLL for (int k = 0; k <= t.nrd; ++k) {
+    w[0] = w[1] = w[2] = w[3] = 0x7fffffff;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k > t.nrd) break;
       const int b = t.blk[k];
       bool dup = false;
-      for (int q = 0; q < nw; ++q) dup |= w[q] == b;
-      if (dup) continue;
-      int q = nw++;
-      while (q > 0 && w[q - 1] > b) {
-        w[q] = w[q - 1];
-        --q;
+      int ins = 0;  // insertion point: the entries below b
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        dup |= q < nw && w[q] == b;
+        ins += q < nw && w[q] < b;
       }
-      w[q] = b;
+      if (dup) continue;
+#pragma unroll
+      for (int q = 3; q > 0; --q)
+        if (q > ins) w[q] = w[q - 1];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == ins) w[q] = b;
+      ++nw;
     }
     return nw;
   }
