@@ -976,13 +976,20 @@ struct Engine {
     }
     TaskMeta m;
     m.pad = 0;
-    NOUNROLL for (int k = 0; k < nr; ++k) {
+    // the 4 block slots with constant indices (the record stays in registers)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= nr) break;
       m.blk[k] = get_or_create(rr[k], rt[k]);
       if (status) return;
     }
-    m.blk[nr] = get_or_create(w, wt);
+    const int wblk = get_or_create(w, wt);
     if (status) return;
-    NOUNROLL for (int k = nr + 1; k < 4; ++k) m.blk[k] = -1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k == nr) m.blk[k] = wblk;
+      else if (k > nr) m.blk[k] = -1;
+    }
     m.kind = (int8_t)kind;
     m.nrd = (int8_t)nr;
     m.b = w.rows;
@@ -995,8 +1002,9 @@ struct Engine {
     const int id = ntasks++;
     if (wp.lane() == 0) {
       tm()[id - n_bt()] = m;
-      NOUNROLL for (int k = 0; k <= nr; ++k)
-        if (m.blk[k] >= n_bb()) ++bref()[m.blk[k] - n_bb()];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k <= nr && m.blk[k] >= n_bb()) ++bref()[m.blk[k] - n_bb()];
     }
     wp.sync();
   }
